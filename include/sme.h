@@ -1,0 +1,226 @@
+/*
+ * sme.h — C-ABI of the B200 max_E SpMV hot path (libsme.so, sm_100a).
+ *
+ * "sme" = SpMV-Entropy.  Every entry point replaces one numpy expression of the
+ * reference package `spmv_entropy` (/root/reference/pkg/src/spmv_entropy/...).
+ * The reference file:line each call stands in for is cited next to it.
+ *
+ * Conventions:
+ *   - plain pointers and sizes only, no torch types;
+ *   - every pointer argument named d_* is DEVICE memory owned by the caller;
+ *   - no allocation inside: scratch comes from a caller buffer sized by the
+ *     matching *_workspace_size() query;
+ *   - every call is stream-ordered on the passed stream and never synchronises
+ *     the host; device-side validation results are written to device flags the
+ *     caller reads when it chooses;
+ *   - return value: SME_OK (0) or a negative SME_E* code; sme_last_error()
+ *     returns a thread-local message for the last failure on this thread.
+ *   - indices are int32 (n_rows, n_cols, nnz < 2^31); values are f64 or f32,
+ *     selected by an sme_dtype argument.  The reference is int64/f64
+ *     (matio.py:42-44, 97-99); parity compares after widening.
+ */
+#ifndef SME_H
+#define SME_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* sme_stream_t; /* a cudaStream_t / CUstream; NULL = legacy default stream */
+
+enum sme_status {
+  SME_OK = 0,
+  SME_EINVAL = -1,   /* bad argument: maps to ValueError at the Python boundary     */
+  SME_ECUDA = -2,    /* CUDA launch/runtime error: maps to RuntimeError              */
+  SME_ENOSPACE = -3, /* workspace smaller than *_workspace_size() said               */
+};
+
+enum sme_dtype { SME_F64 = 0, SME_F32 = 1 };
+
+/* Device-side validation flag bits written by the CSR/COO/perm calls. */
+enum sme_flag_bits {
+  SME_FLAG_RANGE = 1,        /* an index lies outside [0, n)                                  */
+  SME_FLAG_NOT_BIJECTION = 2,/* permutation is not a bijection (permute.py:34-36)              */
+  SME_FLAG_DUPLICATE = 4,    /* duplicate (row, col) pair (matio.py:59-64, 288-291)            */
+  SME_FLAG_ROWPTR = 8,       /* row_ptr decreasing / bad endpoints (matio.py:109-112)          */
+  SME_FLAG_UNSORTED = 16,    /* columns not strictly increasing within a row (matio.py:116-122)*/
+};
+
+const char* sme_last_error(void);
+int sme_version(void);
+/* Number of SMs of the current device (grid sizing is done inside; exported for the host). */
+int sme_device_sm_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* Permutations — permute.py                                                 */
+/* ------------------------------------------------------------------------ */
+
+/* Permutation.inverse: inv[fwd[i]] = i.  Replaces permute.py:42-45 and the
+ * bijection check of Permutation.__post_init__ (permute.py:29-36): bit
+ * SME_FLAG_RANGE / SME_FLAG_NOT_BIJECTION is OR-ed into *d_flag (int32). */
+int sme_perm_inverse(int64_t n, const int32_t* d_fwd, int32_t* d_inv, int32_t* d_flag,
+                     sme_stream_t stream);
+
+/* permute_vector: out[p[i]] = x[i]  (permute.py:105-112).  Bit-exact value moves. */
+int sme_permute_vector(int dtype, int64_t n, const int32_t* d_p, const void* d_x, void* d_out,
+                       sme_stream_t stream);
+
+/* Gather: out[i] = x[idx[i]].  With idx = inverse(p) this equals permute_vector;
+ * with int32 data it is compose(after, first) = after.forward[first.forward]
+ * (permute.py:64-68) — pass dtype = -1 for int32 payloads. */
+int sme_gather(int dtype, int64_t n, const int32_t* d_idx, const void* d_x, void* d_out,
+               sme_stream_t stream);
+
+/* permute_matrix on COO: (p_r[row], p_c[col], v) in ORIGINAL entry order
+ * (permute.py:98-102, permute_rows/permute_cols :84-95).  Either map may be NULL
+ * (identity).  Values are not touched (the caller shares or copies them). */
+int sme_coo_remap(int64_t nnz, const int32_t* d_row, const int32_t* d_col, const int32_t* d_row_map,
+                  const int32_t* d_col_map, int32_t* d_row_out, int32_t* d_col_out,
+                  sme_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* CSR construction — matio.py:281-300 and permute.py:98 (fused)              */
+/* ------------------------------------------------------------------------ */
+
+/* Scratch for the two row_ptr builders (row counts + scan partials). */
+int sme_row_ptr_workspace_size(int64_t n_rows, size_t* bytes);
+
+/* Step 1 of coo_to_csr (matio.py:292-293, cumsum(bincount(row))): row counts of
+ * the (optionally row-mapped) COO and their exclusive scan -> row_ptr[n_rows+1].
+ * Range violations of row/col are OR-ed into *d_flag as SME_FLAG_RANGE. */
+int sme_coo_row_ptr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row,
+                    const int32_t* d_col, const int32_t* d_row_map, int32_t* d_row_ptr_out,
+                    void* d_ws, size_t ws_bytes, int32_t* d_flag, sme_stream_t stream);
+
+/* Step 2 of coo_to_csr (matio.py:281-294), optionally through row/col maps so
+ * that coo_to_csr(permute_matrix(m, p_r, p_c)) is one pipeline: scatter into
+ * the rows of d_row_ptr (from step 1), then a segmented column sort inside each
+ * row; values move bit-exactly.  Duplicates are OR-ed into *d_flag; the
+ * smallest duplicate (row << 32 | col) in row-major order goes to *d_dup_key
+ * (uint64, caller initialises it to UINT64_MAX) — the first duplicate the
+ * reference's lexsort reports (matio.py:288-291).  long_nnz = sum of the
+ * lengths of rows longer than SME_SORT_SMEM_MAX (sme_long_row_nnz). */
+int sme_coo_to_csr_workspace_size(int64_t n_rows, int64_t nnz, int64_t long_nnz, size_t* bytes);
+int sme_coo_to_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row,
+                   const int32_t* d_col, const void* d_val, const int32_t* d_row_map,
+                   const int32_t* d_col_map, const int32_t* d_row_ptr, int32_t* d_col_out,
+                   void* d_val_out, void* d_ws, size_t ws_bytes, int64_t long_nnz,
+                   int32_t* d_flag, uint64_t* d_dup_key, sme_stream_t stream);
+
+/* Permuted CSR directly from CSR (K4): new row r is old
+ * row inv_r[r], columns mapped through col_map (old -> new; NULL = identity),
+ * then sorted within the row; bit-identical to
+ * coo_to_csr(permute_matrix(csr_to_coo(A), p_r, p_c)).  d_inv_row may be NULL
+ * (identity rows). */
+int sme_permute_csr_row_ptr(int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_inv_row,
+                            int32_t* d_row_ptr_out, void* d_ws, size_t ws_bytes,
+                            sme_stream_t stream); /* ws: sme_row_ptr_workspace_size */
+int sme_permute_csr_workspace_size(int64_t n_rows, int64_t nnz, int64_t long_nnz, size_t* bytes);
+int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                    const int32_t* d_row_ptr, const int32_t* d_col, const void* d_val,
+                    const int32_t* d_inv_row, const int32_t* d_col_map,
+                    const int32_t* d_row_ptr_out /* from sme_permute_csr_row_ptr */,
+                    int32_t* d_col_out, void* d_val_out, void* d_ws, size_t ws_bytes,
+                    int64_t long_nnz, int32_t* d_flag, uint64_t* d_dup_key, sme_stream_t stream);
+
+/* Rows longer than this are sorted through global scratch (long-row path). */
+#define SME_SORT_SMEM_MAX 4096
+/* Sum of the lengths of rows longer than SME_SORT_SMEM_MAX -> *d_out (int64). */
+int sme_long_row_nnz(int64_t n_rows, const int32_t* d_row_ptr, int64_t* d_out, sme_stream_t stream);
+
+/* CsrMatrix.__post_init__ checks (matio.py:105-122) on device: OR-s
+ * SME_FLAG_ROWPTR / SME_FLAG_RANGE / SME_FLAG_UNSORTED into *d_flag. */
+int sme_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row_ptr,
+                     const int32_t* d_col, int32_t* d_flag, sme_stream_t stream);
+
+/* csr_to_coo row expansion (matio.py:297-300): row_idx[k] = row of entry k. */
+int sme_csr_expand_rows(int64_t n_rows, const int32_t* d_row_ptr, int32_t* d_row_out,
+                        sme_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Entropy histogram — entropy.py                                            */
+/* ------------------------------------------------------------------------ */
+
+/* histogram_2d (entropy.py:91-101) from CSR: counts[br*bc] (int64, row-major),
+ * bins per _bin_index (entropy.py:65-67): width = n // bins, last bin absorbs
+ * the remainder.  ACCUMULATES into d_counts (caller zeroes it). */
+int sme_hist2d_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row_ptr,
+                   const int32_t* d_col, int32_t bins_r, int32_t bins_c, int64_t* d_counts,
+                   sme_stream_t stream);
+/* Same from COO triplets in any order (the reference's own input type). */
+int sme_hist2d_coo(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row,
+                   const int32_t* d_col, int32_t bins_r, int32_t bins_c, int64_t* d_counts,
+                   sme_stream_t stream);
+/* row_histogram from CSR (entropy.py:77-81): counts[b] = row_ptr[e_{b+1}] - row_ptr[e_b]. */
+int sme_row_hist_csr(int64_t n_rows, const int32_t* d_row_ptr, int32_t bins, int64_t* d_counts,
+                     sme_stream_t stream);
+
+/* shannon_entropy / _entropy_of_counts (entropy.py:104-119):
+ * -sum_{c>0} p log_base p, p = c / total, one deterministic block reduction.
+ * *d_out (double) receives the entropy; *d_total (int64, may be NULL) the total. */
+int sme_entropy(int64_t n_bins, const int64_t* d_counts, double base, double* d_out,
+                int64_t* d_total, sme_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* SpMV — kernels.py                                                        */
+/* ------------------------------------------------------------------------ */
+
+/* Merge-path (nnz+row balanced) CSR SpMV, the drop-in for spmv_csr
+ * (kernels.py:59-78).  A per-matrix plan (tile coordinates on the merge path
+ * of row ends and nonzeros) is built once and reused across calls:
+ *   plan: (n_tiles + 1) int2 = (row, nnz) split points; carry: n_tiles x
+ *   (int32 row + value) scratch.
+ * accumulate = 0: y = A x;  accumulate = 1: y += A x (column-panel passes). */
+int sme_spmv_merge_tiles(int64_t n_rows, int64_t nnz, int64_t* n_tiles);
+int sme_spmv_merge_plan(int64_t n_rows, int64_t nnz, const int32_t* d_row_ptr, int32_t* d_plan,
+                        sme_stream_t stream);
+int sme_spmv_merge_carry_bytes(int dtype, int64_t n_tiles, size_t* bytes);
+int sme_spmv_merge(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                   const int32_t* d_row_ptr, const int32_t* d_col, const void* d_val,
+                   const void* d_x, void* d_y, const int32_t* d_plan, int64_t n_tiles,
+                   void* d_carry, int accumulate, sme_stream_t stream);
+
+/* CSR-vector ("warp-per-row") SpMV: `lanes` in {1,2,4,8,16,32} threads per row,
+ * lane-strided partial sums combined by a butterfly shuffle.  The per-row
+ * reduction order depends only on `lanes`, so any row partition
+ * (spmv_csr_parallel, kernels.py:102-128; multi-GPU row shards) is bitwise
+ * equal to the unpartitioned call. */
+int sme_spmv_vector(int dtype, int lanes, int64_t n_rows, int64_t n_cols,
+                    const int32_t* d_row_ptr, const int32_t* d_col, const void* d_val,
+                    const void* d_x, void* d_y, int accumulate, sme_stream_t stream);
+
+/* Bit-exact restatement of the reference reduction on the GPU: y_i =
+ * prod[s] + numpy_pairwise_sum(prod[s+1:e]) with separately rounded multiplies
+ * and adds (kernels.py:59-70; numpy's add.reduceat order, SURVEY.md App. A
+ * item 1).  f64 only.  Slow (thread per row); parity tool. */
+int sme_spmv_reduceat_exact(int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_col,
+                            const double* d_val, const double* d_x, double* d_y,
+                            sme_stream_t stream);
+
+/* COO SpMV (spmv_coo, kernels.py:81-86): y = 0; y[row[k]] += v[k] * x[col[k]].
+ * Fixed-point-free floating atomics: order-dependent in the last ulps. */
+int sme_spmv_coo(int dtype, int64_t n_rows, int64_t nnz, const int32_t* d_row, const int32_t* d_col,
+                 const void* d_val, const void* d_x, void* d_y, sme_stream_t stream);
+
+/* relative_error (kernels.py:131-142) helper: d_out[0] = max|got - exp|,
+ * d_out[1] = max|exp| (f64, caller zeroes). */
+int sme_maxabs_diff(int dtype, int64_t n, const void* d_got, const void* d_exp, double* d_out,
+                    sme_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Row sharding (multi-GPU) — kernels.py:38-49 make_row_partition           */
+/* ------------------------------------------------------------------------ */
+
+/* Column ids -> positions in the padded all-gathered x of `parts` equal slots of
+ * `pad` entries: rank k owns the make_row_partition range [b_k, b_{k+1}) and its
+ * slice lands at k * pad.  col_out may alias col_in. */
+int sme_rowshard_remap_cols(int64_t nnz, int64_t n_cols, int32_t parts, int64_t pad,
+                            const int32_t* d_col_in, int32_t* d_col_out, sme_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SME_H */

@@ -1,0 +1,28 @@
+/*
+ * sme_synth.h — device generators for the synthetic matrices of BASELINE.json
+ * (SURVEY.md §8d).  Benchmark/test inputs only; not part of the reference path.
+ * Bit-identical numpy restatements live in paper_2308_00106_b200/synth.py.
+ */
+#ifndef SME_SYNTH_H
+#define SME_SYNTH_H
+#include "sme.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* 5-point Laplacian on a g x g grid (C2: g = 2000, C5: g = 2828): row r = i*g + j
+ * holds r-g, r-1, r, r+1, r+g (those inside the grid), values -1, -1, 4, -1, -1.
+ * row_ptr: g*g + 1 int32; col/val: 5g^2 - 4g entries. */
+int sme_synth_laplacian5(int dtype, int64_t g, int32_t* d_row_ptr, int32_t* d_col, void* d_val,
+                         sme_stream_t stream);
+
+/* Random-structured rows (C4): every row has k (<= 32) distinct columns, the first
+ * k distinct draws of hash3(seed, r, t) mapped to [0, n_cols), sorted ascending;
+ * value of sorted slot s = U[-1,1) from hash3(seed ^ 0x5DEECE66D, r, s). */
+int sme_synth_random_rows(int dtype, int64_t n_rows, int64_t n_cols, int32_t k, uint64_t seed,
+                          int32_t* d_row_ptr, int32_t* d_col, void* d_val, sme_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

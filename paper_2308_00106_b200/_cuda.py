@@ -1,0 +1,100 @@
+"""Torch plumbing for the C-ABI: device tensors, the current stream, scratch.
+
+PyTorch provides device memory (its caching allocator), streams and host<->
+device copies; every computation on the path is a libsme.so kernel.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+INT32_MAX = 2**31 - 1
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "a CUDA device is required: the max_E SpMV path runs only as sm_100a kernels "
+            "(no CPU fallback)"
+        )
+    _lib.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def sme_dtype(t: torch.Tensor) -> int:
+    if t.dtype == torch.float64:
+        return _lib.SME_F64
+    if t.dtype == torch.float32:
+        return _lib.SME_F32
+    if t.dtype == torch.int32:
+        return _lib.SME_I32
+    raise ValueError(f"unsupported dtype {t.dtype}")
+
+
+def workspace(nbytes: int) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=require_cuda())
+
+
+def as_index_tensor(a, what: str, n_max: int | None = None) -> torch.Tensor:
+    """1-D int32 device tensor from numpy / list / torch input (values are range-checked
+    on the device by the caller; here only representability in int32 is checked)."""
+    dev = require_cuda()
+    if isinstance(a, torch.Tensor):
+        if a.dtype == torch.int32:
+            return a.to(dev).contiguous()
+        a64 = a.to(torch.int64)
+        if a64.numel() and (int(a64.min()) < -INT32_MAX or int(a64.max()) > INT32_MAX):
+            raise ValueError(f"{what} outside int32 range")
+        return a64.to(dev, torch.int32).contiguous()
+    arr = np.asarray(a, dtype=np.int64)
+    if arr.ndim != 1:
+        raise ValueError(f"{what} must be a 1-D array")
+    if arr.size and (arr.min() < -INT32_MAX or arr.max() > INT32_MAX):
+        raise ValueError(f"{what} outside int32 range")
+    return torch.from_numpy(arr.astype(np.int32)).to(dev)
+
+
+def as_value_tensor(a, dtype: torch.dtype) -> torch.Tensor:
+    dev = require_cuda()
+    if isinstance(a, torch.Tensor):
+        return a.to(dev, dtype).contiguous()
+    arr = np.asarray(a, dtype=np.float64)
+    return torch.from_numpy(np.ascontiguousarray(arr)).to(dev, dtype)
+
+
+class DeviceFlags:
+    """An int32 validation flag word plus a uint64 'first duplicate' key on the device."""
+
+    def __init__(self):
+        dev = require_cuda()
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.dup = torch.full((1,), -1, dtype=torch.int64, device=dev)  # 0xFFFF...FFFF
+
+    @property
+    def flag_ptr(self) -> int:
+        return self.flag.data_ptr()
+
+    @property
+    def dup_ptr(self) -> int:
+        return self.dup.data_ptr()
+
+    def read(self) -> tuple[int, int]:
+        """Synchronising read: (flag bits, duplicate key as unsigned)."""
+        f = int(self.flag.item())
+        d = int(self.dup.item()) & 0xFFFFFFFFFFFFFFFF
+        return f, d
+
+
+def to_host(t: torch.Tensor, dtype) -> np.ndarray:
+    return t.detach().to("cpu").numpy().astype(dtype, copy=False)

@@ -1,0 +1,116 @@
+"""ctypes binding of libsme.so — the C-ABI declared in include/sme.h.
+
+This module is the only place that touches the shared library.  Loading it is
+lazy; a missing library or a missing CUDA device raises immediately (there is
+no CPU fallback anywhere on the product path).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libsme.so"
+
+SME_OK, SME_EINVAL, SME_ECUDA, SME_ENOSPACE = 0, -1, -2, -3
+SME_F64, SME_F32, SME_I32 = 0, 1, -1
+FLAG_RANGE, FLAG_NOT_BIJECTION, FLAG_DUPLICATE, FLAG_ROWPTR, FLAG_UNSORTED = 1, 2, 4, 8, 16
+SORT_SMEM_MAX = 4096
+
+p = C.c_void_p
+i32 = C.c_int32
+i64 = C.c_int64
+u64 = C.c_uint64
+f64 = C.c_double
+sz = C.c_size_t
+psz = C.POINTER(C.c_size_t)
+pi64 = C.POINTER(C.c_int64)
+
+# name -> argtypes (restype is int unless listed in _RESTYPES)
+SIGNATURES: dict[str, list] = {
+    "sme_last_error": [],
+    "sme_version": [],
+    "sme_device_sm_count": [],
+    "sme_perm_inverse": [i64, p, p, p, p],
+    "sme_permute_vector": [C.c_int, i64, p, p, p, p],
+    "sme_gather": [C.c_int, i64, p, p, p, p],
+    "sme_coo_remap": [i64, p, p, p, p, p, p, p],
+    "sme_row_ptr_workspace_size": [i64, psz],
+    "sme_coo_row_ptr": [i64, i64, i64, p, p, p, p, p, sz, p, p],
+    "sme_coo_to_csr_workspace_size": [i64, i64, i64, psz],
+    "sme_coo_to_csr": [C.c_int, i64, i64, i64, p, p, p, p, p, p, p, p, p, sz, i64, p, p, p],
+    "sme_permute_csr_row_ptr": [i64, p, p, p, p, sz, p],
+    "sme_permute_csr_workspace_size": [i64, i64, i64, psz],
+    "sme_permute_csr": [C.c_int, i64, i64, i64, p, p, p, p, p, p, p, p, p, sz, i64, p, p, p],
+    "sme_long_row_nnz": [i64, p, p, p],
+    "sme_csr_validate": [i64, i64, i64, p, p, p, p],
+    "sme_csr_expand_rows": [i64, p, p, p],
+    "sme_hist2d_csr": [i64, i64, i64, p, p, i32, i32, p, p],
+    "sme_hist2d_coo": [i64, i64, i64, p, p, i32, i32, p, p],
+    "sme_row_hist_csr": [i64, p, i32, p, p],
+    "sme_entropy": [i64, p, f64, p, p, p],
+    "sme_spmv_merge_tiles": [i64, i64, pi64],
+    "sme_spmv_merge_plan": [i64, i64, p, p, p],
+    "sme_spmv_merge_carry_bytes": [C.c_int, i64, psz],
+    "sme_spmv_merge": [C.c_int, i64, i64, i64, p, p, p, p, p, p, i64, p, C.c_int, p],
+    "sme_spmv_vector": [C.c_int, C.c_int, i64, i64, p, p, p, p, p, C.c_int, p],
+    "sme_spmv_reduceat_exact": [i64, p, p, p, p, p, p],
+    "sme_spmv_coo": [C.c_int, i64, i64, p, p, p, p, p, p],
+    "sme_maxabs_diff": [C.c_int, i64, p, p, p, p],
+    "sme_rowshard_remap_cols": [i64, i64, i32, i64, p, p, p],
+    # sme_synth.h
+    "sme_synth_laplacian5": [C.c_int, i64, p, p, p, p],
+    "sme_synth_random_rows": [C.c_int, i64, i64, i32, u64, p, p, p, p],
+}
+_RESTYPES = {"sme_last_error": C.c_char_p}
+
+_lock = threading.Lock()
+_lib: C.CDLL | None = None
+
+
+def load() -> C.CDLL:
+    """Load libsme.so and declare every exported signature (no CUDA needed)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RuntimeError(
+                    f"{LIB_PATH.name} is not built: run `python -m paper_2308_00106_b200._build` "
+                    "(the max_E SpMV path has no CPU fallback)"
+                )
+            lib = C.CDLL(str(LIB_PATH))
+            for name, argtypes in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.argtypes = argtypes
+                fn.restype = _RESTYPES.get(name, C.c_int)
+            _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    msg = load().sme_last_error()
+    return msg.decode() if msg else ""
+
+
+def call(name: str, *args) -> None:
+    """Invoke an sme_* entry point; a non-zero status raises (EINVAL -> ValueError)."""
+    status = getattr(load(), name)(*args)
+    if status == SME_OK:
+        return
+    msg = f"{name}: {last_error()}"
+    if status == SME_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def query_size(name: str, *args) -> int:
+    out = C.c_size_t(0)
+    call(name, *args, C.byref(out))
+    return int(out.value)
+
+
+def query_i64(name: str, *args) -> int:
+    out = C.c_int64(0)
+    call(name, *args, C.byref(out))
+    return int(out.value)

@@ -1,0 +1,175 @@
+// common.cuh — shared helpers for the sm_100a kernels of libsme.so.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "../../include/sme.h"
+
+#define SME_API extern "C" __attribute__((visibility("default")))
+
+namespace sme {
+
+// thread-local error message (sme_abi.cu)
+void set_error(const char* fmt, ...);
+
+inline cudaStream_t as_stream(sme_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count();
+
+// Grid for a grid-stride loop: enough CTAs to fill every SM `per_sm` times, never more
+// than the work needs.
+inline int grid_for(int64_t work_items, int threads, int per_sm = 8) {
+  int64_t need = (work_items + threads - 1) / threads;
+  int64_t cap = (int64_t)sm_count() * per_sm;
+  if (need < 1) need = 1;
+  return (int)(need < cap ? need : cap);
+}
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+}  // namespace sme
+
+#define SME_CHECK_LAUNCH(what)                                                        \
+  do {                                                                                \
+    cudaError_t _e = cudaGetLastError();                                              \
+    if (_e != cudaSuccess) {                                                          \
+      sme::set_error("%s: %s", what, cudaGetErrorString(_e));                         \
+      return SME_ECUDA;                                                               \
+    }                                                                                 \
+  } while (0)
+
+#define SME_CUDA(call)                                                                \
+  do {                                                                                \
+    cudaError_t _e = (call);                                                          \
+    if (_e != cudaSuccess) {                                                          \
+      sme::set_error("%s: %s", #call, cudaGetErrorString(_e));                        \
+      return SME_ECUDA;                                                               \
+    }                                                                                 \
+  } while (0)
+
+#define SME_REQUIRE(cond, ...)                                                        \
+  do {                                                                                \
+    if (!(cond)) {                                                                    \
+      sme::set_error(__VA_ARGS__);                                                    \
+      return SME_EINVAL;                                                              \
+    }                                                                                 \
+  } while (0)
+
+namespace sme {
+
+// ---------------------------------------------------------------------------
+// cache-policy loads (PTX createpolicy + L2::cache_hint)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// streaming 128-bit loads: no L1 allocation, L2 evict-first
+__device__ __forceinline__ int4 ld_stream_i4(const int4* p, uint64_t pol) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream_d2(const double2* p, uint64_t pol) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float4 ld_stream_f4(const float4* p, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ int ld_stream_i1(const int* p, uint64_t pol) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+               : "=r"(r)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(r)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_stream(const float* p, uint64_t pol) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+               : "=f"(r)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+// gathers of x: read-only path, L2 evict-last so the vector stays resident
+__device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
+  double r;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_keep(const float* p, uint64_t pol) {
+  float r;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
+// streaming store (evict-first)
+__device__ __forceinline__ void st_stream(double* p, double v) {
+  asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v));
+}
+__device__ __forceinline__ void st_stream(float* p, float v) {
+  asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v));
+}
+
+// ---------------------------------------------------------------------------
+// exact division by an invariant divisor: q = (n * m) >> s, exact for
+// 0 <= n < 2^31 and 1 <= d < 2^31 (m = ceil(2^s / d), s = 32 + ceil(log2 d)).
+// ---------------------------------------------------------------------------
+struct FastDiv {
+  uint64_t m;
+  uint32_t s;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  uint32_t s = 32 + l;
+  unsigned __int128 num = ((unsigned __int128)1) << s;
+  uint64_t m = (uint64_t)((num + d - 1) / d);
+  return FastDiv{m, s};
+}
+__device__ __forceinline__ uint32_t fastdiv(uint32_t n, FastDiv f) {
+  return (uint32_t)(((uint64_t)n * f.m) >> f.s);
+}
+
+// _bin_index (entropy.py:65-67): min(idx // (n // bins), bins - 1)
+struct Binner {
+  FastDiv div;
+  int32_t last;
+};
+inline Binner make_binner(int64_t n, int32_t bins) {
+  int64_t width = n / bins;
+  return Binner{make_fastdiv((uint32_t)width), bins - 1};
+}
+__device__ __forceinline__ int32_t bin_of(int32_t idx, Binner b) {
+  int32_t q = (int32_t)fastdiv((uint32_t)idx, b.div);
+  return q < b.last ? q : b.last;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+}  // namespace sme

@@ -1,0 +1,519 @@
+// csr_build.cu — COO->CSR and the fused permuted-CSR build (K4 in SURVEY.md §2.2).
+//
+// Reference: coo_to_csr (matio.py:281-294) = lexsort((col,row)) + duplicate
+// check + cumsum(bincount(row)); permute_matrix (permute.py:98-102) = index
+// remap in entry order, after which the reference runs coo_to_csr again.
+//
+// GPU algorithm (same output bits):
+//   1. row lengths of the result (COO: atomic count per row; CSR: gather of
+//      the old row length through inv_r) -> exclusive scan -> row_ptr;
+//   2. COO only: stable-free scatter of (mapped col, value) into the row's
+//      slots (order inside a row is arbitrary here);
+//   3. segmented sort inside every row by (mapped) column, values following
+//      bit-exactly, adjacent-equal columns flagged as duplicates.  Rows are
+//      dispatched by length: <= 32 -> sub-warp bitonic network in registers
+//      (G = next_pow2(max len in the warp's 32 rows) lanes per row);
+//      <= SME_SORT_SMEM_MAX -> one CTA, bitonic in shared memory;
+//      longer -> one CTA, shared-memory chunk sort + global merge passes.
+// Because (row, col) pairs are unique the sorted CSR is unique, so the result
+// is independent of the scatter order and bit-identical to the reference.
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace sme {
+
+constexpr int LONG_CHUNK = SME_SORT_SMEM_MAX;  // keys per shared-memory chunk
+constexpr int SORT_NT = 256;
+constexpr int LONG_NT = 512;
+
+struct SortLists {
+  int32_t* med;       // [n_rows] row ids with 32 < len <= SMEM_MAX
+  int32_t* lng;       // [n_rows] row ids with len > SMEM_MAX
+  int64_t* lng_off;   // [n_rows] offset of each long row in the long scratch
+  int32_t* counters;  // [0] = #med, [1] = #long
+  unsigned long long* lng_cursor;  // running long scratch offset
+  uint64_t* scratch_a;             // long_nnz keys
+  uint64_t* scratch_b;             // long_nnz keys
+};
+
+inline size_t lists_bytes(int64_t n_rows, int64_t long_nnz) {
+  return align_up(n_rows * 4) * 2 + align_up(n_rows * 8) + align_up(64) + align_up(long_nnz * 8) * 2;
+}
+
+inline SortLists carve_lists(char* p, int64_t n_rows, int64_t long_nnz) {
+  SortLists L;
+  L.med = (int32_t*)p;           p += align_up(n_rows * 4);
+  L.lng = (int32_t*)p;           p += align_up(n_rows * 4);
+  L.lng_off = (int64_t*)p;       p += align_up(n_rows * 8);
+  L.counters = (int32_t*)p;
+  L.lng_cursor = (unsigned long long*)(p + 16);
+  p += align_up(64);
+  L.scratch_a = (uint64_t*)p;    p += align_up(long_nnz * 8);
+  L.scratch_b = (uint64_t*)p;
+  return L;
+}
+
+// Where the entries of output row r are read from.
+struct SrcGather {  // permuted CSR: old row inv[r] of the source CSR
+  const int32_t* old_ptr;
+  const int32_t* inv;
+  __device__ __forceinline__ int64_t start(int32_t r, int32_t /*dst*/) const {
+    return old_ptr[inv ? inv[r] : r];
+  }
+};
+struct SrcStaged {  // COO path: the row's slots in the staging arrays
+  __device__ __forceinline__ int64_t start(int32_t /*r*/, int32_t dst) const { return dst; }
+};
+
+__device__ __forceinline__ void report_dup(int32_t row, uint32_t col, int32_t* flag,
+                                           unsigned long long* dup_key) {
+  atomicOr(flag, SME_FLAG_DUPLICATE);
+  atomicMin(dup_key, ((unsigned long long)(uint32_t)row << 32) | col);
+}
+
+__device__ __forceinline__ uint32_t map_col(const int32_t* __restrict__ cmap, int32_t c) {
+  return (uint32_t)(cmap ? __ldg(cmap + c) : c);
+}
+
+// ---------------------------------------------------------------------------
+// rows with len <= 32: sub-warp bitonic sort in registers
+// ---------------------------------------------------------------------------
+template <typename T, class Src>
+__global__ void __launch_bounds__(SORT_NT) k_sort_rows_warp(
+    int32_t n_rows, const int32_t* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
+    const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
+    T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_groups = ((int64_t)n_rows + 31) / 32;
+  const int64_t warp_global = ((int64_t)blockIdx.x * SORT_NT + threadIdx.x) >> 5;
+  const int64_t warps_total = ((int64_t)gridDim.x * SORT_NT) >> 5;
+  for (int64_t g = warp_global; g < n_groups; g += warps_total) {
+    const int32_t r = (int32_t)(g * 32 + lane);
+    int32_t dst = 0, len = 0;
+    int64_t from = 0;
+    if (r < n_rows) {
+      dst = new_ptr[r];
+      len = new_ptr[r + 1] - dst;
+      if (len > 0) from = src.start(r, dst);
+    }
+    if (len > 32) {
+      if (len <= SME_SORT_SMEM_MAX) {
+        int slot = atomicAdd(&L.counters[0], 1);
+        L.med[slot] = r;
+      } else {
+        int slot = atomicAdd(&L.counters[1], 1);
+        L.lng[slot] = r;
+        L.lng_off[slot] = (int64_t)atomicAdd(L.lng_cursor, (unsigned long long)len);
+      }
+      len = 0;
+    }
+    int maxlen = len;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    if (maxlen == 0) continue;
+    int G = 1;
+    while (G < maxlen) G <<= 1;
+    const int per_pass = 32 / G;
+    const int li = lane & (G - 1);
+    const int sub = lane / G;
+    for (int b = 0; b < 32; b += per_pass) {
+      const int rr = b + sub;  // row of this lane's sub-group, within the group of 32
+      const int32_t my_len = __shfl_sync(0xffffffffu, len, rr);
+      const int32_t my_dst = __shfl_sync(0xffffffffu, dst, rr);
+      const int64_t my_from = __shfl_sync(0xffffffffu, from, rr);
+      uint64_t v = ~0ull;
+      if (li < my_len) v = ((uint64_t)map_col(cmap, src_col[my_from + li]) << 32) | (uint32_t)li;
+      for (int k = 2; k <= G; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          uint64_t o = __shfl_xor_sync(0xffffffffu, v, j);
+          bool asc = (li & k) == 0;
+          bool lower = (li & j) == 0;
+          uint64_t mn = v < o ? v : o, mx = v < o ? o : v;
+          v = (lower == asc) ? mn : mx;
+        }
+      }
+      uint64_t prev = __shfl_up_sync(0xffffffffu, v, 1);
+      if (li < my_len) {
+        uint32_t key = (uint32_t)(v >> 32);
+        uint32_t idx = (uint32_t)v;
+        if (li > 0 && (uint32_t)(prev >> 32) == key) report_dup((int32_t)(g * 32 + rr), key, flag, dup_key);
+        out_col[my_dst + li] = (int32_t)key;
+        out_val[my_dst + li] = src_val[my_from + idx];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// block-level bitonic sort of P (power of two) keys in shared memory
+// ---------------------------------------------------------------------------
+template <int NT>
+__device__ void smem_bitonic(uint64_t* s, int P) {
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += NT) {
+        int p = i ^ j;
+        if (p > i) {
+          uint64_t a = s[i], b = s[p];
+          bool asc = (i & k) == 0;
+          if ((a > b) == asc) {
+            s[i] = b;
+            s[p] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// rows with 32 < len <= SME_SORT_SMEM_MAX: one CTA per row
+template <typename T, class Src>
+__global__ void __launch_bounds__(SORT_NT) k_sort_rows_block(
+    const int32_t* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
+    const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
+    T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key) {
+  __shared__ uint64_t s[SME_SORT_SMEM_MAX];
+  const int count = L.counters[0];
+  for (int it = blockIdx.x; it < count; it += gridDim.x) {
+    const int32_t r = L.med[it];
+    const int32_t dst = new_ptr[r];
+    const int32_t len = new_ptr[r + 1] - dst;
+    const int64_t from = src.start(r, dst);
+    int P = 64;
+    while (P < len) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += SORT_NT)
+      s[i] = i < len ? (((uint64_t)map_col(cmap, src_col[from + i]) << 32) | (uint32_t)i) : ~0ull;
+    __syncthreads();
+    smem_bitonic<SORT_NT>(s, P);
+    for (int i = threadIdx.x; i < len; i += SORT_NT) {
+      uint64_t v = s[i];
+      uint32_t key = (uint32_t)(v >> 32);
+      if (i > 0 && (uint32_t)(s[i - 1] >> 32) == key) report_dup(r, key, flag, dup_key);
+      out_col[dst + i] = (int32_t)key;
+      out_val[dst + i] = src_val[from + (uint32_t)v];
+    }
+    __syncthreads();
+  }
+}
+
+// rows with len > SME_SORT_SMEM_MAX: chunk sort in smem, then merge passes
+// between two global scratch buffers; one CTA per row.
+template <typename T, class Src>
+__global__ void __launch_bounds__(LONG_NT) k_sort_rows_long(
+    const int32_t* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
+    const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
+    T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key) {
+  __shared__ uint64_t s[LONG_CHUNK];
+  const int count = L.counters[1];
+  for (int it = blockIdx.x; it < count; it += gridDim.x) {
+    const int32_t r = L.lng[it];
+    const int32_t dst = new_ptr[r];
+    const int64_t len = new_ptr[r + 1] - dst;
+    const int64_t from = src.start(r, dst);
+    uint64_t* a = L.scratch_a + L.lng_off[it];
+    uint64_t* b = L.scratch_b + L.lng_off[it];
+    // 1. sorted chunks
+    for (int64_t c0 = 0; c0 < len; c0 += LONG_CHUNK) {
+      int n = (int)min((int64_t)LONG_CHUNK, len - c0);
+      int P = 64;
+      while (P < n) P <<= 1;
+      for (int i = threadIdx.x; i < P; i += LONG_NT)
+        s[i] = i < n ? (((uint64_t)map_col(cmap, src_col[from + c0 + i]) << 32) | (uint32_t)(c0 + i))
+                     : ~0ull;
+      __syncthreads();
+      smem_bitonic<LONG_NT>(s, P);
+      for (int i = threadIdx.x; i < n; i += LONG_NT) a[c0 + i] = s[i];
+      __syncthreads();
+    }
+    // 2. merge passes a -> b, swap
+    for (int64_t w = LONG_CHUNK; w < len; w <<= 1) {
+      // thread t produces outputs [o0, o1) of the whole row
+      int64_t o0 = len * threadIdx.x / LONG_NT, o1 = len * (threadIdx.x + 1) / LONG_NT;
+      int64_t o = o0;
+      while (o < o1) {
+        int64_t ps = (o / (2 * w)) * (2 * w);  // pair start
+        int64_t la = min(w, len - ps);
+        int64_t lb = min(w, max((int64_t)0, len - ps - w));
+        const uint64_t* A = a + ps;
+        const uint64_t* B = a + ps + la;
+        int64_t pend = min(o1, ps + la + lb);
+        int64_t d = o - ps;
+        int64_t lo = max((int64_t)0, d - lb), hi = min(d, la);
+        while (lo < hi) {
+          int64_t mid = (lo + hi) >> 1;
+          if (A[mid] <= B[d - 1 - mid]) lo = mid + 1; else hi = mid;
+        }
+        int64_t ia = lo, ib = d - lo;
+        for (; o < pend; ++o) {
+          bool takeA = ib >= lb || (ia < la && A[ia] <= B[ib]);
+          b[o] = takeA ? A[ia++] : B[ib++];
+        }
+      }
+      __syncthreads();
+      uint64_t* t = a; a = b; b = t;
+      __syncthreads();
+    }
+    // 3. emit
+    for (int64_t i = threadIdx.x; i < len; i += LONG_NT) {
+      uint64_t v = a[i];
+      uint32_t key = (uint32_t)(v >> 32);
+      if (i > 0 && (uint32_t)(a[i - 1] >> 32) == key) report_dup(r, key, flag, dup_key);
+      out_col[dst + i] = (int32_t)key;
+      out_val[dst + i] = src_val[from + (uint32_t)v];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// COO phase kernels
+// ---------------------------------------------------------------------------
+__global__ void k_coo_count(int64_t nnz, int64_t n_rows, int64_t n_cols, const int32_t* __restrict__ row,
+                            const int32_t* __restrict__ col, const int32_t* __restrict__ rmap,
+                            int32_t* __restrict__ counts, int32_t* flag) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
+    int32_t r = row[k], c = col[k];
+    if (r < 0 || r >= n_rows || c < 0 || c >= n_cols) {
+      atomicOr(flag, SME_FLAG_RANGE);
+      continue;
+    }
+    if (rmap) r = rmap[r];
+    atomicAdd(&counts[r], 1);
+  }
+}
+
+template <typename T>
+__global__ void k_coo_scatter(int64_t nnz, int64_t n_rows, int64_t n_cols, const int32_t* __restrict__ row,
+                              const int32_t* __restrict__ col, const T* __restrict__ val,
+                              const int32_t* __restrict__ rmap, int32_t* __restrict__ cursor,
+                              int32_t* __restrict__ st_col, T* __restrict__ st_val) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
+    int32_t r = row[k], c = col[k];
+    if (r < 0 || r >= n_rows || c < 0 || c >= n_cols) continue;
+    if (rmap) r = rmap[r];
+    int32_t pos = atomicAdd(&cursor[r], 1);
+    st_col[pos] = c;  // column mapping is applied by the sort
+    st_val[pos] = val[k];
+  }
+}
+
+struct LenFromCounts {
+  const int32_t* counts;
+  __device__ __forceinline__ int64_t operator()(int64_t k) const { return counts[k]; }
+};
+struct LenFromGather {
+  const int32_t* ptr;
+  const int32_t* inv;
+  __device__ __forceinline__ int64_t operator()(int64_t k) const {
+    int32_t o = inv ? inv[k] : (int32_t)k;
+    return (int64_t)ptr[o + 1] - ptr[o];
+  }
+};
+
+__global__ void k_long_row_nnz(int64_t n_rows, const int32_t* __restrict__ ptr, unsigned long long* out) {
+  unsigned long long s = 0;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += stride) {
+    int32_t l = ptr[r + 1] - ptr[r];
+    if (l > SME_SORT_SMEM_MAX) s += (unsigned long long)l;
+  }
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+__global__ void k_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* __restrict__ ptr,
+                               const int32_t* __restrict__ col, int32_t* flag) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int bits = 0;
+  int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid == 0 && (ptr[0] != 0 || ptr[n_rows] != nnz)) bits |= SME_FLAG_ROWPTR;
+  for (int64_t r = tid; r < n_rows; r += stride) {
+    int32_t a = ptr[r], b = ptr[r + 1];
+    if (b < a) {
+      bits |= SME_FLAG_ROWPTR;
+      continue;
+    }
+    if (a < 0 || b > nnz) {
+      bits |= SME_FLAG_ROWPTR;
+      continue;
+    }
+    int32_t prev = -1;
+    for (int32_t k = a; k < b; ++k) {
+      int32_t c = col[k];
+      if (c < 0 || c >= n_cols) bits |= SME_FLAG_RANGE;
+      if (k > a && c <= prev) bits |= SME_FLAG_UNSORTED;
+      prev = c;
+    }
+  }
+  // also catch out-of-range columns outside any row span (corrupt row_ptr handled above)
+  for (int o = 16; o; o >>= 1) bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+  if ((threadIdx.x & 31) == 0 && bits) atomicOr(flag, bits);
+}
+
+__global__ void k_csr_expand_rows(int64_t n_rows, const int32_t* __restrict__ ptr, int32_t* __restrict__ row_out) {
+  // warp per row: rows are short on average, long rows are strided over lanes
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int lane = threadIdx.x & 31;
+  for (int64_t r = warp; r < n_rows; r += nw) {
+    int32_t a = ptr[r], b = ptr[r + 1];
+    for (int32_t k = a + lane; k < b; k += 32) row_out[k] = (int32_t)r;
+  }
+}
+
+template <typename T, class Src>
+int launch_sorts(int64_t n_rows, const int32_t* new_ptr, Src src, const int32_t* src_col, const T* src_val,
+                 const int32_t* cmap, int32_t* out_col, T* out_val, SortLists L, int32_t* flag,
+                 uint64_t* dup_key, cudaStream_t s) {
+  int64_t groups = (n_rows + 31) / 32;
+  int blocks = grid_for(groups * 32, SORT_NT, 8);
+  k_sort_rows_warp<T, Src><<<blocks, SORT_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val, cmap,
+                                                      out_col, out_val, L, flag, (unsigned long long*)dup_key);
+  SME_CHECK_LAUNCH("k_sort_rows_warp");
+  k_sort_rows_block<T, Src><<<sm_count() * 4, SORT_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
+                                                                out_val, L, flag, (unsigned long long*)dup_key);
+  SME_CHECK_LAUNCH("k_sort_rows_block");
+  k_sort_rows_long<T, Src><<<sm_count(), LONG_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
+                                                           out_val, L, flag, (unsigned long long*)dup_key);
+  SME_CHECK_LAUNCH("k_sort_rows_long");
+  return SME_OK;
+}
+
+inline size_t coo_stage_bytes(int64_t n_rows, int64_t nnz) {
+  return align_up(n_rows * 4) + align_up(nnz * 4) + align_up(nnz * 8);
+}
+
+}  // namespace sme
+
+using namespace sme;
+
+#define CHECK_SIZES(n_rows, n_cols, nnz)                                                         \
+  SME_REQUIRE((n_rows) >= 0 && (n_rows) < INT32_MAX && (n_cols) >= 0 && (n_cols) < INT32_MAX,   \
+              "matrix dimensions must be non-negative and < 2^31-1");                            \
+  SME_REQUIRE((nnz) >= 0 && (nnz) < INT32_MAX, "nnz %lld exceeds int32 offsets", (long long)(nnz))
+
+SME_API int sme_row_ptr_workspace_size(int64_t n_rows, size_t* bytes) {
+  SME_REQUIRE(bytes, "null pointer");
+  *bytes = align_up(n_rows * 4) + scan_workspace_bytes(n_rows);
+  return SME_OK;
+}
+
+SME_API int sme_coo_row_ptr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row, const int32_t* col,
+                            const int32_t* row_map, int32_t* row_ptr_out, void* ws, size_t ws_bytes,
+                            int32_t* flag, sme_stream_t stream) {
+  CHECK_SIZES(n_rows, n_cols, nnz);
+  size_t need = align_up(n_rows * 4) + scan_workspace_bytes(n_rows);
+  SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = as_stream(stream);
+  int32_t* counts = (int32_t*)ws;
+  void* scan_ws = (char*)ws + align_up(n_rows * 4);
+  if (n_rows > 0) SME_CUDA(cudaMemsetAsync(counts, 0, n_rows * 4, s));
+  if (nnz > 0) {
+    k_coo_count<<<grid_for(nnz, 256), 256, 0, s>>>(nnz, n_rows, n_cols, row, col, row_map, counts, flag);
+    SME_CHECK_LAUNCH("k_coo_count");
+  }
+  return exclusive_scan_lengths(n_rows, LenFromCounts{counts}, row_ptr_out, scan_ws, flag, s);
+}
+
+SME_API int sme_permute_csr_row_ptr(int64_t n_rows, const int32_t* row_ptr, const int32_t* inv_row,
+                                    int32_t* row_ptr_out, void* ws, size_t ws_bytes, sme_stream_t stream) {
+  SME_REQUIRE(n_rows >= 0 && n_rows < INT32_MAX, "bad n_rows");
+  size_t need = scan_workspace_bytes(n_rows);
+  SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
+  return exclusive_scan_lengths(n_rows, LenFromGather{row_ptr, inv_row}, row_ptr_out, ws, nullptr,
+                                as_stream(stream));
+}
+
+SME_API int sme_long_row_nnz(int64_t n_rows, const int32_t* row_ptr, int64_t* out, sme_stream_t stream) {
+  cudaStream_t s = as_stream(stream);
+  SME_CUDA(cudaMemsetAsync(out, 0, 8, s));
+  if (n_rows == 0) return SME_OK;
+  k_long_row_nnz<<<grid_for(n_rows, 256, 4), 256, 0, s>>>(n_rows, row_ptr, (unsigned long long*)out);
+  SME_CHECK_LAUNCH("k_long_row_nnz");
+  return SME_OK;
+}
+
+SME_API int sme_coo_to_csr_workspace_size(int64_t n_rows, int64_t nnz, int64_t long_nnz, size_t* bytes) {
+  SME_REQUIRE(bytes && n_rows >= 0 && nnz >= 0 && long_nnz >= 0, "bad arguments");
+  *bytes = coo_stage_bytes(n_rows, nnz) + lists_bytes(n_rows, long_nnz);
+  return SME_OK;
+}
+
+SME_API int sme_coo_to_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row,
+                           const int32_t* col, const void* val, const int32_t* row_map, const int32_t* col_map,
+                           const int32_t* row_ptr, int32_t* col_out, void* val_out, void* ws, size_t ws_bytes,
+                           int64_t long_nnz, int32_t* flag, uint64_t* dup_key, sme_stream_t stream) {
+  CHECK_SIZES(n_rows, n_cols, nnz);
+  SME_REQUIRE(dtype == SME_F64 || dtype == SME_F32, "unknown dtype %d", dtype);
+  size_t need = coo_stage_bytes(n_rows, nnz) + lists_bytes(n_rows, long_nnz);
+  SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
+  if (nnz == 0 || n_rows == 0) return SME_OK;
+  cudaStream_t s = as_stream(stream);
+  char* p = (char*)ws;
+  int32_t* cursor = (int32_t*)p;  p += align_up(n_rows * 4);
+  int32_t* st_col = (int32_t*)p;  p += align_up(nnz * 4);
+  void* st_val = p;               p += align_up(nnz * 8);
+  SortLists L = carve_lists(p, n_rows, long_nnz);
+  SME_CUDA(cudaMemsetAsync(L.counters, 0, 64, s));
+  SME_CUDA(cudaMemcpyAsync(cursor, row_ptr, n_rows * 4, cudaMemcpyDeviceToDevice, s));
+  if (dtype == SME_F64) {
+    k_coo_scatter<double><<<grid_for(nnz, 256), 256, 0, s>>>(nnz, n_rows, n_cols, row, col, (const double*)val,
+                                                            row_map, cursor, st_col, (double*)st_val);
+    SME_CHECK_LAUNCH("k_coo_scatter");
+    return launch_sorts<double>(n_rows, row_ptr, SrcStaged{}, st_col, (const double*)st_val, col_map, col_out,
+                                (double*)val_out, L, flag, dup_key, s);
+  } else {
+    k_coo_scatter<float><<<grid_for(nnz, 256), 256, 0, s>>>(nnz, n_rows, n_cols, row, col, (const float*)val,
+                                                           row_map, cursor, st_col, (float*)st_val);
+    SME_CHECK_LAUNCH("k_coo_scatter");
+    return launch_sorts<float>(n_rows, row_ptr, SrcStaged{}, st_col, (const float*)st_val, col_map, col_out,
+                               (float*)val_out, L, flag, dup_key, s);
+  }
+}
+
+SME_API int sme_permute_csr_workspace_size(int64_t n_rows, int64_t nnz, int64_t long_nnz, size_t* bytes) {
+  SME_REQUIRE(bytes && n_rows >= 0 && nnz >= 0 && long_nnz >= 0, "bad arguments");
+  *bytes = lists_bytes(n_rows, long_nnz);
+  return SME_OK;
+}
+
+SME_API int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row_ptr,
+                            const int32_t* col, const void* val, const int32_t* inv_row, const int32_t* col_map,
+                            const int32_t* row_ptr_out, int32_t* col_out, void* val_out, void* ws,
+                            size_t ws_bytes, int64_t long_nnz, int32_t* flag, uint64_t* dup_key,
+                            sme_stream_t stream) {
+  CHECK_SIZES(n_rows, n_cols, nnz);
+  SME_REQUIRE(dtype == SME_F64 || dtype == SME_F32, "unknown dtype %d", dtype);
+  size_t need = lists_bytes(n_rows, long_nnz);
+  SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
+  if (nnz == 0 || n_rows == 0) return SME_OK;
+  cudaStream_t s = as_stream(stream);
+  SortLists L = carve_lists((char*)ws, n_rows, long_nnz);
+  SME_CUDA(cudaMemsetAsync(L.counters, 0, 64, s));
+  SrcGather src{row_ptr, inv_row};
+  if (dtype == SME_F64)
+    return launch_sorts<double>(n_rows, row_ptr_out, src, col, (const double*)val, col_map, col_out,
+                                (double*)val_out, L, flag, dup_key, s);
+  return launch_sorts<float>(n_rows, row_ptr_out, src, col, (const float*)val, col_map, col_out,
+                             (float*)val_out, L, flag, dup_key, s);
+}
+
+SME_API int sme_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row_ptr,
+                             const int32_t* col, int32_t* flag, sme_stream_t stream) {
+  CHECK_SIZES(n_rows, n_cols, nnz);
+  cudaStream_t s = as_stream(stream);
+  k_csr_validate<<<grid_for(n_rows + 1, 256), 256, 0, s>>>(n_rows, n_cols, nnz, row_ptr, col, flag);
+  SME_CHECK_LAUNCH("k_csr_validate");
+  return SME_OK;
+}
+
+SME_API int sme_csr_expand_rows(int64_t n_rows, const int32_t* row_ptr, int32_t* row_out, sme_stream_t stream) {
+  if (n_rows == 0) return SME_OK;
+  cudaStream_t s = as_stream(stream);
+  k_csr_expand_rows<<<grid_for(n_rows * 32, 256), 256, 0, s>>>(n_rows, row_ptr, row_out);
+  SME_CHECK_LAUNCH("k_csr_expand_rows");
+  return SME_OK;
+}

@@ -1,0 +1,284 @@
+// hist.cu — 2-D tile histogram and its Shannon entropy (K5/K6).
+//
+// Reference: histogram_2d / _counts_2d (entropy.py:91-101) = bincount of
+// rbin * bc + cbin with _bin_index (entropy.py:65-67): width = n // bins and
+// the last bin absorbs the remainder; shannon_entropy (entropy.py:104-119).
+//
+// CSR path: the row bin of a nonzero only depends on which [row_ptr[e_b],
+// row_ptr[e_{b+1}]) span holds its position, so the kernel never reads row ids:
+// it streams col_idx once (4 B/nnz, the whole algorithmic traffic), keeps a
+// window of the count grid in shared memory (u32), aggregates equal bins of a
+// warp with __match_any_sync + ballot-popc before the shared atomics, and
+// flushes the touched part of the window with one u64 global atomic per
+// non-zero counter.  Counts are integers, so the result is bit-exact.
+#include "common.cuh"
+
+namespace sme {
+
+constexpr int H_NT = 512;
+constexpr int H_WIN = 16384;       // u32 counters in shared memory (64 KB)
+constexpr int H_EDGE_SMEM = 4096;  // row-bin edges cached in shared memory
+
+// add `cnt` (1..4) to flat bin `bin` (-1 = nothing) with warp aggregation
+__device__ __forceinline__ void warp_agg_add(int64_t bin, int cnt, uint32_t* s_cnt, int64_t win_base,
+                                             int64_t win_len, unsigned long long* g_counts) {
+  const int lane = threadIdx.x & 31;
+  const bool valid = bin >= 0;
+  // invalid lanes get a unique key so they never match anyone
+  long long key = valid ? (long long)bin : -1ll - lane;
+  unsigned mask = __match_any_sync(0xffffffffu, key);
+  unsigned b1 = __ballot_sync(0xffffffffu, cnt >= 1), b2 = __ballot_sync(0xffffffffu, cnt >= 2);
+  unsigned b3 = __ballot_sync(0xffffffffu, cnt >= 3), b4 = __ballot_sync(0xffffffffu, cnt >= 4);
+  if (valid && lane == __ffs(mask) - 1) {
+    unsigned tot = __popc(mask & b1) + __popc(mask & b2) + __popc(mask & b3) + __popc(mask & b4);
+    int64_t off = bin - win_base;
+    if (off >= 0 && off < win_len)
+      atomicAdd(&s_cnt[off], tot);
+    else
+      atomicAdd(&g_counts[bin], (unsigned long long)tot);
+  }
+}
+
+// Fold 4 flat bins (-1 = absent) into up to 4 (bin, count) slots, equal
+// adjacent bins merged; returns the slot count.
+__device__ __forceinline__ int fold4(const int64_t fb[4], int64_t ob[4], int oc[4]) {
+  int n = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (fb[i] < 0) continue;
+    if (n > 0 && ob[n - 1] == fb[i]) {
+      oc[n - 1]++;
+    } else {
+      ob[n] = fb[i];
+      oc[n] = 1;
+      ++n;
+    }
+  }
+  return n;
+}
+
+template <bool SMEM_EDGES>
+__global__ void __launch_bounds__(H_NT) k_hist2d_csr(int64_t n_rows, int64_t nnz, const int32_t* __restrict__ row_ptr,
+                                                     const int32_t* __restrict__ col, int32_t br, int32_t bc,
+                                                     int64_t width_r, Binner cb, unsigned long long* counts,
+                                                     int64_t chunk, bool vec_ok) {
+  extern __shared__ uint32_t smem[];
+  uint32_t* s_cnt = smem;
+  int32_t* s_edge = (int32_t*)(smem + H_WIN);
+  auto edge = [&](int32_t b) -> int32_t {
+    if (SMEM_EDGES) return s_edge[b];
+    return row_ptr[b < br ? (int64_t)b * width_r : n_rows];
+  };
+  if (SMEM_EDGES) {
+    for (int b = threadIdx.x; b <= br; b += H_NT) s_edge[b] = row_ptr[b < br ? (int64_t)b * width_r : n_rows];
+    __syncthreads();
+  }
+  // largest b in [0, br) with edge(b) <= k
+  auto rowbin = [&](int64_t k) -> int32_t {
+    int32_t lo = 0, hi = br - 1;
+    while (lo < hi) {
+      int32_t mid = (lo + hi + 1) >> 1;
+      if (edge(mid) <= k) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  };
+  const int64_t total_grid = (int64_t)br * bc;
+  const uint64_t pol = policy_evict_first();
+  for (int64_t k0 = (int64_t)blockIdx.x * chunk; k0 < nnz; k0 += (int64_t)gridDim.x * chunk) {
+    const int64_t k1 = min(nnz, k0 + chunk);
+    const int32_t b_lo = rowbin(k0), b_hi = rowbin(k1 - 1);
+    const int64_t win_base = (int64_t)b_lo * bc;
+    const int64_t win_len = min((int64_t)H_WIN, min(total_grid, (int64_t)(b_hi + 1) * bc) - win_base);
+    for (int64_t i = threadIdx.x; i < win_len; i += H_NT) s_cnt[i] = 0;
+    __syncthreads();
+    // groups of 4 consecutive positions, k0 is a multiple of 4
+    const int64_t n_groups = (k1 - k0 + 3) >> 2;
+    for (int64_t g0 = 0; g0 < n_groups; g0 += H_NT) {
+      const int64_t g = g0 + threadIdx.x;
+      int64_t fb[4] = {-1, -1, -1, -1};
+      if (g < n_groups) {
+        const int64_t e = k0 + g * 4;
+        int c[4];
+        if (vec_ok && e + 3 < k1) {
+          int4 v = ld_stream_i4(reinterpret_cast<const int4*>(col + e), pol);
+          c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) c[i] = (e + i < k1) ? col[e + i] : -1;
+        }
+        int32_t rb = rowbin(e);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (c[i] < 0) continue;
+          while (rb + 1 < br && edge(rb + 1) <= e + i) ++rb;
+          fb[i] = (int64_t)rb * bc + bin_of(c[i], cb);
+        }
+      }
+      int64_t ob[4];
+      int oc[4] = {0, 0, 0, 0};
+      int ns = fold4(fb, ob, oc);
+      int nmax = ns;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+      for (int sl = 0; sl < nmax; ++sl)
+        warp_agg_add(sl < ns ? ob[sl] : -1, sl < ns ? oc[sl] : 0, s_cnt, win_base, win_len, counts);
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < win_len; i += H_NT)
+      if (s_cnt[i]) atomicAdd(&counts[win_base + i], (unsigned long long)s_cnt[i]);
+    __syncthreads();
+  }
+}
+
+// COO triplets in any order: full grid in shared memory when it fits (window at 0),
+// otherwise the out-of-window bins go to global atomics.
+__global__ void __launch_bounds__(H_NT) k_hist2d_coo(int64_t nnz, const int32_t* __restrict__ row,
+                                                     const int32_t* __restrict__ col, int32_t bc, Binner rb,
+                                                     Binner cb, int64_t total_grid, unsigned long long* counts) {
+  extern __shared__ uint32_t s_cnt[];
+  const int64_t win_len = min((int64_t)H_WIN, total_grid);
+  for (int64_t i = threadIdx.x; i < win_len; i += H_NT) s_cnt[i] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * H_NT;
+  const int64_t n_iter = (nnz + stride - 1) / stride;
+  for (int64_t it = 0; it < n_iter; ++it) {
+    int64_t k = it * stride + (int64_t)blockIdx.x * H_NT + threadIdx.x;
+    int64_t b = -1;
+    if (k < nnz) b = (int64_t)bin_of(row[k], rb) * bc + bin_of(col[k], cb);
+    warp_agg_add(b, b >= 0 ? 1 : 0, s_cnt, 0, win_len, counts);
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < win_len; i += H_NT)
+    if (s_cnt[i]) atomicAdd(&counts[i], (unsigned long long)s_cnt[i]);
+}
+
+__global__ void k_row_hist_csr(int64_t n_rows, const int32_t* __restrict__ row_ptr, int32_t bins, int64_t width,
+                               int64_t* counts) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < bins; b += gridDim.x * blockDim.x) {
+    int64_t lo = (int64_t)b * width, hi = (b + 1 < bins) ? (int64_t)(b + 1) * width : n_rows;
+    counts[b] += (int64_t)row_ptr[hi] - row_ptr[lo];
+  }
+}
+
+// -sum p log p over the bins in a fixed order (thread-strided sums, then a fixed
+// tree): deterministic.  total by exact int64 reduction first.
+__global__ void __launch_bounds__(1024) k_entropy(int64_t n, const int64_t* __restrict__ counts, double base,
+                                                  double* out, int64_t* total_out) {
+  __shared__ long long s_tot[32];
+  __shared__ double s_h[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long t = 0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) t += counts[i];
+  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) s_tot[warp] = t;
+  __syncthreads();
+  if (warp == 0) {
+    long long v = s_tot[lane];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) s_tot[0] = v;
+  }
+  __syncthreads();
+  const long long total = s_tot[0];
+  const bool base2 = (base == 2.0);
+  double h = 0.0;
+  if (total > 0) {
+    const double dt = (double)total;
+    for (int64_t i = threadIdx.x; i < n; i += 1024) {
+      long long c = counts[i];
+      if (c > 0) {
+        double p = (double)c / dt;
+        h += p * (base2 ? log2(p) : log(p));
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if (lane == 0) s_h[warp] = h;
+  __syncthreads();
+  if (warp == 0) {
+    double v = s_h[lane];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) {
+      double r = -v;
+      if (!base2) r = r / log(base);
+      *out = r;
+      if (total_out) *total_out = total;
+    }
+  }
+}
+
+}  // namespace sme
+
+using namespace sme;
+
+static int check_bins(int64_t n, int32_t bins, const char* what) {
+  SME_REQUIRE(bins >= 1, "%s bin count must be >= 1", what);
+  SME_REQUIRE(bins <= n, "%s bin count %d exceeds dimension %lld", what, bins, (long long)n);
+  return SME_OK;
+}
+
+SME_API int sme_hist2d_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row_ptr, const int32_t* col,
+                           int32_t bins_r, int32_t bins_c, int64_t* counts, sme_stream_t stream) {
+  int rc;
+  if ((rc = check_bins(n_rows, bins_r, "row")) != SME_OK) return rc;
+  if ((rc = check_bins(n_cols, bins_c, "column")) != SME_OK) return rc;
+  SME_REQUIRE(nnz >= 0 && nnz < INT32_MAX && n_cols < INT32_MAX, "sizes exceed int32");
+  if (nnz == 0) return SME_OK;
+  cudaStream_t s = as_stream(stream);
+  Binner cb = make_binner(n_cols, bins_c);
+  int64_t width_r = n_rows / bins_r;
+  int blocks_cap = sm_count() * 2;
+  int64_t chunk = (nnz + blocks_cap - 1) / blocks_cap;
+  chunk = ((chunk + 4095) / 4096) * 4096;  // multiple of 4 (aligned int4) and of the tile
+  int blocks = (int)((nnz + chunk - 1) / chunk);
+  size_t smem = H_WIN * 4 + (H_EDGE_SMEM + 1) * 4;
+  const bool vec_ok = ((uintptr_t)col & 15) == 0;
+  if (bins_r <= H_EDGE_SMEM) {
+    SME_CUDA(cudaFuncSetAttribute(k_hist2d_csr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_hist2d_csr<true><<<blocks, H_NT, smem, s>>>(n_rows, nnz, row_ptr, col, bins_r, bins_c, width_r, cb,
+                                                  (unsigned long long*)counts, chunk, vec_ok);
+  } else {
+    SME_CUDA(cudaFuncSetAttribute(k_hist2d_csr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_hist2d_csr<false><<<blocks, H_NT, smem, s>>>(n_rows, nnz, row_ptr, col, bins_r, bins_c, width_r, cb,
+                                                   (unsigned long long*)counts, chunk, vec_ok);
+  }
+  SME_CHECK_LAUNCH("k_hist2d_csr");
+  return SME_OK;
+}
+
+SME_API int sme_hist2d_coo(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row, const int32_t* col,
+                           int32_t bins_r, int32_t bins_c, int64_t* counts, sme_stream_t stream) {
+  int rc;
+  if ((rc = check_bins(n_rows, bins_r, "row")) != SME_OK) return rc;
+  if ((rc = check_bins(n_cols, bins_c, "column")) != SME_OK) return rc;
+  SME_REQUIRE(nnz >= 0 && nnz < INT32_MAX && n_rows < INT32_MAX && n_cols < INT32_MAX, "sizes exceed int32");
+  if (nnz == 0) return SME_OK;
+  cudaStream_t s = as_stream(stream);
+  Binner rb = make_binner(n_rows, bins_r), cb = make_binner(n_cols, bins_c);
+  size_t smem = H_WIN * 4;
+  SME_CUDA(cudaFuncSetAttribute(k_hist2d_coo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int blocks = grid_for(nnz, H_NT, 2);
+  k_hist2d_coo<<<blocks, H_NT, smem, s>>>(nnz, row, col, bins_c, rb, cb, (int64_t)bins_r * bins_c,
+                                          (unsigned long long*)counts);
+  SME_CHECK_LAUNCH("k_hist2d_coo");
+  return SME_OK;
+}
+
+SME_API int sme_row_hist_csr(int64_t n_rows, const int32_t* row_ptr, int32_t bins, int64_t* counts,
+                             sme_stream_t stream) {
+  int rc;
+  if ((rc = check_bins(n_rows, bins, "row")) != SME_OK) return rc;
+  cudaStream_t s = as_stream(stream);
+  k_row_hist_csr<<<(bins + 255) / 256, 256, 0, s>>>(n_rows, row_ptr, bins, n_rows / bins, counts);
+  SME_CHECK_LAUNCH("k_row_hist_csr");
+  return SME_OK;
+}
+
+SME_API int sme_entropy(int64_t n_bins, const int64_t* counts, double base, double* out, int64_t* total,
+                        sme_stream_t stream) {
+  SME_REQUIRE(n_bins >= 1, "histogram has no bins");
+  SME_REQUIRE(base > 1.0, "entropy base must be > 1");
+  cudaStream_t s = as_stream(stream);
+  k_entropy<<<1, 1024, 0, s>>>(n_bins, counts, base, out, total);
+  SME_CHECK_LAUNCH("k_entropy");
+  return SME_OK;
+}

@@ -1,0 +1,136 @@
+// scan.cuh — exclusive prefix sum of per-row lengths into an int32 row_ptr.
+//
+// Reduce-then-scan in three launches (tile sums, one-block scan of tile sums,
+// tile scan + offset).  The lengths come from a functor so the permuted row
+// lengths (a gather through inv_r) never hit memory: bytes = 2 reads + 1 write
+// of n int32 (the functor is evaluated twice).  Used for coo_to_csr's
+// cumsum(bincount) (matio.py:292-293) and the permuted row_ptr.
+#pragma once
+#include "common.cuh"
+
+namespace sme {
+
+constexpr int SCAN_NT = 256;
+constexpr int SCAN_IPT = 16;
+constexpr int SCAN_TILE = SCAN_NT * SCAN_IPT;
+
+inline int64_t scan_tiles(int64_t n) { return (n + SCAN_TILE - 1) / SCAN_TILE; }
+inline size_t scan_workspace_bytes(int64_t n) { return align_up((size_t)(scan_tiles(n) + 1) * 8); }
+
+// block-wide exclusive scan of one int64 per thread; returns the block total via *total
+template <int NT>
+__device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t* total) {
+  __shared__ int64_t s_warp[NT / 32];
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < NT / 32 ? s_warp[lane] : 0;
+    int64_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < NT / 32) s_warp[lane] = wi - w;  // exclusive warp offsets
+    if (lane == NT / 32 - 1) *total = wi;
+  }
+  __syncthreads();
+  int64_t r = s_warp[warp] + incl - v;
+  __syncthreads();
+  return r;
+}
+
+template <class LenFn>
+__global__ void __launch_bounds__(SCAN_NT) k_scan_tile_sums(int64_t n, LenFn len, int64_t* tile_sums) {
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  int64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_IPT; ++i) {
+    int64_t k = base + (int64_t)i * SCAN_NT + threadIdx.x;
+    if (k < n) s += len(k);
+  }
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ int64_t sw[SCAN_NT / 32];
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < SCAN_NT / 32; ++w) t += sw[w];
+    tile_sums[blockIdx.x] = t;
+  }
+}
+
+// one block: exclusive scan of tile sums in place; tile_sums[n_tiles] = grand total
+__global__ void __launch_bounds__(1024) k_scan_tile_offsets(int64_t n_tiles, int64_t* tile_sums) {
+  __shared__ int64_t s_total;
+  int64_t carry = 0;
+  for (int64_t b = 0; b < n_tiles; b += 1024) {
+    int64_t k = b + threadIdx.x;
+    int64_t v = k < n_tiles ? tile_sums[k] : 0;
+    int64_t t;
+    int64_t ex = block_exclusive_scan<1024>(v, &s_total);
+    __syncthreads();
+    t = s_total;
+    if (k < n_tiles) tile_sums[k] = carry + ex;
+    carry += t;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_sums[n_tiles] = carry;
+}
+
+// out[k] = exclusive prefix (k < n); out[n] = total.  Items are thread-strided
+// (coalesced) inside a tile: item i of thread t is k = base + i*NT + t, so the
+// scan order within the tile is item-major — handled by scanning each item
+// column across the block in turn.
+template <class LenFn>
+__global__ void __launch_bounds__(SCAN_NT) k_scan_apply(int64_t n, LenFn len, const int64_t* tile_offsets,
+                                                        int32_t* out, int32_t* flag) {
+  __shared__ int64_t s_total;
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  int64_t run = tile_offsets[blockIdx.x];
+#pragma unroll 1
+  for (int i = 0; i < SCAN_IPT; ++i) {
+    int64_t k = base + (int64_t)i * SCAN_NT + threadIdx.x;
+    int64_t v = k < n ? len(k) : 0;
+    int64_t ex = block_exclusive_scan<SCAN_NT>(v, &s_total);
+    __syncthreads();
+    int64_t pos = run + ex;
+    if (k < n) {
+      if (pos > INT32_MAX && flag) atomicOr(flag, SME_FLAG_RANGE);
+      out[k] = (int32_t)pos;
+    }
+    run += s_total;
+    __syncthreads();
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    if (run > INT32_MAX && flag) atomicOr(flag, SME_FLAG_RANGE);
+    out[n] = (int32_t)run;
+  }
+}
+
+// Launch the three phases.  ws must hold scan_workspace_bytes(n).
+template <class LenFn>
+int exclusive_scan_lengths(int64_t n, LenFn len, int32_t* out, void* ws, int32_t* flag, cudaStream_t s) {
+  if (n == 0) {
+    SME_CUDA(cudaMemsetAsync(out, 0, sizeof(int32_t), s));
+    return SME_OK;
+  }
+  int64_t tiles = scan_tiles(n);
+  int64_t* sums = reinterpret_cast<int64_t*>(ws);
+  k_scan_tile_sums<<<(unsigned)tiles, SCAN_NT, 0, s>>>(n, len, sums);
+  SME_CHECK_LAUNCH("k_scan_tile_sums");
+  k_scan_tile_offsets<<<1, 1024, 0, s>>>(tiles, sums);
+  SME_CHECK_LAUNCH("k_scan_tile_offsets");
+  k_scan_apply<<<(unsigned)tiles, SCAN_NT, 0, s>>>(n, len, sums, out, flag);
+  SME_CHECK_LAUNCH("k_scan_apply");
+  return SME_OK;
+}
+
+}  // namespace sme

@@ -1,0 +1,214 @@
+"""SpMV on the GPU: CSR (CSR-vector and merge-path), row-partitioned CSR, COO.
+
+Drop-in for `spmv_entropy.kernels` (reference
+/root/reference/pkg/src/spmv_entropy/kernels.py).  All kernels are pure and
+deterministic (the COO kernel excepted: floating-point atomics).
+
+Input/output convention: a host array x gives a host numpy float64 y (H2D of
+x, kernel, D2H of y — the reference-facing call); a CUDA tensor x gives a CUDA
+tensor y of the matrix's dtype with nothing crossing PCIe (the resident path
+used by repeated SpMV).
+
+Kernels (spmv.cu):
+  "vector"  CSR-vector, `lanes` threads per row (default: next power of two of
+            the mean row length, at most 32).  Row-partition invariant, so
+            spmv_csr_parallel is bitwise equal to spmv_csr, as in the reference.
+  "merge"   merge-path tiles balanced over rows + nonzeros; the load-balanced
+            kernel for ragged / power-law rows.  Per-matrix plan cached.
+  "exact"   numpy add.reduceat association restated on the GPU (f64): bitwise
+            equal to the reference spmv_csr; a parity tool, not a fast path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _cuda, _lib
+from ._cuda import ptr, stream
+from .matio import CooMatrix, CsrMatrix
+
+KERNELS = ("vector", "merge", "exact")
+
+
+@dataclass(frozen=True, eq=False)
+class RowPartition:
+    """Even split of [0, n_rows) into `workers` contiguous ranges (kernels.py:20-35)."""
+
+    boundaries: np.ndarray
+    workers: int
+
+    def __post_init__(self):
+        b = np.asarray(self.boundaries, dtype=np.int64)
+        object.__setattr__(self, "boundaries", b)
+        if b.size != self.workers + 1 or b[0] != 0 or np.any(np.diff(b) < 0):
+            raise ValueError("boundaries must be a non-decreasing array of workers + 1 offsets starting at 0")
+
+
+def make_row_partition(n_rows: int, workers: int) -> RowPartition:
+    """Split rows evenly: the first n_rows % workers parts get one extra row (kernels.py:38-49)."""
+    if workers < 1:
+        raise ValueError("worker count must be >= 1")
+    if workers > n_rows:
+        raise ValueError(f"worker count {workers} exceeds row count {n_rows}")
+    base, extra = divmod(n_rows, workers)
+    sizes = np.full(workers, base, dtype=np.int64)
+    sizes[:extra] += 1
+    boundaries = np.zeros(workers + 1, dtype=np.int64)
+    np.cumsum(sizes, out=boundaries[1:])
+    return RowPartition(boundaries, workers)
+
+
+def default_lanes(m: CsrMatrix) -> int:
+    """Threads per row of the CSR-vector kernel: next power of two >= mean row length, <= 32."""
+    if "lanes" not in m._cache:
+        mean = m.nnz / max(1, m.n_rows)
+        lanes = 1
+        while lanes < 32 and lanes < mean:
+            lanes <<= 1
+        m._cache["lanes"] = lanes
+    return m._cache["lanes"]
+
+
+class MergePlan:
+    """Per-matrix state of the merge-path kernel: tile split points + carry scratch."""
+
+    def __init__(self, m: CsrMatrix):
+        self.n_tiles = _lib.query_i64("sme_spmv_merge_tiles", m.n_rows, m.nnz)
+        dev = m.d_row_ptr.device
+        self.plan = torch.empty(2 * (self.n_tiles + 1), dtype=torch.int32, device=dev)
+        _lib.call("sme_spmv_merge_plan", m.n_rows, m.nnz, ptr(m.d_row_ptr), ptr(self.plan), stream())
+        self.carry = _cuda.workspace(
+            _lib.query_size("sme_spmv_merge_carry_bytes", _cuda.sme_dtype(m.d_values), self.n_tiles)
+        )
+
+
+def merge_plan(m: CsrMatrix) -> MergePlan:
+    if "merge" not in m._cache:
+        m._cache["merge"] = MergePlan(m)
+    return m._cache["merge"]
+
+
+def _x_device(x, n: int, dtype: torch.dtype, dev) -> tuple[torch.Tensor, str]:
+    """x on the device plus the caller's mode: 'device' (CUDA tensor in/out), 'host'
+    (CPU torch tensor in/out; async copies when pinned), 'numpy' (numpy in/out)."""
+    if isinstance(x, torch.Tensor):
+        if x.dim() != 1 or x.numel() != n:
+            raise ValueError(f"input vector length {tuple(x.shape)} does not match n_cols {n}")
+        if x.is_cuda:
+            return x.to(dtype).contiguous(), "device"
+        return x.to(dev, dtype, non_blocking=x.is_pinned()), "host"
+    xa = np.asarray(x, dtype=np.float64)
+    if xa.shape != (n,):
+        raise ValueError(f"input vector length {xa.shape} does not match n_cols {n}")
+    return torch.from_numpy(np.ascontiguousarray(xa)).to(dev, dtype), "numpy"
+
+
+def _y_out(y: torch.Tensor, mode: str):
+    if mode == "device":
+        return y
+    if mode == "host":
+        yh = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
+        yh.copy_(y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return yh
+    return y.to("cpu").numpy().astype(np.float64, copy=False)
+
+
+def spmv_into(m: CsrMatrix, xd: torch.Tensor, y: torch.Tensor, kernel: str = "vector", *, lanes: int | None = None,
+              accumulate: bool = False) -> None:
+    """Launch y (+)= A x on device tensors (no checks beyond the C-ABI's; stream-ordered)."""
+    dt = _cuda.sme_dtype(m.d_values)
+    if kernel == "vector":
+        _lib.call("sme_spmv_vector", dt, lanes or default_lanes(m), m.n_rows, m.n_cols, ptr(m.d_row_ptr),
+                  ptr(m.d_col_idx), ptr(m.d_values), ptr(xd), ptr(y), int(accumulate), stream())
+    elif kernel == "merge":
+        pl = merge_plan(m)
+        _lib.call("sme_spmv_merge", dt, m.n_rows, m.n_cols, m.nnz, ptr(m.d_row_ptr), ptr(m.d_col_idx),
+                  ptr(m.d_values), ptr(xd), ptr(y), ptr(pl.plan), pl.n_tiles, ptr(pl.carry), int(accumulate),
+                  stream())
+    elif kernel == "exact":
+        if m.d_values.dtype != torch.float64 or accumulate:
+            raise ValueError("the exact (reduceat-order) kernel is f64, non-accumulating")
+        _lib.call("sme_spmv_reduceat_exact", m.n_rows, ptr(m.d_row_ptr), ptr(m.d_col_idx), ptr(m.d_values),
+                  ptr(xd), ptr(y), stream())
+    else:
+        raise ValueError(f"unknown kernel {kernel!r}; expected one of {KERNELS}")
+
+
+def spmv_csr(m: CsrMatrix, x, kernel: str = "vector", *, out: torch.Tensor | None = None):
+    """y[i] = sum over row i of values[k] * x[col_idx[k]] (kernels.py:73-78)."""
+    if not isinstance(m, CsrMatrix):
+        raise TypeError("spmv_csr expects a CsrMatrix of this package (see matio.from_reference)")
+    dev = m.d_row_ptr.device
+    xd, mode = _x_device(x, m.n_cols, m.dtype, dev)
+    y = out if out is not None else torch.empty(m.n_rows, dtype=m.dtype, device=dev)
+    spmv_into(m, xd, y, kernel)
+    return _y_out(y, mode)
+
+
+def spmv_csr_parallel(m: CsrMatrix, x, workers: int, reuse_pool: bool = True, kernel: str = "vector"):
+    """Row-partitioned CSR SpMV (kernels.py:102-128): each of `workers` even row
+    ranges (make_row_partition) is one CSR-vector launch over its rows; every
+    launch writes a disjoint y slice, so the result is bitwise equal to
+    spmv_csr(m, x) for every worker count.  `reuse_pool` is accepted for
+    signature compatibility (there is no thread pool).  Multi-GPU sharding of
+    the same partition is rowshard.RowShardedSpMV."""
+    del reuse_pool
+    if not isinstance(m, CsrMatrix):
+        raise TypeError("spmv_csr_parallel expects a CsrMatrix of this package")
+    dev = m.d_row_ptr.device
+    xd, mode = _x_device(x, m.n_cols, m.dtype, dev)
+    part = make_row_partition(m.n_rows, workers)
+    y = torch.empty(m.n_rows, dtype=m.dtype, device=dev)
+    if kernel != "vector":
+        raise ValueError("spmv_csr_parallel shards the partition-invariant CSR-vector kernel")
+    lanes = default_lanes(m)
+    dt = _cuda.sme_dtype(m.d_values)
+    es = m.d_row_ptr.element_size()
+    ys = y.element_size()
+    for lo, hi in zip(part.boundaries[:-1], part.boundaries[1:]):
+        lo, hi = int(lo), int(hi)
+        if hi == lo:
+            continue
+        _lib.call("sme_spmv_vector", dt, lanes, hi - lo, m.n_cols, ptr(m.d_row_ptr) + lo * es, ptr(m.d_col_idx),
+                  ptr(m.d_values), ptr(xd), ptr(y) + lo * ys, 0, stream())
+    return _y_out(y, mode)
+
+
+def spmv_coo(m: CooMatrix, x):
+    """y = 0; y[row_idx[k]] += values[k] * x[col_idx[k]] (kernels.py:81-86), with device atomics."""
+    if not isinstance(m, CooMatrix):
+        raise TypeError("spmv_coo expects a CooMatrix of this package")
+    dev = m.d_row_idx.device
+    xd, mode = _x_device(x, m.n_cols, m.dtype, dev)
+    y = torch.empty(m.n_rows, dtype=m.dtype, device=dev)
+    _lib.call("sme_spmv_coo", _cuda.sme_dtype(m.d_values), m.n_rows, m.nnz, ptr(m.d_row_idx), ptr(m.d_col_idx),
+              ptr(m.d_values), ptr(xd), ptr(y), stream())
+    return _y_out(y, mode)
+
+
+def relative_error(got, expected) -> float:
+    """max|got - expected| / max|expected| (absolute if expected is all zero) (kernels.py:131-142).
+
+    Computed by one device reduction (sme_maxabs_diff); NaN propagates."""
+    dev = _cuda.require_cuda()
+
+    def dev_f64(a) -> torch.Tensor:
+        if isinstance(a, torch.Tensor):
+            return a.to(dev, torch.float64).contiguous().reshape(-1) if a.dim() else a.to(dev, torch.float64).reshape(1)
+        return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64))).to(dev).reshape(-1)
+
+    g_shape = tuple(got.shape) if hasattr(got, "shape") else np.shape(got)
+    e_shape = tuple(expected.shape) if hasattr(expected, "shape") else np.shape(expected)
+    if tuple(g_shape) != tuple(e_shape):
+        raise ValueError("shape mismatch")
+    g, e = dev_f64(got), dev_f64(expected)
+    if g.numel() == 0:
+        return 0.0
+    out = torch.zeros(2, dtype=torch.float64, device=dev)
+    _lib.call("sme_maxabs_diff", _lib.SME_F64, g.numel(), ptr(g), ptr(e), ptr(out), stream())
+    diff, scale = (float(v) for v in out.cpu())
+    return diff / scale if scale > 0 else diff

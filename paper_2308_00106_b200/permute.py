@@ -1,0 +1,364 @@
+"""Row/column permutations: generation on the host, application on the GPU.
+
+Drop-in for `spmv_entropy.permute` (reference
+/root/reference/pkg/src/spmv_entropy/permute.py).  Permutation GENERATION
+(random_permutation, the riffle strategies, build_strategy) stays on the host
+with numpy's PCG64, exactly as in the reference, so permutation vectors are
+bit-identical by construction (SURVEY.md §7 design principles).  Everything
+that APPLIES a permutation — the bijection check / inverse, compose,
+permute_vector, permute_rows/cols/matrix and the fused permuted-CSR build —
+is an sm_100a kernel (perm.cu, csr_build.cu).
+"""
+
+from __future__ import annotations
+
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _cuda, _lib
+from ._cuda import DeviceFlags, ptr, stream
+from .matio import CooMatrix, CsrMatrix
+
+
+class Permutation:
+    """A bijection on [0, n): forward[i] is the new position of index i (permute.py:23-50).
+
+    The bijection check runs on the GPU (sme_perm_inverse) and leaves the
+    inverse behind, cached for inverse() and for the row-gather of permute_csr.
+    """
+
+    def __init__(self, forward, *, _trusted: bool = False, _host: np.ndarray | None = None):
+        if isinstance(forward, torch.Tensor):
+            if forward.dim() != 1 or forward.numel() == 0:
+                raise ValueError("forward must be a non-empty 1-D array")
+            self.d_forward = _cuda.as_index_tensor(forward, "forward")
+            self._fwd_host = _host
+        else:
+            fwd = np.asarray(forward, dtype=np.int64)
+            if fwd.ndim != 1 or fwd.size == 0:
+                raise ValueError("forward must be a non-empty 1-D array")
+            if fwd.min() < 0 or fwd.max() >= fwd.size:
+                raise ValueError("forward is not a bijection on [0, n)")
+            self.d_forward = _cuda.as_index_tensor(fwd, "forward")
+            self._fwd_host = fwd
+        self._d_inverse: torch.Tensor | None = None
+        if not _trusted:
+            self._compute_inverse(check=True)
+
+    def _compute_inverse(self, check: bool) -> torch.Tensor:
+        inv = torch.empty_like(self.d_forward)
+        fl = DeviceFlags()
+        _lib.call("sme_perm_inverse", self.n, ptr(self.d_forward), ptr(inv), fl.flag_ptr, stream())
+        if check:
+            bits, _ = fl.read()
+            if bits & (_lib.FLAG_RANGE | _lib.FLAG_NOT_BIJECTION):
+                raise ValueError("forward is not a bijection on [0, n)")
+        self._d_inverse = inv
+        return inv
+
+    @property
+    def d_inverse(self) -> torch.Tensor:
+        return self._d_inverse if self._d_inverse is not None else self._compute_inverse(check=False)
+
+    @property
+    def n(self) -> int:
+        return int(self.d_forward.numel())
+
+    @property
+    def forward(self) -> np.ndarray:
+        if self._fwd_host is None:
+            self._fwd_host = _cuda.to_host(self.d_forward, np.int64)
+            self._fwd_host.flags.writeable = False
+        return self._fwd_host
+
+    def inverse(self) -> "Permutation":
+        q = Permutation(self.d_inverse, _trusted=True)
+        q._d_inverse = self.d_forward
+        return q
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, Permutation):
+            return NotImplemented
+        return self.n == other.n and torch.equal(self.d_forward, other.d_forward)
+
+    __hash__ = object.__hash__
+
+    def __repr__(self) -> str:
+        return f"Permutation(n={self.n})"
+
+
+def _as_perm(p) -> Permutation:
+    if isinstance(p, Permutation):
+        return p
+    fwd = getattr(p, "forward", None)  # a reference spmv_entropy.Permutation
+    if fwd is not None:
+        return Permutation(fwd)
+    return Permutation(p)
+
+
+def identity_permutation(n: int) -> Permutation:
+    if n < 1:
+        raise ValueError("permutation size must be >= 1")
+    dev = _cuda.require_cuda()
+    return Permutation(torch.arange(n, dtype=torch.int32, device=dev), _trusted=True)
+
+
+def inverse(p: Permutation) -> Permutation:
+    """The permutation q with p.forward[q.forward[i]] = i for all i (permute.py:53-55)."""
+    return _as_perm(p).inverse()
+
+
+def compose(after: Permutation, first: Permutation) -> Permutation:
+    """Permutation equivalent to applying `first`, then `after` (permute.py:64-68)."""
+    after, first = _as_perm(after), _as_perm(first)
+    if after.n != first.n:
+        raise ValueError("size mismatch")
+    out = torch.empty_like(first.d_forward)
+    _lib.call("sme_gather", _lib.SME_I32, first.n, ptr(first.d_forward), ptr(after.d_forward), ptr(out), stream())
+    return Permutation(out, _trusted=True)
+
+
+def random_permutation_forward(n: int, seed: int) -> np.ndarray:
+    """Host generation, identical to the reference (permute.py:71-81): numpy PCG64 shuffle."""
+    if n < 1:
+        raise ValueError("permutation size must be >= 1")
+    if seed < 0:
+        raise ValueError("seed must be non-negative")
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.permutation(n).astype(np.int64)
+
+
+def random_permutation(n: int, seed: int) -> Permutation:
+    """Uniform permutation from a seeded PCG64 generator (Fisher-Yates), bit-identical to the reference."""
+    fwd = random_permutation_forward(n, seed)
+    # a shuffle of arange is a bijection by construction
+    dev = _cuda.require_cuda()
+    return Permutation(torch.from_numpy(fwd.astype(np.int32)).to(dev), _trusted=True, _host=fwd)
+
+
+# ---------------------------------------------------------------------------
+# application on the GPU
+# ---------------------------------------------------------------------------
+def permute_rows(m: CooMatrix, p: Permutation) -> CooMatrix:
+    """Move entry (i, j, v) to (p.forward[i], j, v) (permute.py:84-88)."""
+    p = _as_perm(p)
+    if p.n != m.n_rows:
+        raise ValueError("permutation size must equal n_rows")
+    return _permute_coo(m, p, None)
+
+
+def permute_cols(m: CooMatrix, p: Permutation) -> CooMatrix:
+    """Move entry (i, j, v) to (i, p.forward[j], v) (permute.py:91-95)."""
+    p = _as_perm(p)
+    if p.n != m.n_cols:
+        raise ValueError("permutation size must equal n_cols")
+    return _permute_coo(m, None, p)
+
+
+def permute_matrix(m: CooMatrix, p_r: Permutation, p_c: Permutation) -> CooMatrix:
+    """Apply a (row, column) permutation pair in one pass (permute.py:98-102).
+
+    Returns the COO in the ORIGINAL entry order with remapped indices (one
+    remap kernel).  Its CSR (coo_to_csr) is then produced by the fused
+    row-gather + segmented-sort kernel from the source's CSR, never by a
+    global sort.
+    """
+    p_r, p_c = _as_perm(p_r), _as_perm(p_c)
+    if p_r.n != m.n_rows or p_c.n != m.n_cols:
+        raise ValueError("permutation sizes must match matrix dimensions")
+    return _permute_coo(m, p_r, p_c)
+
+
+def _permute_coo(m: CooMatrix, p_r: Permutation | None, p_c: Permutation | None) -> CooMatrix:
+    if not isinstance(m, CooMatrix):
+        raise TypeError("expected a CooMatrix (use permute_csr for CsrMatrix)")
+    dev = m.d_row_idx.device
+    row = torch.empty_like(m.d_row_idx) if p_r is not None else m.d_row_idx.clone()
+    col = torch.empty_like(m.d_col_idx) if p_c is not None else m.d_col_idx.clone()
+    _lib.call("sme_coo_remap", m.nnz, ptr(m.d_row_idx), ptr(m.d_col_idx),
+              ptr(p_r.d_forward if p_r is not None else None), ptr(p_c.d_forward if p_c is not None else None),
+              ptr(row) if p_r is not None else None, ptr(col) if p_c is not None else None, stream())
+    src = m
+
+    def thunk() -> CsrMatrix:
+        from .matio import coo_to_csr
+
+        return permute_csr(coo_to_csr(src), p_r, p_c)
+
+    del dev
+    return CooMatrix._from_device(m.n_rows, m.n_cols, row, col, m.d_values.clone(), csr_thunk=thunk)
+
+
+def permute_csr(m: CsrMatrix, p_r: Permutation | None, p_c: Permutation | None) -> CsrMatrix:
+    """P_r A P_c directly on CSR (K4): row gather through inverse(p_r), column remap
+    through p_c, segmented sort inside each row.  Bit-identical to
+    coo_to_csr(permute_matrix(csr_to_coo(m), p_r, p_c))."""
+    if p_r is not None:
+        p_r = _as_perm(p_r)
+        if p_r.n != m.n_rows:
+            raise ValueError("permutation sizes must match matrix dimensions")
+    if p_c is not None:
+        p_c = _as_perm(p_c)
+        if p_c.n != m.n_cols:
+            raise ValueError("permutation sizes must match matrix dimensions")
+    dev = m.d_row_ptr.device
+    inv_r = p_r.d_inverse if p_r is not None else None
+    row_ptr = torch.empty(m.n_rows + 1, dtype=torch.int32, device=dev)
+    ws1 = _cuda.workspace(_lib.query_size("sme_row_ptr_workspace_size", m.n_rows))
+    _lib.call("sme_permute_csr_row_ptr", m.n_rows, ptr(m.d_row_ptr), ptr(inv_r), ptr(row_ptr), ptr(ws1),
+              ws1.numel(), stream())
+    long_nnz = m.long_row_nnz()
+    ws2 = _cuda.workspace(_lib.query_size("sme_permute_csr_workspace_size", m.n_rows, m.nnz, long_nnz))
+    col = torch.empty_like(m.d_col_idx)
+    val = torch.empty_like(m.d_values)
+    fl = DeviceFlags()
+    _lib.call("sme_permute_csr", _cuda.sme_dtype(m.d_values), m.n_rows, m.n_cols, m.nnz, ptr(m.d_row_ptr),
+              ptr(m.d_col_idx), ptr(m.d_values), ptr(inv_r), ptr(p_c.d_forward if p_c is not None else None),
+              ptr(row_ptr), ptr(col), ptr(val), ptr(ws2), ws2.numel(), long_nnz, fl.flag_ptr, fl.dup_ptr,
+              stream())
+    out = CsrMatrix._from_device(m.n_rows, m.n_cols, row_ptr, col, val)
+    out._cache["long_nnz"] = long_nnz
+    return out
+
+
+def permute_vector(x, p: Permutation):
+    """Return `out` with out[p.forward[i]] = x[i] (permute.py:105-112).
+
+    Host array in -> host numpy float64 out (one H2D, one scatter kernel, one
+    D2H); CUDA tensor in -> CUDA tensor out (device-resident, f64 or f32)."""
+    p = _as_perm(p)
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        if x.dim() != 1 or x.numel() != p.n:
+            raise ValueError("vector length must equal permutation size")
+        xs = x.contiguous()
+        if xs.dtype not in (torch.float64, torch.float32):
+            xs = xs.to(torch.float64)
+        out = torch.empty_like(xs)
+        _lib.call("sme_permute_vector", _cuda.sme_dtype(xs), p.n, ptr(p.d_forward), ptr(xs), ptr(out), stream())
+        return out
+    xa = np.asarray(x, dtype=np.float64)
+    if xa.shape != (p.n,):
+        raise ValueError("vector length must equal permutation size")
+    xd = torch.from_numpy(np.ascontiguousarray(xa)).to(p.d_forward.device)
+    out = torch.empty_like(xd)
+    _lib.call("sme_permute_vector", _lib.SME_F64, p.n, ptr(p.d_forward), ptr(xd), ptr(out), stream())
+    return out.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# strategies (host-side generation, as in the reference; permute.py:115-250)
+# ---------------------------------------------------------------------------
+def gradient_pivot(h) -> int:
+    """Index of the steepest histogram increase (permute.py:115-126)."""
+    counts = np.asarray(h.counts)
+    if counts.ndim != 1:
+        raise ValueError("gradient pivot requires a 1-D histogram")
+    if counts.size < 2:
+        raise ValueError("gradient pivot requires at least 2 bins")
+    grad = counts[1:] - counts[:-1]
+    return int(np.asarray(h.edges[0])[int(np.argmax(grad)) + 1])
+
+
+def _interleave_forward(n: int, pivot: int) -> np.ndarray:
+    a, b = pivot, n - pivot
+    short = min(a, b)
+    fwd = np.empty(n, dtype=np.int64)
+    ka = np.arange(a, dtype=np.int64)
+    kb = np.arange(b, dtype=np.int64)
+    fwd[:a] = np.where(ka < short, 2 * ka, ka + b)
+    fwd[a:] = np.where(kb < short, 2 * kb + 1, kb + a)
+    return fwd
+
+
+def riffle_shuffle_permutation(n: int, pivot: int, seed: int) -> Permutation:
+    """Riffle [0, pivot) and [pivot, n) (permute.py:142-157): local PCG64 shuffles, then interleave."""
+    if not 0 < pivot < n:
+        raise ValueError(f"pivot {pivot} out of range (0, {n})")
+    if seed < 0:
+        raise ValueError("seed must be non-negative")
+    rng = np.random.Generator(np.random.PCG64(seed))
+    local = np.empty(n, dtype=np.int64)
+    local[:pivot] = rng.permutation(pivot)
+    local[pivot:] = pivot + rng.permutation(n - pivot)
+    return compose(Permutation(_interleave_forward(n, pivot)), Permutation(local))
+
+
+class StrategyKind(Enum):
+    """The identity baseline plus the four randomization formats (permute.py:160-201)."""
+
+    REGULAR = "regular"
+    ROW_PERMUTE = "row_permute"
+    ROW_COLUMN_PERMUTE = "row_column_permute"
+    ROW_GRADIENT = "row_gradient"
+    COLUMN_GRADIENT = "column_gradient"
+
+    @property
+    def code(self) -> str:
+        return _CODES[self]
+
+    @property
+    def label(self) -> str:
+        return _LABELS[self]
+
+
+_CODES = {
+    StrategyKind.REGULAR: "reg",
+    StrategyKind.ROW_PERMUTE: "r",
+    StrategyKind.ROW_COLUMN_PERMUTE: "rc",
+    StrategyKind.ROW_GRADIENT: "gr",
+    StrategyKind.COLUMN_GRADIENT: "gc",
+}
+_LABELS = {
+    StrategyKind.REGULAR: "Regular",
+    StrategyKind.ROW_PERMUTE: "Row-Permute",
+    StrategyKind.ROW_GRADIENT: "Row-Gradient",
+    StrategyKind.COLUMN_GRADIENT: "Column-Gradient",
+    StrategyKind.ROW_COLUMN_PERMUTE: "Row-Column-Permute",
+}
+TABLE_ORDER = (
+    StrategyKind.REGULAR,
+    StrategyKind.ROW_PERMUTE,
+    StrategyKind.ROW_GRADIENT,
+    StrategyKind.COLUMN_GRADIENT,
+    StrategyKind.ROW_COLUMN_PERMUTE,
+)
+_ROW_STREAM, _COL_STREAM = 0, 1
+
+
+def axis_seed(seed: int, axis: int) -> int:
+    """permute.py:206-207: SeedSequence(seed, spawn_key=(axis,)) -> one uint64."""
+    return int(np.random.SeedSequence(seed, spawn_key=(axis,)).generate_state(1, np.uint64)[0])
+
+
+def build_strategy(m, kind: StrategyKind, seed: int, bins: int = 512, column_gradient_both_axes: bool = True):
+    """(row, column) permutation pair for a strategy (permute.py:210-250).
+
+    `m` is a CooMatrix or CsrMatrix of this package; the gradient strategies
+    take their 1-D histograms from the GPU histogram kernels.
+    """
+    from .entropy import col_histogram, row_histogram
+
+    if seed < 0:
+        raise ValueError("seed must be non-negative")
+    row_seed = axis_seed(seed, _ROW_STREAM)
+    col_seed = axis_seed(seed, _COL_STREAM)
+    if kind is StrategyKind.REGULAR:
+        return identity_permutation(m.n_rows), identity_permutation(m.n_cols)
+    if kind is StrategyKind.ROW_PERMUTE:
+        return random_permutation(m.n_rows, row_seed), identity_permutation(m.n_cols)
+    if kind is StrategyKind.ROW_COLUMN_PERMUTE:
+        return random_permutation(m.n_rows, row_seed), random_permutation(m.n_cols, col_seed)
+
+    def riffled(n: int, histogram, axis_seed_: int) -> Permutation:
+        return riffle_shuffle_permutation(n, gradient_pivot(histogram), axis_seed_)
+
+    if kind is StrategyKind.ROW_GRADIENT:
+        return riffled(m.n_rows, row_histogram(m, min(bins, m.n_rows)), row_seed), identity_permutation(m.n_cols)
+    if kind is StrategyKind.COLUMN_GRADIENT:
+        p_c = riffled(m.n_cols, col_histogram(m, min(bins, m.n_cols)), col_seed)
+        if not column_gradient_both_axes:
+            return identity_permutation(m.n_rows), p_c
+        return riffled(m.n_rows, row_histogram(m, min(bins, m.n_rows)), row_seed), p_c
+    raise ValueError(f"unknown strategy {kind!r}")

@@ -1,0 +1,129 @@
+"""Row-sharded multi-GPU SpMV with an x all-gather between iterations (K8).
+
+The reference's only parallelism is the even row split of spmv_csr_parallel
+(kernels.py:38-49, 102-128): disjoint output row ranges, no reduction.  Here
+each rank (one process per GPU, torch.distributed over NCCL) owns the rows
+[r_k, r_{k+1}) of make_row_partition(n_rows, world) and the same-index slice
+of x (square matrices).  One step is
+
+    all_gather(x slices -> padded full x)   (NCCL over NVLink / NVSwitch)
+    y_k = A_k x                              (libsme CSR kernel on the shard)
+
+Slices are padded to pad = ceil(n / world) entries so the gather is one
+equal-chunk all_gather_into_tensor; the shard's column ids are remapped once
+(sme_rowshard_remap_cols) from matrix columns to slots of the padded vector.
+With the CSR-vector kernel and the parent matrix's lanes the sharded y is
+bitwise equal to the 1-GPU y (no row's reduction order changes).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _cuda, _lib
+from ._cuda import ptr, stream
+from .kernels import default_lanes, make_row_partition, spmv_into
+from .matio import CsrMatrix
+
+
+class ShardPlan:
+    """Host-side partition of rows (and of x) over `world` ranks."""
+
+    def __init__(self, n_rows: int, n_cols: int, world: int):
+        if world < 1:
+            raise ValueError("world size must be >= 1")
+        self.n_rows, self.n_cols, self.world = int(n_rows), int(n_cols), int(world)
+        self.rows = make_row_partition(self.n_rows, self.world).boundaries
+        self.cols = make_row_partition(self.n_cols, self.world).boundaries
+        self.pad = -(-self.n_cols // self.world)
+
+    def row_range(self, rank: int) -> tuple[int, int]:
+        return int(self.rows[rank]), int(self.rows[rank + 1])
+
+    def col_range(self, rank: int) -> tuple[int, int]:
+        return int(self.cols[rank]), int(self.cols[rank + 1])
+
+    def slot_of(self, col: np.ndarray) -> np.ndarray:
+        """Host statement of the column -> padded-slot map (the kernel is the product path)."""
+        col = np.asarray(col, dtype=np.int64)
+        part = np.searchsorted(self.cols, col, side="right") - 1
+        return part * self.pad + (col - self.cols[part])
+
+    def pad_slice(self, x_local: torch.Tensor) -> torch.Tensor:
+        """x slice of this rank padded to `pad` entries (the all-gather chunk)."""
+        out = torch.zeros(self.pad, dtype=x_local.dtype, device=x_local.device)
+        out[: x_local.numel()] = x_local
+        return out
+
+    def unpad(self, x_full_padded: torch.Tensor) -> torch.Tensor:
+        parts = [x_full_padded[k * self.pad : k * self.pad + (self.cols[k + 1] - self.cols[k])] for k in range(self.world)]
+        return torch.cat(parts)
+
+
+def allgather_padded(x_full: torch.Tensor, x_chunk: torch.Tensor, group=None) -> None:
+    """x_full[k*pad:(k+1)*pad] <- rank k's chunk.  NCCL: one all_gather_into_tensor;
+    other backends (gloo, for CPU tests): all_gather into views."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(x_full, x_chunk, group=group)
+    else:
+        world = dist.get_world_size(group)
+        views = list(x_full.view(world, -1).unbind(0))
+        dist.all_gather(views, x_chunk, group=group)
+
+
+class RowShardedSpMV:
+    """One rank's shard of A plus the gathered-x buffer; step() = all-gather + SpMV."""
+
+    def __init__(self, m: CsrMatrix, plan: ShardPlan, rank: int, kernel: str = "vector", lanes: int | None = None):
+        self.plan, self.rank, self.kernel = plan, rank, kernel
+        lo, hi = plan.row_range(rank)
+        self.row_lo, self.row_hi = lo, hi
+        p0, p1 = int(m.d_row_ptr[lo]), int(m.d_row_ptr[hi])
+        dev = m.d_row_ptr.device
+        row_ptr = (m.d_row_ptr[lo : hi + 1] - p0).contiguous()
+        col = torch.empty(p1 - p0, dtype=torch.int32, device=dev)
+        _lib.call("sme_rowshard_remap_cols", p1 - p0, m.n_cols, plan.world, plan.pad, ptr(m.d_col_idx) + 4 * p0,
+                  ptr(col), stream())
+        val = m.d_values[p0:p1].clone()
+        self.local = CsrMatrix._from_device(hi - lo, plan.world * plan.pad, row_ptr, col, val)
+        # the parent's lanes keep every row's reduction order -> bitwise equal to 1 GPU
+        self.lanes = lanes or (default_lanes(m) if kernel == "vector" else None)
+        self.x_full = torch.zeros(plan.world * plan.pad, dtype=m.dtype, device=dev)
+        self.y = torch.empty(hi - lo, dtype=m.dtype, device=dev)
+
+    @property
+    def nnz(self) -> int:
+        return self.local.nnz
+
+    def spmv(self, x_full: torch.Tensor | None = None) -> torch.Tensor:
+        spmv_into(self.local, self.x_full if x_full is None else x_full, self.y, self.kernel, lanes=self.lanes)
+        return self.y
+
+    def step(self, x_chunk: torch.Tensor, group=None) -> torch.Tensor:
+        """All-gather the padded x chunks of every rank, then y_local = A_local x."""
+        allgather_padded(self.x_full, x_chunk, group)
+        return self.spmv()
+
+
+def virtual_ranks(m: CsrMatrix, world: int, kernel: str = "vector") -> list[RowShardedSpMV]:
+    """All `world` shards on the current device (single-GPU test of the multi-GPU path)."""
+    plan = ShardPlan(m.n_rows, m.n_cols, world)
+    return [RowShardedSpMV(m, plan, k, kernel) for k in range(world)]
+
+
+def virtual_step(shards: list[RowShardedSpMV], x: torch.Tensor) -> torch.Tensor:
+    """The all-gather replaced by device copies: every shard sees the same padded x."""
+    plan = shards[0].plan
+    x_full = torch.zeros(plan.world * plan.pad, dtype=x.dtype, device=x.device)
+    for k in range(plan.world):
+        lo, hi = plan.col_range(k)
+        x_full[k * plan.pad : k * plan.pad + hi - lo] = x[lo:hi]
+    return torch.cat([s.spmv(x_full).clone() for s in shards])
+
+
+def require_cuda_rank(local_rank: int) -> torch.device:
+    _cuda.require_cuda()
+    torch.cuda.set_device(local_rank)
+    return torch.device("cuda", local_rank)

@@ -1,0 +1,78 @@
+"""Host-side logic of the package (no GPU): partitions, protocol helpers, strategies."""
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import oracle as O
+from paper_2308_00106_b200 import bench as B
+from paper_2308_00106_b200.kernels import make_row_partition
+from paper_2308_00106_b200.permute import (
+    TABLE_ORDER,
+    StrategyKind,
+    _interleave_forward,
+    axis_seed,
+    random_permutation_forward,
+)
+from paper_2308_00106_b200.rowshard import ShardPlan
+
+
+def test_make_row_partition_examples():  # reference test_kernels.py:92-96
+    assert make_row_partition(10, 2).boundaries.tolist() == [0, 5, 10]
+    assert make_row_partition(10, 3).boundaries.tolist() == [0, 4, 7, 10]
+    assert make_row_partition(5, 5).boundaries.tolist() == [0, 1, 2, 3, 4, 5]
+    with pytest.raises(ValueError):
+        make_row_partition(10, 0)
+    with pytest.raises(ValueError):
+        make_row_partition(3, 4)
+
+
+@given(st.integers(1, 200), st.data())
+@settings(max_examples=60, deadline=None)
+def test_partition_matches_oracle(n_rows, data):
+    w = data.draw(st.integers(1, n_rows))
+    assert np.array_equal(make_row_partition(n_rows, w).boundaries, O.make_row_partition(n_rows, w))
+
+
+def test_protocol_helpers_match_reference_semantics():
+    assert B.gflops(1000, 1e-6) == pytest.approx(2.0)
+    assert B.gflops(0, 1.0) == 0.0
+    with pytest.raises(ValueError):
+        B.gflops(10, 0.0)
+    assert B.choose_iterations(1e-6) == 5000 and B.choose_iterations(1.0) == 1000
+    assert B.derived_seed(0, 3) == O.derived_seed(0, 3)
+    assert np.array_equal(B.input_vector(0, 17), O.input_vector(0, 17))
+    # SURVEY.md §8d byte counts
+    assert B.spmv_bytes(10_000, 10_000, 100_000) == 1_400_004
+    assert B.spmv_bytes(4_000_000, 4_000_000, 19_992_000) == 319_904_004
+    assert B.spmv_bytes(50_000_000, 50_000_000, 1_000_000_000) == 13_000_000_004
+
+
+def test_host_permutation_generation_is_the_references(golden):
+    assert np.array_equal(random_permutation_forward(31, 5), golden["perm/rp_31_5"])
+    assert np.array_equal(random_permutation_forward(1000, 123), golden["perm/rp_1000_123"])
+    assert [axis_seed(7, 0), axis_seed(7, 1)] == [int(v) for v in golden["perm/axis_seed_7"]]
+    with pytest.raises(ValueError):
+        random_permutation_forward(0, 1)
+    with pytest.raises(ValueError):
+        random_permutation_forward(5, -1)
+
+
+def test_strategy_table_and_interleave():
+    assert [k.code for k in TABLE_ORDER] == ["reg", "r", "gr", "gc", "rc"]
+    assert StrategyKind.ROW_COLUMN_PERMUTE.label == "Row-Column-Permute"
+    # permute.py:129-139: alternate the two parts, then the remainder
+    assert _interleave_forward(5, 2).tolist() == [0, 2, 1, 3, 4]
+    assert sorted(_interleave_forward(9, 4).tolist()) == list(range(9))
+
+
+@pytest.mark.parametrize("n,world", [(10, 1), (10, 3), (103, 4), (8, 8), (50_000_000, 8)])
+def test_shard_plan(n, world):
+    plan = ShardPlan(n, n, world)
+    assert plan.rows[0] == 0 and plan.rows[-1] == n
+    assert plan.pad * world >= n and plan.pad - (n // world) <= 1
+    sizes = np.diff(plan.cols)
+    assert sizes.max() <= plan.pad
+    cols = np.unique(np.r_[0, n - 1, plan.cols[:-1], np.minimum(plan.cols[1:], n - 1)])
+    assert np.array_equal(plan.slot_of(cols), O.rowshard_remap_cols(cols, n, world, plan.pad))
