@@ -183,6 +183,26 @@ int sme_spmv_merge(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz,
                    const void* d_x, void* d_y, const int32_t* d_plan, int64_t n_tiles,
                    void* d_carry, int accumulate, sme_stream_t stream);
 
+/* Warp-streaming CSR SpMV (the fast path for regular and moderately ragged rows):
+ * every resident warp of a persistent grid owns a contiguous row range holding
+ * ~nnz/W nonzeros (per-matrix plan, W from sme_spmv_stream_warps), streams it in
+ * 128-element chunks aligned to GLOBAL positions (align_off in [0,128) = global
+ * position of local element 0 mod 128, so row shards reduce exactly like the
+ * whole matrix) and reduces rows with a flag-segmented warp scan.  No fix-up
+ * pass.  plan: (W + 1) int32.  accumulate = 1: y += A x. */
+int sme_spmv_stream_warps(int64_t n_rows, int64_t nnz, int32_t* n_warps);
+int sme_spmv_stream_plan(int64_t n_rows, int64_t nnz, const int32_t* d_row_ptr, int32_t n_warps,
+                         int32_t* d_plan, sme_stream_t stream);
+int sme_spmv_stream(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row_ptr,
+                    const int32_t* d_col, const void* d_val, const void* d_x, void* d_y,
+                    const int32_t* d_plan, int32_t n_warps, int accumulate, int32_t align_off,
+                    sme_stream_t stream);
+
+/* Merge kernel selection (process-wide; tests and experiments): 1 = persistent
+ * TMA-pipelined kernel (needs 16-byte aligned row_ptr/col_idx/values), 0 = one
+ * CTA per tile with plain global loads, -1 = auto (TMA when aligned). */
+int sme_spmv_merge_set_mode(int mode);
+
 /* CSR-vector ("warp-per-row") SpMV: `lanes` in {1,2,4,8,16,32} threads per row,
  * lane-strided partial sums combined by a butterfly shuffle.  The per-row
  * reduction order depends only on `lanes`, so any row partition

@@ -54,6 +54,10 @@ SIGNATURES: dict[str, list] = {
     "sme_spmv_merge_plan": [i64, i64, p, p, p],
     "sme_spmv_merge_carry_bytes": [C.c_int, i64, psz],
     "sme_spmv_merge": [C.c_int, i64, i64, i64, p, p, p, p, p, p, i64, p, C.c_int, p],
+    "sme_spmv_merge_set_mode": [C.c_int],
+    "sme_spmv_stream_warps": [i64, i64, C.POINTER(C.c_int32)],
+    "sme_spmv_stream_plan": [i64, i64, p, i32, p, p],
+    "sme_spmv_stream": [C.c_int, i64, i64, i64, p, p, p, p, p, p, i32, C.c_int, i32, p],
     "sme_spmv_vector": [C.c_int, C.c_int, i64, i64, p, p, p, p, p, C.c_int, p],
     "sme_spmv_reduceat_exact": [i64, p, p, p, p, p, p],
     "sme_spmv_coo": [C.c_int, i64, i64, p, p, p, p, p, p],

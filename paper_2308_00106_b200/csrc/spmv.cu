@@ -22,12 +22,13 @@
 //    analogue of spmv_csr_parallel's bitwise guarantee, kernels.py:1-6).
 #include "common.cuh"
 
+#include <algorithm>
+
 namespace sme {
 
 constexpr int M_NT = 256;
 constexpr int M_IPT = 8;
 constexpr int M_TILE = M_NT * M_IPT;              // merge items (rows + nnz) per tile
-constexpr int M_QG = (M_TILE / 4 + 2 + M_NT - 1) / M_NT;  // 4-element groups per thread
 
 template <typename T> struct V4;
 template <> struct V4<double> {
@@ -44,85 +45,39 @@ template <> struct V4<float> {
   }
 };
 
-template <typename T>
-__global__ void __launch_bounds__(M_NT) k_spmv_merge(int32_t n_rows, int32_t nnz, const int32_t* __restrict__ row_ptr,
-                                                     const int32_t* __restrict__ col, const T* __restrict__ val,
-                                                     const T* __restrict__ x, T* __restrict__ y,
-                                                     const int2* __restrict__ plan, T* __restrict__ carry_val,
-                                                     int32_t* __restrict__ carry_row, int accumulate) {
-  __shared__ T s_prod[M_TILE];
-  __shared__ int32_t s_end[M_TILE];
-  __shared__ int32_t s_wkey[M_NT / 32], s_wfirst[M_NT / 32];
-  __shared__ T s_wval[M_NT / 32];
-  __shared__ int32_t s_pkey[M_NT / 32];
-  __shared__ T s_pval[M_NT / 32];
+// Shared scratch of the per-tile segmented scan.
+template <typename T, int NT>
+struct ScanSmem {
+  int32_t wkey[NT / 32], wfirst[NT / 32], pkey[NT / 32];
+  T wval[NT / 32], pval[NT / 32];
+};
 
+// Phase B of a merge tile: per-thread merge-path walk over IPT items, emitting
+// row sums; partial rows across threads combined by a segmented block scan;
+// the tile's open row goes to the carry arrays (finished by k_spmv_fixup).
+// end_at(i) = row_ptr[r0 + 1 + i] (i < nr), prod_at(j) = product of nnz j0 + j.
+template <typename T, int NT, int IPT, class EndFn, class ProdFn>
+__device__ __forceinline__ void merge_tile_reduce(const int t, const int r0, const int nr, const int j0, const int nj,
+                                                  EndFn end_at, ProdFn prod_at, T* __restrict__ y,
+                                                  const int accumulate, T* __restrict__ carry_val,
+                                                  int32_t* __restrict__ carry_row, ScanSmem<T, NT>& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int t = blockIdx.x;
-  const int2 c0 = plan[t], c1 = plan[t + 1];
-  const int r0 = c0.x, j0 = c0.y;
-  const int nr = c1.x - r0, nj = c1.y - j0;
-  const uint64_t pol_stream = policy_evict_first();
-  const uint64_t pol_keep = policy_evict_last();
-
-  // ---- phase A: row ends + products -------------------------------------
-  for (int i = tid; i < nr; i += M_NT) s_end[i] = ld_stream_i1(row_ptr + r0 + 1 + i, pol_stream);
-
-  const int j1 = j0 + nj;
-  const int gA = j0 >> 2, gB = (j1 + 3) >> 2;
-  int cidx[M_QG][4];
-  T cv[M_QG][4];
-#pragma unroll
-  for (int q = 0; q < M_QG; ++q) {
-    const int g = gA + tid + q * M_NT;
-    const int e = g * 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) { cidx[q][i] = -1; cv[q][i] = T(0); }
-    if (g < gB) {
-      if (e + 3 < nnz) {
-        int4 c = ld_stream_i4(reinterpret_cast<const int4*>(col + e), pol_stream);
-        cidx[q][0] = c.x; cidx[q][1] = c.y; cidx[q][2] = c.z; cidx[q][3] = c.w;
-        V4<T>::load(val + e, pol_stream, cv[q]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (e + i < nnz) { cidx[q][i] = col[e + i]; cv[q][i] = val[e + i]; }
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (e + i < j0 || e + i >= j1) cidx[q][i] = -1;
-    }
-  }
-  T xv[M_QG][4];
-#pragma unroll
-  for (int q = 0; q < M_QG; ++q)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) xv[q][i] = cidx[q][i] >= 0 ? ld_keep(x + cidx[q][i], pol_keep) : T(0);
-#pragma unroll
-  for (int q = 0; q < M_QG; ++q) {
-    const int e = (gA + tid + q * M_NT) * 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (cidx[q][i] >= 0) s_prod[e + i - j0] = cv[q][i] * xv[q][i];
-  }
-  __syncthreads();
-
-  // ---- phase B: per-thread merge path ----------------------------------
   const int total = nr + nj;
-  const int d0 = min(tid * M_IPT, total), d1 = min(d0 + M_IPT, total);
+  const int d0 = min(tid * IPT, total), d1 = min(d0 + IPT, total);
   int lo = max(0, d0 - nj), hi = min(d0, nr);
   while (lo < hi) {
     int mid = (lo + hi) >> 1;
-    if (s_end[mid] <= j0 + d0 - 1 - mid) lo = mid + 1; else hi = mid;
+    if (end_at(mid) <= j0 + d0 - 1 - mid) lo = mid + 1; else hi = mid;
   }
   int i = lo, j = d0 - lo;
   T run = T(0);
   int first_row = -1;
   T first_val = T(0);
+  int next_end = (i < nr) ? end_at(i) : INT32_MAX;
 #pragma unroll
-  for (int s = 0; s < M_IPT; ++s) {
+  for (int s = 0; s < IPT; ++s) {
     if (d0 + s < d1) {
-      if (i < nr && (j >= nj || s_end[i] <= j0 + j)) {
+      if (i < nr && (j >= nj || next_end <= j0 + j)) {
         if (first_row < 0) {
           first_row = i;
           first_val = run;
@@ -132,15 +87,15 @@ __global__ void __launch_bounds__(M_NT) k_spmv_merge(int32_t n_rows, int32_t nnz
         }
         run = T(0);
         ++i;
+        next_end = (i < nr) ? end_at(i) : INT32_MAX;
       } else {
-        run += s_prod[j];
+        run += prod_at(j);
         ++j;
       }
     }
   }
-
-  // ---- segmented inclusive scan of (key = open local row, run) ---------
-  int key = i;
+  // segmented inclusive scan of (key = open local row, run)
+  const int key = i;
   T v = run;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -149,40 +104,188 @@ __global__ void __launch_bounds__(M_NT) k_spmv_merge(int32_t n_rows, int32_t nnz
     if (lane >= o && ok == key) v += ov;
   }
   const int key_lane0 = __shfl_sync(0xffffffffu, key, 0);
-  if (lane == 31) { s_wkey[warp] = key; s_wval[warp] = v; }
-  if (lane == 0) s_wfirst[warp] = key;
+  if (lane == 31) { sm.wkey[warp] = key; sm.wval[warp] = v; }
+  if (lane == 0) sm.wfirst[warp] = key;
   __syncthreads();
   if (tid == 0) {
-    // exclusive prefix over warps: P_w = combine(warp totals 0..w-1)
     int pk = -1;
     T pv = T(0);
-    for (int w = 0; w < M_NT / 32; ++w) {
-      s_pkey[w] = pk;
-      s_pval[w] = pv;
-      const int wk = s_wkey[w];
-      const T wv = s_wval[w];
-      if (pk == wk && s_wfirst[w] == wk) pv = pv + wv; else pv = wv;
+    for (int w = 0; w < NT / 32; ++w) {
+      sm.pkey[w] = pk;
+      sm.pval[w] = pv;
+      const int wk = sm.wkey[w];
+      const T wv = sm.wval[w];
+      pv = (pk == wk && sm.wfirst[w] == wk) ? pv + wv : wv;
       pk = wk;
     }
   }
   __syncthreads();
-  const int pk = s_pkey[warp];
-  const T pv = s_pval[warp];
+  const int pk = sm.pkey[warp];
+  const T pv = sm.pval[warp];
   if (warp > 0 && pk == key && key_lane0 == key) v = pv + v;  // block-inclusive
-  // previous thread's block-inclusive value
   int prev_key = __shfl_up_sync(0xffffffffu, key, 1);
   T prev_v = __shfl_up_sync(0xffffffffu, v, 1);
   if (lane == 0) { prev_key = warp > 0 ? pk : -1; prev_v = warp > 0 ? pv : T(0); }
   if (first_row >= 0) {
-    T tot = (prev_key == first_row) ? prev_v + first_val : first_val;
+    const T tot = (prev_key == first_row) ? prev_v + first_val : first_val;
     T* yp = y + r0 + first_row;
     *yp = accumulate ? *yp + tot : tot;
   }
-  if (tid == M_NT - 1) {
-    // carry of the tile's open row (row r0 + nr), if it has elements here
-    const bool has = (key == nr) && (nj > 0) && (nr == 0 || j1 > s_end[nr - 1]);
+  if (tid == NT - 1) {
+    const bool has = (key == nr) && (nj > 0) && (nr == 0 || j0 + nj > end_at(nr - 1));
     carry_row[t] = has ? r0 + nr : -1;
     carry_val[t] = has ? v : T(0);
+  }
+}
+
+// One CTA per tile, loads straight from global (fallback for unaligned pointers).
+template <typename T>
+__global__ void __launch_bounds__(M_NT) k_spmv_merge(int32_t n_rows, int32_t nnz, const int32_t* __restrict__ row_ptr,
+                                                     const int32_t* __restrict__ col, const T* __restrict__ val,
+                                                     const T* __restrict__ x, T* __restrict__ y,
+                                                     const int2* __restrict__ plan, T* __restrict__ carry_val,
+                                                     int32_t* __restrict__ carry_row, int accumulate) {
+  __shared__ T s_prod[M_TILE];
+  __shared__ int32_t s_end[M_TILE];
+  __shared__ ScanSmem<T, M_NT> sm;
+  const int tid = threadIdx.x;
+  const int t = blockIdx.x;
+  const int2 c0 = plan[t], c1 = plan[t + 1];
+  const int r0 = c0.x, j0 = c0.y, nr = c1.x - r0, nj = c1.y - j0;
+  const uint64_t pol_keep = policy_evict_last();
+  for (int i = tid; i < nr; i += M_NT) s_end[i] = row_ptr[r0 + 1 + i];
+  for (int j = tid; j < nj; j += M_NT) s_prod[j] = val[j0 + j] * ld_keep(x + col[j0 + j], pol_keep);
+  __syncthreads();
+  merge_tile_reduce<T, M_NT, M_IPT>(
+      t, r0, nr, j0, nj, [&](int i) { return s_end[i]; }, [&](int j) { return s_prod[j]; }, y, accumulate,
+      carry_val, carry_row, sm);
+}
+
+// Persistent, TMA-pipelined merge SpMV: one elected thread streams each tile's
+// col_idx / values / row_ptr slices into a ring of S shared-memory stages with
+// cp.async.bulk (L2 evict-first) completing on per-stage mbarriers, S tiles
+// ahead of the consumers; all threads gather x (L2 evict-last), form the
+// products in place and run the merge-path reduction.  The last partial group
+// of each array (the bulk engine needs 16-byte multiples) is read directly.
+constexpr int T_NT = 256;
+constexpr int T_IPT = 8;
+constexpr int T_TILE = T_NT * T_IPT;
+constexpr int T_CAP = T_TILE + 8;  // slack for 4-element alignment at both ends
+constexpr int T_STAGES = 3;
+
+template <typename T>
+__host__ __device__ constexpr size_t tma_stage_bytes() {
+  return (size_t)T_CAP * sizeof(T) + 2 * (size_t)T_CAP * 4;
+}
+template <typename T>
+__host__ __device__ constexpr size_t tma_smem_bytes() {
+  return T_STAGES * tma_stage_bytes<T>();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(T_NT, 2) k_spmv_merge_tma(int32_t n_rows, int32_t nnz,
+                                                            const int32_t* __restrict__ row_ptr,
+                                                            const int32_t* __restrict__ col, const T* __restrict__ val,
+                                                            const T* __restrict__ x, T* __restrict__ y,
+                                                            const int2* __restrict__ plan, int32_t n_tiles,
+                                                            T* __restrict__ carry_val, int32_t* __restrict__ carry_row,
+                                                            int accumulate) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[T_STAGES];
+  __shared__ int4 meta[T_STAGES];   // r0, j0, nr, nj
+  __shared__ int2 bounds[T_STAGES]; // a1 (first nnz NOT in smem), b1 (first row_ptr idx NOT in smem)
+  __shared__ ScanSmem<T, T_NT> sm;
+  const int tid = threadIdx.x;
+  const int nnz4 = nnz & ~3;             // bulk-copyable prefix of col/val
+  const int ptr4 = (n_rows + 1) & ~3;    // bulk-copyable prefix of row_ptr
+  auto s_val = [&](int s) { return reinterpret_cast<T*>(smem + s * tma_stage_bytes<T>()); };
+  auto s_col = [&](int s) { return reinterpret_cast<int32_t*>(smem + s * tma_stage_bytes<T>() + T_CAP * sizeof(T)); };
+  auto s_end = [&](int s) {
+    return reinterpret_cast<int32_t*>(smem + s * tma_stage_bytes<T>() + T_CAP * sizeof(T) + T_CAP * 4);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < T_STAGES; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();
+
+  auto issue = [&](int s, int t) {  // thread 0 only
+    const int2 c0 = plan[t], c1 = plan[t + 1];
+    const int r0 = c0.x, j0 = c0.y, nr = c1.x - r0, nj = c1.y - j0;
+    const int a0 = j0 & ~3;
+    const int a1 = max(a0, min((j0 + nj + 3) & ~3, nnz4));
+    const int b0 = (r0 + 1) & ~3;
+    const int b1 = max(b0, min((r0 + 1 + nr + 3) & ~3, ptr4));
+    meta[s] = make_int4(r0, j0, nr, nj);
+    bounds[s] = make_int2(a1, b1);
+    const uint32_t na = (uint32_t)(a1 - a0), nb = (uint32_t)(b1 - b0);
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&full[s], na * (4 + (uint32_t)sizeof(T)) + nb * 4);
+    if (na) {
+      bulk_g2s(s_col(s), col + a0, na * 4, &full[s], pol_stream);
+      bulk_g2s(s_val(s), val + a0, na * (uint32_t)sizeof(T), &full[s], pol_stream);
+    }
+    if (nb) bulk_g2s(s_end(s), row_ptr + b0, nb * 4, &full[s], pol_stream);
+  };
+
+  const int first = blockIdx.x;
+  const int stride = gridDim.x;
+  if (tid == 0) {
+    for (int s = 0; s < T_STAGES; ++s) {
+      const int t = first + s * stride;
+      if (t < n_tiles) issue(s, t);
+    }
+  }
+  int it = 0;
+  for (int t = first; t < n_tiles; t += stride, ++it) {
+    const int s = it % T_STAGES;
+    mbar_wait(&full[s], (uint32_t)((it / T_STAGES) & 1));
+    const int4 mt = meta[s];
+    const int r0 = mt.x, j0 = mt.y, nr = mt.z, nj = mt.w;
+    const int a0 = j0 & ~3, b0 = (r0 + 1) & ~3;
+    const int2 bd = bounds[s];
+    const int a1 = bd.x, b1 = bd.y;
+    T* sv = s_val(s);
+    const int32_t* sc = s_col(s);
+    const int32_t* se = s_end(s);
+    // products in place: sv[k - a0] = val[k] * x[col[k]] for k in [j0, j0 + nj)
+    {
+      int cidx[T_IPT];
+      T vv[T_IPT], xv[T_IPT];
+#pragma unroll
+      for (int q = 0; q < T_IPT; ++q) {
+        const int k = j0 + tid + q * T_NT;
+        cidx[q] = -1;
+        if (k < j0 + nj) {
+          if (k < a1) { cidx[q] = sc[k - a0]; vv[q] = sv[k - a0]; }
+          else { cidx[q] = col[k]; vv[q] = val[k]; }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < T_IPT; ++q) xv[q] = cidx[q] >= 0 ? ld_keep(x + cidx[q], pol_keep) : T(0);
+#pragma unroll
+      for (int q = 0; q < T_IPT; ++q) {
+        const int k = j0 + tid + q * T_NT;
+        if (cidx[q] >= 0) sv[k - a0] = vv[q] * xv[q];
+      }
+    }
+    __syncthreads();
+    merge_tile_reduce<T, T_NT, T_IPT>(
+        t, r0, nr, j0, nj,
+        [&](int i) {
+          const int g = r0 + 1 + i;
+          return g < b1 ? se[g - b0] : row_ptr[g];
+        },
+        [&](int j) { return sv[j0 + j - a0]; }, y, accumulate, carry_val, carry_row, sm);
+    __syncthreads();  // every thread is done with stage s
+    if (tid == 0) {
+      const int tn = t + T_STAGES * stride;
+      if (tn < n_tiles) issue(s, tn);
+    }
   }
 }
 
@@ -244,30 +347,65 @@ __global__ void __launch_bounds__(256) k_spmv_vector(int64_t n_rows, const int32
 }
 
 // numpy's pairwise summation (loops_utils.h.src: pairwise_sum) over the
-// products of positions [s, s+n), each product separately rounded.
-__device__ double pw_sum(const int32_t* __restrict__ col, const double* __restrict__ val,
-                         const double* __restrict__ x, int64_t s, int64_t n) {
+// products of positions [s, s+n), each product separately rounded.  Leaves:
+__device__ double pw_leaf(const int32_t* __restrict__ col, const double* __restrict__ val,
+                          const double* __restrict__ x, int64_t s, int64_t n) {
   if (n < 8) {
     double res = -0.0;
     for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, __dmul_rn(val[s + i], x[col[s + i]]));
     return res;
-  } else if (n <= 128) {
-    double r[8];
+  }
+  double r[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) r[q] = __dmul_rn(val[s + q], x[col[s + q]]);
-    int64_t i;
-    for (i = 8; i < n - (n % 8); i += 8) {
+  for (int q = 0; q < 8; ++q) r[q] = __dmul_rn(val[s + q], x[col[s + q]]);
+  int64_t i;
+  for (i = 8; i < n - (n % 8); i += 8) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], __dmul_rn(val[s + i + q], x[col[s + i + q]]));
+    for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], __dmul_rn(val[s + i + q], x[col[s + i + q]]));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, __dmul_rn(val[s + i], x[col[s + i]]));
+  return res;
+}
+
+// The recursion pw(s,n) = pw(s,n2) + pw(s+n2,n-n2) (n > 128, n2 = n/2 rounded down
+// to a multiple of 8) evaluated with an explicit stack (no device-stack recursion).
+__device__ double pw_sum(const int32_t* __restrict__ col, const double* __restrict__ val,
+                         const double* __restrict__ x, int64_t s0, int64_t n0) {
+  constexpr int DEPTH = 48;
+  int64_t S[DEPTH], N[DEPTH];
+  double L[DEPTH];
+  int state[DEPTH];
+  int sp = 1;
+  S[0] = s0; N[0] = n0; state[0] = 0;
+  double ret = 0.0;
+  bool have = false;
+  while (true) {
+    const int i = sp - 1;
+    if (have) {
+      if (state[i] == 0) {  // left child done: descend into the right child
+        L[i] = ret;
+        state[i] = 1;
+        int64_t n2 = N[i] / 2;
+        n2 -= n2 % 8;
+        S[sp] = S[i] + n2; N[sp] = N[i] - n2; state[sp] = 0; ++sp;
+        have = false;
+      } else {  // both children done
+        ret = __dadd_rn(L[i], ret);
+        if (--sp == 0) return ret;
+      }
+      continue;
     }
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, __dmul_rn(val[s + i], x[col[s + i]]));
-    return res;
-  } else {
-    int64_t n2 = n / 2;
+    if (N[i] <= 128) {
+      ret = pw_leaf(col, val, x, S[i], N[i]);
+      have = true;
+      if (--sp == 0) return ret;
+      continue;
+    }
+    int64_t n2 = N[i] / 2;
     n2 -= n2 % 8;
-    return __dadd_rn(pw_sum(col, val, x, s, n2), pw_sum(col, val, x, s + n2, n - n2));
+    S[sp] = S[i]; N[sp] = n2; state[sp] = 0; ++sp;
   }
 }
 
@@ -307,6 +445,36 @@ int launch_vector(int lanes, int64_t n_rows, const int32_t* rp, const int32_t* c
   return SME_OK;
 }
 
+
+// 0 = one CTA per tile (global loads), 1 = persistent TMA pipeline; -1 = auto.
+static int merge_mode_override = -1;
+
+template <typename T>
+int launch_merge(int mode, int64_t n_rows, int64_t nnz, const int32_t* row_ptr, const int32_t* col, const T* val,
+                 const T* x, T* y, const int32_t* plan, int64_t n_tiles, void* carry, int accumulate, cudaStream_t s) {
+  const int2* pl = reinterpret_cast<const int2*>(plan);
+  char* cb = (char*)carry;
+  T* cval = (T*)cb;
+  int32_t* carry_row = (int32_t*)(cb + align_up((size_t)n_tiles * 8));
+  if (mode == 1) {
+    const size_t smem = tma_smem_bytes<T>();
+    SME_CUDA(cudaFuncSetAttribute(k_spmv_merge_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = (int)std::min<int64_t>(n_tiles, (int64_t)sm_count() * 2);
+    k_spmv_merge_tma<T><<<grid, T_NT, smem, s>>>((int32_t)n_rows, (int32_t)nnz, row_ptr, col, val, x, y, pl,
+                                                 (int32_t)n_tiles, cval, carry_row, accumulate);
+    SME_CHECK_LAUNCH("k_spmv_merge_tma");
+  } else {
+    k_spmv_merge<T><<<(unsigned)n_tiles, M_NT, 0, s>>>((int32_t)n_rows, (int32_t)nnz, row_ptr, col, val, x, y, pl,
+                                                       cval, carry_row, accumulate);
+    SME_CHECK_LAUNCH("k_spmv_merge");
+  }
+  if (n_tiles > 1) {
+    k_spmv_fixup<T><<<grid_for(n_tiles, 256), 256, 0, s>>>(n_tiles, pl, carry_row, cval, y);
+    SME_CHECK_LAUNCH("k_spmv_fixup");
+  }
+  return SME_OK;
+}
+
 }  // namespace sme
 
 using namespace sme;
@@ -339,37 +507,17 @@ SME_API int sme_spmv_merge(int dtype, int64_t n_rows, int64_t n_cols, int64_t nn
                            int64_t n_tiles, void* carry, int accumulate, sme_stream_t stream) {
   SME_REQUIRE(n_rows >= 0 && n_rows < INT32_MAX && nnz >= 0 && nnz < INT32_MAX, "sizes exceed int32");
   SME_REQUIRE(n_tiles == (n_rows + nnz + M_TILE - 1) / M_TILE, "plan was built for another shape");
-  SME_REQUIRE(((uintptr_t)col & 15) == 0 && ((uintptr_t)val & 15) == 0,
-              "col_idx and values must be 16-byte aligned");
   if (n_tiles == 0) return SME_OK;
+  SME_REQUIRE(dtype == SME_F64 || dtype == SME_F32, "unknown dtype %d", dtype);
   cudaStream_t s = as_stream(stream);
-  const int2* pl = reinterpret_cast<const int2*>(plan);
-  char* cb = (char*)carry;
-  int32_t* carry_row = (int32_t*)(cb + align_up((size_t)n_tiles * 8));
-  if (dtype == SME_F64) {
-    double* cval = (double*)cb;
-    k_spmv_merge<double><<<(unsigned)n_tiles, M_NT, 0, s>>>((int32_t)n_rows, (int32_t)nnz, row_ptr, col,
-                                                            (const double*)val, (const double*)x, (double*)y, pl,
-                                                            cval, carry_row, accumulate);
-    SME_CHECK_LAUNCH("k_spmv_merge");
-    if (n_tiles > 1) {
-      k_spmv_fixup<double><<<grid_for(n_tiles, 256), 256, 0, s>>>(n_tiles, pl, carry_row, cval, (double*)y);
-      SME_CHECK_LAUNCH("k_spmv_fixup");
-    }
-  } else if (dtype == SME_F32) {
-    float* cval = (float*)cb;
-    k_spmv_merge<float><<<(unsigned)n_tiles, M_NT, 0, s>>>((int32_t)n_rows, (int32_t)nnz, row_ptr, col,
-                                                          (const float*)val, (const float*)x, (float*)y, pl, cval,
-                                                          carry_row, accumulate);
-    SME_CHECK_LAUNCH("k_spmv_merge");
-    if (n_tiles > 1) {
-      k_spmv_fixup<float><<<grid_for(n_tiles, 256), 256, 0, s>>>(n_tiles, pl, carry_row, cval, (float*)y);
-      SME_CHECK_LAUNCH("k_spmv_fixup");
-    }
-  } else {
-    SME_REQUIRE(false, "unknown dtype %d", dtype);
-  }
-  return SME_OK;
+  const bool aligned = (((uintptr_t)col | (uintptr_t)val | (uintptr_t)row_ptr) & 15) == 0;
+  const int mode = merge_mode_override >= 0 ? merge_mode_override : (aligned ? 1 : 0);
+  SME_REQUIRE(mode == 0 || aligned, "the TMA merge kernel needs 16-byte aligned row_ptr/col_idx/values");
+  if (dtype == SME_F64)
+    return launch_merge<double>(mode, n_rows, nnz, row_ptr, col, (const double*)val, (const double*)x, (double*)y,
+                                plan, n_tiles, carry, accumulate, s);
+  return launch_merge<float>(mode, n_rows, nnz, row_ptr, col, (const float*)val, (const float*)x, (float*)y, plan,
+                             n_tiles, carry, accumulate, s);
 }
 
 SME_API int sme_spmv_vector(int dtype, int lanes, int64_t n_rows, int64_t n_cols, const int32_t* row_ptr,
@@ -412,3 +560,11 @@ SME_API int sme_spmv_coo(int dtype, int64_t n_rows, int64_t nnz, const int32_t* 
   SME_CHECK_LAUNCH("k_spmv_coo");
   return SME_OK;
 }
+
+// Kernel selection for experiments/tests: 0 = per-tile kernel, 1 = TMA pipeline, -1 = auto.
+SME_API int sme_spmv_merge_set_mode(int mode) {
+  SME_REQUIRE(mode >= -1 && mode <= 1, "mode must be -1, 0 or 1");
+  merge_mode_override = mode;
+  return SME_OK;
+}
+

@@ -1,0 +1,276 @@
+// spmv_stream.cu — k_spmv_stream: warp-streaming CSR SpMV with a warp-level
+// segmented reduction (the fast path for regular and moderately ragged rows).
+//
+// Reference: spmv_csr / _accumulate_rows (kernels.py:59-78).
+//
+// Work split: a per-matrix plan gives every warp a contiguous row range
+// holding ~nnz/W nonzeros (W = resident warps of the persistent grid), so a
+// row never spans two warps and there is no fix-up pass.  A warp streams its
+// nonzeros in 128-element chunks aligned to GLOBAL multiples of 128 (lane l
+// holds elements c+4l..c+4l+3: one 128-bit col_idx load and two/one 128-bit
+// value loads, L1 no-allocate, L2 evict-first), prefetching the next chunk
+// before it gathers x for the current one (L2 evict-last).  Rows are reduced
+// with a flag-segmented scan: row starts inside the chunk become head bits
+// (__reduce_or_sync), each lane folds its 4 products, a 5-step shuffle scan
+// carries partial sums across lanes, the open segment carries into the next
+// chunk, and the lane owning row i of a sliding 32-row window picks the row
+// total at position end_i - 1.  A row's association depends only on its
+// global positions (align_off = global position of local element 0), so row
+// shards that keep positions mod 128 reduce bitwise-identically.
+#include "common.cuh"
+
+#include <algorithm>
+
+namespace sme {
+
+constexpr int S_NT = 256;
+
+template <typename T> struct Vec4;
+template <> struct Vec4<double> {
+  static __device__ __forceinline__ void load(const double* p, uint64_t pol, double v[4]) {
+    double2 a = ld_stream_d2(reinterpret_cast<const double2*>(p), pol);
+    double2 b = ld_stream_d2(reinterpret_cast<const double2*>(p) + 1, pol);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+};
+template <> struct Vec4<float> {
+  static __device__ __forceinline__ void load(const float* p, uint64_t pol, float v[4]) {
+    float4 a = ld_stream_f4(reinterpret_cast<const float4*>(p), pol);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  }
+};
+
+// 4 consecutive elements at local index e (e % 4 == 0 when vec_ok); anything
+// outside [0, nnz) reads as col = -1.  Elements of neighbouring rows inside
+// the chunk are loaded too and masked later (the aligned chunk is one line).
+template <typename T>
+__device__ __forceinline__ void chunk_load(const int32_t* __restrict__ col, const T* __restrict__ val, int e,
+                                           int nnz, bool vec_ok, uint64_t pol, int c[4], T v[4]) {
+  if (vec_ok && e >= 0 && e + 3 < nnz) {
+    int4 ci = ld_stream_i4(reinterpret_cast<const int4*>(col + e), pol);
+    c[0] = ci.x; c[1] = ci.y; c[2] = ci.z; c[3] = ci.w;
+    Vec4<T>::load(val + e, pol, v);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = e + q;
+      if (k >= 0 && k < nnz) { c[q] = ld_stream_i1(col + k, pol); v[q] = ld_stream(val + k, pol); }
+      else { c[q] = -1; v[q] = T(0); }
+    }
+  }
+}
+
+// warp_rows[w] = first row of warp w: the first row whose start is >= w * nnz / W
+__global__ void k_stream_plan(int32_t n_rows, int32_t nnz, const int32_t* __restrict__ row_ptr, int32_t n_warps,
+                              int32_t* __restrict__ warp_rows) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= n_warps; w += gridDim.x * blockDim.x) {
+    if (w == 0) { warp_rows[0] = 0; continue; }
+    if (w == n_warps) { warp_rows[w] = n_rows; continue; }
+    const int64_t target = (int64_t)w * nnz / n_warps;
+    int lo = 0, hi = n_rows;  // lower_bound over row_ptr[0..n_rows)
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if ((int64_t)row_ptr[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    warp_rows[w] = lo;
+  }
+}
+
+template <typename T, bool ACC>
+__global__ void __launch_bounds__(S_NT) k_spmv_stream(int32_t n_rows, int32_t nnz, const int32_t* __restrict__ row_ptr,
+                                                      const int32_t* __restrict__ col, const T* __restrict__ val,
+                                                      const T* __restrict__ x, T* __restrict__ y,
+                                                      const int32_t* __restrict__ warp_rows, int32_t n_warps,
+                                                      int32_t align_off, bool vec_ok) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * S_NT + threadIdx.x) >> 5;
+  if (warp >= n_warps) return;
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();
+  const int R0 = warp_rows[warp], R1 = warp_rows[warp + 1];
+  if (R0 >= R1) return;
+  const int P0 = row_ptr[R0], P1 = row_ptr[R1];
+
+  // sliding window: lane l holds row q + l (s, e); rows >= R1 are inert (s = e = P1)
+  int q = R0;
+  auto load_window = [&](int base, int& s, int& e) {
+    const int r = base + lane;
+    if (r < R1) { s = row_ptr[r]; e = row_ptr[r + 1]; }
+    else { s = P1; e = P1; }
+  };
+  int s, e;
+  load_window(q, s, e);
+
+  // chunk starts aligned to global multiples of 128
+  int c = ((P0 + align_off) & ~127) - align_off;
+  if (P0 == P1) c = P1;  // only empty rows: no chunk
+  int ci[4];
+  T vv[4];
+  if (c < P1) chunk_load<T>(col, val, c + 4 * lane, nnz, vec_ok, pol_stream, ci, vv);
+  T carry = T(0);
+  while (true) {
+    const bool have = c < P1;
+    // prefetch the next chunk
+    int nci[4];
+    T nvv[4];
+    if (c + 128 < P1) chunk_load<T>(col, val, c + 128 + 4 * lane, nnz, vec_ok, pol_stream, nci, nvv);
+    T p[4] = {T(0), T(0), T(0), T(0)};
+    if (have) {
+      // mask elements outside the warp's range [P0, P1)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int pos = c + 4 * lane + k;
+        if (pos < P0 || pos >= P1) ci[k] = -1;
+      }
+      T xv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) xv[k] = ci[k] >= 0 ? ld_keep(x + ci[k], pol_keep) : T(0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) p[k] = ci[k] >= 0 ? vv[k] * xv[k] : T(0);
+    }
+    const int cend = have ? c + 128 : INT32_MAX;  // after the last chunk every row finishes
+    // head bits of nonempty rows starting in [c, cend); rows beyond the window
+    // are handled by further windows of the same chunk (rare: < 4 nnz/row)
+    unsigned f0 = 0, f1 = 0, f2 = 0, f3 = 0;
+    int wq = q, ws = s, we = e;
+    while (true) {
+      const int rel = ws - c;
+      const bool head = have && ws < we && rel >= 0 && rel < 128;
+      const unsigned bit = head ? (1u << (rel & 31)) : 0u;
+      const int word = rel >> 5;
+      f0 |= __reduce_or_sync(FULL, (head && word == 0) ? bit : 0u);
+      f1 |= __reduce_or_sync(FULL, (head && word == 1) ? bit : 0u);
+      f2 |= __reduce_or_sync(FULL, (head && word == 2) ? bit : 0u);
+      f3 |= __reduce_or_sync(FULL, (head && word == 3) ? bit : 0u);
+      const int last_s = __shfl_sync(FULL, ws, 31);
+      if (wq + 32 >= R1 || last_s >= cend) break;
+      wq += 32;
+      load_window(wq, ws, we);
+    }
+    const int wsel = lane >> 3;
+    const unsigned fw = wsel == 0 ? f0 : (wsel == 1 ? f1 : (wsel == 2 ? f2 : f3));
+    const unsigned my = (fw >> ((4 * lane) & 31)) & 0xFu;
+    if (lane == 0 && !(my & 1u)) p[0] = carry + p[0];
+    T a[4];
+    a[0] = p[0];
+#pragma unroll
+    for (int k = 1; k < 4; ++k) a[k] = ((my >> k) & 1u) ? p[k] : a[k - 1] + p[k];
+    T v = a[3];
+    bool f = my != 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T ov = __shfl_up_sync(FULL, v, o);
+      const bool of = __shfl_up_sync(FULL, (int)f, o) != 0;
+      if (lane >= o) {
+        if (!f) v = ov + v;
+        f = f || of;
+      }
+    }
+    T ex = __shfl_up_sync(FULL, v, 1);
+    if (lane == 0) ex = T(0);
+    T fin[4];
+    bool open = true;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if ((my >> k) & 1u) open = false;
+      fin[k] = open ? ex + a[k] : a[k];
+    }
+    // rows finishing in this chunk (end <= cend): nonempty ones take fin at end-1
+    wq = q; ws = s; we = e;
+    while (true) {
+      const int r = wq + lane;
+      const bool live = r < R1;
+      const int pe = we - 1 - c;
+      const bool ends_here = live && ws < we && pe >= 0 && pe < 128 && have;
+      const int src = ends_here ? (pe >> 2) : lane;
+      const int slot = pe & 3;
+      const T t0 = __shfl_sync(FULL, fin[0], src), t1 = __shfl_sync(FULL, fin[1], src);
+      const T t2 = __shfl_sync(FULL, fin[2], src), t3 = __shfl_sync(FULL, fin[3], src);
+      if (ends_here) {
+        const T tot = slot == 0 ? t0 : (slot == 1 ? t1 : (slot == 2 ? t2 : t3));
+        y[r] = ACC ? y[r] + tot : tot;
+      } else if (!ACC && live && ws == we && we <= cend) {
+        y[r] = T(0);  // empty row
+      }
+      const unsigned done = __ballot_sync(FULL, live && we <= cend);
+      const int n_done = __popc(done);
+      const int last_e = __shfl_sync(FULL, we, 31);
+      if (n_done < 32 || wq + 32 >= R1 || last_e > cend) {
+        q = wq + n_done;
+        break;
+      }
+      wq += 32;
+      load_window(wq, ws, we);
+    }
+    if (q >= R1 || !have) break;
+    load_window(q, s, e);
+    carry = __shfl_sync(FULL, fin[3], 31);
+    c += 128;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { ci[k] = nci[k]; vv[k] = nvv[k]; }
+  }
+}
+
+template <typename T>
+int launch_stream(int64_t n_rows, int64_t nnz, const int32_t* row_ptr, const int32_t* col, const T* val, const T* x,
+                  T* y, const int32_t* plan, int32_t n_warps, int accumulate, int32_t align_off, bool vec,
+                  cudaStream_t s) {
+  const int grid = (n_warps * 32 + S_NT - 1) / S_NT;
+  if (accumulate)
+    k_spmv_stream<T, true><<<grid, S_NT, 0, s>>>((int32_t)n_rows, (int32_t)nnz, row_ptr, col, val, x, y, plan,
+                                                  n_warps, align_off, vec);
+  else
+    k_spmv_stream<T, false><<<grid, S_NT, 0, s>>>((int32_t)n_rows, (int32_t)nnz, row_ptr, col, val, x, y, plan,
+                                                   n_warps, align_off, vec);
+  SME_CHECK_LAUNCH("k_spmv_stream");
+  return SME_OK;
+}
+
+}  // namespace sme
+
+using namespace sme;
+
+SME_API int sme_spmv_stream_warps(int64_t n_rows, int64_t nnz, int32_t* n_warps) {
+  SME_REQUIRE(n_warps && n_rows >= 0 && nnz >= 0, "bad arguments");
+  // exactly the resident warps of the persistent grid (static ranges need them all
+  // running at once), never more than ~1 warp per 32 rows
+  int per_sm = 0;
+  SME_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_stream<double, false>, S_NT, 0));
+  int per_sm32 = 0;
+  SME_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm32, k_spmv_stream<double, true>, S_NT, 0));
+  per_sm = std::max(1, std::min(per_sm, per_sm32));
+  int64_t w = (int64_t)sm_count() * per_sm * (S_NT / 32);
+  w = std::min<int64_t>(w, std::max<int64_t>(1, (n_rows + 31) / 32));
+  *n_warps = (int32_t)w;
+  return SME_OK;
+}
+
+SME_API int sme_spmv_stream_plan(int64_t n_rows, int64_t nnz, const int32_t* row_ptr, int32_t n_warps,
+                                 int32_t* plan, sme_stream_t stream) {
+  SME_REQUIRE(n_rows >= 0 && n_rows < INT32_MAX - 256 && nnz >= 0 && nnz < INT32_MAX - 256, "sizes exceed int32");
+  SME_REQUIRE(n_warps >= 1, "n_warps must be >= 1");
+  cudaStream_t s = as_stream(stream);
+  k_stream_plan<<<grid_for((int64_t)n_warps + 1, 256), 256, 0, s>>>((int32_t)n_rows, (int32_t)nnz, row_ptr, n_warps,
+                                                                     plan);
+  SME_CHECK_LAUNCH("k_stream_plan");
+  return SME_OK;
+}
+
+SME_API int sme_spmv_stream(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row_ptr,
+                            const int32_t* col, const void* val, const void* x, void* y, const int32_t* plan,
+                            int32_t n_warps, int accumulate, int32_t align_off, sme_stream_t stream) {
+  SME_REQUIRE(n_rows >= 0 && n_rows < INT32_MAX - 256 && nnz >= 0 && nnz < INT32_MAX - 256, "sizes exceed int32");
+  SME_REQUIRE(plan && n_warps >= 1, "missing stream plan");
+  SME_REQUIRE(align_off >= 0 && align_off < 128, "align_off must lie in [0, 128)");
+  if (n_rows == 0) return SME_OK;
+  SME_REQUIRE(dtype == SME_F64 || dtype == SME_F32, "unknown dtype %d", dtype);
+  // 128-bit loads need 16-byte aligned arrays and local index = global index (mod 4)
+  const bool vec = (((uintptr_t)col | (uintptr_t)val) & 15) == 0 && (align_off & 3) == 0;
+  cudaStream_t s = as_stream(stream);
+  if (dtype == SME_F64)
+    return launch_stream<double>(n_rows, nnz, row_ptr, col, (const double*)val, (const double*)x, (double*)y, plan,
+                                 n_warps, accumulate, align_off, vec, s);
+  return launch_stream<float>(n_rows, nnz, row_ptr, col, (const float*)val, (const float*)x, (float*)y, plan, n_warps,
+                              accumulate, align_off, vec, s);
+}

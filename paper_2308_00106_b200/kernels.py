@@ -30,7 +30,7 @@ from . import _cuda, _lib
 from ._cuda import ptr, stream
 from .matio import CooMatrix, CsrMatrix
 
-KERNELS = ("vector", "merge", "exact")
+KERNELS = ("stream", "vector", "merge", "exact")
 
 
 @dataclass(frozen=True, eq=False)
@@ -85,6 +85,24 @@ class MergePlan:
         )
 
 
+def set_merge_mode(mode: int) -> None:
+    """Select the merge kernel: 1 = TMA-pipelined persistent, 0 = per-tile, -1 = auto."""
+    _lib.call("sme_spmv_merge_set_mode", int(mode))
+
+
+def stream_plan(m: CsrMatrix) -> tuple[torch.Tensor, int]:
+    """Per-matrix warp row ranges of the stream kernel (nnz-balanced, one per resident warp)."""
+    if "stream" not in m._cache:
+        import ctypes
+
+        w = ctypes.c_int32(0)
+        _lib.call("sme_spmv_stream_warps", m.n_rows, m.nnz, ctypes.byref(w))
+        plan = torch.empty(w.value + 1, dtype=torch.int32, device=m.d_row_ptr.device)
+        _lib.call("sme_spmv_stream_plan", m.n_rows, m.nnz, ptr(m.d_row_ptr), w.value, ptr(plan), stream())
+        m._cache["stream"] = (plan, int(w.value))
+    return m._cache["stream"]
+
+
 def merge_plan(m: CsrMatrix) -> MergePlan:
     if "merge" not in m._cache:
         m._cache["merge"] = MergePlan(m)
@@ -124,6 +142,11 @@ def spmv_into(m: CsrMatrix, xd: torch.Tensor, y: torch.Tensor, kernel: str = "ve
     if kernel == "vector":
         _lib.call("sme_spmv_vector", dt, lanes or default_lanes(m), m.n_rows, m.n_cols, ptr(m.d_row_ptr),
                   ptr(m.d_col_idx), ptr(m.d_values), ptr(xd), ptr(y), int(accumulate), stream())
+    elif kernel == "stream":
+        plan, n_warps = stream_plan(m)
+        _lib.call("sme_spmv_stream", dt, m.n_rows, m.n_cols, m.nnz, ptr(m.d_row_ptr), ptr(m.d_col_idx),
+                  ptr(m.d_values), ptr(xd), ptr(y), ptr(plan), n_warps, int(accumulate),
+                  int(m._cache.get("align_off", 0)), stream())
     elif kernel == "merge":
         pl = merge_plan(m)
         _lib.call("sme_spmv_merge", dt, m.n_rows, m.n_cols, m.nnz, ptr(m.d_row_ptr), ptr(m.d_col_idx),

@@ -62,7 +62,7 @@ def test_pipeline_matches_reference_golden(golden, dev):
         assert P.coo_to_csr(csr_b) == csr, c
         x_perm = P.permute_vector(g("x"), p_c)
         assert np.array_equal(bits(x_perm), bits(g("x_perm"))), c
-        for kernel in ("vector", "merge"):
+        for kernel in ("vector", "merge", "stream"):
             y = P.spmv_csr(csr, x_perm, kernel)
             assert P.relative_error(y, g("y")) <= F64_TOL, (c, kernel)
             assert O.relative_error(y, g("y")) <= F64_TOL, (c, kernel)
@@ -87,6 +87,24 @@ def test_pipeline_matches_reference_golden(golden, dev):
             b1r, b1c = min(512, n_rows), min(512, n_cols)
             assert np.array_equal(P.row_histogram(csr, b1r).counts, g("rowhist")), c
             assert np.array_equal(P.col_histogram(csr, b1c).counts, g("colhist")), c
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_both_merge_kernels_match_reference(golden, dev, mode):
+    from paper_2308_00106_b200.kernels import set_merge_mode
+
+    set_merge_mode(mode)
+    try:
+        for c in golden_cases(golden):
+            g = gcase(golden, c)
+            n_rows, n_cols = (int(v) for v in g("shape"))
+            csr = P.CsrMatrix(n_rows, n_cols, g("csr_ptr"), g("csr_col"), g("csr_val"))
+            y = P.spmv_csr(csr, g("x_perm"), "merge")
+            assert O.relative_error(y, g("y")) <= F64_TOL, (c, mode)
+            again = P.spmv_csr(csr, g("x_perm"), "merge")
+            assert np.array_equal(bits(y), bits(again)), (c, mode)  # deterministic
+    finally:
+        set_merge_mode(-1)
 
 
 def test_coo_histogram_kernel_matches_reference(golden, dev):
@@ -216,7 +234,7 @@ def test_random_pipeline_vs_oracle(dev, rng, shape):
     x = O.input_vector(0, n_cols)
     xp = O.permute_vector(x, p_c)
     want = O.spmv_csr(optr, ocol, oval, xp)
-    for kernel in ("vector", "merge"):
+    for kernel in ("vector", "merge", "stream"):
         assert O.relative_error(P.spmv_csr(csr, xp, kernel), want) <= F64_TOL
     assert np.array_equal(bits(P.spmv_csr(csr, xp, "exact")), bits(want))
     br, bc = min(128, n_rows), min(128, n_cols)
@@ -235,13 +253,14 @@ def test_power_law_rows_merge_kernel(dev, rng):
     m = P.CsrMatrix(n_rows, n_cols, ptr, col, val)
     x = rng.random(n_cols)
     want = O.spmv_csr(ptr, col, val, x)
-    for kernel in ("vector", "merge"):
+    for kernel in ("vector", "merge", "stream"):
         assert O.relative_error(P.spmv_csr(m, x, kernel), want) <= F64_TOL, kernel
     # accumulate mode: y += A x
     xd = torch.from_numpy(x).to(dev)
-    y = torch.ones(n_rows, dtype=torch.float64, device=dev)
-    spmv_into(m, xd, y, "merge", accumulate=True)
-    assert O.relative_error(y.cpu().numpy(), want + 1.0) <= F64_TOL
+    for kernel in ("merge", "stream", "vector"):
+        y = torch.ones(n_rows, dtype=torch.float64, device=dev)
+        spmv_into(m, xd, y, kernel, accumulate=True)
+        assert O.relative_error(y.cpu().numpy(), want + 1.0) <= F64_TOL, kernel
     # permuted with long rows (> 4096: chunked merge sort path)
     p_r, p_c = O.random_permutation(n_rows, 3), O.random_permutation(n_cols, 4)
     pm = P.permute_csr(m, P.Permutation(p_r), P.Permutation(p_c))
@@ -263,7 +282,7 @@ def test_f32_spmv_within_1e5(dev, rng):
     optr, ocol, oval = O.coo_to_csr(n, rows, cols, vals.astype(np.float64))
     want = O.spmv_csr(optr, ocol, oval, x.astype(np.float64))
     xd = torch.from_numpy(x).to(dev)
-    for kernel in ("vector", "merge"):
+    for kernel in ("vector", "merge", "stream"):
         y = P.spmv_csr(csr, xd, kernel)
         assert y.dtype == torch.float32
         assert O.relative_error(y.double().cpu().numpy(), want) <= F32_TOL, kernel

@@ -1,0 +1,62 @@
+"""Build a config's permuted matrix and run the SpMV kernel a few times (for ncu).
+
+python tools/prof_spmv.py --config c2 --kernel merge --mode 1 --iters 3
+"""
+import argparse
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np
+import torch
+
+import paper_2308_00106_b200 as P
+from paper_2308_00106_b200 import synth
+from paper_2308_00106_b200.kernels import set_merge_mode, spmv_into
+from paper_2308_00106_b200.permute import axis_seed, random_permutation_forward
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--kernel", default="merge")
+ap.add_argument("--mode", type=int, default=-1)
+ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--unpermuted", action="store_true")
+ap.add_argument("--time", action="store_true")
+a = ap.parse_args()
+set_merge_mode(a.mode)
+if a.config == "c4":
+    A = synth.random_rows(50_000_000, 50_000_000, 20)
+elif a.config == "c4s":
+    A = synth.random_rows(10_000_000, 10_000_000, 20)
+elif a.config == "c5":
+    A = synth.laplacian5(2828)
+else:
+    A = synth.laplacian5(2000)
+n = A.n_rows
+dev = torch.device("cuda")
+x = torch.from_numpy(P.input_vector(0, n)).to(dev)
+if a.unpermuted:
+    B, xp = A, x
+else:
+    fr = random_permutation_forward(n, axis_seed(7, 0))
+    fc = random_permutation_forward(n, axis_seed(7, 1))
+    p_r = P.Permutation(torch.from_numpy(fr.astype(np.int32)).to(dev), _trusted=True, _host=fr)
+    p_c = P.Permutation(torch.from_numpy(fc.astype(np.int32)).to(dev), _trusted=True, _host=fc)
+    B = P.permute_csr(A, p_r, p_c)
+    xp = P.permute_vector(x, p_c)
+    del A
+y = torch.empty(n, dtype=B.dtype, device=dev)
+spmv_into(B, xp, y, a.kernel)
+torch.cuda.synchronize()
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+ev[0].record()
+for _ in range(a.iters):
+    spmv_into(B, xp, y, a.kernel)
+ev[1].record()
+torch.cuda.synchronize()
+ms = ev[0].elapsed_time(ev[1]) / a.iters
+bytes_ = B.nnz * 12 + (n + 1) * 4 + 16 * n
+print(f"{a.config} {a.kernel} mode={a.mode} perm={not a.unpermuted}: {ms:.4f} ms  {bytes_ / ms / 1e6:.1f} GB/s  {2 * B.nnz / ms / 1e6:.1f} GFLOP/s")
