@@ -198,6 +198,21 @@ int sme_spmv_stream(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, cons
                     const int32_t* d_plan, int32_t n_warps, int accumulate, int32_t align_off,
                     sme_stream_t stream);
 
+/* Column panels (x-locality layout, panel.cu): split a column-sorted CSR into
+ * n_panels CSRs by column ranges [bounds[p], bounds[p+1]) so that the SpMV can
+ * run one accumulating pass per panel with that panel's x slice L2-resident.
+ * Step 1 writes panel_ptr (n_panels x (n_rows+1), relative row pointers);
+ * step 2 scatters entries to out_col/out_val at offsets[p] (int64 device,
+ * multiples of 128 elements).  Columns stay global and ascending per row. */
+int sme_panel_count_workspace_size(int64_t n_rows, int32_t n_panels, size_t* bytes);
+int sme_panel_row_ptrs(int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_col, int32_t n_panels,
+                       const int32_t* d_bounds, int32_t* d_panel_ptr, void* d_ws, size_t ws_bytes,
+                       sme_stream_t stream);
+int sme_panel_scatter(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_col,
+                      const void* d_val, int32_t n_panels, const int32_t* d_bounds,
+                      const int32_t* d_panel_ptr, const int64_t* d_offsets, int32_t* d_out_col,
+                      void* d_out_val, sme_stream_t stream);
+
 /* Merge kernel selection (process-wide; tests and experiments): 1 = persistent
  * TMA-pipelined kernel (needs 16-byte aligned row_ptr/col_idx/values), 0 = one
  * CTA per tile with plain global loads, -1 = auto (TMA when aligned). */

@@ -55,6 +55,9 @@ SIGNATURES: dict[str, list] = {
     "sme_spmv_merge_carry_bytes": [C.c_int, i64, psz],
     "sme_spmv_merge": [C.c_int, i64, i64, i64, p, p, p, p, p, p, i64, p, C.c_int, p],
     "sme_spmv_merge_set_mode": [C.c_int],
+    "sme_panel_count_workspace_size": [i64, i32, psz],
+    "sme_panel_row_ptrs": [i64, p, p, i32, p, p, p, sz, p],
+    "sme_panel_scatter": [C.c_int, i64, p, p, p, i32, p, p, p, p, p, p],
     "sme_spmv_stream_warps": [i64, i64, C.POINTER(C.c_int32)],
     "sme_spmv_stream_plan": [i64, i64, p, i32, p, p],
     "sme_spmv_stream": [C.c_int, i64, i64, i64, p, p, p, p, p, p, i32, C.c_int, i32, p],

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan_tile_sums(int64_t n, LenFn len
 }
 
 // one block: exclusive scan of tile sums in place; tile_sums[n_tiles] = grand total
-__global__ void __launch_bounds__(1024) k_scan_tile_offsets(int64_t n_tiles, int64_t* tile_sums) {
+static __global__ void __launch_bounds__(1024) k_scan_tile_offsets(int64_t n_tiles, int64_t* tile_sums) {
   __shared__ int64_t s_total;
   int64_t carry = 0;
   for (int64_t b = 0; b < n_tiles; b += 1024) {
@@ -114,6 +114,11 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan_apply(int64_t n, LenFn len, co
     out[n] = (int32_t)run;
   }
 }
+
+struct LenFromArray {
+  const int32_t* a;
+  __device__ __forceinline__ int64_t operator()(int64_t k) const { return a[k]; }
+};
 
 // Launch the three phases.  ws must hold scan_workspace_bytes(n).
 template <class LenFn>

@@ -82,8 +82,13 @@ __global__ void __launch_bounds__(S_NT) k_spmv_stream(int32_t n_rows, int32_t nn
                                                       const T* __restrict__ x, T* __restrict__ y,
                                                       const int32_t* __restrict__ warp_rows, int32_t n_warps,
                                                       int32_t align_off, bool vec_ok) {
+  constexpr int CH = 128;       // chunk = 32 lanes x 4 elements
+  constexpr int LOOP_MAX = 24;  // per-lane row loops up to this overlap, else segmented scan
+  __shared__ T s_buf[S_NT / 32][CH];
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  T* buf = s_buf[wib];
   const int warp = (blockIdx.x * S_NT + threadIdx.x) >> 5;
   if (warp >= n_warps) return;
   const uint64_t pol_stream = policy_evict_first();
@@ -92,121 +97,147 @@ __global__ void __launch_bounds__(S_NT) k_spmv_stream(int32_t n_rows, int32_t nn
   if (R0 >= R1) return;
   const int P0 = row_ptr[R0], P1 = row_ptr[R1];
 
-  // sliding window: lane l holds row q + l (s, e); rows >= R1 are inert (s = e = P1)
+  // window: lane l holds row q + l: its [s, e) and the partial sum acc
   int q = R0;
-  auto load_window = [&](int base, int& s, int& e) {
-    const int r = base + lane;
-    if (r < R1) { s = row_ptr[r]; e = row_ptr[r + 1]; }
-    else { s = P1; e = P1; }
-  };
-  int s, e;
-  load_window(q, s, e);
+  int r = q + lane;
+  bool live = r < R1;
+  int s = live ? row_ptr[r] : P1;
+  int e = live ? row_ptr[r + 1] : P1;
+  T acc = T(0);
 
-  // chunk starts aligned to global multiples of 128
-  int c = ((P0 + align_off) & ~127) - align_off;
-  if (P0 == P1) c = P1;  // only empty rows: no chunk
+  int c = ((P0 + align_off) & ~(CH - 1)) - align_off;
   int ci[4];
   T vv[4];
-  if (c < P1) chunk_load<T>(col, val, c + 4 * lane, nnz, vec_ok, pol_stream, ci, vv);
-  T carry = T(0);
-  while (true) {
+  if (P0 < P1) chunk_load<T>(col, val, c + 4 * lane, nnz, vec_ok, pol_stream, ci, vv);
+  else c = P1;  // only empty rows
+  while (q < R1) {
     const bool have = c < P1;
-    // prefetch the next chunk
+    const int cend = have ? c + CH : INT32_MAX;
     int nci[4];
     T nvv[4];
-    if (c + 128 < P1) chunk_load<T>(col, val, c + 128 + 4 * lane, nnz, vec_ok, pol_stream, nci, nvv);
-    T p[4] = {T(0), T(0), T(0), T(0)};
+    if (c + CH < P1) chunk_load<T>(col, val, c + CH + 4 * lane, nnz, vec_ok, pol_stream, nci, nvv);
     if (have) {
-      // mask elements outside the warp's range [P0, P1)
+      T xv[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int pos = c + 4 * lane + k;
         if (pos < P0 || pos >= P1) ci[k] = -1;
+        xv[k] = ci[k] >= 0 ? ld_keep(x + ci[k], pol_keep) : T(0);
       }
-      T xv[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) xv[k] = ci[k] >= 0 ? ld_keep(x + ci[k], pol_keep) : T(0);
+      T p[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) p[k] = ci[k] >= 0 ? vv[k] * xv[k] : T(0);
-    }
-    const int cend = have ? c + 128 : INT32_MAX;  // after the last chunk every row finishes
-    // head bits of nonempty rows starting in [c, cend); rows beyond the window
-    // are handled by further windows of the same chunk (rare: < 4 nnz/row)
-    unsigned f0 = 0, f1 = 0, f2 = 0, f3 = 0;
-    int wq = q, ws = s, we = e;
-    while (true) {
-      const int rel = ws - c;
-      const bool head = have && ws < we && rel >= 0 && rel < 128;
-      const unsigned bit = head ? (1u << (rel & 31)) : 0u;
-      const int word = rel >> 5;
-      f0 |= __reduce_or_sync(FULL, (head && word == 0) ? bit : 0u);
-      f1 |= __reduce_or_sync(FULL, (head && word == 1) ? bit : 0u);
-      f2 |= __reduce_or_sync(FULL, (head && word == 2) ? bit : 0u);
-      f3 |= __reduce_or_sync(FULL, (head && word == 3) ? bit : 0u);
-      const int last_s = __shfl_sync(FULL, ws, 31);
-      if (wq + 32 >= R1 || last_s >= cend) break;
-      wq += 32;
-      load_window(wq, ws, we);
-    }
-    const int wsel = lane >> 3;
-    const unsigned fw = wsel == 0 ? f0 : (wsel == 1 ? f1 : (wsel == 2 ? f2 : f3));
-    const unsigned my = (fw >> ((4 * lane) & 31)) & 0xFu;
-    if (lane == 0 && !(my & 1u)) p[0] = carry + p[0];
-    T a[4];
-    a[0] = p[0];
+      // overlap of every window row with this chunk decides the reduction
+      const int lo0 = max(s, c), hi0 = min(e, cend);
+      const unsigned ov0 = live && hi0 > lo0 ? (unsigned)(hi0 - lo0) : 0u;
+      const unsigned maxov = __reduce_max_sync(FULL, ov0);
+      if (maxov > LOOP_MAX) {
+        // long rows: flag-segmented scan restarting at the chunk start; afterwards
+        // buf[j] = sum of the row segment ending at position c + j inside the chunk
+        unsigned f0 = 0, f1 = 0, f2 = 0, f3 = 0;
+        {
+          int wq = q, ws = s, we = e;
+          while (true) {
+            const int rel = ws - c;
+            const bool head = wq + lane < R1 && ws < we && rel >= 0 && rel < CH;
+            const unsigned bit = head ? (1u << (rel & 31)) : 0u;
+            const int word = rel >> 5;
+            f0 |= __reduce_or_sync(FULL, (head && word == 0) ? bit : 0u);
+            f1 |= __reduce_or_sync(FULL, (head && word == 1) ? bit : 0u);
+            f2 |= __reduce_or_sync(FULL, (head && word == 2) ? bit : 0u);
+            f3 |= __reduce_or_sync(FULL, (head && word == 3) ? bit : 0u);
+            const int last_s = __shfl_sync(FULL, ws, 31);
+            if (wq + 32 >= R1 || last_s >= cend) break;
+            wq += 32;
+            const int rr = wq + lane;
+            ws = rr < R1 ? row_ptr[rr] : P1;
+            we = rr < R1 ? row_ptr[rr + 1] : P1;
+          }
+        }
+        const int wsel = lane >> 3;
+        const unsigned fw = wsel == 0 ? f0 : (wsel == 1 ? f1 : (wsel == 2 ? f2 : f3));
+        const unsigned my = (fw >> ((4 * lane) & 31)) & 0xFu;
+        T a[4];
+        a[0] = p[0];
 #pragma unroll
-    for (int k = 1; k < 4; ++k) a[k] = ((my >> k) & 1u) ? p[k] : a[k - 1] + p[k];
-    T v = a[3];
-    bool f = my != 0u;
+        for (int k = 1; k < 4; ++k) a[k] = ((my >> k) & 1u) ? p[k] : a[k - 1] + p[k];
+        T v = a[3];
+        bool f = my != 0u;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const T ov = __shfl_up_sync(FULL, v, o);
-      const bool of = __shfl_up_sync(FULL, (int)f, o) != 0;
-      if (lane >= o) {
-        if (!f) v = ov + v;
-        f = f || of;
+        for (int o = 1; o < 32; o <<= 1) {
+          const T ov = __shfl_up_sync(FULL, v, o);
+          const bool of = __shfl_up_sync(FULL, (int)f, o) != 0;
+          if (lane >= o) {
+            if (!f) v = ov + v;
+            f = f || of;
+          }
+        }
+        T ex = __shfl_up_sync(FULL, v, 1);
+        if (lane == 0) ex = T(0);
+        bool open = true;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if ((my >> k) & 1u) open = false;
+          buf[4 * lane + k] = open ? ex + a[k] : a[k];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) buf[4 * lane + k] = p[k];
       }
-    }
-    T ex = __shfl_up_sync(FULL, v, 1);
-    if (lane == 0) ex = T(0);
-    T fin[4];
-    bool open = true;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if ((my >> k) & 1u) open = false;
-      fin[k] = open ? ex + a[k] : a[k];
-    }
-    // rows finishing in this chunk (end <= cend): nonempty ones take fin at end-1
-    wq = q; ws = s; we = e;
-    while (true) {
-      const int r = wq + lane;
-      const bool live = r < R1;
-      const int pe = we - 1 - c;
-      const bool ends_here = live && ws < we && pe >= 0 && pe < 128 && have;
-      const int src = ends_here ? (pe >> 2) : lane;
-      const int slot = pe & 3;
-      const T t0 = __shfl_sync(FULL, fin[0], src), t1 = __shfl_sync(FULL, fin[1], src);
-      const T t2 = __shfl_sync(FULL, fin[2], src), t3 = __shfl_sync(FULL, fin[3], src);
-      if (ends_here) {
-        const T tot = slot == 0 ? t0 : (slot == 1 ? t1 : (slot == 2 ? t2 : t3));
-        y[r] = ACC ? y[r] + tot : tot;
-      } else if (!ACC && live && ws == we && we <= cend) {
-        y[r] = T(0);  // empty row
+      __syncwarp();
+      const bool scanned = maxov > LOOP_MAX;
+      // every window row adds its overlap with the chunk; finished rows retire and
+      // the window refills (several passes when rows are shorter than ~4 nnz)
+      bool counted = false;
+      while (true) {
+        if (!counted && live) {
+          const int lo = max(s, c), hi = min(e, cend);
+          if (hi > lo) {
+            if (scanned) {
+              acc += buf[hi - 1 - c];
+            } else {
+              T t = T(0);
+              for (int k = lo; k < hi; ++k) t += buf[k - c];
+              acc += t;
+            }
+          }
+          counted = true;
+        }
+        const unsigned done = __ballot_sync(FULL, live && e <= cend);
+        const int n_done = __popc(done);  // finished rows form a prefix of the window
+        if (lane < n_done) y[r] = ACC ? y[r] + acc : acc;
+        if (n_done == 0) break;
+        q += n_done;
+        const T acc_n = __shfl_down_sync(FULL, acc, n_done);
+        const int s_n = __shfl_down_sync(FULL, s, n_done), e_n = __shfl_down_sync(FULL, e, n_done);
+        const bool cnt_n = __shfl_down_sync(FULL, (int)counted, n_done) != 0;
+        r = q + lane;
+        live = r < R1;
+        if (lane < 32 - n_done) {
+          acc = acc_n; s = s_n; e = e_n; counted = cnt_n;
+        } else {
+          acc = T(0);
+          s = live ? row_ptr[r] : P1;
+          e = live ? row_ptr[r + 1] : P1;
+          counted = false;
+        }
+        // stop when no uncounted live row reaches into this chunk
+        if (!__any_sync(FULL, live && !counted && s < cend) && !__any_sync(FULL, live && e <= cend)) break;
+        if (q >= R1) break;
       }
-      const unsigned done = __ballot_sync(FULL, live && we <= cend);
+      __syncwarp();
+    } else {
+      // no nonzeros left: the remaining rows of the range are empty
+      const unsigned done = __ballot_sync(FULL, live);
       const int n_done = __popc(done);
-      const int last_e = __shfl_sync(FULL, we, 31);
-      if (n_done < 32 || wq + 32 >= R1 || last_e > cend) {
-        q = wq + n_done;
-        break;
-      }
-      wq += 32;
-      load_window(wq, ws, we);
+      if (live && !ACC) y[r] = T(0);
+      q += n_done;
+      r = q + lane;
+      live = r < R1;
+      s = e = P1;
+      continue;
     }
-    if (q >= R1 || !have) break;
-    load_window(q, s, e);
-    carry = __shfl_sync(FULL, fin[3], 31);
-    c += 128;
+    c += CH;
 #pragma unroll
     for (int k = 0; k < 4; ++k) { ci[k] = nci[k]; vv[k] = nvv[k]; }
   }

@@ -30,7 +30,7 @@ from . import _cuda, _lib
 from ._cuda import ptr, stream
 from .matio import CooMatrix, CsrMatrix
 
-KERNELS = ("stream", "vector", "merge", "exact")
+KERNELS = ("stream", "panel", "vector", "merge", "exact")
 
 
 @dataclass(frozen=True, eq=False)
@@ -142,6 +142,12 @@ def spmv_into(m: CsrMatrix, xd: torch.Tensor, y: torch.Tensor, kernel: str = "ve
     if kernel == "vector":
         _lib.call("sme_spmv_vector", dt, lanes or default_lanes(m), m.n_rows, m.n_cols, ptr(m.d_row_ptr),
                   ptr(m.d_col_idx), ptr(m.d_values), ptr(xd), ptr(y), int(accumulate), stream())
+    elif kernel == "panel":
+        from .panels import panels_of
+
+        if accumulate:
+            raise ValueError("the panel kernel does not accumulate")
+        panels_of(m).spmv_into(xd, y, "stream")
     elif kernel == "stream":
         plan, n_warps = stream_plan(m)
         _lib.call("sme_spmv_stream", dt, m.n_rows, m.n_cols, m.nnz, ptr(m.d_row_ptr), ptr(m.d_col_idx),

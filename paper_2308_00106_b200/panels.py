@@ -1,0 +1,87 @@
+"""Column-panel layout of a CSR matrix for L2-resident x gathers (panel.cu).
+
+For a matrix whose x does not fit in L2 (C4: 400 MB of x against 126 MB of
+L2) random gathers miss to DRAM; splitting the columns into P panels and
+running P accumulating SpMV passes (y = A_0 x_0; y += A_p x_p) keeps each
+pass's x slice resident.  Each panel is an ordinary CsrMatrix sharing one
+col/val buffer, so every SpMV kernel runs on it unchanged.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _cuda, _lib
+from ._cuda import ptr, stream
+from .matio import CsrMatrix
+
+CHUNK = 128  # panel offsets keep the global 128-element chunk alignment
+
+
+def l2_bytes() -> int:
+    dev = _cuda.require_cuda()
+    return int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 126 * 2**20))
+
+
+def auto_panels(m: CsrMatrix, l2_fraction: float = 0.5) -> int:
+    """Smallest P whose x slice fits in `l2_fraction` of L2."""
+    xb = m.n_cols * m.d_values.element_size()
+    return max(1, math.ceil(xb / (l2_bytes() * l2_fraction)))
+
+
+class PanelCsr:
+    """P column panels of a CsrMatrix (bounds b_p = p * n_cols // P)."""
+
+    def __init__(self, m: CsrMatrix, n_panels: int):
+        if n_panels < 1 or n_panels > max(1, m.n_cols):
+            raise ValueError("panel count must lie in [1, n_cols]")
+        dev = m.d_row_ptr.device
+        P, n = int(n_panels), m.n_rows
+        self.n_rows, self.n_cols, self.n_panels = m.n_rows, m.n_cols, P
+        bounds = np.array([p * m.n_cols // P for p in range(P + 1)], dtype=np.int32)
+        self.bounds = torch.from_numpy(bounds).to(dev)
+        self.panel_ptr = torch.empty(P * (n + 1), dtype=torch.int32, device=dev)
+        ws = _cuda.workspace(_lib.query_size("sme_panel_count_workspace_size", n, P))
+        _lib.call("sme_panel_row_ptrs", n, ptr(m.d_row_ptr), ptr(m.d_col_idx), P, ptr(self.bounds),
+                  ptr(self.panel_ptr), ptr(ws), ws.numel(), stream())
+        nnz_p = self.panel_ptr.view(P, n + 1)[:, -1].to(torch.int64).cpu().numpy()
+        offs = np.zeros(P + 1, dtype=np.int64)
+        for p in range(P):
+            offs[p + 1] = offs[p] + -(-int(nnz_p[p]) // CHUNK) * CHUNK
+        total = int(offs[-1])
+        self.col = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        self.val = torch.empty(max(total, 1), dtype=m.dtype, device=dev)
+        d_offs = torch.from_numpy(offs[:P].copy()).to(dev)
+        _lib.call("sme_panel_scatter", _cuda.sme_dtype(m.d_values), n, ptr(m.d_row_ptr), ptr(m.d_col_idx),
+                  ptr(m.d_values), P, ptr(self.bounds), ptr(self.panel_ptr), ptr(d_offs), ptr(self.col),
+                  ptr(self.val), stream())
+        self.panels = []
+        for p in range(P):
+            a, k = int(offs[p]), int(nnz_p[p])
+            rp = self.panel_ptr[p * (n + 1) : (p + 1) * (n + 1)]
+            self.panels.append(CsrMatrix._from_device(n, m.n_cols, rp, self.col[a : a + k], self.val[a : a + k]))
+        self.nnz = int(nnz_p.sum())
+        self.offsets = offs
+
+    def spmv_into(self, xd: torch.Tensor, y: torch.Tensor, kernel: str = "stream") -> None:
+        from .kernels import spmv_into
+
+        for p, a in enumerate(self.panels):
+            spmv_into(a, xd, y, kernel, accumulate=p > 0)
+
+    def algorithmic_extra_bytes(self) -> int:
+        """Bytes the panel passes add to one SpMV: (P-1) y read+write and P-1 more row_ptr arrays."""
+        vb = self.val.element_size()
+        return (self.n_panels - 1) * (2 * self.n_rows * vb + (self.n_rows + 1) * 4)
+
+
+def panels_of(m: CsrMatrix, n_panels: int | None = None) -> PanelCsr:
+    """The cached panel layout of m (built on first use)."""
+    P = n_panels or m._cache.get("n_panels") or auto_panels(m)
+    key = ("panels", P)
+    if key not in m._cache:
+        m._cache[key] = PanelCsr(m, P)
+    return m._cache[key]

@@ -374,3 +374,30 @@ def test_gpu_kernelspecs_plug_into_protocol(dev, golden):
         secs, y = time_kernel(spec.fn, ops, g("x_perm"), 3)
         assert secs > 0
         assert O.relative_error(np.asarray(y), g("y_expected")) <= F64_TOL, spec.kernel_id
+
+
+@pytest.mark.parametrize("n_panels", [1, 2, 3, 7])
+def test_panel_layout_matches_oracle(dev, rng, n_panels):
+    from paper_2308_00106_b200.panels import PanelCsr
+
+    n_rows, n_cols = 3000, 5000
+    lens = rng.integers(0, 60, n_rows)
+    ptr = np.zeros(n_rows + 1, dtype=np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    col = np.concatenate([np.sort(rng.choice(n_cols, L, replace=False)) for L in lens])
+    val = rng.random(col.size) * 2 - 1
+    m = P.CsrMatrix(n_rows, n_cols, ptr, col, val)
+    pc = PanelCsr(m, n_panels)
+    assert pc.nnz == m.nnz
+    b = [p * n_cols // n_panels for p in range(n_panels + 1)]
+    for p, a in enumerate(pc.panels):
+        # each panel is the column slice of every row, columns still ascending
+        rows = O.csr_to_coo_rows(ptr)
+        sel = (col >= b[p]) & (col < b[p + 1])
+        optr, ocol, oval = O.coo_to_csr(n_rows, rows[sel], col[sel], val[sel])
+        assert np.array_equal(a.row_ptr, optr) and np.array_equal(a.col_idx, ocol)
+        assert np.array_equal(bits(a.values), bits(oval))
+    x = rng.random(n_cols)
+    m._cache["n_panels"] = n_panels
+    want = O.spmv_csr(ptr, col, val, x)
+    assert O.relative_error(P.spmv_csr(m, x, "panel"), want) <= F64_TOL

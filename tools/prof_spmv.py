@@ -25,6 +25,7 @@ ap.add_argument("--mode", type=int, default=-1)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--unpermuted", action="store_true")
 ap.add_argument("--time", action="store_true")
+ap.add_argument("--panels", type=int, default=0)
 a = ap.parse_args()
 set_merge_mode(a.mode)
 if a.config == "c4":
@@ -48,6 +49,8 @@ else:
     B = P.permute_csr(A, p_r, p_c)
     xp = P.permute_vector(x, p_c)
     del A
+if a.panels:
+    B._cache["n_panels"] = a.panels
 y = torch.empty(n, dtype=B.dtype, device=dev)
 spmv_into(B, xp, y, a.kernel)
 torch.cuda.synchronize()
@@ -59,4 +62,4 @@ ev[1].record()
 torch.cuda.synchronize()
 ms = ev[0].elapsed_time(ev[1]) / a.iters
 bytes_ = B.nnz * 12 + (n + 1) * 4 + 16 * n
-print(f"{a.config} {a.kernel} mode={a.mode} perm={not a.unpermuted}: {ms:.4f} ms  {bytes_ / ms / 1e6:.1f} GB/s  {2 * B.nnz / ms / 1e6:.1f} GFLOP/s")
+print(f"{a.config} {a.kernel} P={a.panels} mode={a.mode} perm={not a.unpermuted}: {ms:.4f} ms  {bytes_ / ms / 1e6:.1f} GB/s  {2 * B.nnz / ms / 1e6:.1f} GFLOP/s")
