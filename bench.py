@@ -82,7 +82,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=self.file, stderr=subprocess.DEVNULL)
+                 "-lms", "50"], stdout=self.file, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
 
@@ -268,7 +268,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         log(f"[bench] cpu baseline: {cpu}")
         del ptr_h, col_h, val_h, x_h
 
-    def timed(matrix, xv, kernel: str, steps: int, warmup: int, shard=None, chunk=None):
+    def timed(matrix, xv, kernel: str, steps: int, warmup: int, shard=None, chunk=None, preload_s: float = 0.0):
         """Device-timed loop: per-step events on the launching stream + whole-region events."""
         y = torch.empty(matrix.n_rows if shard is None else shard.local.n_rows, dtype=matrix.dtype, device=dev)
 
@@ -278,6 +278,11 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
             else:
                 shard.step(chunk)
 
+        if preload_s > 0:  # keep the GPU loaded so the clock sampler sees the timed region's clocks
+            t_end_pre = time.perf_counter() + preload_s
+            while time.perf_counter() < t_end_pre:
+                step()
+                torch.cuda.synchronize()
         for _ in range(warmup):
             step()
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
@@ -301,18 +306,30 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
             total = float(tt.item())
         return total, per
 
-    kernels_per_step = 2 if args.kernel == "merge" else 1
+    from paper_2308_00106_b200.kernels import auto_kernel
+
+    resolved = auto_kernel(B) if args.kernel == "auto" else args.kernel
+    if resolved == "panel":
+        from paper_2308_00106_b200.panels import panels_of
+
+        kernels_per_step = panels_of(B).n_panels
+    else:
+        kernels_per_step = 2 if resolved == "merge" else 1
     if world == 1:
         # warm the plan outside the timed region (per-matrix metadata, like cuSPARSE's analysis)
         spmv_into(B, xp, torch.empty(n, dtype=B.dtype, device=dev), args.kernel)
         spmv_into(A, x, torch.empty(n, dtype=A.dtype, device=dev), args.kernel)
         clocks = Clocks(torch.cuda.current_device())
         clocks.start()
-        total_ms, per = timed(B, xp, args.kernel, args.steps, args.warmup)
+        total_ms, per = timed(B, xp, args.kernel, args.steps, args.warmup, preload_s=1.0)
         clk = clocks.stop()
         un_total, un_per = timed(A, x, args.kernel, args.steps, args.warmup)
-        other = "vector" if args.kernel == "merge" else "merge"
-        ot_total, _ = timed(B, xp, other, max(3, args.steps // 2), 2)
+        others = {}
+        for other in ("stream", "vector", "merge"):
+            if other != resolved:
+                o_total, _ = timed(B, xp, other, max(3, args.steps // 4), 2)
+                others[other] = round(2 * nnz / (o_total / max(3, args.steps // 4) * 1e-3) / 1e9, 3)
+        ot_total = None
         nnz_total = nnz
         bytes_step = spmv_bytes(n, A.n_cols, nnz, B.d_values.element_size(), 4)
     else:
@@ -325,7 +342,8 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         shard.step(chunk)
         clocks = Clocks(torch.cuda.current_device())
         clocks.start()
-        total_ms, per = timed(shard.local, None, args.kernel, args.steps, args.warmup, shard=shard, chunk=chunk)
+        total_ms, per = timed(shard.local, None, args.kernel, args.steps, args.warmup, shard=shard, chunk=chunk,
+                              preload_s=1.0)
         clk = clocks.stop()
         un_total = ot_total = None
         un_per = None
@@ -336,6 +354,34 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
     gflops = 2 * nnz_total / (ms_per_step * 1e-3) / 1e9
     kern_ms = statistics.mean(per)
     peak, peak_src = measured_peaks()
+    # second ceiling of a randomly-permuted SpMV: one random x gather per nonzero.
+    # Measured live: the device's random 8-byte gather rate with an L2-resident
+    # 64 MB vector (diag.cu) — the best case every panel pass aims for.
+    gather_roof = None
+    if world == 1:
+        from paper_2308_00106_b200 import _lib
+        from paper_2308_00106_b200._cuda import ptr as _ptr, stream as _stream
+
+        gx = torch.rand(64 * 2**20 // 8, dtype=torch.float64, device=dev)
+        gblocks, gper = torch.cuda.get_device_properties(dev).multi_processor_count * 32, 256
+        gout = torch.empty(gblocks * 256, dtype=torch.float64, device=dev)
+        for _ in range(2):
+            _lib.call("sme_diag_gather", _ptr(gx), gx.numel(), gblocks, gper, 1, _ptr(gout), _stream())
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(5):
+            _lib.call("sme_diag_gather", _ptr(gx), gx.numel(), gblocks, gper, 1, _ptr(gout), _stream())
+        g1.record()
+        torch.cuda.synchronize()
+        ceil_gps = gblocks * 256 * gper / (g0.elapsed_time(g1) / 5 * 1e-3)
+        ach_gps = nnz / (kern_ms * 1e-3)
+        gather_roof = {"gathers_per_step": nnz, "achieved_gps": round(ach_gps / 1e9, 2),
+                       "ceiling_gps": round(ceil_gps / 1e9, 2), "unit": "G gathers/s",
+                       "frac": round(ach_gps / ceil_gps, 4),
+                       "ceiling_source": "measured in this run: random 8-B gathers from a 64 MB L2-resident "
+                                         "vector (sme_diag_gather)",
+                       "min_step_ms_at_ceiling": round(nnz / ceil_gps * 1e3, 4)}
+        del gx, gout
     achieved = bytes_step / (kern_ms * 1e-3) / 1e9
 
     # e2e through the public API with pinned host buffers (H2D x + SpMV + D2H y every step)
@@ -385,7 +431,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         "data": "synthetic (device generator, seeded; numpy PCG64 permutations, seed 7)",
         "config": {
             "workload": cfg["workload"],
-            "kernel": args.kernel,
+            "kernel": resolved + (f" ({kernels_per_step} column panels x k_spmv_stream)" if resolved == "panel" else ""),
             "n_rows": n, "nnz": nnz,
             "parallelism": f"row-shard x{world} + NCCL all_gather of x" if world > 1 else "1 GPU",
             "l2": "inputs (13 GB/pass for C4) far exceed the 126 MB L2; no flush needed" if cfg["kind"] == "random_rows"
@@ -398,9 +444,8 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
             "unpermuted_gflops": round(2 * nnz / (un_total / args.steps * 1e-3) / 1e9, 3),
             "ratio": round((un_total / args.steps) / ms_per_step, 4),
         },
-        "other_kernel": None if ot_total is None else {
-            "kernel": "vector" if args.kernel == "merge" else "merge",
-            "gflops": round(2 * nnz / (ot_total / max(3, args.steps // 2) * 1e-3) / 1e9, 3)},
+        "other_kernels_gflops": others if world == 1 else None,
+        "gather_roofline": gather_roof,
         "entropy_bits": {"unpermuted": round(H_before, 6), "permuted": round(H_after, 6), "max": 14.0},
         "permute_ms": round(permute_ms, 2),
         "hist_ms": round(hist_ms, 3),
@@ -409,8 +454,10 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_step,
                      "kernel_ms": round(kern_ms, 5),
-                     "timed": "per-step CUDA events on the launch stream around sme_spmv_"
-                              + args.kernel + (" (+ all_gather)" if world > 1 else "")},
+                     "timed": f"per-step CUDA events on the launch stream around the {kernels_per_step} "
+                              f"launch(es) of one SpMV ({resolved})" + (" + all_gather" if world > 1 else ""),
+                     "note": "achieved = algorithmic bytes (SURVEY.md 8d formula) / kernel time; a randomly "
+                             "permuted SpMV is additionally bounded by the random-gather ceiling (gather_roofline)"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clk,
@@ -430,7 +477,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c4")
-    ap.add_argument("--kernel", choices=["merge", "vector"], default="merge")
+    ap.add_argument("--kernel", choices=["auto", "panel", "stream", "vector", "merge"], default="auto")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

@@ -53,6 +53,13 @@ const char* sme_last_error(void);
 int sme_version(void);
 /* Number of SMs of the current device (grid sizing is done inside; exported for the host). */
 int sme_device_sm_count(void);
+/* out[6]: L2 bytes, max persisting L2 bytes, max access-policy window bytes, SMs,
+ * shared memory per SM, max opt-in shared memory per block. */
+int sme_device_info(int64_t* out);
+/* L2 residency control for the x slice of a column-panel pass: reserve persisting
+ * L2 (device-wide) and set/clear the access-policy window of a stream. */
+int sme_l2_set_persisting(size_t bytes);
+int sme_l2_window(const void* d_ptr, size_t bytes, float hit_ratio, sme_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* Permutations — permute.py                                                 */
@@ -130,6 +137,9 @@ int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz,
 #define SME_SORT_SMEM_MAX 4096
 /* Sum of the lengths of rows longer than SME_SORT_SMEM_MAX -> *d_out (int64). */
 int sme_long_row_nnz(int64_t n_rows, const int32_t* d_row_ptr, int64_t* d_out, sme_stream_t stream);
+
+/* Row-length statistics for kernel selection: out[0] = max row length, out[1] = empty rows. */
+int sme_row_stats(int64_t n_rows, const int32_t* d_row_ptr, int64_t* d_out, sme_stream_t stream);
 
 /* CsrMatrix.__post_init__ checks (matio.py:105-122) on device: OR-s
  * SME_FLAG_ROWPTR / SME_FLAG_RANGE / SME_FLAG_UNSORTED into *d_flag. */

@@ -22,6 +22,12 @@ int sme_synth_laplacian5(int dtype, int64_t g, int32_t* d_row_ptr, int32_t* d_co
 int sme_synth_random_rows(int dtype, int64_t n_rows, int64_t n_cols, int32_t k, uint64_t seed,
                           int32_t* d_row_ptr, int32_t* d_col, void* d_val, sme_stream_t stream);
 
+/* Diagnostic (roofline) microbenchmark: blocks x 256 threads each gather
+ * per_thread (multiple of 8) hash-random elements of x[n] (keep = L2 evict-last)
+ * and write one sum to out[thread]. */
+int sme_diag_gather(const double* d_x, int64_t n, int32_t blocks, int32_t per_thread, int32_t keep,
+                    double* d_out, sme_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,6 +32,9 @@ SIGNATURES: dict[str, list] = {
     "sme_last_error": [],
     "sme_version": [],
     "sme_device_sm_count": [],
+    "sme_device_info": [p],
+    "sme_l2_set_persisting": [sz],
+    "sme_l2_window": [p, sz, C.c_float, p],
     "sme_perm_inverse": [i64, p, p, p, p],
     "sme_permute_vector": [C.c_int, i64, p, p, p, p],
     "sme_gather": [C.c_int, i64, p, p, p, p],
@@ -45,6 +48,7 @@ SIGNATURES: dict[str, list] = {
     "sme_permute_csr": [C.c_int, i64, i64, i64, p, p, p, p, p, p, p, p, p, sz, i64, p, p, p],
     "sme_long_row_nnz": [i64, p, p, p],
     "sme_csr_validate": [i64, i64, i64, p, p, p, p],
+    "sme_row_stats": [i64, p, p, p],
     "sme_csr_expand_rows": [i64, p, p, p],
     "sme_hist2d_csr": [i64, i64, i64, p, p, i32, i32, p, p],
     "sme_hist2d_coo": [i64, i64, i64, p, p, i32, i32, p, p],
@@ -69,6 +73,7 @@ SIGNATURES: dict[str, list] = {
     # sme_synth.h
     "sme_synth_laplacian5": [C.c_int, i64, p, p, p, p],
     "sme_synth_random_rows": [C.c_int, i64, i64, i32, u64, p, p, p, p],
+    "sme_diag_gather": [p, i64, i32, i32, i32, p, p],
 }
 _RESTYPES = {"sme_last_error": C.c_char_p}
 

@@ -116,6 +116,23 @@ __device__ __forceinline__ float ld_stream(const float* p, uint64_t pol) {
   return r;
 }
 
+// read-only loads that allocate in L1 (lines re-read by neighbouring lanes), L2 hint
+__device__ __forceinline__ double ld_l1(const double* p, uint64_t pol) {
+  double r;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_l1(const float* p, uint64_t pol) {
+  float r;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ int ld_l1(const int* p, uint64_t pol) {
+  int r;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
 // gathers of x: read-only path, L2 evict-last so the vector stays resident
 __device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
   double r;

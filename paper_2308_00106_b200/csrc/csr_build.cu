@@ -324,6 +324,24 @@ __global__ void k_long_row_nnz(int64_t n_rows, const int32_t* __restrict__ ptr, 
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
+// out[0] = max row length, out[1] = number of empty rows (out zeroed by the caller)
+__global__ void k_row_stats(int64_t n_rows, const int32_t* __restrict__ ptr, unsigned long long* out) {
+  unsigned long long mx = 0, empty = 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t l = ptr[r + 1] - ptr[r];
+    mx = max(mx, (unsigned long long)l);
+    empty += l == 0;
+  }
+  for (int o = 16; o; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    empty += __shfl_xor_sync(0xffffffffu, empty, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, mx);
+    if (empty) atomicAdd(out + 1, empty);
+  }
+}
+
 __global__ void k_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* __restrict__ ptr,
                                const int32_t* __restrict__ col, int32_t* flag) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -499,6 +517,15 @@ SME_API int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t n
                                 (double*)val_out, L, flag, dup_key, s);
   return launch_sorts<float>(n_rows, row_ptr_out, src, col, (const float*)val, col_map, col_out,
                              (float*)val_out, L, flag, dup_key, s);
+}
+
+SME_API int sme_row_stats(int64_t n_rows, const int32_t* row_ptr, int64_t* out, sme_stream_t stream) {
+  cudaStream_t s = as_stream(stream);
+  SME_CUDA(cudaMemsetAsync(out, 0, 16, s));
+  if (n_rows == 0) return SME_OK;
+  k_row_stats<<<grid_for(n_rows, 256, 4), 256, 0, s>>>(n_rows, row_ptr, (unsigned long long*)out);
+  SME_CHECK_LAUNCH("k_row_stats");
+  return SME_OK;
 }
 
 SME_API int sme_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row_ptr,

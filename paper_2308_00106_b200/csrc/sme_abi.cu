@@ -36,3 +36,43 @@ SME_API const char* sme_last_error(void) { return sme::g_err; }
 SME_API int sme_version(void) { return 1; }
 
 SME_API int sme_device_sm_count(void) { return sme::sm_count(); }
+
+// out[0] = L2 bytes, out[1] = max persisting L2 bytes, out[2] = max access-policy window bytes,
+// out[3] = SM count, out[4] = shared memory per SM, out[5] = max shared memory per block (opt-in)
+SME_API int sme_device_info(int64_t* out) {
+  SME_REQUIRE(out, "null pointer");
+  int dev = 0;
+  SME_CUDA(cudaGetDevice(&dev));
+  int v = 0;
+  SME_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev)); out[0] = v;
+  SME_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev)); out[1] = v;
+  SME_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev)); out[2] = v;
+  SME_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev)); out[3] = v;
+  SME_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev)); out[4] = v;
+  SME_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)); out[5] = v;
+  return SME_OK;
+}
+
+// Reserve `bytes` of L2 for persisting accesses (device-wide limit; 0 releases it).
+SME_API int sme_l2_set_persisting(size_t bytes) {
+  SME_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes));
+  return SME_OK;
+}
+
+// Access-policy window on `stream`: [ptr, ptr + bytes) persists with probability hit_ratio
+// (bytes = 0 clears the window and resets persisting lines to normal).
+SME_API int sme_l2_window(const void* ptr, size_t bytes, float hit_ratio, sme_stream_t stream) {
+  cudaStreamAttrValue attr = {};
+  if (bytes) {
+    attr.accessPolicyWindow.base_ptr = const_cast<void*>(ptr);
+    attr.accessPolicyWindow.num_bytes = bytes;
+    attr.accessPolicyWindow.hitRatio = hit_ratio;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  } else {
+    attr.accessPolicyWindow.num_bytes = 0;
+  }
+  SME_CUDA(cudaStreamSetAttribute(sme::as_stream(stream), cudaStreamAttributeAccessPolicyWindow, &attr));
+  if (!bytes) SME_CUDA(cudaCtxResetPersistingL2Cache());
+  return SME_OK;
+}

@@ -338,7 +338,12 @@ __global__ void __launch_bounds__(256) k_spmv_vector(int64_t n_rows, const int32
     if (r < n_rows) {
       const int32_t a = row_ptr[r], b = row_ptr[r + 1];
       for (int32_t k = a + li; k < b; k += L)
-        s += ld_stream(val + k, pol_stream) * ld_keep(x + ld_stream_i1(col + k, pol_stream), pol_keep);
+        if (L >= 8) {
+          s += ld_stream(val + k, pol_stream) * ld_keep(x + ld_stream_i1(col + k, pol_stream), pol_keep);
+        } else {
+          // narrow groups touch each line several times: let L1 keep it (evict-first in L2)
+          s += ld_l1(val + k, pol_stream) * ld_keep(x + ld_l1(col + k, pol_stream), pol_keep);
+        }
     }
 #pragma unroll
     for (int o = L / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);

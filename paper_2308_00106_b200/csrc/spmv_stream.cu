@@ -104,6 +104,9 @@ __global__ void __launch_bounds__(S_NT) k_spmv_stream(int32_t n_rows, int32_t nn
   int s = live ? row_ptr[r] : P1;
   int e = live ? row_ptr[r + 1] : P1;
   T acc = T(0);
+  // accumulate mode: y of a window row is fetched when the row enters the window,
+  // long before it retires, so the read-modify-write never waits on DRAM
+  T yv = (ACC && live) ? y[r] : T(0);
 
   int c = ((P0 + align_off) & ~(CH - 1)) - align_off;
   int ci[4];
@@ -205,20 +208,23 @@ __global__ void __launch_bounds__(S_NT) k_spmv_stream(int32_t n_rows, int32_t nn
         }
         const unsigned done = __ballot_sync(FULL, live && e <= cend);
         const int n_done = __popc(done);  // finished rows form a prefix of the window
-        if (lane < n_done) y[r] = ACC ? y[r] + acc : acc;
+        if (lane < n_done) y[r] = ACC ? yv + acc : acc;
         if (n_done == 0) break;
         q += n_done;
         const T acc_n = __shfl_down_sync(FULL, acc, n_done);
+        const T yv_n = ACC ? __shfl_down_sync(FULL, yv, n_done) : T(0);
         const int s_n = __shfl_down_sync(FULL, s, n_done), e_n = __shfl_down_sync(FULL, e, n_done);
         const bool cnt_n = __shfl_down_sync(FULL, (int)counted, n_done) != 0;
         r = q + lane;
         live = r < R1;
         if (lane < 32 - n_done) {
           acc = acc_n; s = s_n; e = e_n; counted = cnt_n;
+          if (ACC) yv = yv_n;
         } else {
           acc = T(0);
           s = live ? row_ptr[r] : P1;
           e = live ? row_ptr[r + 1] : P1;
+          if (ACC) yv = live ? y[r] : T(0);
           counted = false;
         }
         // stop when no uncounted live row reaches into this chunk

@@ -26,6 +26,9 @@ ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--unpermuted", action="store_true")
 ap.add_argument("--time", action="store_true")
 ap.add_argument("--panels", type=int, default=0)
+ap.add_argument("--persist", action="store_true")
+ap.add_argument("--inner", default="stream")
+ap.add_argument("--lanes", type=int, default=0)
 a = ap.parse_args()
 set_merge_mode(a.mode)
 if a.config == "c4":
@@ -49,8 +52,17 @@ else:
     B = P.permute_csr(A, p_r, p_c)
     xp = P.permute_vector(x, p_c)
     del A
+if a.lanes:
+    B._cache["lanes"] = a.lanes
 if a.panels:
+    from paper_2308_00106_b200.panels import device_info, panels_of
+
     B._cache["n_panels"] = a.panels
+    pc = panels_of(B)
+    pc.inner = a.inner
+    pc.lanes = a.lanes or None
+    if a.persist:
+        pc.enable_persistence(True)
 y = torch.empty(n, dtype=B.dtype, device=dev)
 spmv_into(B, xp, y, a.kernel)
 torch.cuda.synchronize()
@@ -62,4 +74,4 @@ ev[1].record()
 torch.cuda.synchronize()
 ms = ev[0].elapsed_time(ev[1]) / a.iters
 bytes_ = B.nnz * 12 + (n + 1) * 4 + 16 * n
-print(f"{a.config} {a.kernel} P={a.panels} mode={a.mode} perm={not a.unpermuted}: {ms:.4f} ms  {bytes_ / ms / 1e6:.1f} GB/s  {2 * B.nnz / ms / 1e6:.1f} GFLOP/s")
+print(f"{a.config} {a.kernel} P={a.panels} inner={a.inner} L={a.lanes} persist={a.persist} mode={a.mode} perm={not a.unpermuted}: {ms:.4f} ms  {bytes_ / ms / 1e6:.1f} GB/s  {2 * B.nnz / ms / 1e6:.1f} GFLOP/s")
