@@ -107,6 +107,15 @@ __global__ void __launch_bounds__(S_NT) k_spmv_stream(int32_t n_rows, int32_t nn
   // accumulate mode: y of a window row is fetched when the row enters the window,
   // long before it retires, so the read-modify-write never waits on DRAM
   T yv = (ACC && live) ? y[r] : T(0);
+  // prefetched next window W1: rows q + 32 + lane
+  int s1, e1;
+  T yv1 = T(0);
+  {
+    const int r1 = r + 32;
+    s1 = r1 < R1 ? row_ptr[r1] : P1;
+    e1 = r1 < R1 ? row_ptr[r1 + 1] : P1;
+    if (ACC && r1 < R1) yv1 = y[r1];
+  }
 
   int c = ((P0 + align_off) & ~(CH - 1)) - align_off;
   int ci[4];
@@ -215,17 +224,28 @@ __global__ void __launch_bounds__(S_NT) k_spmv_stream(int32_t n_rows, int32_t nn
         const T yv_n = ACC ? __shfl_down_sync(FULL, yv, n_done) : T(0);
         const int s_n = __shfl_down_sync(FULL, s, n_done), e_n = __shfl_down_sync(FULL, e, n_done);
         const bool cnt_n = __shfl_down_sync(FULL, (int)counted, n_done) != 0;
+        // rotate the prefetched window: lane l reads W1[(l + n) % 32]; W0's new tail
+        // lanes take W1's head, W1 shifts down and loads its new tail (needed ~32 rows
+        // later, so that latency is hidden)
+        const int rot = (lane + n_done) & 31;
+        const int s_w = __shfl_sync(FULL, s1, rot), e_w = __shfl_sync(FULL, e1, rot);
+        const T y_w = ACC ? __shfl_sync(FULL, yv1, rot) : T(0);
         r = q + lane;
         live = r < R1;
         if (lane < 32 - n_done) {
           acc = acc_n; s = s_n; e = e_n; counted = cnt_n;
           if (ACC) yv = yv_n;
+          s1 = s_w; e1 = e_w;
+          if (ACC) yv1 = y_w;
         } else {
           acc = T(0);
-          s = live ? row_ptr[r] : P1;
-          e = live ? row_ptr[r + 1] : P1;
-          if (ACC) yv = live ? y[r] : T(0);
+          s = s_w; e = e_w;
+          if (ACC) yv = y_w;
           counted = false;
+          const int r1 = r + 32;
+          s1 = r1 < R1 ? row_ptr[r1] : P1;
+          e1 = r1 < R1 ? row_ptr[r1 + 1] : P1;
+          if (ACC) yv1 = r1 < R1 ? y[r1] : T(0);
         }
         // stop when no uncounted live row reaches into this chunk
         if (!__any_sync(FULL, live && !counted && s < cend) && !__any_sync(FULL, live && e <= cend)) break;
