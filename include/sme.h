@@ -201,6 +201,9 @@ int sme_spmv_merge(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz,
  * whole matrix) and reduces rows with a flag-segmented warp scan.  No fix-up
  * pass.  plan: (W + 1) int32.  accumulate = 1: y += A x. */
 int sme_spmv_stream_warps(int64_t n_rows, int64_t nnz, int32_t* n_warps);
+/* Chunk-stream source: 0 = 128-bit register loads one chunk ahead (default),
+ * 1 = per-lane cp.async (LDGSTS) shared-memory ring, 3 chunks ahead. */
+int sme_spmv_stream_set_mode(int mode);
 int sme_spmv_stream_plan(int64_t n_rows, int64_t nnz, const int32_t* d_row_ptr, int32_t n_warps,
                          int32_t* d_plan, sme_stream_t stream);
 int sme_spmv_stream(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row_ptr,

@@ -76,7 +76,13 @@ __global__ void k_stream_plan(int32_t n_rows, int32_t nnz, const int32_t* __rest
   }
 }
 
-template <typename T, bool ACC>
+// TMA = true: the chunk stream (col_idx, values) arrives through a per-warp ring of
+// STAGES shared-memory slots filled by cp.async.bulk (L2 evict-first), STAGES
+// chunks ahead, each slot completing on its own mbarrier; TMA = false (unaligned
+// arrays): 128-bit register loads prefetched one chunk ahead.
+constexpr int S_STAGES = 3;
+
+template <typename T, bool ACC, bool TMA>
 __global__ void __launch_bounds__(S_NT) k_spmv_stream(int32_t n_rows, int32_t nnz, const int32_t* __restrict__ row_ptr,
                                                       const int32_t* __restrict__ col, const T* __restrict__ val,
                                                       const T* __restrict__ x, T* __restrict__ y,
@@ -84,11 +90,15 @@ __global__ void __launch_bounds__(S_NT) k_spmv_stream(int32_t n_rows, int32_t nn
                                                       int32_t align_off, bool vec_ok) {
   constexpr int CH = 128;       // chunk = 32 lanes x 4 elements
   constexpr int LOOP_MAX = 24;  // per-lane row loops up to this overlap, else segmented scan
+  constexpr int SST = TMA ? S_STAGES : 1;
   __shared__ T s_buf[S_NT / 32][CH];
+  __shared__ __align__(16) int32_t s_col[S_NT / 32][SST][CH];
+  __shared__ __align__(16) T s_val[S_NT / 32][SST][CH];
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   T* buf = s_buf[wib];
+  const int nnz4 = nnz & ~3;  // bulk-copyable prefix of col/val
   const int warp = (blockIdx.x * S_NT + threadIdx.x) >> 5;
   if (warp >= n_warps) return;
   const uint64_t pol_stream = policy_evict_first();
@@ -118,16 +128,56 @@ __global__ void __launch_bounds__(S_NT) k_spmv_stream(int32_t n_rows, int32_t nn
   }
 
   int c = ((P0 + align_off) & ~(CH - 1)) - align_off;
+  // async copy of this lane's 4-element group of chunk cc into ring slot st
+  // (LDGSTS; the group is copied only when it lies inside [0, nnz4), the rest is
+  // read directly at consume time).  Every call commits one group, possibly empty.
+  auto issue = [&](int st, int cc) {
+    const int e0 = cc + 4 * lane;
+    if (cc < P1 && e0 >= 0 && e0 + 3 < nnz4) {
+      cp_async16(&s_col[wib][st][4 * lane], col + e0, 16, pol_stream);
+      for (int h = 0; h < (int)sizeof(T) / 4; ++h)
+        cp_async16(&s_val[wib][st][4 * lane + 4 / ((int)sizeof(T) / 4) * h], val + e0 + 4 / ((int)sizeof(T) / 4) * h,
+                   16, pol_stream);
+    }
+    cp_async_commit();
+  };
   int ci[4];
   T vv[4];
-  if (P0 < P1) chunk_load<T>(col, val, c + 4 * lane, nnz, vec_ok, pol_stream, ci, vv);
-  else c = P1;  // only empty rows
+  int it = 0;  // chunk counter (ring slot = it % SST)
+  if (TMA) {
+    if (P0 >= P1) c = P1;
+#pragma unroll
+    for (int st = 0; st < SST; ++st) issue(st, c + st * CH);
+  } else {
+    if (P0 < P1) chunk_load<T>(col, val, c + 4 * lane, nnz, vec_ok, pol_stream, ci, vv);
+    else c = P1;  // only empty rows
+  }
   while (q < R1) {
     const bool have = c < P1;
     const int cend = have ? c + CH : INT32_MAX;
     int nci[4];
     T nvv[4];
-    if (c + CH < P1) chunk_load<T>(col, val, c + CH + 4 * lane, nnz, vec_ok, pol_stream, nci, nvv);
+    if (!TMA && c + CH < P1) chunk_load<T>(col, val, c + CH + 4 * lane, nnz, vec_ok, pol_stream, nci, nvv);
+    if (TMA && have) {
+      const int st = it % SST;
+      cp_async_wait<SST - 1>();  // this lane's copies of chunk `it` have landed
+      const int a = max(c, 0), b = nnz4;
+      const int e0 = c + 4 * lane;
+      if (e0 >= a && e0 + 3 < b) {
+        const int4 cc4 = *reinterpret_cast<const int4*>(&s_col[wib][st][4 * lane]);
+        ci[0] = cc4.x; ci[1] = cc4.y; ci[2] = cc4.z; ci[3] = cc4.w;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) vv[k] = s_val[wib][st][4 * lane + k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int pos = e0 + k;
+          // partial groups (array ends) were not copied: read them directly
+          if (pos >= 0 && pos < nnz) { ci[k] = col[pos]; vv[k] = val[pos]; }
+          else { ci[k] = -1; vv[k] = T(0); }
+        }
+      }
+    }
     if (have) {
       T xv[4];
 #pragma unroll
@@ -263,23 +313,38 @@ __global__ void __launch_bounds__(S_NT) k_spmv_stream(int32_t n_rows, int32_t nn
       s = e = P1;
       continue;
     }
-    c += CH;
+    if (TMA) {
+      // this lane is done with its slot: refill it STAGES chunks ahead
+      if (have) {
+        issue(it % SST, c + SST * CH);
+        ++it;
+      }
+    } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) { ci[k] = nci[k]; vv[k] = nvv[k]; }
+      for (int k = 0; k < 4; ++k) { ci[k] = nci[k]; vv[k] = nvv[k]; }
+    }
+    c += CH;
   }
 }
+
+static int stream_ring_mode = 0;  // 0 = register prefetch, 1 = per-lane cp.async ring
 
 template <typename T>
 int launch_stream(int64_t n_rows, int64_t nnz, const int32_t* row_ptr, const int32_t* col, const T* val, const T* x,
                   T* y, const int32_t* plan, int32_t n_warps, int accumulate, int32_t align_off, bool vec,
                   cudaStream_t s) {
   const int grid = (n_warps * 32 + S_NT - 1) / S_NT;
-  if (accumulate)
-    k_spmv_stream<T, true><<<grid, S_NT, 0, s>>>((int32_t)n_rows, (int32_t)nnz, row_ptr, col, val, x, y, plan,
-                                                  n_warps, align_off, vec);
-  else
-    k_spmv_stream<T, false><<<grid, S_NT, 0, s>>>((int32_t)n_rows, (int32_t)nnz, row_ptr, col, val, x, y, plan,
-                                                   n_warps, align_off, vec);
+#define SME_LAUNCH_STREAM(ACC, TMA)                                                                          \
+  k_spmv_stream<T, ACC, TMA><<<grid, S_NT, 0, s>>>((int32_t)n_rows, (int32_t)nnz, row_ptr, col, val, x, y, plan, \
+                                                   n_warps, align_off, vec)
+  // the cp.async ring measured slower than the one-chunk register prefetch on B200
+  // (C4 panel SpMV 7.99 vs 6.36 ms): it is opt-in (sme_spmv_stream_set_mode(1))
+  if (vec && stream_ring_mode == 1) {
+    if (accumulate) SME_LAUNCH_STREAM(true, true); else SME_LAUNCH_STREAM(false, true);
+  } else {
+    if (accumulate) SME_LAUNCH_STREAM(true, false); else SME_LAUNCH_STREAM(false, false);
+  }
+#undef SME_LAUNCH_STREAM
   SME_CHECK_LAUNCH("k_spmv_stream");
   return SME_OK;
 }
@@ -288,15 +353,27 @@ int launch_stream(int64_t n_rows, int64_t nnz, const int32_t* row_ptr, const int
 
 using namespace sme;
 
+SME_API int sme_spmv_stream_set_mode(int mode) {
+  SME_REQUIRE(mode == 0 || mode == 1, "mode must be 0 (register prefetch) or 1 (cp.async ring)");
+  stream_ring_mode = mode;
+  return SME_OK;
+}
+
 SME_API int sme_spmv_stream_warps(int64_t n_rows, int64_t nnz, int32_t* n_warps) {
   SME_REQUIRE(n_warps && n_rows >= 0 && nnz >= 0, "bad arguments");
   // exactly the resident warps of the persistent grid (static ranges need them all
   // running at once), never more than ~1 warp per 32 rows
   int per_sm = 0;
-  SME_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_stream<double, false>, S_NT, 0));
-  int per_sm32 = 0;
-  SME_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm32, k_spmv_stream<double, true>, S_NT, 0));
-  per_sm = std::max(1, std::min(per_sm, per_sm32));
+  per_sm = 1 << 20;
+  auto occ = [&](const void* fn) {
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, S_NT, 0) == cudaSuccess) per_sm = std::min(per_sm, v);
+  };
+  occ((const void*)k_spmv_stream<double, false, true>);
+  occ((const void*)k_spmv_stream<double, true, true>);
+  occ((const void*)k_spmv_stream<double, false, false>);
+  occ((const void*)k_spmv_stream<double, true, false>);
+  per_sm = std::max(1, per_sm);
   int64_t w = (int64_t)sm_count() * per_sm * (S_NT / 32);
   w = std::min<int64_t>(w, std::max<int64_t>(1, (n_rows + 31) / 32));
   *n_warps = (int32_t)w;
