@@ -259,6 +259,23 @@ int sme_maxabs_diff(int dtype, int64_t n, const void* d_got, const void* d_exp, 
                     sme_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
+/* Iterative drivers (C5: power iteration / CG on the permuted matrix)       */
+/* ------------------------------------------------------------------------ */
+
+/* Deterministic BLAS-1 with device-resident scalars (graph-capturable).
+ * scal = [rr, alpha, beta, inv_norm] (4 doubles, device); partial: sme_blas_partials doubles.
+ * sme_dot mode: 0 plain, 1 alpha = scal[0]/dot, 2 beta = dot/scal[0] & scal[0] = dot,
+ * 3 scal[3] = 1/sqrt(dot).  sme_cg_update: x += a p; r -= a Ap; rr' = r.r; b = rr'/rr; p = r + b p. */
+int sme_blas_partials(int64_t* n_partials);
+int sme_dot(int dtype, int64_t n, const void* d_x, const void* d_y, double* d_partial, double* d_out,
+            double* d_scal, int mode, sme_stream_t stream);
+int sme_cg_update(int dtype, int64_t n, void* d_x, void* d_r, void* d_p, const void* d_ap, double* d_scal,
+                  double* d_partial, sme_stream_t stream);
+int sme_scale(int dtype, int64_t n, void* d_y, const void* d_x, const double* d_scal, int idx,
+              sme_stream_t stream);
+int sme_axpby(int dtype, int64_t n, double a, const void* d_x, double b, void* d_y, sme_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
 /* Row sharding (multi-GPU) — kernels.py:38-49 make_row_partition           */
 /* ------------------------------------------------------------------------ */
 

@@ -35,6 +35,8 @@ __all__ = [
     "spmv_csr_parallel",
     "spmv_coo",
     "relative_error",
+    "power_iteration",
+    "conjugate_gradient",
     "make_row_partition",
     "gflops",
     "rowshard_remap_cols",
@@ -284,6 +286,37 @@ def relative_error(got, expected) -> float:
     diff = float(np.max(np.abs(got - expected))) if got.size else 0.0
     scale = float(np.max(np.abs(expected))) if expected.size else 0.0
     return diff / scale if scale > 0 else diff
+
+
+def power_iteration(row_ptr, col, val, x0, steps: int):
+    """Reference-style loop over spmv_csr (the paper's reuse premise; no solver exists in
+    the reference): x <- A x / ||A x||_2; returns (x, ||A x_last||)."""
+    x = np.asarray(x0, dtype=np.float64)
+    x = x / np.sqrt(np.dot(x, x))
+    lam = 0.0
+    for _ in range(steps):
+        y = spmv_csr(row_ptr, col, val, x)
+        lam = float(np.sqrt(np.dot(y, y)))
+        x = y / lam
+    return x, lam
+
+
+def conjugate_gradient(row_ptr, col, val, b, steps: int):
+    """Textbook CG from x0 = 0 over spmv_csr; returns (x, r.r)."""
+    b = np.asarray(b, dtype=np.float64)
+    x = np.zeros_like(b)
+    r = b.copy()
+    p = r.copy()
+    rr = float(np.dot(r, r))
+    for _ in range(steps):
+        ap = spmv_csr(row_ptr, col, val, p)
+        alpha = rr / float(np.dot(p, ap))
+        x += alpha * p
+        r -= alpha * ap
+        rr_new = float(np.dot(r, r))
+        p = r + (rr_new / rr) * p
+        rr = rr_new
+    return x, rr
 
 
 def gflops(nnz: int, seconds_per_call: float) -> float:

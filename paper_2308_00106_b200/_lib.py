@@ -71,6 +71,11 @@ SIGNATURES: dict[str, list] = {
     "sme_spmv_coo": [C.c_int, i64, i64, p, p, p, p, p, p],
     "sme_maxabs_diff": [C.c_int, i64, p, p, p, p],
     "sme_rowshard_remap_cols": [i64, i64, i32, i64, p, p, p],
+    "sme_blas_partials": [pi64],
+    "sme_dot": [C.c_int, i64, p, p, p, p, p, C.c_int, p],
+    "sme_cg_update": [C.c_int, i64, p, p, p, p, p, p, p],
+    "sme_scale": [C.c_int, i64, p, p, p, C.c_int, p],
+    "sme_axpby": [C.c_int, i64, f64, p, f64, p, p],
     # sme_synth.h
     "sme_synth_laplacian5": [C.c_int, i64, p, p, p, p],
     "sme_synth_random_rows": [C.c_int, i64, i64, i32, u64, p, p, p, p],

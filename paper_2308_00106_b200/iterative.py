@@ -1,0 +1,193 @@
+"""Iterative drivers on the permuted matrix (C5).
+
+The paper's premise is that the matrix is reused many times, so the one-time
+permutation cost amortises over iterations.  The
+reference has no solver; its oracle is a numpy loop over spmv_csr.  Here one
+iteration is a fixed launch sequence with every scalar in device memory
+(blas1.cu), so K iterations are captured once in a CUDA graph and replayed.
+
+PermutedOperator keeps the iterate in permuted coordinates:
+    z_k = P_c^-1 x_k   (z[p_c[i]] = x[i], i.e. permute_vector(x, p_c))
+    B z_k = P_r A x_k  (the permuted matrix of permute_csr)
+    z_{k+1} = P_c^-1 (A x_k) = (B z_k)[q],  q = p_r o inverse(p_c)
+so an iteration costs one SpMV on B plus one gather, instead of two vector
+permutations; with a symmetric permutation (p_c = p_r, B = P A P^T) q is the
+identity and no gather is needed (the SPD case CG requires).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _cuda, _lib
+from ._cuda import ptr, stream
+from .kernels import spmv_into
+from .matio import CsrMatrix
+from .permute import Permutation, compose, inverse, permute_csr, permute_vector
+
+
+def _scratch(dev) -> tuple[torch.Tensor, torch.Tensor]:
+    n_part = _lib.query_i64("sme_blas_partials")
+    return (torch.zeros(4, dtype=torch.float64, device=dev),
+            torch.zeros(n_part, dtype=torch.float64, device=dev))
+
+
+class PermutedOperator:
+    """y = A x applied through B = P_r A P_c in permuted coordinates."""
+
+    def __init__(self, A: CsrMatrix, p_r: Permutation | None = None, p_c: Permutation | None = None,
+                 kernel: str = "auto"):
+        if A.n_rows != A.n_cols:
+            raise ValueError("iterative drivers need a square matrix")
+        self.A, self.kernel = A, kernel
+        self.p_r, self.p_c = p_r, p_c
+        self.B = permute_csr(A, p_r, p_c) if (p_r is not None or p_c is not None) else A
+        self.q = None  # gather index mapping B z back into permuted coordinates
+        if p_r is not None or p_c is not None:
+            same = p_r is not None and p_c is not None and p_r == p_c
+            if not same:
+                pr = p_r if p_r is not None else _ident(A.n_rows)
+                pc = p_c if p_c is not None else _ident(A.n_cols)
+                self.q = compose(pr, inverse(pc)).d_forward
+        self.n = A.n_rows
+        self.dtype = A.dtype
+        self.dev = A.d_row_ptr.device
+        self._tmp = torch.empty(self.n, dtype=self.dtype, device=self.dev)
+
+    def to_permuted(self, x) -> torch.Tensor:
+        """z = P_c^-1 x (x in original coordinates)."""
+        xd = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, dtype=np.float64))
+        xd = xd.to(self.dev, self.dtype)
+        return permute_vector(xd, self.p_c) if self.p_c is not None else xd.clone()
+
+    def from_permuted(self, z: torch.Tensor) -> torch.Tensor:
+        """x = P_c z."""
+        if self.p_c is None:
+            return z.clone()
+        out = torch.empty_like(z)
+        _lib.call("sme_gather", _cuda.sme_dtype(z), self.n, ptr(self.p_c.d_forward), ptr(z), ptr(out), stream())
+        return out
+
+    def apply(self, z: torch.Tensor, out: torch.Tensor) -> None:
+        """out = P_c^-1 A P_c z (stream-ordered; no allocation: graph-capturable)."""
+        if self.q is None:
+            spmv_into(self.B, z, out, self.kernel)
+        else:
+            spmv_into(self.B, z, self._tmp, self.kernel)
+            _lib.call("sme_gather", _cuda.sme_dtype(out), self.n, ptr(self.q), ptr(self._tmp), ptr(out), stream())
+
+
+def _ident(n: int) -> Permutation:
+    from .permute import identity_permutation
+
+    return identity_permutation(n)
+
+
+class PowerIteration:
+    """x_{k+1} = A x_k / ||A x_k|| (2-norm); eigenvalue estimate ||A x_k||."""
+
+    def __init__(self, op: PermutedOperator, x0):
+        self.op = op
+        self.z = op.to_permuted(x0)
+        self.y = torch.empty_like(self.z)
+        self.scal, self.partial = _scratch(op.dev)
+        self.norm2 = torch.zeros(1, dtype=torch.float64, device=op.dev)
+        self.graph: torch.cuda.CUDAGraph | None = None
+        self.graph_steps = 0
+        dt = _cuda.sme_dtype(self.z)
+        s = stream()
+        # normalise x0
+        _lib.call("sme_dot", dt, op.n, ptr(self.z), ptr(self.z), ptr(self.partial), ptr(self.norm2), ptr(self.scal), 3, s)
+        _lib.call("sme_scale", dt, op.n, ptr(self.z), ptr(self.z), ptr(self.scal), 3, s)
+
+    def _step(self) -> None:
+        dt = _cuda.sme_dtype(self.z)
+        self.op.apply(self.z, self.y)
+        _lib.call("sme_dot", dt, self.op.n, ptr(self.y), ptr(self.y), ptr(self.partial), ptr(self.norm2),
+                  ptr(self.scal), 3, stream())
+        _lib.call("sme_scale", dt, self.op.n, ptr(self.z), ptr(self.y), ptr(self.scal), 3, stream())
+
+    def capture(self, steps: int) -> None:
+        """Record `steps` iterations into one CUDA graph (after one eager warm-up step)."""
+        self._step()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(steps):
+                self._step()
+        self.graph, self.graph_steps = g, steps
+
+    def run(self, steps: int) -> None:
+        if self.graph is not None and steps % self.graph_steps == 0:
+            for _ in range(steps // self.graph_steps):
+                self.graph.replay()
+        else:
+            for _ in range(steps):
+                self._step()
+
+    @property
+    def eigenvalue(self) -> float:
+        return math.sqrt(float(self.norm2.item()))
+
+    def x(self) -> torch.Tensor:
+        return self.op.from_permuted(self.z)
+
+
+class ConjugateGradient:
+    """CG for SPD A (use a symmetric permutation p_c = p_r so that B = P A P^T is SPD)."""
+
+    def __init__(self, op: PermutedOperator, b, x0=None):
+        if op.q is not None:
+            raise ValueError("CG needs a symmetric permutation (p_c == p_r) so that B stays SPD")
+        self.op = op
+        dev, dt = op.dev, op.dtype
+        self.b = op.to_permuted(b)
+        self.x = torch.zeros_like(self.b) if x0 is None else op.to_permuted(x0)
+        self.r = self.b.clone()
+        if x0 is not None:  # r = b - B x
+            tmp = torch.empty_like(self.b)
+            op.apply(self.x, tmp)
+            _lib.call("sme_axpby", _cuda.sme_dtype(tmp), op.n, -1.0, ptr(tmp), 1.0, ptr(self.r), stream())
+        self.p = self.r.clone()
+        self.ap = torch.empty_like(self.b)
+        self.scal, self.partial = _scratch(dev)
+        self.graph: torch.cuda.CUDAGraph | None = None
+        self.graph_steps = 0
+        _lib.call("sme_dot", _cuda.sme_dtype(self.r), op.n, ptr(self.r), ptr(self.r), ptr(self.partial),
+                  ptr(self.scal), ptr(self.scal), 0, stream())  # scal[0] = r.r
+        del dt
+
+    def _step(self) -> None:
+        dt = _cuda.sme_dtype(self.r)
+        self.op.apply(self.p, self.ap)
+        _lib.call("sme_dot", dt, self.op.n, ptr(self.p), ptr(self.ap), ptr(self.partial), None, ptr(self.scal), 1,
+                  stream())
+        _lib.call("sme_cg_update", dt, self.op.n, ptr(self.x), ptr(self.r), ptr(self.p), ptr(self.ap),
+                  ptr(self.scal), ptr(self.partial), stream())
+
+    def capture(self, steps: int) -> None:
+        self._step()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(steps):
+                self._step()
+        self.graph, self.graph_steps = g, steps
+
+    def run(self, steps: int) -> None:
+        if self.graph is not None and steps % self.graph_steps == 0:
+            for _ in range(steps // self.graph_steps):
+                self.graph.replay()
+        else:
+            for _ in range(steps):
+                self._step()
+
+    @property
+    def residual_norm2(self) -> float:
+        return float(self.scal[0].item())
+
+    def solution(self) -> torch.Tensor:
+        return self.op.from_permuted(self.x)
