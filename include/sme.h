@@ -138,6 +138,20 @@ int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz,
 /* Sum of the lengths of rows longer than SME_SORT_SMEM_MAX -> *d_out (int64). */
 int sme_long_row_nnz(int64_t n_rows, const int32_t* d_row_ptr, int64_t* d_out, sme_stream_t stream);
 
+/* Dedupe variant of sme_coo_to_csr (no maps): duplicate (row, col) pairs stay as
+ * col = -1 holes instead of an error; sme_csr_compact then removes the holes and
+ * keeps at most `cap` entries per row (the smallest columns).  Used to build
+ * graphs from generated edge lists (C3 R-MAT: dedupe + degree cap). */
+int sme_coo_to_csr_dedup(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row,
+                         const int32_t* d_col, const void* d_val, const int32_t* d_row_ptr,
+                         int32_t* d_col_out, void* d_val_out, void* d_ws, size_t ws_bytes, int64_t long_nnz,
+                         int32_t* d_flag, sme_stream_t stream);
+int sme_csr_compact_row_ptr(int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_col, int32_t cap,
+                            int32_t* d_out_row_ptr, void* d_ws, size_t ws_bytes, sme_stream_t stream);
+int sme_csr_compact(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_col, const void* d_val,
+                    int32_t cap, const int32_t* d_out_row_ptr, int32_t* d_out_col, void* d_out_val,
+                    sme_stream_t stream);
+
 /* Row-length statistics for kernel selection: out[0] = max row length, out[1] = empty rows. */
 int sme_row_stats(int64_t n_rows, const int32_t* d_row_ptr, int64_t* d_out, sme_stream_t stream);
 

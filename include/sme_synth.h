@@ -22,6 +22,15 @@ int sme_synth_laplacian5(int dtype, int64_t g, int32_t* d_row_ptr, int32_t* d_co
 int sme_synth_random_rows(int dtype, int64_t n_rows, int64_t n_cols, int32_t k, uint64_t seed,
                           int32_t* d_row_ptr, int32_t* d_col, void* d_val, sme_stream_t stream);
 
+/* R-MAT edges (C3): edge e, level l: u = U[0,1)(hash3(seed, e, l)); quadrant (0,0) if
+ * u < a, (0,1) if u < a+b, (1,0) if u < a+b+c, else (1,1); bits appended MSB first.
+ * Dedupe/cap through sme_coo_to_csr_dedup + sme_csr_compact; values per (row, slot)
+ * by sme_synth_row_values: U[-1,1)(hash3(seed ^ 0x5DEECE66D, row, slot)). */
+int sme_synth_rmat_edges(int64_t n_edges, int32_t scale, double a, double b, double c, uint64_t seed,
+                         int32_t* d_row, int32_t* d_col, sme_stream_t stream);
+int sme_synth_row_values(int dtype, int64_t n_rows, const int32_t* d_row_ptr, uint64_t seed, void* d_val,
+                         sme_stream_t stream);
+
 /* Diagnostic (roofline) microbenchmark: blocks x 256 threads each gather
  * per_thread (multiple of 8) hash-random elements of x[n] (keep = L2 evict-last)
  * and write one sum to out[thread]. */

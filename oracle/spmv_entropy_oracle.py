@@ -43,6 +43,8 @@ __all__ = [
     "laplacian5",
     "random_rows",
     "random_rows_fast",
+    "rmat_edges",
+    "rmat_csr",
     "hash3",
 ]
 
@@ -396,6 +398,41 @@ def random_rows(rows, n_cols: int, k: int, seed: int):
     h = hash3(seed ^ 0x5DEECE66D, rows[:, None].astype(np.uint64), np.arange(k, dtype=np.uint64)[None, :])
     vals = (h >> np.uint64(11)).astype(np.float64) * 2.0**-52 - 1.0
     return cols, vals
+
+
+def rmat_edges(edge_ids, scale: int, a: float, b: float, c: float, seed: int):
+    """synth_rmat.cu k_rmat_edges for the given edge ids."""
+    e = np.asarray(edge_ids, dtype=np.uint64)
+    r = np.zeros(e.size, dtype=np.int64)
+    cc = np.zeros(e.size, dtype=np.int64)
+    ab, abc = a + b, a + b + c
+    for lvl in range(scale):
+        u = (hash3(seed, e, np.uint64(lvl)) >> np.uint64(11)).astype(np.float64) * 2.0**-53
+        rb = (u >= ab).astype(np.int64)
+        cb = (((u >= a) & (u < ab)) | (u >= abc)).astype(np.int64)
+        r = (r << 1) | rb
+        cc = (cc << 1) | cb
+    return r, cc
+
+
+def rmat_csr(scale: int, edge_factor: int, a: float, b: float, c: float, seed: int, cap: int):
+    """Full C3 construction at small scale: edges -> dedupe -> keep the `cap` smallest
+    columns per row -> values U[-1,1) per (row, slot) (synth.rmat)."""
+    n = 1 << scale
+    r, cc = rmat_edges(np.arange(edge_factor * n), scale, a, b, c, seed)
+    key = np.unique(r * n + cc)
+    r, cc = key // n, key % n
+    counts = np.bincount(r, minlength=n)
+    starts = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=starts[1:])
+    slot = np.arange(key.size) - starts[r]
+    keep = slot < cap
+    r, cc, slot = r[keep], cc[keep], slot[keep]
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=n), out=row_ptr[1:])
+    h = hash3(seed ^ 0x5DEECE66D, r.astype(np.uint64), slot.astype(np.uint64))
+    vals = (h >> np.uint64(11)).astype(np.float64) * 2.0**-52 - 1.0
+    return row_ptr, cc, vals
 
 
 def random_rows_fast(rows, n_cols: int, k: int, seed: int):

@@ -80,6 +80,11 @@ SIGNATURES: dict[str, list] = {
     "sme_synth_laplacian5": [C.c_int, i64, p, p, p, p],
     "sme_synth_random_rows": [C.c_int, i64, i64, i32, u64, p, p, p, p],
     "sme_diag_gather": [p, i64, i32, i32, i32, p, p],
+    "sme_synth_rmat_edges": [i64, i32, f64, f64, f64, u64, p, p, p],
+    "sme_synth_row_values": [C.c_int, i64, p, u64, p, p],
+    "sme_coo_to_csr_dedup": [C.c_int, i64, i64, i64, p, p, p, p, p, p, p, sz, i64, p, p],
+    "sme_csr_compact_row_ptr": [i64, p, p, i32, p, p, sz, p],
+    "sme_csr_compact": [C.c_int, i64, p, p, p, i32, p, p, p, p],
 }
 _RESTYPES = {"sme_last_error": C.c_char_p}
 

@@ -34,6 +34,7 @@ struct SortLists {
   unsigned long long* lng_cursor;  // running long scratch offset
   uint64_t* scratch_a;             // long_nnz keys
   uint64_t* scratch_b;             // long_nnz keys
+  int mark_dups;                   // 1: duplicates become col = -1 (dedupe) instead of an error
 };
 
 inline size_t lists_bytes(int64_t n_rows, int64_t long_nnz) {
@@ -50,6 +51,7 @@ inline SortLists carve_lists(char* p, int64_t n_rows, int64_t long_nnz) {
   p += align_up(64);
   L.scratch_a = (uint64_t*)p;    p += align_up(long_nnz * 8);
   L.scratch_b = (uint64_t*)p;
+  L.mark_dups = 0;
   return L;
 }
 
@@ -136,8 +138,9 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_rows_warp(
       if (li < my_len) {
         uint32_t key = (uint32_t)(v >> 32);
         uint32_t idx = (uint32_t)v;
-        if (li > 0 && (uint32_t)(prev >> 32) == key) report_dup((int32_t)(g * 32 + rr), key, flag, dup_key);
-        out_col[my_dst + li] = (int32_t)key;
+        const bool dup = li > 0 && (uint32_t)(prev >> 32) == key;
+        if (dup && !L.mark_dups) report_dup((int32_t)(g * 32 + rr), key, flag, dup_key);
+        out_col[my_dst + li] = (dup && L.mark_dups) ? -1 : (int32_t)key;
         out_val[my_dst + li] = src_val[my_from + idx];
       }
     }
@@ -189,8 +192,9 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_rows_block(
     for (int i = threadIdx.x; i < len; i += SORT_NT) {
       uint64_t v = s[i];
       uint32_t key = (uint32_t)(v >> 32);
-      if (i > 0 && (uint32_t)(s[i - 1] >> 32) == key) report_dup(r, key, flag, dup_key);
-      out_col[dst + i] = (int32_t)key;
+      const bool dup = i > 0 && (uint32_t)(s[i - 1] >> 32) == key;
+      if (dup && !L.mark_dups) report_dup(r, key, flag, dup_key);
+      out_col[dst + i] = (dup && L.mark_dups) ? -1 : (int32_t)key;
       out_val[dst + i] = src_val[from + (uint32_t)v];
     }
     __syncthreads();
@@ -258,8 +262,9 @@ __global__ void __launch_bounds__(LONG_NT) k_sort_rows_long(
     for (int64_t i = threadIdx.x; i < len; i += LONG_NT) {
       uint64_t v = a[i];
       uint32_t key = (uint32_t)(v >> 32);
-      if (i > 0 && (uint32_t)(a[i - 1] >> 32) == key) report_dup(r, key, flag, dup_key);
-      out_col[dst + i] = (int32_t)key;
+      const bool dup = i > 0 && (uint32_t)(a[i - 1] >> 32) == key;
+      if (dup && !L.mark_dups) report_dup(r, key, flag, dup_key);
+      out_col[dst + i] = (dup && L.mark_dups) ? -1 : (int32_t)key;
       out_val[dst + i] = src_val[from + (uint32_t)v];
     }
     __syncthreads();
@@ -460,10 +465,33 @@ SME_API int sme_coo_to_csr_workspace_size(int64_t n_rows, int64_t nnz, int64_t l
   return SME_OK;
 }
 
+static int coo_to_csr_impl(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row,
+                           const int32_t* col, const void* val, const int32_t* row_map, const int32_t* col_map,
+                           const int32_t* row_ptr, int32_t* col_out, void* val_out, void* ws, size_t ws_bytes,
+                           int64_t long_nnz, int32_t* flag, uint64_t* dup_key, sme_stream_t stream, int mark);
+
 SME_API int sme_coo_to_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row,
                            const int32_t* col, const void* val, const int32_t* row_map, const int32_t* col_map,
                            const int32_t* row_ptr, int32_t* col_out, void* val_out, void* ws, size_t ws_bytes,
                            int64_t long_nnz, int32_t* flag, uint64_t* dup_key, sme_stream_t stream) {
+  return coo_to_csr_impl(dtype, n_rows, n_cols, nnz, row, col, val, row_map, col_map, row_ptr, col_out, val_out, ws,
+                         ws_bytes, long_nnz, flag, dup_key, stream, 0);
+}
+
+// Same, but duplicates are kept as col = -1 holes (no error) for sme_csr_compact:
+// the dedupe step of generated graphs (R-MAT edge lists).
+SME_API int sme_coo_to_csr_dedup(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row,
+                                 const int32_t* col, const void* val, const int32_t* row_ptr, int32_t* col_out,
+                                 void* val_out, void* ws, size_t ws_bytes, int64_t long_nnz, int32_t* flag,
+                                 sme_stream_t stream) {
+  return coo_to_csr_impl(dtype, n_rows, n_cols, nnz, row, col, val, nullptr, nullptr, row_ptr, col_out, val_out, ws,
+                         ws_bytes, long_nnz, flag, nullptr, stream, 1);
+}
+
+static int coo_to_csr_impl(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row,
+                           const int32_t* col, const void* val, const int32_t* row_map, const int32_t* col_map,
+                           const int32_t* row_ptr, int32_t* col_out, void* val_out, void* ws, size_t ws_bytes,
+                           int64_t long_nnz, int32_t* flag, uint64_t* dup_key, sme_stream_t stream, int mark) {
   CHECK_SIZES(n_rows, n_cols, nnz);
   SME_REQUIRE(dtype == SME_F64 || dtype == SME_F32, "unknown dtype %d", dtype);
   size_t need = coo_stage_bytes(n_rows, nnz) + lists_bytes(n_rows, long_nnz);
@@ -475,6 +503,7 @@ SME_API int sme_coo_to_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nn
   int32_t* st_col = (int32_t*)p;  p += align_up(nnz * 4);
   void* st_val = p;               p += align_up(nnz * 8);
   SortLists L = carve_lists(p, n_rows, long_nnz);
+  L.mark_dups = mark;
   SME_CUDA(cudaMemsetAsync(L.counters, 0, 64, s));
   SME_CUDA(cudaMemcpyAsync(cursor, row_ptr, n_rows * 4, cudaMemcpyDeviceToDevice, s));
   if (dtype == SME_F64) {
@@ -542,5 +571,58 @@ SME_API int sme_csr_expand_rows(int64_t n_rows, const int32_t* row_ptr, int32_t*
   cudaStream_t s = as_stream(stream);
   k_csr_expand_rows<<<grid_for(n_rows * 32, 256), 256, 0, s>>>(n_rows, row_ptr, row_out);
   SME_CHECK_LAUNCH("k_csr_expand_rows");
+  return SME_OK;
+}
+
+// ---------------------------------------------------------------------------
+// compaction: drop col = -1 holes and keep at most `cap` entries per row (the
+// first ones in column order) — the dedupe + degree cap of generated graphs
+// ---------------------------------------------------------------------------
+namespace sme {
+struct LenCompact {
+  const int32_t* ptr;
+  const int32_t* col;
+  int32_t cap;
+  __device__ __forceinline__ int64_t operator()(int64_t r) const {
+    int32_t n = 0;
+    for (int32_t k = ptr[r]; k < ptr[r + 1] && n < cap; ++k) n += col[k] >= 0;
+    return n;
+  }
+};
+
+template <typename T>
+__global__ void k_csr_compact(int64_t n_rows, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                              const T* __restrict__ val, int32_t cap, const int32_t* __restrict__ out_ptr,
+                              int32_t* __restrict__ out_col, T* __restrict__ out_val) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+    int32_t o = out_ptr[r];
+    const int32_t end = out_ptr[r + 1];
+    for (int32_t k = ptr[r]; k < ptr[r + 1] && o < end; ++k)
+      if (col[k] >= 0) { out_col[o] = col[k]; out_val[o] = val[k]; ++o; }
+  }
+}
+}  // namespace sme
+
+SME_API int sme_csr_compact_row_ptr(int64_t n_rows, const int32_t* row_ptr, const int32_t* col, int32_t cap,
+                                    int32_t* out_row_ptr, void* ws, size_t ws_bytes, sme_stream_t stream) {
+  SME_REQUIRE(cap >= 1, "cap must be >= 1");
+  SME_REQUIRE(ws_bytes >= scan_workspace_bytes(n_rows), "workspace too small");
+  return exclusive_scan_lengths(n_rows, LenCompact{row_ptr, col, cap}, out_row_ptr, ws, nullptr, as_stream(stream));
+}
+
+SME_API int sme_csr_compact(int dtype, int64_t n_rows, const int32_t* row_ptr, const int32_t* col, const void* val,
+                            int32_t cap, const int32_t* out_row_ptr, int32_t* out_col, void* out_val,
+                            sme_stream_t stream) {
+  if (n_rows == 0) return SME_OK;
+  cudaStream_t s = as_stream(stream);
+  if (dtype == SME_F64)
+    k_csr_compact<double><<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, row_ptr, col, (const double*)val, cap,
+                                                               out_row_ptr, out_col, (double*)out_val);
+  else if (dtype == SME_F32)
+    k_csr_compact<float><<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, row_ptr, col, (const float*)val, cap,
+                                                              out_row_ptr, out_col, (float*)out_val);
+  else
+    SME_REQUIRE(false, "unknown dtype %d", dtype);
+  SME_CHECK_LAUNCH("k_csr_compact");
   return SME_OK;
 }
