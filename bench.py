@@ -45,6 +45,9 @@ CONFIGS = {
                workload="C2: 5-point Laplacian 2000^2 (4M rows, 19,992,000 nnz), f64, row+col permuted"),
     "c5": dict(kind="laplacian", g=2828, dtype="f64",
                workload="C5: 5-point Laplacian 2828^2 (7,997,584 rows), f64, row+col permuted"),
+    "c3": dict(kind="rmat", scale=24, ef=16, cap=1024, dtype="f32",
+               workload="C3: R-MAT scale 24 (16,777,216 rows), edge factor 16, (a,b,c)=(0.57,0.19,0.19), deduped, "
+                        "degree cap 1024, f32, row+col permuted"),
 }
 PERM_SEED = 7  # strategy seed 7 for every config
 CPU_SAMPLE_NNZ = 20_000_000
@@ -127,7 +130,23 @@ def build_matrix(cfg: dict):
 
     if cfg["kind"] == "random_rows":
         return synth.random_rows(cfg["n"], cfg["n"], cfg["k"], seed=synth.C4_SEED)
+    if cfg["kind"] == "rmat":
+        return synth.rmat(cfg["scale"], cfg["ef"], cap=cfg["cap"], dtype=np.float32)
     return synth.laplacian5(cfg["g"])
+
+
+def load_balance(row_ptr_dev, n_rows: int, parts: int = 148) -> dict:
+    """Per-SM nnz spread of an even `parts`-way row split (make_row_partition, the
+    reference's static partition, kernels.py:38-49): max/mean of nnz per part."""
+    from paper_2308_00106_b200.kernels import make_row_partition
+
+    b = make_row_partition(n_rows, min(parts, n_rows)).boundaries
+    import torch
+
+    pos = row_ptr_dev[torch.from_numpy(b).to(row_ptr_dev.device)].to(torch.int64).cpu().numpy()
+    per = np.diff(pos)
+    return {"parts": int(per.size), "max_over_mean": round(float(per.max() / max(per.mean(), 1e-9)), 4),
+            "min_over_mean": round(float(per.min() / max(per.mean(), 1e-9)), 4)}
 
 
 def cpu_sample_rows(n_rows: int, nnz: int) -> int:
@@ -176,6 +195,16 @@ def run_reference(args, cfg) -> dict:
         vals = np.take_along_axis(vals, order, axis=1)
         ptr = np.arange(R + 1, dtype=np.int64) * cfg["k"]
         col, val = cols.ravel(), vals.ravel()
+    elif cfg["kind"] == "rmat":
+        # bounded sample: the same construction at scale 20 (1/16 of C3), row+col permuted
+        sc = 20
+        ptr0, col0, val0 = O.rmat_csr(sc, cfg["ef"], 0.57, 0.19, 0.19, 0x5EED_C3, cfg["cap"])
+        val0 = val0.astype(np.float32).astype(np.float64)
+        n = 1 << sc
+        fr, fc = host_perms(n, n)
+        pr, pc = O.permute_coo(O.csr_to_coo_rows(ptr0), col0, fr, fc)
+        ptr, col, val = O.coo_to_csr(n, pr, pc, val0)
+        R = n
     else:
         g = cfg["g"]
         n = g * g
@@ -249,8 +278,10 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
     rel_err = P.relative_error(y_perm, P.permute_vector(y_ref, p_r))
     log(f"[bench] permute {permute_ms:.1f} ms, hist {hist_ms:.2f} ms, H {H_before:.4f} -> {H_after:.4f}, "
         f"round-trip rel err {rel_err:.2e}")
-    if rel_err > 1e-12:
-        raise SystemExit(f"permuted SpMV failed the 1e-12 round-trip check: {rel_err}")
+    tol = 1e-12 if B.dtype == torch.float64 else 1e-5
+    if rel_err > tol:
+        raise SystemExit(f"permuted SpMV failed the {tol} round-trip check: {rel_err}")
+    balance = {"unpermuted": load_balance(A.d_row_ptr, n), "permuted": load_balance(B.d_row_ptr, n)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -447,6 +478,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         "other_kernels_gflops": others if world == 1 else None,
         "gather_roofline": gather_roof,
         "entropy_bits": {"unpermuted": round(H_before, 6), "permuted": round(H_after, 6), "max": 14.0},
+        "load_balance_148_even_rows": balance,
         "permute_ms": round(permute_ms, 2),
         "hist_ms": round(hist_ms, 3),
         "roundtrip_rel_err": rel_err,

@@ -60,17 +60,23 @@ __device__ __forceinline__ void chunk_load(const int32_t* __restrict__ col, cons
   }
 }
 
-// warp_rows[w] = first row of warp w: the first row whose start is >= w * nnz / W
+// warp_rows[w] = first row of warp w: balanced on the cost nnz + 2 * rows (a row
+// costs about two nonzeros of window bookkeeping), so matrices with many empty
+// rows (R-MAT) do not hand one warp millions of rows: the first row r with
+// row_ptr[r] + 2 r >= w * (nnz + 2 n_rows) / W.
+constexpr int64_t S_ROW_COST = 2;
+
 __global__ void k_stream_plan(int32_t n_rows, int32_t nnz, const int32_t* __restrict__ row_ptr, int32_t n_warps,
                               int32_t* __restrict__ warp_rows) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= n_warps; w += gridDim.x * blockDim.x) {
     if (w == 0) { warp_rows[0] = 0; continue; }
     if (w == n_warps) { warp_rows[w] = n_rows; continue; }
-    const int64_t target = (int64_t)w * nnz / n_warps;
-    int lo = 0, hi = n_rows;  // lower_bound over row_ptr[0..n_rows)
+    const int64_t total = (int64_t)nnz + S_ROW_COST * n_rows;
+    const int64_t target = (int64_t)w * total / n_warps;
+    int lo = 0, hi = n_rows;  // lower_bound of the monotone cost row_ptr[r] + 2 r
     while (lo < hi) {
       int mid = (lo + hi) >> 1;
-      if ((int64_t)row_ptr[mid] < target) lo = mid + 1; else hi = mid;
+      if ((int64_t)row_ptr[mid] + S_ROW_COST * mid < target) lo = mid + 1; else hi = mid;
     }
     warp_rows[w] = lo;
   }

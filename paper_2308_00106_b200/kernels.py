@@ -75,14 +75,22 @@ def default_lanes(m: CsrMatrix) -> int:
 
 
 def auto_kernel(m: CsrMatrix) -> str:
-    """'panel' when x exceeds half of L2 (random gathers would miss to DRAM:
-    62 G gathers/s at 400 MB vs 287 G/s L2-resident, tools/gather_roofline.py),
-    else the CSR-vector kernel (partition-invariant, fastest on regular rows)."""
+    """Kernel policy (measured on B200):
+    * 'panel' when x exceeds 60 % of L2 — random gathers would miss to DRAM
+      (62 G gathers/s at 400 MB vs 287 G/s L2-resident, tools/gather_roofline.py);
+    * 'stream' for ragged rows (max row > 8 x mean + 32: C3 R-MAT 405 GFLOP/s vs
+      214 for CSR-vector);
+    * else 'vector' (partition-invariant; fastest on regular rows: C2 0.103 ms)."""
     if "auto" not in m._cache:
         from .panels import l2_bytes
 
         xb = m.n_cols * m.d_values.element_size()
-        m._cache["auto"] = "panel" if xb > l2_bytes() // 2 else "vector"
+        if xb > 0.6 * l2_bytes():
+            m._cache["auto"] = "panel"
+        else:
+            max_len, _ = row_stats(m)
+            mean = m.nnz / max(1, m.n_rows)
+            m._cache["auto"] = "stream" if max_len > 8 * mean + 32 else "vector"
     return m._cache["auto"]
 
 
