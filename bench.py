@@ -368,9 +368,15 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         shard = rowshard.RowShardedSpMV(B, plan, rank, args.kernel)
         c0, c1 = plan.col_range(rank)
         chunk = plan.pad_slice(xp[c0:c1])
+        lo_r, hi_r = plan.row_range(rank)
+        y_ref_slice = y_perm[lo_r:hi_r].clone()
         del A, B
         torch.cuda.empty_cache()
-        shard.step(chunk)
+        # the sharded step (all-gather + local SpMV) must reproduce this rank's rows
+        shard_err = P.relative_error(shard.step(chunk), y_ref_slice)
+        if shard_err > tol:
+            raise SystemExit(f"rank {rank}: sharded SpMV differs from the 1-GPU result: {shard_err}")
+        log(f"[bench] rank {rank}: sharded rows [{lo_r}, {hi_r}) rel err vs 1-GPU {shard_err:.2e}")
         clocks = Clocks(torch.cuda.current_device())
         clocks.start()
         total_ms, per = timed(shard.local, None, args.kernel, args.steps, args.warmup, shard=shard, chunk=chunk,
@@ -437,6 +443,31 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
                "h2d_bytes_per_step": int(x_pin.numel() * x_pin.element_size()),
                "d2h_bytes_per_step": int(yh.numel() * yh.element_size()), "ms_per_step": round(e_ms, 4),
                "api": "paper_2308_00106_b200.spmv_csr(CsrMatrix, pinned host tensor)"}
+    else:
+        # every rank: pinned host x chunk -> device, all-gather + local SpMV, y slice -> host
+        x_pin = torch.empty(plan.pad, dtype=shard.local.dtype, pin_memory=True)
+        x_pin.copy_(chunk.cpu())
+        y_pin = torch.empty(shard.local.n_rows, dtype=shard.local.dtype, pin_memory=True)
+        xc = torch.empty_like(chunk)
+        e_steps = max(3, min(args.steps, 10))
+        dist.barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(e_steps):
+            xc.copy_(x_pin, non_blocking=True)
+            yl = shard.step(xc)
+            y_pin.copy_(yl, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        s1.record()
+        torch.cuda.synchronize()
+        et = torch.tensor([s0.elapsed_time(s1) / e_steps], device=dev)
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e_ms = float(et.item())
+        e2e = {"value": round(2 * nnz_total / (e_ms * 1e-3) / 1e9, 4), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(x_pin.numel() * x_pin.element_size()) * world,
+               "d2h_bytes_per_step": int(nnz and n * y_pin.element_size()), "ms_per_step": round(e_ms, 4),
+               "api": "rowshard.RowShardedSpMV.step (pinned host x chunk in, y slice out, every rank)"}
 
     if rank != 0:
         return None
@@ -464,7 +495,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
             "workload": cfg["workload"],
             "kernel": resolved + (f" ({kernels_per_step} column panels x k_spmv_stream)" if resolved == "panel" else ""),
             "n_rows": n, "nnz": nnz,
-            "parallelism": f"row-shard x{world} + NCCL all_gather of x" if world > 1 else "1 GPU",
+            "parallelism": (f"row-shard x{world} + {dist.get_backend()} all_gather of x" if world > 1 else "1 GPU"),
             "l2": "inputs (13 GB/pass for C4) far exceed the 126 MB L2; no flush needed" if cfg["kind"] == "random_rows"
                   else "x fits L2; matrix streams exceed L2",
         },
@@ -591,11 +622,18 @@ def main() -> None:
 
     import torch
 
-    torch.cuda.set_device(local_rank)
+    # BENCH_SINGLE_DEVICE=1 BENCH_DIST_BACKEND=gloo runs every rank on cuda:0 (a
+    # functional check of the sharded path on a 1-GPU box; NCCL needs one GPU per rank)
+    dev_index = 0 if os.environ.get("BENCH_SINGLE_DEVICE") else local_rank
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(dev_index)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     try:
         if args.iterative:
             if rank == 0:
