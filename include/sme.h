@@ -218,6 +218,8 @@ int sme_spmv_stream_warps(int64_t n_rows, int64_t nnz, int32_t* n_warps);
 /* Chunk-stream source: 0 = 128-bit register loads one chunk ahead (default),
  * 1 = per-lane cp.async (LDGSTS) shared-memory ring, 3 chunks ahead. */
 int sme_spmv_stream_set_mode(int mode);
+/* Plan weight of a row in nonzero units (default 2): warp ranges balance nnz + cost * rows. */
+int sme_spmv_stream_set_row_cost(int cost);
 int sme_spmv_stream_plan(int64_t n_rows, int64_t nnz, const int32_t* d_row_ptr, int32_t n_warps,
                          int32_t* d_plan, sme_stream_t stream);
 int sme_spmv_stream(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row_ptr,

@@ -64,6 +64,7 @@ SIGNATURES: dict[str, list] = {
     "sme_panel_scatter": [C.c_int, i64, p, p, p, i32, p, p, p, p, p, p],
     "sme_spmv_stream_warps": [i64, i64, C.POINTER(C.c_int32)],
     "sme_spmv_stream_set_mode": [C.c_int],
+    "sme_spmv_stream_set_row_cost": [C.c_int],
     "sme_spmv_stream_plan": [i64, i64, p, i32, p, p],
     "sme_spmv_stream": [C.c_int, i64, i64, i64, p, p, p, p, p, p, i32, C.c_int, i32, p],
     "sme_spmv_vector": [C.c_int, C.c_int, i64, i64, p, p, p, p, p, C.c_int, p],

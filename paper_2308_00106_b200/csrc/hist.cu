@@ -91,37 +91,63 @@ __global__ void __launch_bounds__(H_NT) k_hist2d_csr(int64_t n_rows, int64_t nnz
     const int64_t win_len = min((int64_t)H_WIN, min(total_grid, (int64_t)(b_hi + 1) * bc) - win_base);
     for (int64_t i = threadIdx.x; i < win_len; i += H_NT) s_cnt[i] = 0;
     __syncthreads();
-    // groups of 4 consecutive positions, k0 is a multiple of 4
+    // groups of 4 consecutive positions, k0 is a multiple of 4; a thread's groups
+    // are increasing positions, so its row bin only ever advances (no search)
     const int64_t n_groups = (k1 - k0 + 3) >> 2;
-    for (int64_t g0 = 0; g0 < n_groups; g0 += H_NT) {
-      const int64_t g = g0 + threadIdx.x;
+    int32_t rb = b_lo;
+    constexpr int HU = 4;  // groups in flight per thread
+    for (int64_t gb = 0; gb < n_groups; gb += (int64_t)H_NT * HU) {
+      int cu[HU][4];
+#pragma unroll
+      for (int u = 0; u < HU; ++u) {
+        const int64_t g = gb + (int64_t)u * H_NT + threadIdx.x;
+        const int64_t e = k0 + g * 4;
+        if (g < n_groups && vec_ok && e + 3 < k1) {
+          int4 v = ld_stream_i4(reinterpret_cast<const int4*>(col + e), pol);
+          cu[u][0] = v.x; cu[u][1] = v.y; cu[u][2] = v.z; cu[u][3] = v.w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) cu[u][i] = (g < n_groups && e + i < k1) ? col[e + i] : -1;
+        }
+      }
+#pragma unroll 1
+      for (int u = 0; u < HU; ++u) {
+      const int64_t g = gb + (int64_t)u * H_NT + threadIdx.x;
       int64_t fb[4] = {-1, -1, -1, -1};
       if (g < n_groups) {
         const int64_t e = k0 + g * 4;
-        int c[4];
-        if (vec_ok && e + 3 < k1) {
-          int4 v = ld_stream_i4(reinterpret_cast<const int4*>(col + e), pol);
-          c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) c[i] = (e + i < k1) ? col[e + i] : -1;
-        }
-        int32_t rb = rowbin(e);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          if (c[i] < 0) continue;
+          if (cu[u][i] < 0) continue;
           while (rb + 1 < br && edge(rb + 1) <= e + i) ++rb;
-          fb[i] = (int64_t)rb * bc + bin_of(c[i], cb);
+          fb[i] = (int64_t)rb * bc + bin_of(cu[u][i], cb);
         }
       }
       int64_t ob[4];
       int oc[4] = {0, 0, 0, 0};
-      int ns = fold4(fb, ob, oc);
-      int nmax = ns;
+      const int ns = fold4(fb, ob, oc);
+      // banded inputs: the whole warp's group often lands in one bin -> one atomic;
+      // otherwise (random/permuted inputs) plain shared atomics per folded slot
+      const int64_t b0 = __shfl_sync(0xffffffffu, ns > 0 ? ob[0] : -1, 0);
+      const bool uniform = __all_sync(0xffffffffu, ns == 0 || (ns == 1 && ob[0] == b0)) && b0 >= 0;
+      if (uniform) {
+        const unsigned tot = __reduce_add_sync(0xffffffffu, (unsigned)(ns ? oc[0] : 0));
+        if ((threadIdx.x & 31) == 0) {
+          const int64_t off = b0 - win_base;
+          if (off >= 0 && off < win_len) atomicAdd(&s_cnt[off], tot);
+          else atomicAdd(&counts[b0], (unsigned long long)tot);
+        }
+      } else {
 #pragma unroll
-      for (int o = 16; o; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
-      for (int sl = 0; sl < nmax; ++sl)
-        warp_agg_add(sl < ns ? ob[sl] : -1, sl < ns ? oc[sl] : 0, s_cnt, win_base, win_len, counts);
+        for (int sl = 0; sl < 4; ++sl) {
+          if (sl < ns) {
+            const int64_t off = ob[sl] - win_base;
+            if (off >= 0 && off < win_len) atomicAdd(&s_cnt[off], (unsigned)oc[sl]);
+            else atomicAdd(&counts[ob[sl]], (unsigned long long)oc[sl]);
+          }
+        }
+      }
+      }
     }
     __syncthreads();
     for (int64_t i = threadIdx.x; i < win_len; i += H_NT)

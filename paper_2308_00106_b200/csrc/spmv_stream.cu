@@ -64,19 +64,19 @@ __device__ __forceinline__ void chunk_load(const int32_t* __restrict__ col, cons
 // costs about two nonzeros of window bookkeeping), so matrices with many empty
 // rows (R-MAT) do not hand one warp millions of rows: the first row r with
 // row_ptr[r] + 2 r >= w * (nnz + 2 n_rows) / W.
-constexpr int64_t S_ROW_COST = 2;
+static int s_row_cost = 2;  // sme_spmv_stream_set_row_cost
 
 __global__ void k_stream_plan(int32_t n_rows, int32_t nnz, const int32_t* __restrict__ row_ptr, int32_t n_warps,
-                              int32_t* __restrict__ warp_rows) {
+                              int64_t row_cost, int32_t* __restrict__ warp_rows) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= n_warps; w += gridDim.x * blockDim.x) {
     if (w == 0) { warp_rows[0] = 0; continue; }
     if (w == n_warps) { warp_rows[w] = n_rows; continue; }
-    const int64_t total = (int64_t)nnz + S_ROW_COST * n_rows;
+    const int64_t total = (int64_t)nnz + row_cost * n_rows;
     const int64_t target = (int64_t)w * total / n_warps;
-    int lo = 0, hi = n_rows;  // lower_bound of the monotone cost row_ptr[r] + 2 r
+    int lo = 0, hi = n_rows;  // lower_bound of the monotone cost row_ptr[r] + row_cost * r
     while (lo < hi) {
       int mid = (lo + hi) >> 1;
-      if ((int64_t)row_ptr[mid] + S_ROW_COST * mid < target) lo = mid + 1; else hi = mid;
+      if ((int64_t)row_ptr[mid] + row_cost * mid < target) lo = mid + 1; else hi = mid;
     }
     warp_rows[w] = lo;
   }
@@ -359,6 +359,13 @@ int launch_stream(int64_t n_rows, int64_t nnz, const int32_t* row_ptr, const int
 
 using namespace sme;
 
+// Plan weight of one row in nonzero units (warp ranges balance nnz + row_cost * rows).
+SME_API int sme_spmv_stream_set_row_cost(int cost) {
+  SME_REQUIRE(cost >= 0 && cost <= 64, "row cost must lie in [0, 64]");
+  s_row_cost = cost;
+  return SME_OK;
+}
+
 SME_API int sme_spmv_stream_set_mode(int mode) {
   SME_REQUIRE(mode == 0 || mode == 1, "mode must be 0 (register prefetch) or 1 (cp.async ring)");
   stream_ring_mode = mode;
@@ -392,7 +399,7 @@ SME_API int sme_spmv_stream_plan(int64_t n_rows, int64_t nnz, const int32_t* row
   SME_REQUIRE(n_warps >= 1, "n_warps must be >= 1");
   cudaStream_t s = as_stream(stream);
   k_stream_plan<<<grid_for((int64_t)n_warps + 1, 256), 256, 0, s>>>((int32_t)n_rows, (int32_t)nnz, row_ptr, n_warps,
-                                                                     plan);
+                                                                     (int64_t)s_row_cost, plan);
   SME_CHECK_LAUNCH("k_stream_plan");
   return SME_OK;
 }

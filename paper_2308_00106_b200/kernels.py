@@ -224,6 +224,19 @@ def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None 
     if not isinstance(m, CsrMatrix):
         raise TypeError("spmv_csr expects a CsrMatrix of this package (see matio.from_reference)")
     dev = m.d_row_ptr.device
+    if (isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.dtype == m.dtype and x.dim() == 1
+            and x.numel() == m.n_cols and out is None
+            and (auto_kernel(m) if kernel == "auto" else kernel) == "panel"):
+        # host vectors + column panels: x slice p+1 crosses PCIe while pass p runs
+        from .panels import panels_of
+
+        bufs = m._cache.get("host_bufs")
+        if bufs is None:
+            bufs = m._cache["host_bufs"] = (torch.empty(m.n_cols, dtype=m.dtype, device=dev),
+                                            torch.empty(m.n_rows, dtype=m.dtype, device=dev))
+        yh = _pinned((m.n_rows,), m.dtype)
+        panels_of(m).spmv_host(x, yh, bufs[0], bufs[1])
+        return yh
     xd, mode = _x_device(x, m.n_cols, m.dtype, dev)
     y = out if out is not None else torch.empty(m.n_rows, dtype=m.dtype, device=dev)
     spmv_into(m, xd, y, kernel)

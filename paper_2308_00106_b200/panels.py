@@ -95,6 +95,37 @@ class PanelCsr:
         if self.persist:
             _lib.call("sme_l2_window", None, 0, 0.0, stream())
 
+    def spmv_host(self, x_host: torch.Tensor, y_host: torch.Tensor, x_dev: torch.Tensor, y_dev: torch.Tensor,
+                  kernel: str | None = None) -> None:
+        """y_host = A x_host with host (pinned) vectors: the H2D copy of x slice p+1
+        runs on a copy stream while pass p computes (each pass needs only its
+        own slice), then y comes back in one D2H.  Synchronous on return."""
+        from .kernels import spmv_into
+
+        kernel = kernel or self.inner
+        main = torch.cuda.current_stream()
+        cs = self._copy_stream = getattr(self, "_copy_stream", None) or torch.cuda.Stream(device=x_dev.device)
+        cs.wait_stream(main)  # x_dev may still be read by the previous call
+        events = []
+        with torch.cuda.stream(cs):
+            for p in range(self.n_panels):
+                lo, hi = int(self.bounds_host[p]), int(self.bounds_host[p + 1])
+                x_dev[lo:hi].copy_(x_host[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                events.append(ev)
+        vb = x_dev.element_size()
+        for p, a in enumerate(self.panels):
+            main.wait_event(events[p])
+            if self.persist:
+                lo, hi = int(self.bounds_host[p]), int(self.bounds_host[p + 1])
+                _lib.call("sme_l2_window", ptr(x_dev) + lo * vb, (hi - lo) * vb, 1.0, stream())
+            spmv_into(a, x_dev, y_dev, kernel, accumulate=p > 0, lanes=self.lanes)
+        if self.persist:
+            _lib.call("sme_l2_window", None, 0, 0.0, stream())
+        y_host.copy_(y_dev, non_blocking=True)
+        main.synchronize()
+
     def enable_persistence(self, on: bool = True) -> None:
         """Reserve persisting L2 for one x slice (device limit) and pin it per pass."""
         if on:

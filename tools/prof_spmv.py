@@ -29,8 +29,14 @@ ap.add_argument("--panels", type=int, default=0)
 ap.add_argument("--persist", action="store_true")
 ap.add_argument("--inner", default="stream")
 ap.add_argument("--lanes", type=int, default=0)
+ap.add_argument("--row-cost", type=int, default=-1)
+ap.add_argument("--reps", type=int, default=1, help="repeat the timing, print each")
 a = ap.parse_args()
 set_merge_mode(a.mode)
+if a.row_cost >= 0:
+    from paper_2308_00106_b200 import _lib
+
+    _lib.call("sme_spmv_stream_set_row_cost", a.row_cost)
 if a.config == "c4":
     A = synth.random_rows(50_000_000, 50_000_000, 20)
 elif a.config == "c4s":
@@ -66,12 +72,14 @@ if a.panels:
 y = torch.empty(n, dtype=B.dtype, device=dev)
 spmv_into(B, xp, y, a.kernel)
 torch.cuda.synchronize()
-ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-ev[0].record()
-for _ in range(a.iters):
-    spmv_into(B, xp, y, a.kernel)
-ev[1].record()
-torch.cuda.synchronize()
-ms = ev[0].elapsed_time(ev[1]) / a.iters
-bytes_ = B.nnz * 12 + (n + 1) * 4 + 16 * n
-print(f"{a.config} {a.kernel} P={a.panels} inner={a.inner} L={a.lanes} persist={a.persist} mode={a.mode} perm={not a.unpermuted}: {ms:.4f} ms  {bytes_ / ms / 1e6:.1f} GB/s  {2 * B.nnz / ms / 1e6:.1f} GFLOP/s")
+for _rep in range(a.reps):
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(a.iters):
+        spmv_into(B, xp, y, a.kernel)
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / a.iters
+    bytes_ = B.nnz * 12 + (n + 1) * 4 + 16 * n
+    print(f"{a.config} {a.kernel} P={a.panels} inner={a.inner} L={a.lanes} rc={a.row_cost} persist={a.persist} "
+          f"perm={not a.unpermuted}: {ms:.4f} ms  {bytes_ / ms / 1e6:.1f} GB/s  {2 * B.nnz / ms / 1e6:.1f} GFLOP/s")
