@@ -41,13 +41,15 @@ if a.config == "c4":
     A = synth.random_rows(50_000_000, 50_000_000, 20)
 elif a.config == "c4s":
     A = synth.random_rows(10_000_000, 10_000_000, 20)
+elif a.config == "c3":
+    A = synth.rmat(24, 16, cap=1024)
 elif a.config == "c5":
     A = synth.laplacian5(2828)
 else:
     A = synth.laplacian5(2000)
 n = A.n_rows
 dev = torch.device("cuda")
-x = torch.from_numpy(P.input_vector(0, n)).to(dev)
+x = torch.from_numpy(P.input_vector(0, n)).to(dev, A.dtype)
 if a.unpermuted:
     B, xp = A, x
 else:
