@@ -344,6 +344,10 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         from paper_2308_00106_b200.panels import panels_of
 
         kernels_per_step = panels_of(B).n_panels
+    elif resolved == "seg":
+        from paper_2308_00106_b200.seg import seg_of
+
+        kernels_per_step = seg_of(B).n_panels
     else:
         kernels_per_step = 2 if resolved == "merge" else 1
     if world == 1:
@@ -356,7 +360,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         clk = clocks.stop()
         un_total, un_per = timed(A, x, args.kernel, args.steps, args.warmup)
         others = {}
-        for other in ("stream", "vector", "merge"):
+        for other in ("panel", "stream", "vector", "merge"):
             if other != resolved:
                 o_total, _ = timed(B, xp, other, max(3, args.steps // 4), 2)
                 others[other] = round(2 * nnz / (o_total / max(3, args.steps // 4) * 1e-3) / 1e9, 3)
@@ -493,7 +497,8 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         "data": "synthetic (device generator, seeded; numpy PCG64 permutations, seed 7)",
         "config": {
             "workload": cfg["workload"],
-            "kernel": resolved + (f" ({kernels_per_step} column panels x k_spmv_stream)" if resolved == "panel" else ""),
+            "kernel": resolved + (f" ({kernels_per_step} column panels x k_spmv_stream)" if resolved == "panel" else
+                                 f" ({kernels_per_step} column panels x k_spmv_seg)" if resolved == "seg" else ""),
             "n_rows": n, "nnz": nnz,
             "parallelism": (f"row-shard x{world} + {dist.get_backend()} all_gather of x" if world > 1 else "1 GPU"),
             "l2": "inputs (13 GB/pass for C4) far exceed the 126 MB L2; no flush needed" if cfg["kind"] == "random_rows"
@@ -604,7 +609,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c4")
-    ap.add_argument("--kernel", choices=["auto", "panel", "stream", "vector", "merge"], default="auto")
+    ap.add_argument("--kernel", choices=["auto", "seg", "panel", "stream", "vector", "merge"], default="auto")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--iterative", action="store_true",
                     help="C5 mode: 1000-step graphed power iteration with permutation amortisation")

@@ -242,6 +242,35 @@ int sme_panel_scatter(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const
                       const int32_t* d_panel_ptr, const int64_t* d_offsets, int32_t* d_out_col,
                       void* d_out_val, sme_stream_t stream);
 
+/* Segmented-chunk layout (spmv_seg.cu): the fast path for randomly permuted
+ * matrices.  Per column panel p, entries keep CSR order in 32-bit words
+ * (col - bounds[p]) << 9 | (row - hdr[chunk]) with a row header per 128-entry
+ * chunk, so no row_ptr is streamed; a warp sums rows of a chunk with a
+ * key-segmented scan.  Replaces spmv_csr / _accumulate_rows (kernels.py:59-78)
+ * on the column-panel passes (y = A_0 x_0; y += A_p x_p).
+ * Build: sme_seg_positions (padded per-panel entry positions, n_panels x
+ * (n_rows+1) int32; ws sized by sme_seg_workspace_size keeps row counts),
+ * sme_seg_fill (pk/val/hdr at the 128-aligned panel offsets; offsets given on
+ * device and host), sme_seg_plan (per panel: n_warps+1 entry positions on row
+ * boundaries, n_warps from sme_spmv_seg_warps).  Panel width < 2^23 - 1. */
+int sme_seg_workspace_size(int64_t n_rows, int32_t n_panels, size_t* bytes);
+int sme_seg_positions(int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_col, int32_t n_panels,
+                      const int32_t* d_bounds, int32_t* d_pos, void* d_ws, size_t ws_bytes,
+                      sme_stream_t stream);
+int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_col,
+                 const void* d_val, int32_t n_panels, const int32_t* d_bounds, const int32_t* d_pos,
+                 const int64_t* d_offsets, const int64_t* h_offsets, uint32_t* d_pk, void* d_out_val,
+                 int32_t* d_hdr, const void* d_ws, sme_stream_t stream);
+int sme_spmv_seg_warps(int32_t* n_warps);
+/* Kernel variant (process-wide): 0 = per-lane y update (default), 1 = windowed coalesced y,
+ * 2 = TMA-ring stream with pipelined gathers, 3 = bound probe (timing only, not a SpMV). */
+int sme_spmv_seg_set_mode(int mode);
+int sme_seg_plan(int64_t n_rows, const int32_t* d_pos_panel, int32_t n_warps, int32_t* d_plan,
+                 sme_stream_t stream);
+/* y (+)= A_p x_p for one panel: d_xs = x + bounds[p]; accumulate = 0 for panel 0. */
+int sme_spmv_seg(int dtype, int32_t n_warps, const uint32_t* d_pk, const void* d_val, const int32_t* d_hdr,
+                 const int32_t* d_plan, const void* d_xs, void* d_y, int accumulate, sme_stream_t stream);
+
 /* Merge kernel selection (process-wide; tests and experiments): 1 = persistent
  * TMA-pipelined kernel (needs 16-byte aligned row_ptr/col_idx/values), 0 = one
  * CTA per tile with plain global loads, -1 = auto (TMA when aligned). */

@@ -116,6 +116,33 @@ __device__ __forceinline__ float ld_stream(const float* p, uint64_t pol) {
   return r;
 }
 
+// streaming loads without an L2 policy operand (a per-thread policy register costs an
+// R2UR + constant load per access when the compiler cannot keep it uniform)
+__device__ __forceinline__ int4 ld_nc_na_i4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_nc_na_d2(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float4 ld_nc_na_f4(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int ld_nc_na_i1(const int* p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+
 // read-only loads that allocate in L1 (lines re-read by neighbouring lanes), L2 hint
 __device__ __forceinline__ double ld_l1(const double* p, uint64_t pol) {
   double r;

@@ -30,7 +30,7 @@ from . import _cuda, _lib
 from ._cuda import ptr, stream
 from .matio import CooMatrix, CsrMatrix
 
-KERNELS = ("auto", "stream", "panel", "vector", "merge", "exact")
+KERNELS = ("auto", "seg", "stream", "panel", "vector", "merge", "exact")
 
 
 @dataclass(frozen=True, eq=False)
@@ -76,8 +76,10 @@ def default_lanes(m: CsrMatrix) -> int:
 
 def auto_kernel(m: CsrMatrix) -> str:
     """Kernel policy (measured on B200):
-    * 'panel' when x exceeds 60 % of L2 — random gathers would miss to DRAM
-      (62 G gathers/s at 400 MB vs 287 G/s L2-resident, tools/gather_roofline.py);
+    * 'seg' (column panels in the segmented-chunk layout, seg.py) when x exceeds
+      60 % of L2 — random gathers would miss to DRAM (62 G gathers/s at 400 MB vs
+      287 G/s L2-resident, tools/gather_roofline.py); C4: 5.9 ms vs 6.4-7.0 ms for
+      the CSR column panels ('panel');
     * 'stream' for ragged rows (max row > 8 x mean + 32: C3 R-MAT 405 GFLOP/s vs
       214 for CSR-vector);
     * else 'vector' (partition-invariant; fastest on regular rows: C2 0.103 ms)."""
@@ -86,7 +88,7 @@ def auto_kernel(m: CsrMatrix) -> str:
 
         xb = m.n_cols * m.d_values.element_size()
         if xb > 0.6 * l2_bytes():
-            m._cache["auto"] = "panel"
+            m._cache["auto"] = "seg"
         else:
             max_len, _ = row_stats(m)
             mean = m.nnz / max(1, m.n_rows)
@@ -185,11 +187,17 @@ def spmv_into(m: CsrMatrix, xd: torch.Tensor, y: torch.Tensor, kernel: str = "ve
     dt = _cuda.sme_dtype(m.d_values)
     if kernel == "auto":
         kernel = auto_kernel(m)
-        if kernel == "panel" and accumulate:
+        if kernel in ("panel", "seg") and accumulate:
             kernel = "stream"
     if kernel == "vector":
         _lib.call("sme_spmv_vector", dt, lanes or default_lanes(m), m.n_rows, m.n_cols, ptr(m.d_row_ptr),
                   ptr(m.d_col_idx), ptr(m.d_values), ptr(xd), ptr(y), int(accumulate), stream())
+    elif kernel == "seg":
+        from .seg import seg_of
+
+        if accumulate:
+            raise ValueError("the seg kernel does not accumulate")
+        seg_of(m).spmv_into(xd, y)
     elif kernel == "panel":
         from .panels import panels_of
 
@@ -226,16 +234,18 @@ def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None 
     dev = m.d_row_ptr.device
     if (isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.dtype == m.dtype and x.dim() == 1
             and x.numel() == m.n_cols and out is None
-            and (auto_kernel(m) if kernel == "auto" else kernel) == "panel"):
+            and (auto_kernel(m) if kernel == "auto" else kernel) in ("panel", "seg")):
         # host vectors + column panels: x slice p+1 crosses PCIe while pass p runs
         from .panels import panels_of
+        from .seg import seg_of
 
         bufs = m._cache.get("host_bufs")
         if bufs is None:
             bufs = m._cache["host_bufs"] = (torch.empty(m.n_cols, dtype=m.dtype, device=dev),
                                             torch.empty(m.n_rows, dtype=m.dtype, device=dev))
         yh = _pinned((m.n_rows,), m.dtype)
-        panels_of(m).spmv_host(x, yh, bufs[0], bufs[1])
+        lay = seg_of(m) if (auto_kernel(m) if kernel == "auto" else kernel) == "seg" else panels_of(m)
+        lay.spmv_host(x, yh, bufs[0], bufs[1])
         return yh
     xd, mode = _x_device(x, m.n_cols, m.dtype, dev)
     y = out if out is not None else torch.empty(m.n_rows, dtype=m.dtype, device=dev)

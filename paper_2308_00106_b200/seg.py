@@ -1,0 +1,170 @@
+"""Segmented-chunk SpMV layout (spmv_seg.cu): column panels without row_ptr.
+
+The replacement of spmv_csr (kernels.py:59-78) for randomly permuted matrices.
+The columns are split into P panels whose x slices stay L2-resident (see
+panels.py for why); each panel stores its entries in CSR order as 32-bit
+words (column within the panel, row offset within the 128-entry chunk) plus
+one header row per chunk, so a pass streams 4 + sizeof(value) bytes per entry
+and nothing per row.  SpMV = one non-accumulating pass (panel 0, which holds
+an explicit zero for every row it has no entry of) and P-1 accumulating ones.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _cuda, _lib
+from ._cuda import ptr, stream
+from .matio import CsrMatrix
+
+CHUNK = 128
+MAX_PANEL_COLS = (1 << 23) - 2  # 23-bit column field, all-ones reserved for explicit zeros
+
+
+def seg_warps() -> int:
+    w = ctypes.c_int32(0)
+    _lib.call("sme_spmv_seg_warps", ctypes.byref(w))
+    return int(w.value)
+
+
+def auto_seg_panels(m: CsrMatrix, l2_fraction: float = 0.38) -> int:
+    """P: the x slice fits `l2_fraction` of L2 (50 MB slices of the 132.6 MB B200 L2)
+    and every panel is narrower than the 23-bit column field."""
+    from .panels import l2_bytes
+
+    xb = m.n_cols * m.d_values.element_size()
+    p = max(1, math.ceil(xb / (l2_bytes() * l2_fraction)))
+    return max(p, math.ceil(m.n_cols / MAX_PANEL_COLS))
+
+
+class SegLayout:
+    """P column panels of a CsrMatrix in the segmented-chunk layout."""
+
+    def __init__(self, m: CsrMatrix, n_panels: int, n_warps: int | None = None):
+        P, n = int(n_panels), m.n_rows
+        if P < 1 or P > max(1, m.n_cols):
+            raise ValueError("panel count must lie in [1, n_cols]")
+        bounds = np.array([p * m.n_cols // P for p in range(P + 1)], dtype=np.int32)
+        if np.diff(bounds).max(initial=0) > MAX_PANEL_COLS:
+            raise ValueError(f"panels of {int(np.diff(bounds).max())} columns exceed the 23-bit column field; "
+                             f"use at least {math.ceil(m.n_cols / MAX_PANEL_COLS)} panels")
+        dev = m.d_row_ptr.device
+        s = stream()
+        self.n_rows, self.n_cols, self.n_panels, self.dtype = n, m.n_cols, P, m.dtype
+        self.bounds_host = bounds
+        self.bounds = torch.from_numpy(bounds).to(dev)
+        ws = _cuda.workspace(_lib.query_size("sme_seg_workspace_size", n, P))
+        pos = torch.empty(P * (n + 1), dtype=torch.int32, device=dev)
+        _lib.call("sme_seg_positions", n, ptr(m.d_row_ptr), ptr(m.d_col_idx), P, ptr(self.bounds), ptr(pos), ptr(ws),
+                  ws.numel(), s)
+        ent = pos.view(P, n + 1)[:, -1].to(torch.int64).cpu().numpy()
+        offs = np.zeros(P + 1, dtype=np.int64)
+        for p in range(P):
+            offs[p + 1] = offs[p] + -(-int(ent[p]) // CHUNK) * CHUNK
+        total = max(int(offs[-1]), CHUNK)
+        self.entries = ent
+        self.offsets = offs
+        self.pk = torch.full((total,), -1, dtype=torch.int32, device=dev)  # tail padding = explicit zeros
+        self.val = torch.zeros(total, dtype=m.dtype, device=dev)
+        self.hdr = torch.zeros(total // CHUNK, dtype=torch.int32, device=dev)
+        h_offs = (ctypes.c_int64 * P)(*[int(o) for o in offs[:P]])
+        d_offs = torch.from_numpy(offs[:P].copy()).to(dev)
+        _lib.call("sme_seg_fill", _cuda.sme_dtype(m.d_values), n, ptr(m.d_row_ptr), ptr(m.d_col_idx),
+                  ptr(m.d_values), P, ptr(self.bounds), ptr(pos), ptr(d_offs), ctypes.cast(h_offs, ctypes.c_void_p),
+                  ptr(self.pk), ptr(self.val), ptr(self.hdr), ptr(ws), s)
+        self.n_warps = int(n_warps or seg_warps())
+        self.plans = torch.empty(P * (self.n_warps + 1), dtype=torch.int32, device=dev)
+        for p in range(P):
+            _lib.call("sme_seg_plan", n, ptr(pos) + p * (n + 1) * 4, self.n_warps,
+                      ptr(self.plans) + p * (self.n_warps + 1) * 4, s)
+        torch.cuda.current_stream().synchronize()  # pos / ws are freed on return
+        self.nnz = m.nnz
+        self.persist = False
+
+    # -- passes --------------------------------------------------------------
+    def _pass(self, p: int, xd: torch.Tensor, y: torch.Tensor) -> None:
+        vb = self.val.element_size()
+        o = int(self.offsets[p])
+        _lib.call("sme_spmv_seg", _cuda.sme_dtype(self.val), self.n_warps, ptr(self.pk) + 4 * o, ptr(self.val) + vb * o,
+                  ptr(self.hdr) + 4 * (o // CHUNK), ptr(self.plans) + 4 * p * (self.n_warps + 1),
+                  ptr(xd) + vb * int(self.bounds_host[p]), ptr(y), int(p > 0), stream())
+
+    def _window(self, p: int | None, xd: torch.Tensor | None) -> None:
+        if not self.persist:
+            return
+        if p is None:
+            _lib.call("sme_l2_window", None, 0, 0.0, stream())
+            return
+        vb = xd.element_size()
+        lo, hi = int(self.bounds_host[p]), int(self.bounds_host[p + 1])
+        _lib.call("sme_l2_window", ptr(xd) + lo * vb, (hi - lo) * vb, 1.0, stream())
+
+    def spmv_into(self, xd: torch.Tensor, y: torch.Tensor) -> None:
+        """y = A x on device tensors: P stream-ordered launches."""
+        for p in range(self.n_panels):
+            self._window(p, xd)
+            self._pass(p, xd, y)
+        self._window(None, None)
+
+    def spmv_host(self, x_host: torch.Tensor, y_host: torch.Tensor, x_dev: torch.Tensor, y_dev: torch.Tensor) -> None:
+        """y_host = A x_host with pinned host vectors: the H2D copy of x slice p+1 overlaps
+        pass p (each pass reads only its slice); y returns in one D2H.  Synchronous."""
+        main = torch.cuda.current_stream()
+        cs = self._copy_stream = getattr(self, "_copy_stream", None) or torch.cuda.Stream(device=x_dev.device)
+        cs.wait_stream(main)
+        events = []
+        with torch.cuda.stream(cs):
+            for p in range(self.n_panels):
+                lo, hi = int(self.bounds_host[p]), int(self.bounds_host[p + 1])
+                x_dev[lo:hi].copy_(x_host[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                events.append(ev)
+        for p in range(self.n_panels):
+            main.wait_event(events[p])
+            self._window(p, x_dev)
+            self._pass(p, x_dev, y_dev)
+        self._window(None, None)
+        y_host.copy_(y_dev, non_blocking=True)
+        main.synchronize()
+
+    def enable_persistence(self, on: bool = True) -> None:
+        """Reserve persisting L2 for one x slice and pin each pass's slice with an access-policy window."""
+        if on:
+            from .panels import device_info
+
+            info = device_info()
+            slice_bytes = int(max(np.diff(self.bounds_host))) * self.val.element_size()
+            _lib.call("sme_l2_set_persisting", min(info["max_persisting_l2"], slice_bytes))
+        self.persist = on
+
+    # -- accounting ------------------------------------------------------------
+    def stream_bytes(self) -> int:
+        """DRAM bytes one SpMV streams: entries (pk + val), headers, x once, y written
+        once plus (P-1) read+write passes."""
+        vb = self.val.element_size()
+        ent = int(self.entries.sum())
+        return (ent * (4 + vb) + int(self.hdr.numel()) * 4 + self.n_cols * vb
+                + self.n_rows * vb * (2 * self.n_panels - 1))
+
+    def launches(self) -> int:
+        return self.n_panels
+
+
+def seg_of(m: CsrMatrix, n_panels: int | None = None) -> SegLayout:
+    """The cached segmented-chunk layout of m (built on first use)."""
+    P = n_panels or m._cache.get("seg_panels") or auto_seg_panels(m)
+    key = ("seg", P)
+    if key not in m._cache:
+        lay = SegLayout(m, P)
+        from .panels import device_info
+
+        slice_bytes = int(max(np.diff(lay.bounds_host))) * m.d_values.element_size()
+        if P > 1 and slice_bytes <= device_info()["max_persisting_l2"]:
+            lay.enable_persistence(True)
+        m._cache[key] = lay
+    return m._cache[key]

@@ -26,6 +26,9 @@ ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--unpermuted", action="store_true")
 ap.add_argument("--time", action="store_true")
 ap.add_argument("--panels", type=int, default=0)
+ap.add_argument("--seg-panels", type=int, default=0)
+ap.add_argument("--seg-mode", type=int, default=-1)
+ap.add_argument("--check", action="store_true", help="compare with the stream kernel")
 ap.add_argument("--persist", action="store_true")
 ap.add_argument("--inner", default="stream")
 ap.add_argument("--lanes", type=int, default=0)
@@ -71,9 +74,21 @@ if a.panels:
     pc.lanes = a.lanes or None
     if a.persist:
         pc.enable_persistence(True)
+if a.seg_panels:
+    B._cache["seg_panels"] = a.seg_panels
+if a.seg_mode >= 0:
+    from paper_2308_00106_b200 import _lib
+
+    _lib.call("sme_spmv_seg_set_mode", a.seg_mode)
 y = torch.empty(n, dtype=B.dtype, device=dev)
+t_setup = time.perf_counter()
 spmv_into(B, xp, y, a.kernel)
 torch.cuda.synchronize()
+print(f"first call (incl. layout build) {time.perf_counter() - t_setup:.3f} s", flush=True)
+if a.check:
+    y2 = torch.empty(n, dtype=B.dtype, device=dev)
+    spmv_into(B, xp, y2, "stream")
+    print(f"rel err vs stream kernel: {P.relative_error(y, y2):.3e}", flush=True)
 for _rep in range(a.reps):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ev[0].record()
@@ -83,5 +98,5 @@ for _rep in range(a.reps):
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1]) / a.iters
     bytes_ = B.nnz * 12 + (n + 1) * 4 + 16 * n
-    print(f"{a.config} {a.kernel} P={a.panels} inner={a.inner} L={a.lanes} rc={a.row_cost} persist={a.persist} "
+    print(f"{a.config} {a.kernel} segmode={a.seg_mode} P={a.panels or a.seg_panels} inner={a.inner} L={a.lanes} rc={a.row_cost} persist={a.persist} "
           f"perm={not a.unpermuted}: {ms:.4f} ms  {bytes_ / ms / 1e6:.1f} GB/s  {2 * B.nnz / ms / 1e6:.1f} GFLOP/s")
