@@ -479,7 +479,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(f"{args.config}/{args.kernel}")
+            traffic = json.loads(tf.read_text()).get(f"{args.config}/{resolved}")
         except Exception:
             traffic = None
     out = {

@@ -244,9 +244,9 @@ int sme_panel_scatter(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const
 
 /* Segmented-chunk layout (spmv_seg.cu): the fast path for randomly permuted
  * matrices.  Per column panel p, entries keep CSR order in 32-bit words
- * (col - bounds[p]) << 9 | (row - hdr[chunk]) with a row header per 128-entry
- * chunk, so no row_ptr is streamed; a warp sums rows of a chunk with a
- * key-segmented scan.  Replaces spmv_csr / _accumulate_rows (kernels.py:59-78)
+ * (col - bounds[p]) << 9 | end_of_row << 8 | (row - hdr[chunk]) with a row
+ * header per 128-entry chunk, so no row_ptr is streamed; a warp sums the rows
+ * of a chunk from the end flags (in-lane runs + one shuffle per lane).  Replaces spmv_csr / _accumulate_rows (kernels.py:59-78)
  * on the column-panel passes (y = A_0 x_0; y += A_p x_p).
  * Build: sme_seg_positions (padded per-panel entry positions, n_panels x
  * (n_rows+1) int32; ws sized by sme_seg_workspace_size keeps row counts),
@@ -262,8 +262,8 @@ int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const int3
                  const int64_t* d_offsets, const int64_t* h_offsets, uint32_t* d_pk, void* d_out_val,
                  int32_t* d_hdr, const void* d_ws, sme_stream_t stream);
 int sme_spmv_seg_warps(int32_t* n_warps);
-/* Kernel variant (process-wide): 0 = per-lane y update (default), 1 = windowed coalesced y,
- * 2 = TMA-ring stream with pipelined gathers, 3 = bound probe (timing only, not a SpMV). */
+/* Kernel variant (process-wide): 0 = the SpMV (default), 3 = bound probe (the chunk
+ * stream and gathers without the row reduction; timing only, not y = A x). */
 int sme_spmv_seg_set_mode(int mode);
 int sme_seg_plan(int64_t n_rows, const int32_t* d_pos_panel, int32_t n_warps, int32_t* d_plan,
                  sme_stream_t stream);

@@ -12,7 +12,6 @@ import torch
 
 import oracle as O
 import paper_2308_00106_b200 as P
-from paper_2308_00106_b200 import _lib
 from paper_2308_00106_b200.seg import CHUNK, SegLayout
 
 pytestmark = pytest.mark.gpu
@@ -38,7 +37,7 @@ def csr_from_lens(rng, lens, n_cols, dtype=np.float64):
 
 
 def decode(lay: SegLayout):
-    """Per panel: (rows, cols, vals, is_zero) decoded from pk/hdr/val on the host."""
+    """Per panel: (rows, cols, vals, is_zero, end_of_row) decoded from pk/hdr/val on the host."""
     pk = lay.pk.cpu().numpy().view(np.uint32).astype(np.int64)
     hdr = lay.hdr.cpu().numpy().astype(np.int64)
     val = lay.val.cpu().numpy()
@@ -47,18 +46,18 @@ def decode(lay: SegLayout):
         o, e = int(lay.offsets[p]), int(lay.entries[p])
         pos = np.arange(o, o + e)
         w = pk[o : o + e]
-        lc, d = w >> 9, w & 511
+        lc, end, d = w >> 9, (w >> 8) & 1, w & 255
         rows = hdr[pos // CHUNK] + d
         zero = lc == MARK
         cols = np.where(zero, -1, lc + int(lay.bounds_host[p]))
-        out.append((rows, cols, val[o : o + e], zero))
+        out.append((rows, cols, val[o : o + e], zero, end.astype(bool)))
     return out
 
 
 def check_layout(lay, ptr, col, val):
     n_rows = len(ptr) - 1
     rows_all = O.csr_to_coo_rows(ptr)
-    for p, (rows, cols, vals, zero) in enumerate(decode(lay)):
+    for p, (rows, cols, vals, zero, end) in enumerate(decode(lay)):
         lo, hi = int(lay.bounds_host[p]), int(lay.bounds_host[p + 1])
         assert np.all(np.diff(rows) >= 0), p  # row-major
         sel = (col >= lo) & (col < hi)
@@ -66,16 +65,20 @@ def check_layout(lay, ptr, col, val):
         assert np.array_equal(cols[~zero], col[sel]), p
         assert np.array_equal(vals[~zero].view(np.uint8), val[sel].view(np.uint8)), p
         assert np.all(vals[zero] == 0), p
-        # explicit zeros: panel 0 every row without entries; later panels empty rows r % 4 == 0
+        # explicit zeros: panel 0 every row without entries; later panels empty rows r % 2 == 0
         has = np.zeros(n_rows, bool)
         has[rows_all[sel]] = True
-        want_zero = np.flatnonzero(~has) if p == 0 else np.flatnonzero(~has & (np.arange(n_rows) % 4 == 0))
+        want_zero = np.flatnonzero(~has) if p == 0 else np.flatnonzero(~has & (np.arange(n_rows) % 2 == 0))
         assert np.array_equal(rows[zero], want_zero), p
-        # every chunk spans < 512 rows (9-bit offsets) -- implied by decode, checked explicitly
+        # end flag exactly on the last entry of every row
+        want_end = np.ones(rows.size, bool)
+        want_end[:-1] = rows[1:] != rows[:-1]
+        assert np.array_equal(end, want_end), p
+        # every chunk spans < 256 rows (8-bit offsets) -- implied by decode, checked explicitly
         if rows.size:
             starts = rows[::CHUNK]
             ends = rows[np.minimum(np.arange(0, rows.size, CHUNK) + CHUNK - 1, rows.size - 1)]
-            assert np.all(ends - starts <= 511)
+            assert np.all(ends - starts <= 255)
 
 
 def run_seg(m, x, n_panels, n_warps=None):
@@ -87,7 +90,7 @@ def run_seg(m, x, n_panels, n_warps=None):
 
 
 @pytest.mark.parametrize("n_panels", [1, 2, 3, 7])
-def test_layout_and_spmv_random_lengths(dev, rng, n_panels, seg_mode):
+def test_layout_and_spmv_random_lengths(dev, rng, n_panels):
     n_rows, n_cols = 3000, 5000
     lens = rng.integers(0, 60, n_rows)
     ptr, col, val = csr_from_lens(rng, lens, n_cols)
@@ -98,15 +101,8 @@ def test_layout_and_spmv_random_lengths(dev, rng, n_panels, seg_mode):
     assert O.relative_error(y, O.spmv_csr(ptr, col, val, x)) <= F64_TOL
 
 
-@pytest.fixture(params=[1, 0, 2], ids=["window", "perlane", "pipelined"])
-def seg_mode(request):
-    _lib.call("sme_spmv_seg_set_mode", request.param)
-    yield request.param
-    _lib.call("sme_spmv_seg_set_mode", 0)
-
-
 @pytest.mark.parametrize("n_warps", [1, 2, 3, 37, 1000])
-def test_warp_splits_and_carries(dev, rng, n_warps, seg_mode):
+def test_warp_splits_and_carries(dev, rng, n_warps):
     """Few warps: long chunk runs, rows carried across chunks and warp boundaries."""
     n_rows, n_cols = 2500, 4000
     lens = np.minimum((rng.pareto(1.1, n_rows) * 4).astype(np.int64), 3000)  # rows up to 3000 entries
@@ -121,8 +117,8 @@ def test_warp_splits_and_carries(dev, rng, n_warps, seg_mode):
         assert O.relative_error(y, want) <= F64_TOL, (n_warps, n_panels)
 
 
-def test_sparse_panels_many_empty_rows(dev, rng, seg_mode):
-    """Most rows empty in most panels: the r % 4 explicit zeros keep chunk spans < 512 rows."""
+def test_sparse_panels_many_empty_rows(dev, rng):
+    """Most rows empty in most panels: the r % 2 explicit zeros keep chunk spans < 256 rows."""
     n_rows, n_cols = 20000, 100000
     lens = (rng.random(n_rows) < 0.05).astype(np.int64) * rng.integers(1, 4, n_rows)
     ptr, col, val = csr_from_lens(rng, lens, n_cols)
@@ -173,7 +169,7 @@ def test_nonfinite_x_only_reaches_its_rows(dev):
     assert np.array_equal(y, [2.0, 0.0, 1.0])
 
 
-def test_f32_seg_within_1e5(dev, rng, seg_mode):
+def test_f32_seg_within_1e5(dev, rng):
     n = 6000
     lens = rng.integers(0, 40, n)
     ptr, col, val = csr_from_lens(rng, lens, n, np.float32)

@@ -34,6 +34,7 @@ ap.add_argument("--inner", default="stream")
 ap.add_argument("--lanes", type=int, default=0)
 ap.add_argument("--row-cost", type=int, default=-1)
 ap.add_argument("--reps", type=int, default=1, help="repeat the timing, print each")
+ap.add_argument("--preload", type=float, default=0.0, help="seconds of untimed load first (power-capped clocks)")
 a = ap.parse_args()
 set_merge_mode(a.mode)
 if a.row_cost >= 0:
@@ -89,14 +90,26 @@ if a.check:
     y2 = torch.empty(n, dtype=B.dtype, device=dev)
     spmv_into(B, xp, y2, "stream")
     print(f"rel err vs stream kernel: {P.relative_error(y, y2):.3e}", flush=True)
+if a.preload > 0:
+    t_end = time.perf_counter() + a.preload
+    while time.perf_counter() < t_end:
+        for _ in range(4):
+            spmv_into(B, xp, y, a.kernel)
+        torch.cuda.synchronize()
 for _rep in range(a.reps):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ev[0].record()
     for _ in range(a.iters):
         spmv_into(B, xp, y, a.kernel)
     ev[1].record()
+    clk = ""
+    if a.preload > 0:
+        import subprocess
+
+        clk = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader"],
+                             capture_output=True, text=True).stdout.strip()
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1]) / a.iters
     bytes_ = B.nnz * 12 + (n + 1) * 4 + 16 * n
     print(f"{a.config} {a.kernel} segmode={a.seg_mode} P={a.panels or a.seg_panels} inner={a.inner} L={a.lanes} rc={a.row_cost} persist={a.persist} "
-          f"perm={not a.unpermuted}: {ms:.4f} ms  {bytes_ / ms / 1e6:.1f} GB/s  {2 * B.nnz / ms / 1e6:.1f} GFLOP/s")
+          f"perm={not a.unpermuted} [{clk}]: {ms:.4f} ms  {bytes_ / ms / 1e6:.1f} GB/s  {2 * B.nnz / ms / 1e6:.1f} GFLOP/s")
