@@ -253,6 +253,89 @@ def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None 
     return _y_out(y, mode)
 
 
+def spmv_csr_pipelined(m: CsrMatrix, xs, ys=None, kernel: str = "auto") -> list:
+    """y_k = A x_k for a sequence of host vectors, with the PCIe copies of neighbouring
+    steps overlapped: step k+1's x crosses host->device while step k computes and step
+    k-1's y crosses device->host (H2D and D2H use separate copy engines).  Every step
+    still copies its full x in and its full y out; with column panels ('seg'/'panel')
+    pass p of a step starts as soon as its x slice has landed.  Same results as calling
+    spmv_csr(m, x_k) for each k (kernels.py:73-78 per vector).
+
+    xs: CPU tensors (pinned for asynchronous copies) of length n_cols and the matrix's
+    dtype; ys: optional CPU output tensors (pinned); returns the list of outputs."""
+    if not isinstance(m, CsrMatrix):
+        raise TypeError("spmv_csr_pipelined expects a CsrMatrix of this package")
+    xs = list(xs)
+    for x in xs:
+        if not isinstance(x, torch.Tensor) or x.is_cuda or x.dim() != 1 or x.numel() != m.n_cols:
+            raise ValueError(f"inputs must be 1-D host tensors of length n_cols {m.n_cols}")
+    dev = m.d_row_ptr.device
+    if ys is None:
+        ys = [torch.empty(m.n_rows, dtype=m.dtype, pin_memory=True) for _ in xs]
+    ys = list(ys)
+    if len(ys) != len(xs):
+        raise ValueError("need one output per input vector")
+    kern = auto_kernel(m) if kernel == "auto" else kernel
+    lay = None
+    if kern == "seg":
+        from .seg import seg_of
+
+        lay = seg_of(m)
+    elif kern == "panel":
+        from .panels import panels_of
+
+        lay = panels_of(m)
+    bounds = lay.bounds_host if lay is not None else np.array([0, m.n_cols])
+    P = len(bounds) - 1
+    main = torch.cuda.current_stream()
+    h2d = torch.cuda.Stream(device=dev)
+    d2h = torch.cuda.Stream(device=dev)
+    xb = [torch.empty(m.n_cols, dtype=m.dtype, device=dev) for _ in range(2)]
+    yb = [torch.empty(m.n_rows, dtype=m.dtype, device=dev) for _ in range(2)]
+    computed = [None, None]  # event: step using buffer b finished computing
+    copied_out = [None, None]  # event: y buffer b has been copied to the host
+    h2d.wait_stream(main)
+    d2h.wait_stream(main)
+    for k, x in enumerate(xs):
+        b = k & 1
+        xk = x.to(m.dtype) if x.dtype != m.dtype else x
+        slice_ev = []
+        with torch.cuda.stream(h2d):
+            if computed[b] is not None:
+                h2d.wait_event(computed[b])  # x buffer b is free once step k-2 computed
+            for p in range(P):
+                lo, hi = int(bounds[p]), int(bounds[p + 1])
+                xb[b][lo:hi].copy_(xk[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+                slice_ev.append(ev)
+        if copied_out[b] is not None:
+            main.wait_event(copied_out[b])  # y buffer b is free once step k-2's y left
+        if lay is None:
+            main.wait_event(slice_ev[-1])
+            spmv_into(m, xb[b], yb[b], kern)
+        else:
+            for p in range(P):
+                main.wait_event(slice_ev[p])
+                lay._window(p, xb[b])
+                lay._pass(p, xb[b], yb[b]) if kern == "seg" else spmv_into(
+                    lay.panels[p], xb[b], yb[b], lay.inner, accumulate=p > 0, lanes=lay.lanes)
+            lay._window(None, None)
+        done = torch.cuda.Event()
+        done.record(main)
+        computed[b] = done
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(done)
+            ys[k].copy_(yb[b], non_blocking=True)
+            out = torch.cuda.Event()
+            out.record(d2h)
+            copied_out[b] = out
+    d2h.synchronize()
+    main.wait_stream(d2h)
+    main.wait_stream(h2d)
+    return ys
+
+
 def spmv_csr_parallel(m: CsrMatrix, x, workers: int, reuse_pool: bool = True, kernel: str = "vector"):
     """Row-partitioned CSR SpMV (kernels.py:102-128): each of `workers` even row
     ranges (make_row_partition) is one CSR-vector launch over its rows; every

@@ -82,6 +82,17 @@ class PanelCsr:
     inner: str = "stream"  # kernel of each pass
     lanes: int | None = None  # CSR-vector lanes when inner == "vector"
 
+    def _window(self, p: int | None, xd: torch.Tensor | None) -> None:
+        """Pin x slice p in L2 (access-policy window) or clear the window (p None)."""
+        if not self.persist:
+            return
+        if p is None:
+            _lib.call("sme_l2_window", None, 0, 0.0, stream())
+            return
+        vb = xd.element_size()
+        lo, hi = int(self.bounds_host[p]), int(self.bounds_host[p + 1])
+        _lib.call("sme_l2_window", ptr(xd) + lo * vb, (hi - lo) * vb, 1.0, stream())
+
     def spmv_into(self, xd: torch.Tensor, y: torch.Tensor, kernel: str | None = None) -> None:
         from .kernels import spmv_into
 

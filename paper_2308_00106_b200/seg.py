@@ -84,6 +84,7 @@ class SegLayout:
         torch.cuda.current_stream().synchronize()  # pos / ws are freed on return
         self.nnz = m.nnz
         self.persist = False
+        self.hit_ratio = 1.0  # access-policy window hit ratio of the pinned x slice
 
     # -- passes --------------------------------------------------------------
     def _pass(self, p: int, xd: torch.Tensor, y: torch.Tensor) -> None:
@@ -101,7 +102,7 @@ class SegLayout:
             return
         vb = xd.element_size()
         lo, hi = int(self.bounds_host[p]), int(self.bounds_host[p + 1])
-        _lib.call("sme_l2_window", ptr(xd) + lo * vb, (hi - lo) * vb, 1.0, stream())
+        _lib.call("sme_l2_window", ptr(xd) + lo * vb, (hi - lo) * vb, float(self.hit_ratio), stream())
 
     def spmv_into(self, xd: torch.Tensor, y: torch.Tensor) -> None:
         """y = A x on device tensors: P stream-ordered launches."""

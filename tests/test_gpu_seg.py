@@ -200,3 +200,24 @@ def test_panel_width_limit_is_enforced(dev):
         SegLayout(m, 1)
     lay, y = run_seg(m, np.ones(n_cols), 2)
     assert np.array_equal(y, [1.0, 2.0])
+
+
+@pytest.mark.parametrize("kernel", ["seg", "vector", "panel"])
+def test_pipelined_host_stream_equals_per_vector_calls(dev, rng, kernel):
+    """spmv_csr_pipelined: the same outputs as one spmv_csr call per vector (bitwise:
+    same kernels, same order), with copies of neighbouring steps overlapped."""
+    n = 7000
+    lens = rng.integers(0, 30, n)
+    ptr, col, val = csr_from_lens(rng, lens, n)
+    m = P.CsrMatrix(n, n, ptr, col, val)
+    m._cache["seg_panels"] = 3
+    m._cache["n_panels"] = 3
+    xs = [torch.from_numpy(rng.random(n)).pin_memory() for _ in range(5)]
+    ys = P.spmv_csr_pipelined(m, xs, kernel=kernel)
+    assert len(ys) == 5
+    for x, y in zip(xs, ys):
+        want = P.spmv_csr(m, x.cuda(), kernel).cpu()
+        assert torch.equal(y, want)
+        assert O.relative_error(y.numpy(), O.spmv_csr(ptr, col, val, x.numpy())) <= F64_TOL
+    with pytest.raises(ValueError):
+        P.spmv_csr_pipelined(m, [torch.zeros(n + 1)])

@@ -28,6 +28,7 @@ ap.add_argument("--time", action="store_true")
 ap.add_argument("--panels", type=int, default=0)
 ap.add_argument("--seg-panels", type=int, default=0)
 ap.add_argument("--seg-mode", type=int, default=-1)
+ap.add_argument("--seg-hit", type=float, default=-1.0, help="x-slice L2 window hit ratio (0 = no persistence)")
 ap.add_argument("--check", action="store_true", help="compare with the stream kernel")
 ap.add_argument("--persist", action="store_true")
 ap.add_argument("--inner", default="stream")
@@ -77,6 +78,15 @@ if a.panels:
         pc.enable_persistence(True)
 if a.seg_panels:
     B._cache["seg_panels"] = a.seg_panels
+if a.seg_hit >= 0:
+    from paper_2308_00106_b200.seg import seg_of
+
+    lay = seg_of(B)
+    if a.seg_hit == 0:
+        lay.persist = False
+    else:
+        lay.enable_persistence(True)
+        lay.hit_ratio = a.seg_hit
 if a.seg_mode >= 0:
     from paper_2308_00106_b200 import _lib
 
@@ -111,5 +121,5 @@ for _rep in range(a.reps):
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1]) / a.iters
     bytes_ = B.nnz * 12 + (n + 1) * 4 + 16 * n
-    print(f"{a.config} {a.kernel} segmode={a.seg_mode} P={a.panels or a.seg_panels} inner={a.inner} L={a.lanes} rc={a.row_cost} persist={a.persist} "
+    print(f"{a.config} {a.kernel} segmode={a.seg_mode} hit={a.seg_hit} P={a.panels or a.seg_panels} inner={a.inner} L={a.lanes} rc={a.row_cost} persist={a.persist} "
           f"perm={not a.unpermuted} [{clk}]: {ms:.4f} ms  {bytes_ / ms / 1e6:.1f} GB/s  {2 * B.nnz / ms / 1e6:.1f} GFLOP/s")
