@@ -114,14 +114,30 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # workload construction
 # ---------------------------------------------------------------------------
-def host_perms(n_rows: int, n_cols: int):
-    """ROW_COLUMN_PERMUTE with seed 7 (permute.py:234-235): numpy PCG64 on the host."""
+HOST_PERM_S: dict = {}
+
+
+def host_perms(n_rows: int, n_cols: int, native: bool = True):
+    """ROW_COLUMN_PERMUTE with seed 7 (permute.py:234-235), int64 forward vectors.
+
+    native: the package's bit-exact PCG64 generator (sme_host_pcg64_permutation,
+    row and column concurrently); otherwise numpy's own Generator.permutation
+    (the reference arm's setup).
+    """
     from paper_2308_00106_b200.permute import axis_seed, random_permutation_forward
 
     t = time.perf_counter()
-    fr = random_permutation_forward(n_rows, axis_seed(PERM_SEED, 0))
-    fc = random_permutation_forward(n_cols, axis_seed(PERM_SEED, 1))
-    log(f"[bench] host permutations {n_rows:,}+{n_cols:,}: {time.perf_counter() - t:.1f}s")
+    specs = [(n_rows, axis_seed(PERM_SEED, 0)), (n_cols, axis_seed(PERM_SEED, 1))]
+    if native:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=2) as ex:
+            fr, fc = (f.astype(np.int64) for f in ex.map(lambda a: random_permutation_forward(*a), specs))
+    else:
+        fr, fc = (np.random.Generator(np.random.PCG64(sd)).permutation(n) for n, sd in specs)
+    dt = time.perf_counter() - t
+    HOST_PERM_S["native" if native else "numpy"] = round(dt, 3)
+    log(f"[bench] host permutations {n_rows:,}+{n_cols:,} ({'native' if native else 'numpy'}): {dt:.2f}s")
     return fr, fc
 
 
@@ -184,7 +200,7 @@ def run_reference(args, cfg) -> dict:
     t0 = time.perf_counter()
     if cfg["kind"] == "random_rows":
         n = cfg["n"]
-        fr, fc = host_perms(n, n)
+        fr, fc = host_perms(n, n, native=False)
         inv_r = O.inverse(fr)
         R = cpu_sample_rows(n, n * cfg["k"])
         old = inv_r[:R]
@@ -201,14 +217,14 @@ def run_reference(args, cfg) -> dict:
         ptr0, col0, val0 = O.rmat_csr(sc, cfg["ef"], 0.57, 0.19, 0.19, 0x5EED_C3, cfg["cap"])
         val0 = val0.astype(np.float32).astype(np.float64)
         n = 1 << sc
-        fr, fc = host_perms(n, n)
+        fr, fc = host_perms(n, n, native=False)
         pr, pc = O.permute_coo(O.csr_to_coo_rows(ptr0), col0, fr, fc)
         ptr, col, val = O.coo_to_csr(n, pr, pc, val0)
         R = n
     else:
         g = cfg["g"]
         n = g * g
-        fr, fc = host_perms(n, n)
+        fr, fc = host_perms(n, n, native=False)
         ptr0, col0, val0 = O.laplacian5(g)
         R = cpu_sample_rows(n, int(ptr0[-1]))
         rows = np.arange(R)
@@ -535,6 +551,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         "entropy_bits": {"unpermuted": round(H_before, 6), "permuted": round(H_after, 6), "max": 14.0},
         "load_balance_148_even_rows": balance,
         "permute_ms": round(permute_ms, 2),
+        "host_perm_gen_s": HOST_PERM_S.get("native"),
         "hist_ms": round(hist_ms, 3),
         "roundtrip_rel_err": rel_err,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

@@ -65,6 +65,16 @@ int sme_l2_window(const void* d_ptr, size_t bytes, float hit_ratio, sme_stream_t
 /* Permutations — permute.py                                                 */
 /* ------------------------------------------------------------------------ */
 
+/* HOST call (no device memory, no stream): Generator(PCG64).permutation(n) of
+ * numpy, bit-exact — the generation step of random_permutation (permute.py:71-81)
+ * and of each part of riffle_shuffle_permutation (permute.py:150-156).
+ * st[6] = {state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger}, i.e.
+ * numpy's PCG64.state; updated in place to the generator state after the
+ * shuffle (the riffle draws two permutations from one generator).
+ * h_out = int32[n] host buffer, 1 <= n <= 2^31 - 1.  Swap partners are drawn
+ * ahead of the swaps and prefetched (pcg64_host.cpp). */
+int sme_host_pcg64_permutation(uint64_t* st, int64_t n, int32_t* h_out);
+
 /* Permutation.inverse: inv[fwd[i]] = i.  Replaces permute.py:42-45 and the
  * bijection check of Permutation.__post_init__ (permute.py:29-36): bit
  * SME_FLAG_RANGE / SME_FLAG_NOT_BIJECTION is OR-ed into *d_flag (int32). */

@@ -42,7 +42,7 @@ def nvcc() -> str:
 
 
 def _sources() -> list[Path]:
-    return sorted(CSRC.glob("*.cu"))
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
 
 
 def _headers() -> list[Path]:
@@ -72,7 +72,7 @@ def _compile(src: Path, verbose: bool) -> Path:
 
 
 def build_library(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every csrc/*.cu for sm_100a and link libsme.so; incremental."""
+    """Compile every csrc/*.cu for sm_100a (and the host-only csrc/*.cpp) and link libsme.so; incremental."""
     OBJ.mkdir(exist_ok=True)
     if force:
         for o in OBJ.glob("*.o"):

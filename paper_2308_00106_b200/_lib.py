@@ -35,6 +35,7 @@ SIGNATURES: dict[str, list] = {
     "sme_device_info": [p],
     "sme_l2_set_persisting": [sz],
     "sme_l2_window": [p, sz, C.c_float, p],
+    "sme_host_pcg64_permutation": [p, i64, p],
     "sme_perm_inverse": [i64, p, p, p, p],
     "sme_permute_vector": [C.c_int, i64, p, p, p, p],
     "sme_gather": [C.c_int, i64, p, p, p, p],

@@ -1,0 +1,172 @@
+// pcg64_host.cpp — host-side, bit-exact restatement of numpy's
+// Generator(PCG64).permutation(n) (the permutation GENERATION step of
+// random_permutation, permute.py:71-81, and of riffle_shuffle_permutation,
+// permute.py:142-157).  SURVEY.md §8(f) row 2.
+//
+// Why on the host: Fisher–Yates is a chain of n-1 dependent swaps driven by one
+// sequential random stream; its cost at 50M elements is the cache misses of the
+// random swap partner (numpy: ~1.4 s per axis), not arithmetic.  The swap
+// partners depend only on the random stream, never on the array, so they can be
+// drawn ahead and their cache lines prefetched: the loop becomes bandwidth-bound
+// instead of latency-bound.  The output is the int32 forward vector the GPU path
+// uploads directly (half the bytes of numpy's int64 arange).
+//
+// Algorithm (numpy/random/_generator.pyx `shuffle` 1-D fast path + `_shuffle_raw`,
+// numpy/random/src/distributions/distributions.c `random_interval`, pcg64.h):
+//   a = arange(n); for i = n-1 .. 1: j = random_interval(i); swap(a[i], a[j])
+//   random_interval(max): mask = all-ones up to max's top bit; draw
+//     next_uint32() & mask until <= max (max < 2^32 here: n <= 2^31)
+//   next_uint32: the low half of a fresh next_uint64, buffering the high half
+//     for the following call (has_uint32 / uinteger)
+//   next_uint64 (PCG XSL-RR 128/64): state = state * M + inc (mod 2^128);
+//     out = rotr64(hi(state) ^ lo(state), hi(state) >> 58)
+// Pinned by tests/test_host.py against numpy itself (sizes 1..2^20, several
+// seeds, and the two consecutive permutations of one riffle generator).
+#include <stdint.h>
+#include <stddef.h>
+
+#include <sys/mman.h>
+
+#include <algorithm>
+#include <atomic>
+#include <thread>
+#include <vector>
+
+#include "../../include/sme.h"
+
+#define SME_API extern "C" __attribute__((visibility("default")))
+
+namespace sme {
+void set_error(const char* fmt, ...);
+}
+
+namespace {
+
+typedef unsigned __int128 u128;
+
+constexpr u128 kMult = ((u128)2549297995355413924ULL << 64) | (u128)4865540595714422341ULL;
+
+struct Pcg64 {
+  u128 state, inc;
+  bool has32;
+  uint32_t buf32;
+
+  inline uint64_t next64() {
+    state = state * kMult + inc;
+    const uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
+    const unsigned rot = (unsigned)(hi >> 58);
+    const uint64_t x = hi ^ lo;
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+  }
+  inline uint32_t next32() {
+    if (has32) {
+      has32 = false;
+      return buf32;
+    }
+    const uint64_t v = next64();
+    has32 = true;
+    buf32 = (uint32_t)(v >> 32);
+    return (uint32_t)v;
+  }
+  // random_interval(max) for 0 < max <= 0xFFFFFFFF
+  inline uint32_t interval(uint32_t max) {
+    uint32_t mask = max;
+    mask |= mask >> 1;
+    mask |= mask >> 2;
+    mask |= mask >> 4;
+    mask |= mask >> 8;
+    mask |= mask >> 16;
+    uint32_t v;
+    while ((v = (next32() & mask)) > max) {
+    }
+    return v;
+  }
+};
+
+Pcg64 load_state(const uint64_t* st) {
+  Pcg64 g;
+  g.state = ((u128)st[0] << 64) | st[1];
+  g.inc = ((u128)st[2] << 64) | st[3];
+  g.has32 = st[4] != 0;
+  g.buf32 = (uint32_t)st[5];
+  return g;
+}
+
+void store_state(const Pcg64& g, uint64_t* st) {
+  st[0] = (uint64_t)(g.state >> 64);
+  st[1] = (uint64_t)g.state;
+  st[2] = (uint64_t)(g.inc >> 64);
+  st[3] = (uint64_t)g.inc;
+  st[4] = g.has32 ? 1 : 0;
+  st[5] = g.buf32;  // numpy keeps the stale half after consuming it
+}
+
+constexpr int kAhead = 32;           // swaps prefetched ahead
+constexpr int64_t kBlock = 1 << 16;  // swap partners per producer block
+constexpr int kRing = 8;             // producer blocks in flight
+
+// swaps of steps i = hi, hi-1, ..., lo (j[k] is the partner of step hi - k)
+inline void swap_run(int32_t* a, const uint32_t* j, int64_t hi, int64_t lo) {
+  const int64_t m = hi - lo + 1;
+  for (int64_t k = 0; k < m; ++k) {
+    if (k + kAhead < m) __builtin_prefetch(a + j[k + kAhead], 1, 0);
+    const int64_t i = hi - k;
+    const int32_t t = a[i];
+    a[i] = a[j[k]];
+    a[j[k]] = t;
+  }
+}
+
+}  // namespace
+
+// st[6] = {state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger} (numpy
+// PCG64.state), updated in place to the state after the shuffle.
+SME_API int sme_host_pcg64_permutation(uint64_t* st, int64_t n, int32_t* h_out) {
+  if (!st || !h_out || n < 1 || n > INT32_MAX) {
+    sme::set_error("sme_host_pcg64_permutation: bad arguments (n=%lld)", (long long)n);
+    return SME_EINVAL;
+  }
+  Pcg64 g = load_state(st);
+  // The swap partners are uniform over the whole array: with 4 KiB pages nearly
+  // every one is also a TLB miss (which software prefetch does not hide).  Ask
+  // for transparent huge pages on the (not yet touched) buffer before filling it.
+  {
+    const uintptr_t a = ((uintptr_t)h_out + (2u << 20) - 1) & ~(uintptr_t)((2u << 20) - 1);
+    const uintptr_t b = ((uintptr_t)(h_out + n)) & ~(uintptr_t)((2u << 20) - 1);
+    if (b > a) madvise((void*)a, b - a, MADV_HUGEPAGE);  // advisory; failure is harmless
+  }
+  for (int64_t i = 0; i < n; ++i) h_out[i] = (int32_t)i;
+  const int64_t steps = n - 1;  // i = n-1 .. 1
+  if (steps <= 4 * kBlock) {
+    std::vector<uint32_t> j((size_t)steps);
+    for (int64_t k = 0; k < steps; ++k) j[k] = g.interval((uint32_t)(n - 1 - k));
+    if (steps > 0) swap_run(h_out, j.data(), n - 1, 1);
+  } else {
+    // Two-stage pipeline: a producer thread draws the swap partners (the PCG64
+    // chain with its rejection loop, ~12 ns per step) block by block into a
+    // ring; this thread applies the swaps of finished blocks with prefetching
+    // (memory-bound).  The draw order — hence every bit of the output — is
+    // numpy's; only the swaps wait for their block.
+    const int64_t n_blocks = (steps + kBlock - 1) / kBlock;
+    std::vector<uint32_t> ring((size_t)kRing * kBlock);
+    std::atomic<int64_t> produced{0}, consumed{0};
+    std::thread producer([&] {
+      for (int64_t b = 0; b < n_blocks; ++b) {
+        while (b - consumed.load(std::memory_order_acquire) >= kRing) std::this_thread::yield();
+        uint32_t* j = ring.data() + (size_t)(b % kRing) * kBlock;
+        const int64_t hi = n - 1 - b * kBlock, lo = std::max<int64_t>(1, hi - kBlock + 1);
+        for (int64_t i = hi; i >= lo; --i) j[hi - i] = g.interval((uint32_t)i);
+        produced.store(b + 1, std::memory_order_release);
+      }
+    });
+    for (int64_t b = 0; b < n_blocks; ++b) {
+      while (produced.load(std::memory_order_acquire) <= b) std::this_thread::yield();
+      const int64_t hi = n - 1 - b * kBlock, lo = std::max<int64_t>(1, hi - kBlock + 1);
+      swap_run(h_out, ring.data() + (size_t)(b % kRing) * kBlock, hi, lo);
+      consumed.store(b + 1, std::memory_order_release);
+    }
+    producer.join();
+  }
+  store_state(g, st);
+  return SME_OK;
+}

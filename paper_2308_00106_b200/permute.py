@@ -120,27 +120,80 @@ def compose(after: Permutation, first: Permutation) -> Permutation:
     return Permutation(out, _trusted=True)
 
 
-def random_permutation_forward(n: int, seed: int) -> np.ndarray:
-    """Host generation, identical to the reference (permute.py:71-81): numpy PCG64 shuffle."""
+_U64 = (1 << 64) - 1
+
+
+def _pcg64_words(bitgen: np.random.PCG64) -> np.ndarray:
+    """numpy PCG64.state as the six uint64 words sme_host_pcg64_permutation takes."""
+    s = bitgen.state
+    st, inc = s["state"]["state"], s["state"]["inc"]
+    return np.array([st >> 64, st & _U64, inc >> 64, inc & _U64, s["has_uint32"], s["uinteger"]], dtype=np.uint64)
+
+
+def _set_pcg64_words(bitgen: np.random.PCG64, w: np.ndarray) -> None:
+    bitgen.state = {
+        "bit_generator": "PCG64",
+        "state": {"state": (int(w[0]) << 64) | int(w[1]), "inc": (int(w[2]) << 64) | int(w[3])},
+        "has_uint32": int(w[4]),
+        "uinteger": int(w[5]),
+    }
+
+
+def pcg64_permutation(bitgen: np.random.PCG64, n: int) -> np.ndarray:
+    """Generator(bitgen).permutation(n) as int32, bit-exact, advancing `bitgen` like numpy.
+
+    The native generator (sme_host_pcg64_permutation, pcg64_host.cpp) restates
+    numpy's Fisher-Yates shuffle with the swap partners drawn ahead and
+    prefetched; it is a host call (ctypes releases the GIL, so the row and
+    column permutations of a strategy are generated concurrently).
+    """
+    if n < 1 or n > 2**31 - 1:
+        raise ValueError("permutation size must be in [1, 2^31)")
+    words = _pcg64_words(bitgen)
+    out = np.empty(n, dtype=np.int32)
+    _lib.call("sme_host_pcg64_permutation", words.ctypes.data, n, out.ctypes.data)
+    _set_pcg64_words(bitgen, words)
+    return out
+
+
+def _check_perm_args(n: int, seed: int) -> None:
     if n < 1:
         raise ValueError("permutation size must be >= 1")
     if seed < 0:
         raise ValueError("seed must be non-negative")
-    rng = np.random.Generator(np.random.PCG64(seed))
-    return rng.permutation(n).astype(np.int64)
+
+
+def random_permutation_forward(n: int, seed: int) -> np.ndarray:
+    """Host generation, identical to the reference (permute.py:71-81): PCG64 shuffle, int32."""
+    _check_perm_args(n, seed)
+    return pcg64_permutation(np.random.PCG64(seed), n)
+
+
+def _upload_forward(fwd: np.ndarray) -> Permutation:
+    # a shuffle of arange is a bijection by construction
+    dev = _cuda.require_cuda()
+    return Permutation(torch.from_numpy(fwd).to(dev), _trusted=True)
 
 
 def random_permutation(n: int, seed: int) -> Permutation:
     """Uniform permutation from a seeded PCG64 generator (Fisher-Yates), bit-identical to the reference."""
-    fwd = random_permutation_forward(n, seed)
-    # a shuffle of arange is a bijection by construction
-    dev = _cuda.require_cuda()
-    return Permutation(torch.from_numpy(fwd.astype(np.int32)).to(dev), _trusted=True, _host=fwd)
+    return _upload_forward(random_permutation_forward(n, seed))
 
 
-# ---------------------------------------------------------------------------
-# application on the GPU
-# ---------------------------------------------------------------------------
+def random_permutations(specs) -> list[Permutation]:
+    """random_permutation for several (n, seed) pairs, generated concurrently on host threads."""
+    specs = list(specs)
+    for n, seed in specs:
+        _check_perm_args(n, seed)
+    if len(specs) == 1:
+        return [random_permutation(*specs[0])]
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=len(specs)) as ex:
+        fwds = list(ex.map(lambda a: random_permutation_forward(*a), specs))
+    return [_upload_forward(f) for f in fwds]
+
+
 def permute_rows(m: CooMatrix, p: Permutation) -> CooMatrix:
     """Move entry (i, j, v) to (p.forward[i], j, v) (permute.py:84-88)."""
     p = _as_perm(p)
@@ -278,10 +331,10 @@ def riffle_shuffle_permutation(n: int, pivot: int, seed: int) -> Permutation:
         raise ValueError(f"pivot {pivot} out of range (0, {n})")
     if seed < 0:
         raise ValueError("seed must be non-negative")
-    rng = np.random.Generator(np.random.PCG64(seed))
-    local = np.empty(n, dtype=np.int64)
-    local[:pivot] = rng.permutation(pivot)
-    local[pivot:] = pivot + rng.permutation(n - pivot)
+    bitgen = np.random.PCG64(seed)
+    local = np.empty(n, dtype=np.int32)
+    local[:pivot] = pcg64_permutation(bitgen, pivot)
+    local[pivot:] = pivot + pcg64_permutation(bitgen, n - pivot)
     return compose(Permutation(_interleave_forward(n, pivot)), Permutation(local))
 
 
@@ -349,7 +402,8 @@ def build_strategy(m, kind: StrategyKind, seed: int, bins: int = 512, column_gra
     if kind is StrategyKind.ROW_PERMUTE:
         return random_permutation(m.n_rows, row_seed), identity_permutation(m.n_cols)
     if kind is StrategyKind.ROW_COLUMN_PERMUTE:
-        return random_permutation(m.n_rows, row_seed), random_permutation(m.n_cols, col_seed)
+        p_r, p_c = random_permutations([(m.n_rows, row_seed), (m.n_cols, col_seed)])
+        return p_r, p_c
 
     def riffled(n: int, histogram, axis_seed_: int) -> Permutation:
         return riffle_shuffle_permutation(n, gradient_pivot(histogram), axis_seed_)

@@ -13,6 +13,7 @@ from paper_2308_00106_b200.permute import (
     StrategyKind,
     _interleave_forward,
     axis_seed,
+    pcg64_permutation,
     random_permutation_forward,
 )
 from paper_2308_00106_b200.rowshard import ShardPlan
@@ -57,6 +58,30 @@ def test_host_permutation_generation_is_the_references(golden):
         random_permutation_forward(0, 1)
     with pytest.raises(ValueError):
         random_permutation_forward(5, -1)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 64, 65, 1000, 4097, 65536, 1 << 20, 3_000_001])
+@pytest.mark.parametrize("seed", [0, 5, 2**63 + 11])
+def test_native_pcg64_permutation_is_numpys(n, seed):
+    """sme_host_pcg64_permutation == Generator(PCG64(seed)).permutation(n), and it leaves
+    the generator in numpy's state (incl. the buffered uint32 half)."""
+    ours_bg, ref_bg = np.random.PCG64(seed), np.random.PCG64(seed)
+    got = pcg64_permutation(ours_bg, n)
+    ref = np.random.Generator(ref_bg).permutation(n)
+    assert got.dtype == np.int32 and np.array_equal(got, ref)
+    assert ours_bg.state == ref_bg.state
+
+
+def test_native_pcg64_consecutive_draws_like_riffle():
+    """Two permutations from one generator (riffle_shuffle_permutation, permute.py:150-156),
+    then a third with an odd pending uint32, then a float draw: all as numpy."""
+    a, b = np.random.PCG64(99), np.random.PCG64(99)
+    ga = np.random.Generator(a)
+    for n in (12345, 777, 3):
+        assert np.array_equal(pcg64_permutation(b, n), ga.permutation(n))
+    gb = np.random.Generator(b)
+    assert gb.integers(0, 1000, 5).tolist() == ga.integers(0, 1000, 5).tolist()
+    assert gb.random() == ga.random()
 
 
 def test_strategy_table_and_interleave():
