@@ -386,6 +386,8 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
     else:
         plan = rowshard.ShardPlan(n, n, world)
         shard = rowshard.RowShardedSpMV(B, plan, rank, args.kernel)
+        if shard.seg is not None:  # the shard's own panels (aligned to the ranks' x slots)
+            resolved, kernels_per_step = "seg", shard.seg.n_panels
         c0, c1 = plan.col_range(rank)
         chunk = plan.pad_slice(xp[c0:c1])
         lo_r, hi_r = plan.row_range(rank)
@@ -535,7 +537,9 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
             "kernel": resolved + (f" ({kernels_per_step} column panels x k_spmv_stream)" if resolved == "panel" else
                                  f" ({kernels_per_step} column panels x k_spmv_seg)" if resolved == "seg" else ""),
             "n_rows": n, "nnz": nnz,
-            "parallelism": (f"row-shard x{world} + {dist.get_backend()} all_gather of x" if world > 1 else "1 GPU"),
+            "parallelism": ((f"row-shard x{world} + {dist.get_backend()} per-slot x broadcasts pipelined with the panel passes"
+                             if shard.pipelined else f"row-shard x{world} + {dist.get_backend()} all_gather of x")
+                            if world > 1 else "1 GPU"),
             "l2": "inputs (13 GB/pass for C4) far exceed the 126 MB L2; no flush needed" if cfg["kind"] == "random_rows"
                   else "x fits L2; matrix streams exceed L2",
         },

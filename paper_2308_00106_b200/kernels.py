@@ -75,14 +75,18 @@ def default_lanes(m: CsrMatrix) -> int:
 
 
 def auto_kernel(m: CsrMatrix) -> str:
-    """Kernel policy (measured on B200):
+    """Kernel policy (measured on B200, profiles/round1/kernel_compare.txt):
     * 'seg' (column panels in the segmented-chunk layout, seg.py) when x exceeds
       60 % of L2 — random gathers would miss to DRAM (62 G gathers/s at 400 MB vs
       287 G/s L2-resident, tools/gather_roofline.py); C4: 5.9 ms vs 6.4-7.0 ms for
       the CSR column panels ('panel');
-    * 'stream' for ragged rows (max row > 8 x mean + 32: C3 R-MAT 405 GFLOP/s vs
+    * 'seg' also when x exceeds 30 % of L2 and no row is longer than SEG_MAX_ROW
+      (a warp's range holds whole rows): C3 R-MAT 447 vs 409 GFLOP/s ('stream'),
+      C5 307 vs 299 ('vector');
+    * 'stream' for other ragged rows (max row > 8 x mean + 32: C3 405 GFLOP/s vs
       214 for CSR-vector);
-    * else 'vector' (partition-invariant; fastest on regular rows: C2 0.103 ms)."""
+    * else 'vector' (partition-invariant; fastest on regular rows: C2 0.113 ms vs
+      0.115 for 'seg')."""
     if "auto" not in m._cache:
         from .panels import l2_bytes
 
@@ -92,8 +96,33 @@ def auto_kernel(m: CsrMatrix) -> str:
         else:
             max_len, _ = row_stats(m)
             mean = m.nnz / max(1, m.n_rows)
-            m._cache["auto"] = "stream" if max_len > 8 * mean + 32 else "vector"
+            if xb > 0.3 * l2_bytes() and max_len <= SEG_MAX_ROW and not banded(m):
+                m._cache["auto"] = "seg"
+            else:
+                m._cache["auto"] = "stream" if max_len > 8 * mean + 32 else "vector"
     return m._cache["auto"]
+
+
+SEG_MAX_ROW = 4096
+
+
+def banded(m: CsrMatrix, samples: int = 4096) -> bool:
+    """True when sampled rows span a small column window (median last-first column
+    <= n_cols / 256): x gathers then coalesce and the CSR-vector kernel wins
+    (C5 unpermuted: 'vector' 610 GFLOP/s vs 'seg' 497).  Rows are column-sorted,
+    so each sampled row costs two index loads; cached."""
+    if "banded" not in m._cache:
+        dev = m.d_row_ptr.device
+        r = torch.linspace(0, max(0, m.n_rows - 1), min(samples, max(1, m.n_rows)), device=dev).long()
+        a, b = m.d_row_ptr[r].long(), m.d_row_ptr[r + 1].long()
+        ok = b - a >= 2
+        if m.nnz == 0 or not bool(ok.any()):
+            m._cache["banded"] = True
+        else:
+            lo = m.d_col_idx[a[ok]].long()
+            hi = m.d_col_idx[b[ok] - 1].long()
+            m._cache["banded"] = bool((hi - lo).float().median() <= m.n_cols / 256)
+    return m._cache["banded"]
 
 
 def row_stats(m: CsrMatrix) -> tuple[int, int]:

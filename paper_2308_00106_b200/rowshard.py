@@ -14,6 +14,17 @@ equal-chunk all_gather_into_tensor; the shard's column ids are remapped once
 (sme_rowshard_remap_cols) from matrix columns to slots of the padded vector.
 With the CSR-vector kernel and the parent matrix's lanes the sharded y is
 bitwise equal to the 1-GPU y (no row's reduction order changes).
+
+Pipelined exchange (kernel 'seg', the C4 path).  A shard of a randomly permuted
+matrix needs ~all of x, and its SpMV is a sequence of column-panel passes that
+each read ONE x slice.  The shard's panels are aligned to the ranks' padded
+slots (P a multiple of world), so pass p needs only the slot of rank
+p // (P / world).  The exchange is then world broadcasts (rank k's slot from
+rank k, in rank order) on a communication stream, and the compute stream starts
+the passes of slot k as soon as broadcast k has landed: the transfer of slot
+k+1 overlaps the passes of slot k, instead of one all-gather ahead of all
+passes.  The pass order (hence y, bit for bit) is that of the non-pipelined
+seg SpMV of the same shard.
 """
 
 from __future__ import annotations
@@ -73,6 +84,18 @@ def allgather_padded(x_full: torch.Tensor, x_chunk: torch.Tensor, group=None) ->
         dist.all_gather(views, x_chunk, group=group)
 
 
+def pipelined_exchange(x_full: torch.Tensor, x_chunk: torch.Tensor, rank: int, world: int, on_slot, group=None):
+    """Assemble the padded x from every rank's chunk by `world` in-order broadcasts;
+    on_slot(k) runs after slot k is in place (on the caller's side of the stream
+    hand-off: with CUDA tensors the broadcasts run on a side stream and on_slot
+    receives the CUDA event to wait on, see RowShardedSpMV.step)."""
+    pad = x_chunk.numel()
+    x_full[rank * pad : (rank + 1) * pad].copy_(x_chunk)
+    for k in range(world):
+        dist.broadcast(x_full[k * pad : (k + 1) * pad], src=k, group=group)
+        on_slot(k)
+
+
 class RowShardedSpMV:
     """One rank's shard of A plus the gathered-x buffer; step() = all-gather + SpMV."""
 
@@ -92,19 +115,64 @@ class RowShardedSpMV:
         self.lanes = lanes or (default_lanes(m) if kernel == "vector" else None)
         self.x_full = torch.zeros(plan.world * plan.pad, dtype=m.dtype, device=dev)
         self.y = torch.empty(hi - lo, dtype=m.dtype, device=dev)
+        self.seg = None
+        if kernel in ("seg", "auto"):
+            from .kernels import auto_kernel
+            from .seg import auto_seg_panels, seg_of
+
+            if kernel == "seg" or auto_kernel(self.local) == "seg":
+                # panels aligned to the ranks' padded slots: P = world * ceil(P_auto / world)
+                per = -(-auto_seg_panels(self.local) // plan.world)
+                self.seg = seg_of(self.local, plan.world * per)
+                self.kernel = "seg"
+        self._comm = None
 
     @property
     def nnz(self) -> int:
         return self.local.nnz
 
     def spmv(self, x_full: torch.Tensor | None = None) -> torch.Tensor:
-        spmv_into(self.local, self.x_full if x_full is None else x_full, self.y, self.kernel, lanes=self.lanes)
+        xf = self.x_full if x_full is None else x_full
+        if self.seg is not None:
+            self.seg.spmv_into(xf, self.y)
+        else:
+            spmv_into(self.local, xf, self.y, self.kernel, lanes=self.lanes)
         return self.y
 
+    @property
+    def pipelined(self) -> bool:
+        return self.seg is not None and self.plan.world > 1
+
     def step(self, x_chunk: torch.Tensor, group=None) -> torch.Tensor:
-        """All-gather the padded x chunks of every rank, then y_local = A_local x."""
-        allgather_padded(self.x_full, x_chunk, group)
-        return self.spmv()
+        """Exchange the padded x chunks of every rank, then y_local = A_local x.
+
+        seg shards: per-slot broadcasts on a side stream, each slot's panel passes
+        launched as soon as it lands (pipelined_exchange); other kernels: one
+        all-gather, then the SpMV."""
+        if not self.pipelined:
+            allgather_padded(self.x_full, x_chunk, group)
+            return self.spmv()
+        world, lay = self.plan.world, self.seg
+        per = lay.n_panels // world
+        main = torch.cuda.current_stream()
+        comm = self._comm = self._comm or torch.cuda.Stream(device=self.x_full.device)
+        comm.wait_stream(main)  # the previous step's passes are done reading x_full
+        events = []
+
+        def landed(k: int) -> None:
+            ev = torch.cuda.Event()
+            ev.record(comm)
+            events.append(ev)
+
+        with torch.cuda.stream(comm):
+            pipelined_exchange(self.x_full, x_chunk, self.rank, world, landed, group)
+        for p in range(lay.n_panels):
+            if p % per == 0:
+                main.wait_event(events[p // per])
+            lay._window(p, self.x_full)
+            lay._pass(p, self.x_full, self.y)
+        lay._window(None, None)
+        return self.y
 
 
 def virtual_ranks(m: CsrMatrix, world: int, kernel: str = "vector") -> list[RowShardedSpMV]:

@@ -183,6 +183,7 @@ __global__ void __launch_bounds__(P2T) k_combine(int64_t n_rows, int nrb, int nc
     if (r0 + i < n_rows) y[r0 + i] = ys[i];
 }
 
+#ifndef BB_NO_MAIN
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : 50000000;
   const int nrb = (int)((n + RB - 1) / RB);
@@ -237,3 +238,4 @@ int main(int argc, char** argv) {
   printf("total   %.3f ms  -> %.1f GFLOP/s at 2*%.3e flops\n", t1 + t2, 2.0 * E / (t1 + t2) / 1e6, (double)E);
   return 0;
 }
+#endif  // BB_NO_MAIN
