@@ -62,6 +62,28 @@ int sme_l2_set_persisting(size_t bytes);
 int sme_l2_window(const void* d_ptr, size_t bytes, float hit_ratio, sme_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
+/* Matrix Market I/O — matio.py (HOST calls: host buffers, no stream)        */
+/* ------------------------------------------------------------------------ */
+
+/* Entry body of parse_matrix_market (matio.py:196-239), multithreaded: buf/len
+ * = the bytes after the size line, whose first line is number first_line_no.
+ * field 0 real / 1 integer / 2 pattern; rows/cols int32[declared] (0-based),
+ * vals f64[declared].  cr_newline: '\r' and "\r\n" also end lines.  threads <= 0:
+ * all hardware threads.  status[4] = {error code (0 ok, 1 more than declared,
+ * 2 field count, 3 malformed index, 4/5 row/col out of range, 6/7 malformed
+ * integer/real value, 8 non-ASCII), 1-based error line, entries found, byte
+ * offset of the error line in buf}.  Malformed content is reported through
+ * status (return SME_OK); bad arguments return SME_EINVAL. */
+int sme_host_mm_parse(const char* buf, int64_t len, int field, int64_t n_rows, int64_t n_cols, int64_t declared,
+                      int64_t first_line_no, int cr_newline, int threads, int32_t* rows, int32_t* cols,
+                      double* vals, int64_t* status);
+
+/* Entry lines of _write_mm (matio.py:270-274): "i+1 j+1 %.17g\n" per entry into
+ * out (cap >= 72 * n bytes), *out_len = bytes written; multithreaded. */
+int sme_host_mm_format(const int64_t* rows, const int64_t* cols, const double* vals, int64_t n, char* out,
+                       int64_t cap, int threads, int64_t* out_len);
+
+/* ------------------------------------------------------------------------ */
 /* Permutations — permute.py                                                 */
 /* ------------------------------------------------------------------------ */
 
