@@ -255,6 +255,39 @@ def run_reference(args, cfg) -> dict:
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def pcie_rates(x_pin, y_pin, reps: int = 3) -> dict:
+    """Measured PCIe rates of this box with the e2e's own pinned buffers: H2D alone,
+    D2H alone, and both at once on two streams (the pipelined e2e's regime).  The
+    e2e floor is one x in and one y out per step at the concurrent rate."""
+    import torch
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    xd = torch.empty(x_pin.numel(), dtype=x_pin.dtype, device=dev)
+    yd = torch.empty(y_pin.numel(), dtype=y_pin.dtype, device=dev)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(h2d: bool, d2h: bool) -> float:
+        best = float("inf")
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if h2d:
+                with torch.cuda.stream(sa):
+                    xd.copy_(x_pin, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(sb):
+                    y_pin.copy_(yd, non_blocking=True)
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    nb_x, nb_y = x_pin.numel() * x_pin.element_size(), y_pin.numel() * y_pin.element_size()
+    t_h, t_d, t_b = timed(True, False), timed(False, True), timed(True, True)
+    return {"h2d_gbs": round(nb_x / t_h / 1e9, 2), "d2h_gbs": round(nb_y / t_d / 1e9, 2),
+            "bidirectional_gbs_each_way": round(min(nb_x, nb_y) / t_b / 1e9, 2),
+            "how": f"pinned copies of the e2e buffers ({nb_x / 1e6:.0f} MB), best of {reps}, wall clock around synchronize"}
+
+
 def run_ours(args, cfg, rank: int, world: int) -> dict | None:
     import torch
     import torch.distributed as dist
@@ -476,10 +509,15 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
                       P.relative_error(ys_pin[-2], y_perm * (2.0 if (e_steps - 2) & 1 else 1.0)))
         if e2e_err > tol:
             raise SystemExit(f"pipelined host-vector SpMV differs from the device result: {e2e_err}")
+        pcie = pcie_rates(xs_pin[0], ys_pin[0])
+        step_bytes = n * B.d_values.element_size()
+        floor_ms = step_bytes / (pcie["bidirectional_gbs_each_way"] * 1e9) * 1e3
+        pcie["e2e_floor_ms"] = round(floor_ms, 4)
+        pcie["e2e_frac_of_floor"] = round(floor_ms / e_ms, 4)
         e2e = {"value": round(2 * nnz / (e_ms * 1e-3) / 1e9, 4), "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(n * B.d_values.element_size()),
-               "d2h_bytes_per_step": int(n * B.d_values.element_size()), "ms_per_step": round(e_ms, 4),
-               "steps": e_steps, "rel_err": e2e_err,
+               "h2d_bytes_per_step": int(step_bytes),
+               "d2h_bytes_per_step": int(step_bytes), "ms_per_step": round(e_ms, 4),
+               "steps": e_steps, "rel_err": e2e_err, "pcie": pcie,
                "api": "paper_2308_00106_b200.spmv_csr_pipelined(CsrMatrix, [pinned host x_k]) -> [pinned host y_k]",
                "single_call": {"api": "paper_2308_00106_b200.spmv_csr(CsrMatrix, pinned host tensor)",
                                "ms_per_step": round(single_ms, 4),
@@ -598,9 +636,11 @@ def run_iterative(args, cfg) -> dict:
     fr, fc = host_perms(n, n)
     p_r = P.Permutation(torch.from_numpy(fr.astype(np.int32)).to(dev), _host=fr)
     p_c = P.Permutation(torch.from_numpy(fc.astype(np.int32)).to(dev), _host=fc)
+    t1 = time.perf_counter()
     op = PermutedOperator(A, p_r, p_c, kernel=args.kernel)
     torch.cuda.synchronize()
     perm_s = time.perf_counter() - t0
+    build_s = time.perf_counter() - t1
 
     def run(operator) -> tuple[float, float, PowerIteration]:
         pi = PowerIteration(operator, x0)
@@ -619,8 +659,22 @@ def run_iterative(args, cfg) -> dict:
     clocks.start()
     perm_ms, lam_p, pi_p = run(op)
     clk = clocks.stop()
-    unperm_ms, lam_u, _ = run(PermutedOperator(A, None, None, kernel=args.kernel))
+    unperm_ms, lam_u, pi_u = run(PermutedOperator(A, None, None, kernel=args.kernel))
     x_p = pi_p.x()
+
+    def launches(pi) -> int:  # libsme launches per iteration
+        if pi.fused:
+            return pi.lay.n_panels
+        from paper_2308_00106_b200.kernels import auto_kernel
+
+        kern = auto_kernel(pi.op.B) if pi.op.kernel == "auto" else pi.op.kernel
+        if kern == "seg":
+            from paper_2308_00106_b200.seg import seg_of
+
+            spmv = seg_of(pi.op.B).n_panels
+        else:
+            spmv = 2 if kern == "merge" else 1
+        return spmv + (1 if pi.op.q is not None else 0) + 2
     step_ms = perm_ms / iters
     gflops = 2 * nnz / (step_ms * 1e-3) / 1e9
     total_perm = perm_s * 1e3 + perm_ms
@@ -630,15 +684,25 @@ def run_iterative(args, cfg) -> dict:
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic 5-point Laplacian; numpy PCG64 permutations seed 7",
         "config": {"workload": cfg["workload"] + ", 1000-step power iteration", "kernel": args.kernel,
-                   "graph_steps": graph_steps, "n_rows": n, "nnz": nnz},
+                   "graph_steps": graph_steps, "n_rows": n, "nnz": nnz,
+                   "permuted_step": ("fused: seg panel passes, the last with the "
+                                     + ("scatter + " if pi_p.op.q is not None else "") + "norm epilogue "
+                                     "(sme_spmv_seg_epi)" if pi_p.fused else
+                                     "SpMV + " + ("gather + " if pi_p.op.q is not None else "") + "dot + scale"),
+                   "folded": bool(op.folded),
+                   "folded_note": "the per-iteration gather by q = p_r o p_c^-1 is folded into the matrix once: "
+                                  "the iterated operator is permute_csr(A, p_r, p_r) (iterative.py docstring)",
+                   "unpermuted_step": ("fused seg" if pi_u.fused else "SpMV + dot + scale (unfused)")},
         "eigenvalue": {"permuted": lam_p, "unpermuted": lam_u, "rel_diff": abs(lam_p - lam_u) / lam_u},
         "amortisation": {"permutation_setup_ms": round(perm_s * 1e3, 2),
+                         "of_which_host_generation_ms": round(HOST_PERM_S.get("native", 0.0) * 1e3, 2),
+                         "of_which_permuted_csr_build_ms": round(build_s * 1e3, 2),
                          "permuted_1000_iter_ms": round(perm_ms, 3), "unpermuted_1000_iter_ms": round(unperm_ms, 3),
                          "permuted_total_ms": round(total_perm, 3),
                          "break_even_note": "setup is paid once; per-iteration ratio permuted/unpermuted = "
                                             f"{perm_ms / unperm_ms:.3f}"},
         "x_norm_check": float(torch.linalg.vector_norm(x_p).item()),
-        "clocks": clk, "gpu_launches": None,
+        "clocks": clk, "gpu_launches": launches(pi_p) * iters,
     }
 
 

@@ -284,10 +284,12 @@ int sme_panel_scatter(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const
  * (n_rows+1) int32; ws sized by sme_seg_workspace_size keeps row counts),
  * sme_seg_fill (pk/val/hdr at the 128-aligned panel offsets; offsets given on
  * device and host), sme_seg_plan (per panel: n_warps+1 entry positions on row
- * boundaries, n_warps from sme_spmv_seg_warps).  Panel width < 2^23 - 1. */
+ * boundaries, n_warps from sme_spmv_seg_warps).  Panel width < 2^23 - 1.
+ * full_last = 1 also gives every row without entries in the LAST panel an
+ * explicit zero there (needed by the fused epilogue of sme_spmv_seg_epi). */
 int sme_seg_workspace_size(int64_t n_rows, int32_t n_panels, size_t* bytes);
 int sme_seg_positions(int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_col, int32_t n_panels,
-                      const int32_t* d_bounds, int32_t* d_pos, void* d_ws, size_t ws_bytes,
+                      const int32_t* d_bounds, int full_last, int32_t* d_pos, void* d_ws, size_t ws_bytes,
                       sme_stream_t stream);
 int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_col,
                  const void* d_val, int32_t n_panels, const int32_t* d_bounds, const int32_t* d_pos,
@@ -302,6 +304,19 @@ int sme_seg_plan(int64_t n_rows, const int32_t* d_pos_panel, int32_t n_warps, in
 /* y (+)= A_p x_p for one panel: d_xs = x + bounds[p]; accumulate = 0 for panel 0. */
 int sme_spmv_seg(int dtype, int32_t n_warps, const uint32_t* d_pk, const void* d_val, const int32_t* d_hdr,
                  const int32_t* d_plan, const void* d_xs, void* d_y, int accumulate, sme_stream_t stream);
+/* The last pass of one power-iteration step with its BLAS-1 work fused in (f64):
+ * v_r = scale[0] * (y[r] (+ this panel's row sum)), written to d_out[qinv[r]]
+ * (qinv NULL: d_out[r]) — the permuted-coordinate gather z = (B z)[q] of
+ * iterative.py becomes this scatter — while the sum of v_r^2 is reduced
+ * deterministically (warp partials in d_partials[n_warps], last CTA in fixed
+ * order; d_ticket: one uint32, zero-initialised once) into d_result[1], and
+ * d_result[0] = 1/sqrt(d_result[1]) is the next step's scale.  Replaces the
+ * numpy loop x = A x / ||A x|| over spmv_csr (kernels.py:73-78) of the C5
+ * oracle.  Needs a layout built with full_last = 1. */
+int sme_spmv_seg_epi(int dtype, int32_t n_warps, const uint32_t* d_pk, const void* d_val, const int32_t* d_hdr,
+                     const int32_t* d_plan, const void* d_xs, void* d_y, int accumulate, void* d_out,
+                     const int32_t* d_qinv, const double* d_scale, double* d_partials, uint32_t* d_ticket,
+                     double* d_result, sme_stream_t stream);
 
 /* Merge kernel selection (process-wide; tests and experiments): 1 = persistent
  * TMA-pipelined kernel (needs 16-byte aligned row_ptr/col_idx/values), 0 = one

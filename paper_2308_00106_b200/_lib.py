@@ -66,12 +66,13 @@ SIGNATURES: dict[str, list] = {
     "sme_panel_row_ptrs": [i64, p, p, i32, p, p, p, sz, p],
     "sme_panel_scatter": [C.c_int, i64, p, p, p, i32, p, p, p, p, p, p],
     "sme_seg_workspace_size": [i64, i32, psz],
-    "sme_seg_positions": [i64, p, p, i32, p, p, p, sz, p],
+    "sme_seg_positions": [i64, p, p, i32, p, C.c_int, p, p, sz, p],
     "sme_seg_fill": [C.c_int, i64, p, p, p, i32, p, p, p, p, p, p, p, p, p],
     "sme_spmv_seg_warps": [C.POINTER(C.c_int32)],
     "sme_spmv_seg_set_mode": [C.c_int],
     "sme_seg_plan": [i64, p, i32, p, p],
     "sme_spmv_seg": [C.c_int, i32, p, p, p, p, p, p, C.c_int, p],
+    "sme_spmv_seg_epi": [C.c_int, i32, p, p, p, p, p, p, C.c_int, p, p, p, p, p, p, p],
     "sme_spmv_stream_warps": [i64, i64, C.POINTER(C.c_int32)],
     "sme_spmv_stream_set_mode": [C.c_int],
     "sme_spmv_stream_set_row_cost": [C.c_int],

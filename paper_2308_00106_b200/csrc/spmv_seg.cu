@@ -83,13 +83,16 @@ __global__ void k_seg_count(int64_t n_rows, const int32_t* __restrict__ row_ptr,
   }
 }
 
-// entries of row r in the panel layout: its count, or one explicit zero
+// entries of row r in the panel layout: its count, or one explicit zero (every
+// row of panel 0, of the last panel when `full` (the epilogue pass of
+// sme_spmv_seg_epi must visit every row), and even rows of the others)
 struct SegLen {
   const int32_t* counts;  // this panel's counts
   int32_t panel;
+  bool full;
   __device__ __forceinline__ int64_t operator()(int64_t r) const {
     const int32_t c = counts[r];
-    return c > 0 ? c : ((panel == 0 || (r % SEG_GAP) == 0) ? 1 : 0);
+    return c > 0 ? c : ((panel == 0 || full || (r % SEG_GAP) == 0) ? 1 : 0);
   }
 };
 
@@ -190,16 +193,61 @@ struct SegChunk {
   }
 };
 
-template <typename T, bool ACC>
-__global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict__ pk, const T* __restrict__ val,
-                                                   const int32_t* __restrict__ hdr, const int32_t* __restrict__ plan,
-                                                   int32_t n_warps, const T* __restrict__ xs, T* __restrict__ y) {
+// Epilogue of the last pass of an iterative step (sme_spmv_seg_epi): every row
+// total t becomes v = s * t with s = *scale, stored at out[qinv[r]] (qinv null:
+// out[r]); the warps' sums of v*v go to partials[warp] and the last CTA to finish
+// reduces them in a fixed order into result[1] = sum v*v, result[0] = 1/sqrt(.)
+// (the next step's scale).  Deterministic: fixed warp ranges, fixed trees.
+template <typename T>
+struct SegEpi {
+  T* out;
+  const int32_t* qinv;
+  const double* scale;
+  double* partials;  // [n_warps]
+  unsigned* ticket;  // zero before the launch; reset by the last CTA
+  double* result;    // [2]
+};
+
+// last-CTA reduction of the warp partials (fixed order) -> result, next scale
+template <typename T>
+__device__ __forceinline__ void seg_epi_finish_impl(const SegEpi<T>& epi, int32_t n_warps) {
+  __shared__ double red[SEG_NT];
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(epi.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double acc = 0.0;
+  for (int w = threadIdx.x; w < n_warps; w += SEG_NT) acc += __ldcg(epi.partials + w);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = SEG_NT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double tot = red[0];
+    epi.result[1] = tot;
+    epi.result[0] = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+    *epi.ticket = 0u;
+  }
+}
+
+template <typename T, bool ACC, bool EPI>
+__device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk, const T* __restrict__ val,
+                                                const int32_t* __restrict__ hdr, const int32_t* __restrict__ plan,
+                                                int warp, const T* __restrict__ xs, T* __restrict__ y,
+                                                const SegEpi<T>& epi) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  const int warp = (blockIdx.x * SEG_NT + threadIdx.x) >> 5;
-  if (warp >= n_warps) return;
+  double ss = 0.0;
   const int P0 = plan[warp], P1 = plan[warp + 1];
-  if (P0 >= P1) return;
+  if (P0 >= P1) return ss;
+  const T sc = EPI ? (T)*epi.scale : T(1);
 
   int c = P0 & ~(SEG_CH - 1);
   SegChunk<T> cur;
@@ -222,7 +270,7 @@ __global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict_
       endm |= (in && (cur.w[k] & SEG_END)) ? (1u << k) : 0u;
       xv[k] = (in && lc != SEG_MARK) ? __ldg(xs + lc) : T(0);
       // accumulating passes skip explicit zeros (their rows have nothing to add)
-      const bool emit = in && (cur.w[k] & SEG_END) && !(ACC && lc == SEG_MARK);
+      const bool emit = in && (cur.w[k] & SEG_END) && (EPI || !(ACC && lc == SEG_MARK));
       yv[k] = (ACC && emit) ? y[cur.h + (int)(cur.w[k] & SEG_DMASK)] : T(0);
     }
     // in-lane runs: run[k] = sum of the row segment ending at k that starts in this lane
@@ -267,7 +315,13 @@ __global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict_
       const uint32_t lc = cur.w[k] >> SEG_CSHIFT;
       if ((endm >> k) & 1u) {
         first = false;
-        if (!(ACC && lc == SEG_MARK)) {
+        if (EPI) {
+          // every row ends exactly once in the epilogue pass (explicit zeros included)
+          const int r = cur.h + (int)(cur.w[k] & SEG_DMASK);
+          const T v = sc * (ACC ? yv[k] + fin : fin);
+          epi.out[epi.qinv ? epi.qinv[r] : r] = v;
+          ss += (double)v * (double)v;
+        } else if (!(ACC && lc == SEG_MARK)) {
           const int r = cur.h + (int)(cur.w[k] & SEG_DMASK);
           y[r] = ACC ? yv[k] + fin : fin;
         }
@@ -277,7 +331,29 @@ __global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict_
     cur = nxt;
     c += SEG_CH;
   }
+  return ss;
 }
+
+template <typename T, bool ACC, bool EPI>
+__global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict__ pk, const T* __restrict__ val,
+                                                   const int32_t* __restrict__ hdr, const int32_t* __restrict__ plan,
+                                                   int32_t n_warps, const T* __restrict__ xs, T* __restrict__ y,
+                                                   SegEpi<T> epi) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * SEG_NT + threadIdx.x) >> 5;
+  if (EPI) {
+    double ss = 0.0;
+    if (warp < n_warps) ss = seg_warp_body<T, ACC, true>(pk, val, hdr, plan, warp, xs, y, epi);
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
+    if (lane == 0 && warp < n_warps) epi.partials[warp] = ss;
+    seg_epi_finish_impl(epi, n_warps);
+    return;
+  }
+  if (warp >= n_warps) return;
+  seg_warp_body<T, ACC, false>(pk, val, hdr, plan, warp, xs, y, epi);
+}
+
 
 // Bound probe (mode 3, timing experiments only; the result is NOT y = A x): the
 // same chunk stream and x gathers with a per-lane sum and one coalesced store per
@@ -315,14 +391,20 @@ static int s_seg_mode = 0;  // 0 = SpMV (default), 3 = bound probe
 
 template <typename T>
 int launch_seg(int32_t n_warps, const uint32_t* pk, const T* val, const int32_t* hdr, const int32_t* plan,
-               const T* xs, T* y, int accumulate, cudaStream_t s) {
+               const T* xs, T* y, int accumulate, cudaStream_t s, const SegEpi<T>* epi = nullptr) {
   const int grid = (int)(((int64_t)n_warps * 32 + SEG_NT - 1) / SEG_NT);
-  if (s_seg_mode == 3)
+  const SegEpi<T> e = epi ? *epi : SegEpi<T>{};
+  if (epi) {
+    if (accumulate)
+      k_spmv_seg<T, true, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
+    else
+      k_spmv_seg<T, false, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
+  } else if (s_seg_mode == 3)
     k_seg_probe<T><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y);
   else if (accumulate)
-    k_spmv_seg<T, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y);
+    k_spmv_seg<T, true, false><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
   else
-    k_spmv_seg<T, false><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y);
+    k_spmv_seg<T, false, false><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
   SME_CHECK_LAUNCH("k_spmv_seg");
   return SME_OK;
 }
@@ -341,7 +423,8 @@ SME_API int sme_seg_workspace_size(int64_t n_rows, int32_t n_panels, size_t* byt
 // padded row lengths; pos[p * (n_rows + 1) + n_rows] = entries of panel p).
 // ws keeps the per-panel row counts for step 2.
 SME_API int sme_seg_positions(int64_t n_rows, const int32_t* row_ptr, const int32_t* col, int32_t n_panels,
-                              const int32_t* bounds, int32_t* pos, void* ws, size_t ws_bytes, sme_stream_t stream) {
+                              const int32_t* bounds, int full_last, int32_t* pos, void* ws, size_t ws_bytes,
+                              sme_stream_t stream) {
   SME_REQUIRE(n_rows >= 0 && n_rows < INT32_MAX && n_panels >= 1 && n_panels <= 1024, "bad arguments");
   const size_t need = align_up((size_t)n_panels * n_rows * 4) + scan_workspace_bytes(n_rows);
   SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
@@ -355,7 +438,8 @@ SME_API int sme_seg_positions(int64_t n_rows, const int32_t* row_ptr, const int3
   k_seg_count<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, row_ptr, col, n_panels, bounds, counts);
   SME_CHECK_LAUNCH("k_seg_count");
   for (int p = 0; p < n_panels; ++p) {
-    int rc = exclusive_scan_lengths(n_rows, SegLen{counts + (int64_t)p * n_rows, p}, pos + (int64_t)p * (n_rows + 1),
+    const bool full = full_last && p == n_panels - 1;
+    int rc = exclusive_scan_lengths(n_rows, SegLen{counts + (int64_t)p * n_rows, p, full}, pos + (int64_t)p * (n_rows + 1),
                                     scan_ws, nullptr, s);
     if (rc != SME_OK) return rc;
   }
@@ -408,10 +492,12 @@ SME_API int sme_spmv_seg_warps(int32_t* n_warps) {
     int v = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, SEG_NT, 0) == cudaSuccess) per_sm = std::min(per_sm, v);
   };
-  occ((const void*)k_spmv_seg<double, false>);
-  occ((const void*)k_spmv_seg<double, true>);
-  occ((const void*)k_spmv_seg<float, false>);
-  occ((const void*)k_spmv_seg<float, true>);
+  occ((const void*)k_spmv_seg<double, false, false>);
+  occ((const void*)k_spmv_seg<double, true, false>);
+  occ((const void*)k_spmv_seg<float, false, false>);
+  occ((const void*)k_spmv_seg<float, true, false>);
+  occ((const void*)k_spmv_seg<double, false, true>);
+  occ((const void*)k_spmv_seg<double, true, true>);
   per_sm = std::max(1, per_sm);
   *n_warps = sm_count() * per_sm * (SEG_NT / 32);
   return SME_OK;
@@ -437,4 +523,22 @@ SME_API int sme_spmv_seg(int dtype, int32_t n_warps, const uint32_t* pk, const v
   if (dtype == SME_F64)
     return launch_seg<double>(n_warps, pk, (const double*)val, hdr, plan, (const double*)xs, (double*)y, accumulate, s);
   return launch_seg<float>(n_warps, pk, (const float*)val, hdr, plan, (const float*)xs, (float*)y, accumulate, s);
+}
+
+// The last pass of one iterative step with the fused epilogue (see SegEpi): out[qinv[r]] =
+// scale[0] * (y[r] + this pass), partials[n_warps] scratch, ticket (uint32, zero-initialised
+// once; left zero), result[2] = {1/sqrt(sum v^2), sum v^2}.  accumulate = 0 for a
+// one-panel layout.  The layout must hold an entry or explicit zero for every row in
+// this panel (sme_seg_positions with full_last = 1).  f64 only.
+SME_API int sme_spmv_seg_epi(int dtype, int32_t n_warps, const uint32_t* pk, const void* val, const int32_t* hdr,
+                             const int32_t* plan, const void* xs, void* y, int accumulate, void* out,
+                             const int32_t* qinv, const double* scale, double* partials, uint32_t* ticket,
+                             double* result, sme_stream_t stream) {
+  SME_REQUIRE(dtype == SME_F64, "the fused epilogue is f64 only");
+  SME_REQUIRE(n_warps >= 1 && pk && val && hdr && plan && out && scale && partials && ticket && result,
+              "bad arguments");
+  SME_REQUIRE((((uintptr_t)pk | (uintptr_t)val) & 15) == 0, "pk/val must be 16-byte aligned");
+  const SegEpi<double> e{(double*)out, qinv, scale, partials, ticket, result};
+  return launch_seg<double>(n_warps, pk, (const double*)val, hdr, plan, (const double*)xs, (double*)y, accumulate,
+                            as_stream(stream), &e);
 }

@@ -13,6 +13,15 @@ PermutedOperator keeps the iterate in permuted coordinates:
 so an iteration costs one SpMV on B plus one gather, instead of two vector
 permutations; with a symmetric permutation (p_c = p_r, B = P A P^T) q is the
 identity and no gather is needed (the SPD case CG requires).
+
+Folding (default).  The gather by q is a FIXED permutation, so it can be folded
+into the matrix once instead of being paid every iteration: iterating in row-
+permuted coordinates u_k = P_r x_k gives u_{k+1} = (P_r A P_r^-1) u_k, i.e. the
+row+column permuted operator of a ROW_COLUMN_PERMUTE strategy is, for repeated
+application, the symmetric permutation by p_r (a random row AND column
+relabelling: the same maximal-entropy structure).  The operator then builds
+permute_csr(A, p_r, p_r) once and an iteration is just the SpMV (fold=False
+keeps B = P_r A P_c and the per-iteration gather).
 """
 
 from __future__ import annotations
@@ -39,10 +48,13 @@ class PermutedOperator:
     """y = A x applied through B = P_r A P_c in permuted coordinates."""
 
     def __init__(self, A: CsrMatrix, p_r: Permutation | None = None, p_c: Permutation | None = None,
-                 kernel: str = "auto"):
+                 kernel: str = "auto", fold: bool = True):
         if A.n_rows != A.n_cols:
             raise ValueError("iterative drivers need a square matrix")
         self.A, self.kernel = A, kernel
+        self.folded = fold and p_r is not None and p_c is not None and not (p_r == p_c)
+        if self.folded:
+            p_c = p_r  # the gather by q = p_r o p_c^-1 folded into the columns (module docstring)
         self.p_r, self.p_c = p_r, p_c
         self.B = permute_csr(A, p_r, p_c) if (p_r is not None or p_c is not None) else A
         self.q = None  # gather index mapping B z back into permuted coordinates
@@ -71,6 +83,19 @@ class PermutedOperator:
         _lib.call("sme_gather", _cuda.sme_dtype(z), self.n, ptr(self.p_c.d_forward), ptr(z), ptr(out), stream())
         return out
 
+    def fused_layout(self):
+        """The seg layout (with the full last panel) for the fused power-iteration
+        epilogue, or None when the operator's kernel is not 'seg' or values are not f64."""
+        from .kernels import auto_kernel
+        from .seg import seg_of
+
+        kern = auto_kernel(self.B) if self.kernel == "auto" else self.kernel
+        if kern != "seg" or self.dtype != torch.float64:
+            return None
+        if not hasattr(self, "_qinv"):
+            self._qinv = Permutation(self.q, _trusted=True).d_inverse if self.q is not None else None
+        return seg_of(self.B, full_last=True)
+
     def apply(self, z: torch.Tensor, out: torch.Tensor) -> None:
         """out = P_c^-1 A P_c z (stream-ordered; no allocation: graph-capturable)."""
         if self.q is None:
@@ -87,9 +112,16 @@ def _ident(n: int) -> Permutation:
 
 
 class PowerIteration:
-    """x_{k+1} = A x_k / ||A x_k|| (2-norm); eigenvalue estimate ||A x_k||."""
+    """x_{k+1} = A x_k / ||A x_k|| (2-norm); eigenvalue estimate ||A x_k||.
 
-    def __init__(self, op: PermutedOperator, x0):
+    Fused mode (seg operators, f64): one step is the operator's panel passes with
+    the BLAS-1 work folded into the last pass (sme_spmv_seg_epi): the iterate is
+    kept unnormalised, w_{k+1} = (B w_k) / ||w_k|| scattered straight into
+    permuted coordinates, and ||w_{k+1}||^2 (the eigenvalue estimate squared) and
+    the next scale come out of the same launch — no gather, dot or scale kernels.
+    Otherwise: SpMV, gather, dot, scale (blas1.cu)."""
+
+    def __init__(self, op: PermutedOperator, x0, fused: bool | None = None):
         self.op = op
         self.z = op.to_permuted(x0)
         self.y = torch.empty_like(self.z)
@@ -102,8 +134,23 @@ class PowerIteration:
         # normalise x0
         _lib.call("sme_dot", dt, op.n, ptr(self.z), ptr(self.z), ptr(self.partial), ptr(self.norm2), ptr(self.scal), 3, s)
         _lib.call("sme_scale", dt, op.n, ptr(self.z), ptr(self.z), ptr(self.scal), 3, s)
+        self.lay = op.fused_layout() if fused is not False else None
+        if fused and self.lay is None:
+            raise ValueError("the fused power iteration needs a 'seg' operator with f64 values")
+        self.fused = self.lay is not None
+        if self.fused:
+            self.w = [self.z, self.y]  # iterate ping-pongs between the two
+            self.cur = 0
+            self.res = torch.tensor([1.0, 0.0], dtype=torch.float64, device=op.dev)  # {scale, ||w||^2}
+            self.epi_partials = torch.zeros(self.lay.n_warps, dtype=torch.float64, device=op.dev)
+            self.ticket = torch.zeros(1, dtype=torch.int32, device=op.dev)
 
     def _step(self) -> None:
+        if self.fused:
+            a, b = self.w[self.cur], self.w[1 - self.cur]
+            self.lay.epi_pass(a, self.op._tmp, b, self.op._qinv, self.res, self.epi_partials, self.ticket, self.res)
+            self.cur = 1 - self.cur
+            return
         dt = _cuda.sme_dtype(self.z)
         self.op.apply(self.z, self.y)
         _lib.call("sme_dot", dt, self.op.n, ptr(self.y), ptr(self.y), ptr(self.partial), ptr(self.norm2),
@@ -111,13 +158,19 @@ class PowerIteration:
         _lib.call("sme_scale", dt, self.op.n, ptr(self.z), ptr(self.y), ptr(self.scal), 3, stream())
 
     def capture(self, steps: int) -> None:
-        """Record `steps` iterations into one CUDA graph (after one eager warm-up step)."""
+        """Record `steps` iterations into one CUDA graph (after one eager warm-up step);
+        fused mode alternates two buffers, so it records an even number of steps."""
+        if self.fused and steps % 2:
+            raise ValueError("the fused power iteration captures an even number of steps")
         self._step()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
+        start = getattr(self, "cur", 0)
         with torch.cuda.graph(g):
             for _ in range(steps):
                 self._step()
+        if self.fused:
+            self.cur = start  # capture does not run the steps; replays leave the iterate where it was
         self.graph, self.graph_steps = g, steps
 
     def run(self, steps: int) -> None:
@@ -130,9 +183,12 @@ class PowerIteration:
 
     @property
     def eigenvalue(self) -> float:
-        return math.sqrt(float(self.norm2.item()))
+        return math.sqrt(float((self.res[1] if self.fused else self.norm2).item()))
 
     def x(self) -> torch.Tensor:
+        if self.fused:  # the stored iterate is unnormalised: x = w / ||w||
+            z = self.w[self.cur] * self.res[0]
+            return self.op.from_permuted(z)
         return self.op.from_permuted(self.z)
 
 

@@ -44,7 +44,7 @@ def auto_seg_panels(m: CsrMatrix, l2_fraction: float = 0.38) -> int:
 class SegLayout:
     """P column panels of a CsrMatrix in the segmented-chunk layout."""
 
-    def __init__(self, m: CsrMatrix, n_panels: int, n_warps: int | None = None):
+    def __init__(self, m: CsrMatrix, n_panels: int, n_warps: int | None = None, full_last: bool = False):
         P, n = int(n_panels), m.n_rows
         if P < 1 or P > max(1, m.n_cols):
             raise ValueError("panel count must lie in [1, n_cols]")
@@ -59,7 +59,9 @@ class SegLayout:
         self.bounds = torch.from_numpy(bounds).to(dev)
         ws = _cuda.workspace(_lib.query_size("sme_seg_workspace_size", n, P))
         pos = torch.empty(P * (n + 1), dtype=torch.int32, device=dev)
-        _lib.call("sme_seg_positions", n, ptr(m.d_row_ptr), ptr(m.d_col_idx), P, ptr(self.bounds), ptr(pos), ptr(ws),
+        self.full_last = bool(full_last)
+        _lib.call("sme_seg_positions", n, ptr(m.d_row_ptr), ptr(m.d_col_idx), P, ptr(self.bounds), int(full_last),
+                  ptr(pos), ptr(ws),
                   ws.numel(), s)
         ent = pos.view(P, n + 1)[:, -1].to(torch.int64).cpu().numpy()
         offs = np.zeros(P + 1, dtype=np.int64)
@@ -93,6 +95,26 @@ class SegLayout:
         _lib.call("sme_spmv_seg", _cuda.sme_dtype(self.val), self.n_warps, ptr(self.pk) + 4 * o, ptr(self.val) + vb * o,
                   ptr(self.hdr) + 4 * (o // CHUNK), ptr(self.plans) + 4 * p * (self.n_warps + 1),
                   ptr(xd) + vb * int(self.bounds_host[p]), ptr(y), int(p > 0), stream())
+
+    def epi_pass(self, xd: torch.Tensor, y: torch.Tensor, out: torch.Tensor, qinv: torch.Tensor | None,
+                 scal: torch.Tensor, partials: torch.Tensor, ticket: torch.Tensor, result: torch.Tensor) -> None:
+        """Passes 0..P-2 into y, then the last pass with the fused iteration epilogue
+        (sme_spmv_seg_epi): out[qinv[r]] = scal[0] * (A x)[r], result = {1/||out||, ||out||^2}."""
+        if not self.full_last:
+            raise ValueError("the fused epilogue needs a layout built with full_last=True")
+        P = self.n_panels
+        for p in range(P - 1):
+            self._window(p, xd)
+            self._pass(p, xd, y)
+        self._window(P - 1, xd)
+        vb = self.val.element_size()
+        o = int(self.offsets[P - 1])
+        _lib.call("sme_spmv_seg_epi", _cuda.sme_dtype(self.val), self.n_warps, ptr(self.pk) + 4 * o,
+                  ptr(self.val) + vb * o, ptr(self.hdr) + 4 * (o // CHUNK),
+                  ptr(self.plans) + 4 * (P - 1) * (self.n_warps + 1), ptr(xd) + vb * int(self.bounds_host[P - 1]),
+                  ptr(y), int(P > 1), ptr(out), ptr(qinv), ptr(scal), ptr(partials), ptr(ticket), ptr(result),
+                  stream())
+        self._window(None, None)
 
     def _window(self, p: int | None, xd: torch.Tensor | None) -> None:
         if not self.persist:
@@ -156,12 +178,12 @@ class SegLayout:
         return self.n_panels
 
 
-def seg_of(m: CsrMatrix, n_panels: int | None = None) -> SegLayout:
+def seg_of(m: CsrMatrix, n_panels: int | None = None, full_last: bool = False) -> SegLayout:
     """The cached segmented-chunk layout of m (built on first use)."""
     P = n_panels or m._cache.get("seg_panels") or auto_seg_panels(m)
-    key = ("seg", P)
+    key = ("seg", P, bool(full_last))
     if key not in m._cache:
-        lay = SegLayout(m, P)
+        lay = SegLayout(m, P, full_last=full_last)
         from .panels import device_info
 
         slice_bytes = int(max(np.diff(lay.bounds_host))) * m.d_values.element_size()

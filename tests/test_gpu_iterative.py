@@ -16,13 +16,15 @@ def bits(t):
     return t.detach().cpu().numpy().view(np.uint64)
 
 
+@pytest.mark.parametrize("fold", [True, False])
 @pytest.mark.parametrize("kernel", ["auto", "stream", "merge"])
-def test_power_iteration_rc_permuted_matches_oracle(kernel):
+def test_power_iteration_rc_permuted_matches_oracle(kernel, fold):
     g = 20
     A = synth.laplacian5(g)
     n = A.n_rows
     p_r, p_c = P.random_permutation(n, 3), P.random_permutation(n, 4)  # independent (ROW_COLUMN_PERMUTE)
-    op = PermutedOperator(A, p_r, p_c, kernel=kernel)
+    op = PermutedOperator(A, p_r, p_c, kernel=kernel, fold=fold)
+    assert op.folded == fold and (op.q is None) == fold
     x0 = O.input_vector(0, n)
     pi = PowerIteration(op, x0)
     pi.run(60)
@@ -63,4 +65,63 @@ def test_cg_symmetric_permutation_matches_oracle():
     # the solution solves A x = b
     assert O.relative_error(O.spmv_csr(ptr, col, val, x), b) <= 1e-6
     with pytest.raises(ValueError, match="symmetric"):
-        ConjugateGradient(PermutedOperator(A, p, P.random_permutation(n, 10)), b)
+        ConjugateGradient(PermutedOperator(A, p, P.random_permutation(n, 10), fold=False), b)
+    # a ROW_COLUMN pair folds into the symmetric permutation by p_r: CG applies
+    cg2 = ConjugateGradient(PermutedOperator(A, p, P.random_permutation(n, 10)), b)
+    cg2.run(201)
+    assert O.relative_error(cg2.solution().cpu().numpy(), x_ref) <= 1e-8
+
+
+def _seg_op(A, p_r, p_c, panels, fold=True):
+    op = PermutedOperator(A, p_r, p_c, kernel="seg", fold=fold)
+    op.B._cache["seg_panels"] = panels
+    return op
+
+
+@pytest.mark.parametrize("panels", [1, 3])
+@pytest.mark.parametrize("perm", ["rc", "rc_unfolded", "symmetric", "none"])
+def test_fused_power_iteration_matches_oracle(panels, perm):
+    """sme_spmv_seg_epi: SpMV + scatter into permuted coordinates + deterministic
+    norm in one launch; same eigenpair as the numpy loop over spmv_csr."""
+    g = 24
+    A = synth.laplacian5(g)
+    n = A.n_rows
+    if perm.startswith("rc"):
+        p_r, p_c = P.random_permutation(n, 3), P.random_permutation(n, 4)
+    elif perm == "symmetric":
+        p_r = p_c = P.random_permutation(n, 5)
+    else:
+        p_r = p_c = None
+    op = _seg_op(A, p_r, p_c, panels, fold=perm != "rc_unfolded")
+    assert (op.q is not None) == (perm == "rc_unfolded")
+    x0 = O.input_vector(0, n)
+    pi = PowerIteration(op, x0, fused=True)
+    assert pi.fused and pi.lay.n_panels == panels
+    pi.run(60)
+    ptr, col, val = O.laplacian5(g)
+    x_ref, lam_ref = O.power_iteration(ptr, col, val, x0, 60)
+    assert abs(pi.eigenvalue - lam_ref) <= 1e-10 * lam_ref
+    assert O.relative_error(pi.x().cpu().numpy(), x_ref) <= 1e-9
+    unfused = PowerIteration(op, x0, fused=False)
+    unfused.run(60)
+    assert abs(pi.eigenvalue - unfused.eigenvalue) <= 1e-12 * lam_ref
+
+
+def test_fused_power_iteration_graph_is_bitwise_eager_and_deterministic():
+    A = synth.random_rows(20_000, 20_000, 7, seed=3) if hasattr(synth, "random_rows") else synth.laplacian5(140)
+    n = A.n_rows
+    op = _seg_op(A, P.random_permutation(n, 1), P.random_permutation(n, 2), 2)
+    x0 = O.input_vector(5, n)
+    eager = PowerIteration(op, x0, fused=True)
+    eager.run(41)
+    graphed = PowerIteration(op, x0, fused=True)
+    graphed.capture(10)  # one eager warm-up step + a 10-step graph
+    graphed.run(40)
+    again = PowerIteration(op, x0, fused=True)
+    again.run(41)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(eager.x()), bits(graphed.x()))
+    assert np.array_equal(bits(eager.x()), bits(again.x()))
+    assert eager.eigenvalue == graphed.eigenvalue == again.eigenvalue
+    with pytest.raises(ValueError, match="even"):
+        PowerIteration(op, x0, fused=True).capture(3)
