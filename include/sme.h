@@ -296,8 +296,10 @@ int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const int3
                  const int64_t* d_offsets, const int64_t* h_offsets, uint32_t* d_pk, void* d_out_val,
                  int32_t* d_hdr, const void* d_ws, sme_stream_t stream);
 int sme_spmv_seg_warps(int32_t* n_warps);
-/* Kernel variant (process-wide): 0 = the SpMV (default), 3 = bound probe (the chunk
- * stream and gathers without the row reduction; timing only, not y = A x). */
+/* Kernel variant (process-wide): 0 = the SpMV (default; accumulating passes add
+ * with RED.ADD at L2), 3 = bound probe (the chunk stream and gathers without the
+ * row reduction; timing only, not y = A x), 5 = accumulating passes load y, add,
+ * store (same bits, 3-4 % slower on C4). */
 int sme_spmv_seg_set_mode(int mode);
 int sme_seg_plan(int64_t n_rows, const int32_t* d_pos_panel, int32_t n_warps, int32_t* d_plan,
                  sme_stream_t stream);

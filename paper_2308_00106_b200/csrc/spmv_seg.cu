@@ -26,7 +26,9 @@
 //     open tail to the next lane (a longer chain of whole-lane rows takes a
 //     segmented scan, ballot-detected and rare);
 //   * the lane holding a row's last entry writes (panel 0) or accumulates
-//     (panels p > 0) y; its y read is issued with the gathers.
+//     (panels p > 0) y — with a fire-and-forget RED.ADD.F64 at L2, so no y read
+//     crosses back to the SM (each row has one adder per pass and the passes are
+//     ordered launches: deterministic, same bits as load + add + store).
 //
 // Layout of one panel (columns [b_p, b_{p+1})), n_pad = round_up(entries, 128):
 //   pk[n_pad]  uint32  (col - b_p) << 9 | end << 8 | (row - hdr[chunk])
@@ -237,7 +239,7 @@ __device__ __forceinline__ void seg_epi_finish_impl(const SegEpi<T>& epi, int32_
   }
 }
 
-template <typename T, bool ACC, bool EPI>
+template <typename T, bool ACC, bool EPI, bool RED = false>
 __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk, const T* __restrict__ val,
                                                 const int32_t* __restrict__ hdr, const int32_t* __restrict__ plan,
                                                 int warp, const T* __restrict__ xs, T* __restrict__ y,
@@ -271,7 +273,7 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
       xv[k] = (in && lc != SEG_MARK) ? __ldg(xs + lc) : T(0);
       // accumulating passes skip explicit zeros (their rows have nothing to add)
       const bool emit = in && (cur.w[k] & SEG_END) && (EPI || !(ACC && lc == SEG_MARK));
-      yv[k] = (ACC && emit) ? y[cur.h + (int)(cur.w[k] & SEG_DMASK)] : T(0);
+      yv[k] = (ACC && !RED && emit) ? y[cur.h + (int)(cur.w[k] & SEG_DMASK)] : T(0);
     }
     // in-lane runs: run[k] = sum of the row segment ending at k that starts in this lane
     T run[4];
@@ -323,7 +325,10 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
           ss += (double)v * (double)v;
         } else if (!(ACC && lc == SEG_MARK)) {
           const int r = cur.h + (int)(cur.w[k] & SEG_DMASK);
-          y[r] = ACC ? yv[k] + fin : fin;
+          if (ACC && RED)
+            atomicAdd(y + r, fin);  // RED.ADD at L2: one add per row per pass, passes ordered: deterministic
+          else
+            y[r] = ACC ? yv[k] + fin : fin;
         }
       }
     }
@@ -334,7 +339,7 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
   return ss;
 }
 
-template <typename T, bool ACC, bool EPI>
+template <typename T, bool ACC, bool EPI, bool RED = false>
 __global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict__ pk, const T* __restrict__ val,
                                                    const int32_t* __restrict__ hdr, const int32_t* __restrict__ plan,
                                                    int32_t n_warps, const T* __restrict__ xs, T* __restrict__ y,
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict_
     return;
   }
   if (warp >= n_warps) return;
-  seg_warp_body<T, ACC, false>(pk, val, hdr, plan, warp, xs, y, epi);
+  seg_warp_body<T, ACC, false, RED>(pk, val, hdr, plan, warp, xs, y, epi);
 }
 
 
@@ -387,7 +392,9 @@ __global__ void __launch_bounds__(SEG_NT) k_seg_probe(const uint32_t* __restrict
   }
 }
 
-static int s_seg_mode = 0;  // 0 = SpMV (default), 3 = bound probe
+// 0 = SpMV (default: accumulating passes add with RED.ADD.F64 at L2, C4 -3.8 %),
+// 3 = bound probe, 5 = accumulating passes load y, add, store (the previous default)
+static int s_seg_mode = 0;
 
 template <typename T>
 int launch_seg(int32_t n_warps, const uint32_t* pk, const T* val, const int32_t* hdr, const int32_t* plan,
@@ -401,8 +408,10 @@ int launch_seg(int32_t n_warps, const uint32_t* pk, const T* val, const int32_t*
       k_spmv_seg<T, false, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
   } else if (s_seg_mode == 3)
     k_seg_probe<T><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y);
-  else if (accumulate)
+  else if (accumulate && s_seg_mode == 5)
     k_spmv_seg<T, true, false><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
+  else if (accumulate)
+    k_spmv_seg<T, true, false, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
   else
     k_spmv_seg<T, false, false><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
   SME_CHECK_LAUNCH("k_spmv_seg");
@@ -479,7 +488,8 @@ SME_API int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* row_ptr, cons
 // Kernel variant (process-wide; experiments): 0 = the SpMV, 3 = bound probe (the
 // chunk stream and gathers without the row reduction; timing only, not y = A x).
 SME_API int sme_spmv_seg_set_mode(int mode) {
-  SME_REQUIRE(mode == 0 || mode == 3, "mode must be 0 (SpMV) or 3 (bound probe)");
+  SME_REQUIRE(mode == 0 || mode == 3 || mode == 5,
+              "mode must be 0 (SpMV), 3 (bound probe) or 5 (accumulating passes with load + store)");
   s_seg_mode = mode;
   return SME_OK;
 }
