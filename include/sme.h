@@ -319,6 +319,27 @@ int sme_spmv_seg_epi(int dtype, int32_t n_warps, const uint32_t* d_pk, const voi
                      const int32_t* d_plan, const void* d_xs, void* d_y, int accumulate, void* d_out,
                      const int32_t* d_qinv, const double* d_scale, double* d_partials, uint32_t* d_ticket,
                      double* d_result, sme_stream_t stream);
+/* The same epilogue for one row shard of a multi-GPU power iteration (rowshard.py):
+ * v is stored at global index row_offset + r of d_out (this rank's full-length
+ * next iterate) and of every buffer in d_peers[n_peers] (the other ranks' next
+ * iterates, opened with sme_ipc_open — stores over NVLink): the all-gather of the
+ * iterate (ncclAllGather in the unfused path) rides in the SpMV
+ * epilogue.  d_result[1] = this shard's sum of v^2 (the caller all-reduces it). */
+int sme_spmv_seg_epi_peers(int dtype, int32_t n_warps, const uint32_t* d_pk, const void* d_val,
+                           const int32_t* d_hdr, const int32_t* d_plan, const void* d_xs, void* d_y,
+                           int accumulate, void* d_out, int64_t row_offset, void* const* d_peers, int32_t n_peers,
+                           const double* d_scale, double* d_partials, uint32_t* d_ticket, double* d_result,
+                           sme_stream_t stream);
+
+/* CUDA IPC buffers for the fused exchange (ipc.cu): whole cudaMalloc allocations
+ * whose handles (SME_IPC_HANDLE_BYTES bytes) are exchanged between the ranks of a
+ * node (torch.distributed all_gather_object) and opened by the peers. */
+#define SME_IPC_HANDLE_BYTES 64
+int sme_ipc_malloc(size_t bytes, void** d_ptr);
+int sme_ipc_free(void* d_ptr);
+int sme_ipc_get_handle(void* d_ptr, uint8_t* handle);
+int sme_ipc_open(const uint8_t* handle, void** d_ptr);
+int sme_ipc_close(void* d_ptr);
 
 /* Merge kernel selection (process-wide; tests and experiments): 1 = persistent
  * TMA-pipelined kernel (needs 16-byte aligned row_ptr/col_idx/values), 0 = one

@@ -73,6 +73,12 @@ SIGNATURES: dict[str, list] = {
     "sme_seg_plan": [i64, p, i32, p, p],
     "sme_spmv_seg": [C.c_int, i32, p, p, p, p, p, p, C.c_int, p],
     "sme_spmv_seg_epi": [C.c_int, i32, p, p, p, p, p, p, C.c_int, p, p, p, p, p, p, p],
+    "sme_spmv_seg_epi_peers": [C.c_int, i32, p, p, p, p, p, p, C.c_int, p, i64, p, i32, p, p, p, p, p],
+    "sme_ipc_malloc": [sz, C.POINTER(C.c_void_p)],
+    "sme_ipc_free": [p],
+    "sme_ipc_get_handle": [p, p],
+    "sme_ipc_open": [p, C.POINTER(C.c_void_p)],
+    "sme_ipc_close": [p],
     "sme_spmv_stream_warps": [i64, i64, C.POINTER(C.c_int32)],
     "sme_spmv_stream_set_mode": [C.c_int],
     "sme_spmv_stream_set_row_cost": [C.c_int],

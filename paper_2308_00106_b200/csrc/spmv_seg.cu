@@ -208,6 +208,9 @@ struct SegEpi {
   double* partials;  // [n_warps]
   unsigned* ticket;  // zero before the launch; reset by the last CTA
   double* result;    // [2]
+  T* const* peers;   // [n_peers] other ranks' copies of out (peer memory over NVLink), or null
+  int n_peers;
+  int64_t row_offset;  // global index of this shard's row 0 in out / peers
 };
 
 // last-CTA reduction of the warp partials (fixed order) -> result, next scale
@@ -321,7 +324,9 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
           // every row ends exactly once in the epilogue pass (explicit zeros included)
           const int r = cur.h + (int)(cur.w[k] & SEG_DMASK);
           const T v = sc * (ACC ? yv[k] + fin : fin);
-          epi.out[epi.qinv ? epi.qinv[r] : r] = v;
+          const int64_t g = (int64_t)(epi.qinv ? epi.qinv[r] : r) + epi.row_offset;
+          epi.out[g] = v;
+          for (int d = 0; d < epi.n_peers; ++d) epi.peers[d][g] = v;  // the exchange, row by row
           ss += (double)v * (double)v;
         } else if (!(ACC && lc == SEG_MARK)) {
           const int r = cur.h + (int)(cur.w[k] & SEG_DMASK);
@@ -352,6 +357,7 @@ __global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict_
     if (warp < n_warps) ss = seg_warp_body<T, ACC, true>(pk, val, hdr, plan, warp, xs, y, epi);
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
     if (lane == 0 && warp < n_warps) epi.partials[warp] = ss;
+    if (epi.n_peers > 0) __threadfence_system();  // peer stores performed before this launch completes
     seg_epi_finish_impl(epi, n_warps);
     return;
   }
@@ -548,7 +554,29 @@ SME_API int sme_spmv_seg_epi(int dtype, int32_t n_warps, const uint32_t* pk, con
   SME_REQUIRE(n_warps >= 1 && pk && val && hdr && plan && out && scale && partials && ticket && result,
               "bad arguments");
   SME_REQUIRE((((uintptr_t)pk | (uintptr_t)val) & 15) == 0, "pk/val must be 16-byte aligned");
-  const SegEpi<double> e{(double*)out, qinv, scale, partials, ticket, result};
+  const SegEpi<double> e{(double*)out, qinv, scale, partials, ticket, result, nullptr, 0, 0};
+  return launch_seg<double>(n_warps, pk, (const double*)val, hdr, plan, (const double*)xs, (double*)y, accumulate,
+                            as_stream(stream), &e);
+}
+
+// The same epilogue pass for one row shard of a multi-GPU iteration: v is stored at
+// global index row_offset + r of `out` (this rank's full-length next iterate) AND of
+// each of the n_peers buffers in d_peers (the other ranks' next iterates, opened
+// with sme_ipc_open: stores over NVLink), i.e. the all-gather of the iterate is
+// fused into the SpMV epilogue.  result[1] is this shard's sum of v^2 (the caller
+// all-reduces it); qinv must be null.
+SME_API int sme_spmv_seg_epi_peers(int dtype, int32_t n_warps, const uint32_t* pk, const void* val,
+                                   const int32_t* hdr, const int32_t* plan, const void* xs, void* y, int accumulate,
+                                   void* out, int64_t row_offset, void* const* d_peers, int32_t n_peers,
+                                   const double* scale, double* partials, uint32_t* ticket, double* result,
+                                   sme_stream_t stream) {
+  SME_REQUIRE(dtype == SME_F64, "the fused epilogue is f64 only");
+  SME_REQUIRE(n_warps >= 1 && pk && val && hdr && plan && out && scale && partials && ticket && result &&
+                  row_offset >= 0 && n_peers >= 0 && (n_peers == 0 || d_peers),
+              "bad arguments");
+  SME_REQUIRE((((uintptr_t)pk | (uintptr_t)val) & 15) == 0, "pk/val must be 16-byte aligned");
+  const SegEpi<double> e{(double*)out, nullptr, scale, partials, ticket, result, (double* const*)d_peers, n_peers,
+                         row_offset};
   return launch_seg<double>(n_warps, pk, (const double*)val, hdr, plan, (const double*)xs, (double*)y, accumulate,
                             as_stream(stream), &e);
 }

@@ -195,3 +195,144 @@ def require_cuda_rank(local_rank: int) -> torch.device:
     _cuda.require_cuda()
     torch.cuda.set_device(local_rank)
     return torch.device("cuda", local_rank)
+
+
+# ---------------------------------------------------------------------------
+# Multi-GPU power iteration with the exchange fused into the SpMV epilogue
+# ---------------------------------------------------------------------------
+class IpcBuffer:
+    """A whole cudaMalloc allocation (sme_ipc_malloc) shared with the other ranks of the
+    node through a CUDA IPC handle, viewed as a torch tensor without a copy."""
+
+    def __init__(self, n: int, device: torch.device, dtype=torch.float64):
+        import ctypes
+
+        self.n, self.dtype = int(n), dtype
+        esize = torch.empty((), dtype=dtype).element_size()
+        p = ctypes.c_void_p()
+        _lib.call("sme_ipc_malloc", max(1, self.n) * esize, ctypes.byref(p))
+        self.ptr = int(p.value)
+        typestr = {torch.float64: "<f8", torch.float32: "<f4"}[dtype]
+        cai = {"shape": (self.n,), "typestr": typestr, "data": (self.ptr, False), "version": 3, "strides": None}
+        self.tensor = torch.as_tensor(type("CAI", (), {"__cuda_array_interface__": cai})(), device=device)
+
+    def handle(self) -> bytes:
+        import ctypes
+
+        buf = (ctypes.c_uint8 * 64)()
+        _lib.call("sme_ipc_get_handle", self.ptr, buf)
+        return bytes(buf)
+
+    @staticmethod
+    def open(handle: bytes) -> int:
+        import ctypes
+
+        p = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+        _lib.call("sme_ipc_open", buf, ctypes.byref(p))
+        return int(p.value)
+
+    def free(self) -> None:
+        if self.ptr:
+            self.tensor = None
+            _lib.call("sme_ipc_free", self.ptr)
+            self.ptr = 0
+
+
+class DistributedPowerIteration:
+    """Row-sharded power iteration on the symmetric permutation C = P A P^-1 (the
+    folded ROW_COLUMN operator of iterative.py), one rank per GPU.
+
+    Every rank keeps the FULL iterate in two IPC-shared buffers (ping-pong).  One
+    step is the shard's seg panel passes, the last with the epilogue of
+    sme_spmv_seg_epi_peers: each finished row v = s * (C w)[r] is stored into this
+    rank's next buffer and, over NVLink, into every peer's — the all-gather of the
+    iterate is fused into the SpMV, row by row, instead of following it.  Then one
+    8-byte all-reduce of the shards' sums of squares, which is also the step's
+    barrier: no rank starts writing the other buffer before every rank has finished
+    reading it.  Same eigenpair as the one-GPU PowerIteration (rows are disjoint,
+    so nothing else is exchanged).
+    """
+
+    def __init__(self, A: CsrMatrix, p, x0, group=None):
+        from .iterative import PermutedOperator
+        from .seg import seg_of
+
+        self.group = group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        dev = A.d_row_ptr.device
+        op = PermutedOperator(A, p, p)  # C = permute_csr(A, p, p)
+        self.op, self.n = op, A.n_rows
+        plan = ShardPlan(self.n, self.n, self.world)
+        lo, hi = plan.row_range(self.rank)
+        self.row_lo, self.row_hi = lo, hi
+        Cm = op.B
+        p0, p1 = int(Cm.d_row_ptr[lo]), int(Cm.d_row_ptr[hi])
+        local = CsrMatrix._from_device(hi - lo, self.n, (Cm.d_row_ptr[lo : hi + 1] - p0).contiguous(),
+                                       Cm.d_col_idx[p0:p1].clone(), Cm.d_values[p0:p1].clone())
+        self.local = local
+        self.lay = seg_of(local, full_last=True)
+        self.bufs = [IpcBuffer(self.n, dev), IpcBuffer(self.n, dev)]
+        handles = [b.handle() for b in self.bufs]
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, handles, group=group)
+        self.opened: list[int] = []
+        self.peers = []
+        for b in range(2):
+            ptrs = []
+            for j in range(self.world):
+                if j != self.rank:
+                    q = IpcBuffer.open(everyone[j][b])
+                    self.opened.append(q)
+                    ptrs.append(q)
+            self.peers.append(torch.tensor(ptrs or [0], dtype=torch.int64, device=dev))
+        z = op.to_permuted(x0)
+        z = z / torch.linalg.vector_norm(z)
+        self.bufs[0].tensor.copy_(z)
+        self.cur = 0
+        self.res = torch.tensor([1.0, 0.0], dtype=torch.float64, device=dev)
+        self.partials = torch.zeros(self.lay.n_warps, dtype=torch.float64, device=dev)
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.tmp = torch.empty(max(1, hi - lo), dtype=torch.float64, device=dev)
+        torch.cuda.synchronize()
+        dist.barrier(group=group)
+
+    def step(self) -> None:
+        lay, a, b = self.lay, self.bufs[self.cur].tensor, self.bufs[1 - self.cur]
+        P = lay.n_panels
+        for q in range(P - 1):
+            lay._window(q, a)
+            lay._pass(q, a, self.tmp)
+        lay._window(P - 1, a)
+        vb = 8
+        o = int(lay.offsets[P - 1])
+        _lib.call("sme_spmv_seg_epi_peers", _lib.SME_F64, lay.n_warps, ptr(lay.pk) + 4 * o, ptr(lay.val) + vb * o,
+                  ptr(lay.hdr) + 4 * (o // 128), ptr(lay.plans) + 4 * (P - 1) * (lay.n_warps + 1),
+                  ptr(a) + vb * int(lay.bounds_host[P - 1]), ptr(self.tmp), int(P > 1), b.ptr, self.row_lo,
+                  ptr(self.peers[1 - self.cur]), self.world - 1, ptr(self.res), ptr(self.partials), ptr(self.ticket),
+                  ptr(self.res), stream())
+        lay._window(None, None)
+        dist.all_reduce(self.res[1:2], group=self.group)  # global ||w||^2, and the step barrier
+        torch.rsqrt(self.res[1:2], out=self.res[0:1])
+        self.cur = 1 - self.cur
+
+    def run(self, steps: int) -> None:
+        for _ in range(steps):
+            self.step()
+
+    @property
+    def eigenvalue(self) -> float:
+        return float(self.res[1].sqrt().item())
+
+    def x(self) -> torch.Tensor:
+        return self.op.from_permuted(self.bufs[self.cur].tensor * self.res[0])
+
+    def close(self) -> None:
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)  # no peer still stores into our buffers
+        for q in self.opened:
+            _lib.call("sme_ipc_close", q)
+        self.opened = []
+        dist.barrier(group=self.group)
+        for buf in self.bufs:
+            buf.free()
