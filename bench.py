@@ -169,6 +169,17 @@ def cpu_sample_rows(n_rows: int, nnz: int) -> int:
     return max(1, min(n_rows, int(n_rows * CPU_SAMPLE_NNZ / max(1, nnz))))
 
 
+def cpu_model() -> str:
+    """The host CPU model (lscpu's 'Model name'), for the cpu_baseline record."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline_run(ptr, col, val, x, steps: int, warmup: int) -> dict:
     """The reference algorithm (oracle numpy port of kernels.py:59-128) on the host cores."""
     import oracle as O
@@ -247,6 +258,7 @@ def run_reference(args, cfg) -> dict:
         "data": "synthetic", "impl": "reference",
         "config": {"workload": cfg["workload"], "sample": sample},
         "cpu_baseline": {"value": round(v, 4), "unit": "GFLOP/s", "cores": res["cores"], "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": sample, "serial_gflops": round(res["gflops_serial"], 4)},
         "e2e": {"value": round(v, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -342,6 +354,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         x_h = xp.cpu().numpy().astype(np.float64)
         cs = cpu_baseline_run(ptr_h, col_h, val_h, x_h, steps=5, warmup=1)
         cpu = {"value": round(cs["gflops_parallel"], 4), "unit": "GFLOP/s", "cores": cs["cores"], "kind": "port",
+               "cpu_model": cpu_model(),
                "sample": f"rows [0, {R:,}) of the permuted matrix ({cs['nnz']:,} nnz), full permuted x, "
                          f"5 calls; reference algorithm (numpy reduceat, row-partitioned threads)",
                "serial_gflops": round(cs["gflops_serial"], 4)}
