@@ -207,6 +207,15 @@ int sme_hist2d_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d
                    const int32_t* d_col, int32_t bins_r, int32_t bins_c, int64_t* d_counts,
                    sme_stream_t stream);
 /* Same from COO triplets in any order (the reference's own input type). */
+/* Kernel selection of sme_hist2d_csr (process-wide; tests and experiments):
+ * 0 = lane-private u16 counters when bins_c <= 128 (default), 1 = the
+ * shared-memory window with warp-aggregated atomics, 2 = lane counters on one CTA. */
+int sme_hist2d_set_mode(int mode);
+/* Tiling of the lane-counter kernel (experiments): 0 = 864 threads x 4 int4 loads per
+ * lane (default; 768 x 4 when bins_r > ~1500), 1 = 768 x 4, 2 = 512 x 4 + next-iteration
+ * prefetch, 3 = 768 x 2 + prefetch, 4 = 640 x 4 + prefetch, 5 = 864 x 4, 6 = 864 x 2,
+ * 7 = 512 x 8. */
+int sme_hist2d_set_variant(int variant);
 int sme_hist2d_coo(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row,
                    const int32_t* d_col, int32_t bins_r, int32_t bins_c, int64_t* d_counts,
                    sme_stream_t stream);

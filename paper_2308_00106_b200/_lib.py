@@ -55,6 +55,8 @@ SIGNATURES: dict[str, list] = {
     "sme_csr_expand_rows": [i64, p, p, p],
     "sme_hist2d_csr": [i64, i64, i64, p, p, i32, i32, p, p],
     "sme_hist2d_coo": [i64, i64, i64, p, p, i32, i32, p, p],
+    "sme_hist2d_set_mode": [C.c_int],
+    "sme_hist2d_set_variant": [C.c_int],
     "sme_row_hist_csr": [i64, p, i32, p, p],
     "sme_entropy": [i64, p, f64, p, p, p],
     "sme_spmv_merge_tiles": [i64, i64, pi64],
