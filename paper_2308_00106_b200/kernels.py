@@ -282,6 +282,9 @@ def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None 
     return _y_out(y, mode)
 
 
+PIPELINE_BUFFERS = 2  # device x/y buffers of spmv_csr_pipelined (steps in flight)
+
+
 def spmv_csr_pipelined(m: CsrMatrix, xs, ys=None, kernel: str = "auto") -> list:
     """y_k = A x_k for a sequence of host vectors, with the PCIe copies of neighbouring
     steps overlapped: step k+1's x crosses host->device while step k computes and step
@@ -319,14 +322,15 @@ def spmv_csr_pipelined(m: CsrMatrix, xs, ys=None, kernel: str = "auto") -> list:
     main = torch.cuda.current_stream()
     h2d = torch.cuda.Stream(device=dev)
     d2h = torch.cuda.Stream(device=dev)
-    xb = [torch.empty(m.n_cols, dtype=m.dtype, device=dev) for _ in range(2)]
-    yb = [torch.empty(m.n_rows, dtype=m.dtype, device=dev) for _ in range(2)]
-    computed = [None, None]  # event: step using buffer b finished computing
-    copied_out = [None, None]  # event: y buffer b has been copied to the host
+    nb = PIPELINE_BUFFERS
+    xb = [torch.empty(m.n_cols, dtype=m.dtype, device=dev) for _ in range(nb)]
+    yb = [torch.empty(m.n_rows, dtype=m.dtype, device=dev) for _ in range(nb)]
+    computed = [None] * nb  # event: step using buffer b finished computing
+    copied_out = [None] * nb  # event: y buffer b has been copied to the host
     h2d.wait_stream(main)
     d2h.wait_stream(main)
     for k, x in enumerate(xs):
-        b = k & 1
+        b = k % nb
         xk = x.to(m.dtype) if x.dtype != m.dtype else x
         slice_ev = []
         with torch.cuda.stream(h2d):
