@@ -570,7 +570,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         return None
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
-    if tf.exists():
+    if tf.exists() and world == 1:  # the table holds 1-GPU captures (a shard moves less)
         try:
             traffic = json.loads(tf.read_text()).get(f"{args.config}/{resolved}")
         except Exception:
