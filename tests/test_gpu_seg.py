@@ -54,7 +54,7 @@ def decode(lay: SegLayout):
     return out
 
 
-def check_layout(lay, ptr, col, val):
+def check_layout(lay, ptr, col, val, full_last=False):
     n_rows = len(ptr) - 1
     rows_all = O.csr_to_coo_rows(ptr)
     for p, (rows, cols, vals, zero, end) in enumerate(decode(lay)):
@@ -68,7 +68,8 @@ def check_layout(lay, ptr, col, val):
         # explicit zeros: panel 0 every row without entries; later panels empty rows r % 2 == 0
         has = np.zeros(n_rows, bool)
         has[rows_all[sel]] = True
-        want_zero = np.flatnonzero(~has) if p == 0 else np.flatnonzero(~has & (np.arange(n_rows) % 2 == 0))
+        every = p == 0 or (full_last and p == lay.n_panels - 1)
+        want_zero = np.flatnonzero(~has) if every else np.flatnonzero(~has & (np.arange(n_rows) % 2 == 0))
         assert np.array_equal(rows[zero], want_zero), p
         # end flag exactly on the last entry of every row
         want_end = np.ones(rows.size, bool)
@@ -81,23 +82,24 @@ def check_layout(lay, ptr, col, val):
             assert np.all(ends - starts <= 255)
 
 
-def run_seg(m, x, n_panels, n_warps=None):
-    lay = SegLayout(m, n_panels, n_warps)
+def run_seg(m, x, n_panels, n_warps=None, full_last=False):
+    lay = SegLayout(m, n_panels, n_warps, full_last=full_last)
     xd = torch.as_tensor(x).to(m.d_values.device, m.dtype)
     y = torch.full((m.n_rows,), float("nan"), dtype=m.dtype, device=xd.device)  # every row must be written
     lay.spmv_into(xd, y)
     return lay, y.double().cpu().numpy()
 
 
+@pytest.mark.parametrize("full_last", [False, True])
 @pytest.mark.parametrize("n_panels", [1, 2, 3, 7])
-def test_layout_and_spmv_random_lengths(dev, rng, n_panels):
+def test_layout_and_spmv_random_lengths(dev, rng, n_panels, full_last):
     n_rows, n_cols = 3000, 5000
     lens = rng.integers(0, 60, n_rows)
     ptr, col, val = csr_from_lens(rng, lens, n_cols)
     m = P.CsrMatrix(n_rows, n_cols, ptr, col, val)
     x = rng.random(n_cols)
-    lay, y = run_seg(m, x, n_panels)
-    check_layout(lay, ptr, col, val)
+    lay, y = run_seg(m, x, n_panels, full_last=full_last)
+    check_layout(lay, ptr, col, val, full_last)
     assert O.relative_error(y, O.spmv_csr(ptr, col, val, x)) <= F64_TOL
 
 
@@ -221,3 +223,19 @@ def test_pipelined_host_stream_equals_per_vector_calls(dev, rng, kernel):
         assert O.relative_error(y.numpy(), O.spmv_csr(ptr, col, val, x.numpy())) <= F64_TOL
     with pytest.raises(ValueError):
         P.spmv_csr_pipelined(m, [torch.zeros(n + 1)])
+
+
+@pytest.mark.parametrize("n_panels", [1, 4])
+def test_very_long_rows(dev, rng, n_panels):
+    """Rows of 150k and 60k entries (a warp's range always holds whole rows, so one warp
+    walks them chunk by chunk with the carry) next to short and empty rows."""
+    n_rows, n_cols = 400, 200_000
+    lens = rng.integers(0, 5, n_rows)
+    lens[7], lens[300] = 150_000, 60_000
+    ptr, col, val = csr_from_lens(rng, lens, n_cols)
+    m = P.CsrMatrix(n_rows, n_cols, ptr, col, val)
+    x = rng.random(n_cols) * 2 - 1
+    for n_warps in (None, 5):
+        lay, y = run_seg(m, x, n_panels, n_warps)
+        check_layout(lay, ptr, col, val)
+        assert O.relative_error(y, O.spmv_csr(ptr, col, val, x)) <= F64_TOL
