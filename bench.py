@@ -696,6 +696,24 @@ def run_iterative(args, cfg) -> dict:
     step_ms = perm_ms / iters
     gflops = 2 * nnz / (step_ms * 1e-3) / 1e9
     total_perm = perm_s * 1e3 + perm_ms
+    # CG (the SPD solver of C5): symmetric permutation by p_r (the folded operator is SPD)
+    from paper_2308_00106_b200.iterative import ConjugateGradient
+
+    def run_cg(operator) -> tuple[float, float]:
+        cg = ConjugateGradient(operator, P.input_vector(1, n))
+        cg.capture(graph_steps)
+        for _ in range(args.warmup):
+            cg.graph.replay()
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        cg.run(iters)
+        c1.record()
+        torch.cuda.synchronize()
+        return c0.elapsed_time(c1) / iters, cg.residual_norm2
+
+    cg_p_ms, cg_p_rr = run_cg(op)
+    cg_u_ms, cg_u_rr = run_cg(PermutedOperator(A, None, None, kernel=args.kernel))
     return {
         "metric": METRIC + " — C5 iterative reuse", "value": round(gflops, 3), "unit": "GFLOP/s",
         "n_gpus": 1, "steps": iters, "warmup": args.warmup, "ms_per_step": round(step_ms, 5),
@@ -720,6 +738,11 @@ def run_iterative(args, cfg) -> dict:
                          "break_even_note": "setup is paid once; per-iteration ratio permuted/unpermuted = "
                                             f"{perm_ms / unperm_ms:.3f}"},
         "x_norm_check": float(torch.linalg.vector_norm(x_p).item()),
+        "cg": {"permuted_ms_per_iteration": round(cg_p_ms, 5), "unpermuted_ms_per_iteration": round(cg_u_ms, 5),
+               "residual_norm2_permuted": cg_p_rr, "residual_norm2_unpermuted": cg_u_rr,
+               "step": "permuted: seg passes with p.Ap fused into the last (sme_spmv_seg_epi_cg) + x,r update + "
+                       "p update; unpermuted: vector SpMV + dot + x,r update + p update; CUDA graphs",
+               "iterations": iters, "rhs": "input_vector(1, n)"},
         "iterations_total": 1 + args.warmup * graph_steps + iters,
         "clocks": clk, "gpu_launches": launches(pi_p) * iters,
     }

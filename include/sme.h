@@ -340,6 +340,15 @@ int sme_spmv_seg_epi_peers(int dtype, int32_t n_warps, const uint32_t* d_pk, con
                            const double* d_scale, double* d_partials, uint32_t* d_ticket, double* d_result,
                            sme_stream_t stream);
 
+/* The last pass of one CG step (iterative.py) with p.Ap fused in: d_out[r] = (A p)[r],
+ * sum d_out[r] * d_p[r] reduced deterministically, and the last CTA writes
+ * alpha = d_scal[0] / (p.Ap) into d_scal[1] (d_scal[0] = r.r, blas1.cu's CG
+ * scalars) — replaces sme_dot(p, Ap) after the SpMV.  d_xs = d_p + bounds of the
+ * last panel; needs a layout built with full_last = 1. */
+int sme_spmv_seg_epi_cg(int dtype, int32_t n_warps, const uint32_t* d_pk, const void* d_val, const int32_t* d_hdr,
+                        const int32_t* d_plan, const void* d_xs, const void* d_p, void* d_y, int accumulate,
+                        void* d_out, double* d_partials, uint32_t* d_ticket, double* d_scal, sme_stream_t stream);
+
 /* CUDA IPC buffers for the fused exchange (ipc.cu): whole cudaMalloc allocations
  * whose handles (SME_IPC_HANDLE_BYTES bytes) are exchanged between the ranks of a
  * node (torch.distributed all_gather_object) and opened by the peers. */

@@ -211,6 +211,8 @@ struct SegEpi {
   T* const* peers;   // [n_peers] other ranks' copies of out (peer memory over NVLink), or null
   int n_peers;
   int64_t row_offset;  // global index of this shard's row 0 in out / peers
+  const T* dotv;       // null: reduce v*v; else reduce v * dotv[g] (CG's p.Ap)
+  int finish;          // 0: result = {1/sqrt(sum), sum}; 1 (CG alpha): result[1] = result[0] / sum
 };
 
 // last-CTA reduction of the warp partials (fixed order) -> result, next scale
@@ -236,8 +238,12 @@ __device__ __forceinline__ void seg_epi_finish_impl(const SegEpi<T>& epi, int32_
   }
   if (threadIdx.x == 0) {
     const double tot = red[0];
-    epi.result[1] = tot;
-    epi.result[0] = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+    if (epi.finish == 1) {
+      epi.result[1] = epi.result[0] / tot;  // alpha = r.r / p.Ap
+    } else {
+      epi.result[1] = tot;
+      epi.result[0] = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+    }
     *epi.ticket = 0u;
   }
 }
@@ -252,7 +258,7 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
   double ss = 0.0;
   const int P0 = plan[warp], P1 = plan[warp + 1];
   if (P0 >= P1) return ss;
-  const T sc = EPI ? (T)*epi.scale : T(1);
+  const T sc = (EPI && epi.scale) ? (T)*epi.scale : T(1);
 
   int c = P0 & ~(SEG_CH - 1);
   SegChunk<T> cur;
@@ -327,7 +333,7 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
           const int64_t g = (int64_t)(epi.qinv ? epi.qinv[r] : r) + epi.row_offset;
           epi.out[g] = v;
           for (int d = 0; d < epi.n_peers; ++d) epi.peers[d][g] = v;  // the exchange, row by row
-          ss += (double)v * (double)v;
+          ss += (double)v * (double)(epi.dotv ? epi.dotv[g] : v);
         } else if (!(ACC && lc == SEG_MARK)) {
           const int r = cur.h + (int)(cur.w[k] & SEG_DMASK);
           if (ACC && RED)
@@ -554,7 +560,7 @@ SME_API int sme_spmv_seg_epi(int dtype, int32_t n_warps, const uint32_t* pk, con
   SME_REQUIRE(n_warps >= 1 && pk && val && hdr && plan && out && scale && partials && ticket && result,
               "bad arguments");
   SME_REQUIRE((((uintptr_t)pk | (uintptr_t)val) & 15) == 0, "pk/val must be 16-byte aligned");
-  const SegEpi<double> e{(double*)out, qinv, scale, partials, ticket, result, nullptr, 0, 0};
+  const SegEpi<double> e{(double*)out, qinv, scale, partials, ticket, result, nullptr, 0, 0, nullptr, 0};
   return launch_seg<double>(n_warps, pk, (const double*)val, hdr, plan, (const double*)xs, (double*)y, accumulate,
                             as_stream(stream), &e);
 }
@@ -576,7 +582,22 @@ SME_API int sme_spmv_seg_epi_peers(int dtype, int32_t n_warps, const uint32_t* p
               "bad arguments");
   SME_REQUIRE((((uintptr_t)pk | (uintptr_t)val) & 15) == 0, "pk/val must be 16-byte aligned");
   const SegEpi<double> e{(double*)out, nullptr, scale, partials, ticket, result, (double* const*)d_peers, n_peers,
-                         row_offset};
+                         row_offset, nullptr, 0};
+  return launch_seg<double>(n_warps, pk, (const double*)val, hdr, plan, (const double*)xs, (double*)y, accumulate,
+                            as_stream(stream), &e);
+}
+
+// The last pass of one CG step with p.Ap fused in: out[r] = (A p)[r] (no scaling), the
+// sum of out[r] * p[r] reduced deterministically, and the last CTA writes alpha =
+// scal[0] / (p.Ap) into scal[1] (scal[0] = r.r, the layout of blas1.cu's CG
+// scalars), replacing sme_dot(p, Ap) of the unfused step.  Square matrix, xs = p (full).
+SME_API int sme_spmv_seg_epi_cg(int dtype, int32_t n_warps, const uint32_t* pk, const void* val, const int32_t* hdr,
+                                const int32_t* plan, const void* xs, const void* p, void* y, int accumulate,
+                                void* out, double* partials, uint32_t* ticket, double* scal, sme_stream_t stream) {
+  SME_REQUIRE(dtype == SME_F64, "the fused epilogue is f64 only");
+  SME_REQUIRE(n_warps >= 1 && pk && val && hdr && plan && p && out && partials && ticket && scal, "bad arguments");
+  SME_REQUIRE((((uintptr_t)pk | (uintptr_t)val) & 15) == 0, "pk/val must be 16-byte aligned");
+  const SegEpi<double> e{(double*)out, nullptr, nullptr, partials, ticket, scal, nullptr, 0, 0, (const double*)p, 1};
   return launch_seg<double>(n_warps, pk, (const double*)val, hdr, plan, (const double*)xs, (double*)y, accumulate,
                             as_stream(stream), &e);
 }

@@ -193,9 +193,13 @@ class PowerIteration:
 
 
 class ConjugateGradient:
-    """CG for SPD A (use a symmetric permutation p_c = p_r so that B = P A P^T is SPD)."""
+    """CG for SPD A (use a symmetric permutation p_c = p_r so that B = P A P^T is SPD).
 
-    def __init__(self, op: PermutedOperator, b, x0=None):
+    Fused mode (seg operators, f64): p.Ap is reduced inside the SpMV's last pass
+    and alpha written by its last CTA (sme_spmv_seg_epi_cg), so a step is the
+    panel passes + the x/r update + the p update."""
+
+    def __init__(self, op: PermutedOperator, b, x0=None, fused: bool | None = None):
         if op.q is not None:
             raise ValueError("CG needs a symmetric permutation (p_c == p_r) so that B stays SPD")
         self.op = op
@@ -215,12 +219,22 @@ class ConjugateGradient:
         _lib.call("sme_dot", _cuda.sme_dtype(self.r), op.n, ptr(self.r), ptr(self.r), ptr(self.partial),
                   ptr(self.scal), ptr(self.scal), 0, stream())  # scal[0] = r.r
         del dt
+        self.lay = op.fused_layout() if fused is not False else None
+        if fused and self.lay is None:
+            raise ValueError("the fused CG needs a 'seg' operator with f64 values")
+        self.fused = self.lay is not None
+        if self.fused:
+            self.epi_partials = torch.zeros(self.lay.n_warps, dtype=torch.float64, device=dev)
+            self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
 
     def _step(self) -> None:
         dt = _cuda.sme_dtype(self.r)
-        self.op.apply(self.p, self.ap)
-        _lib.call("sme_dot", dt, self.op.n, ptr(self.p), ptr(self.ap), ptr(self.partial), None, ptr(self.scal), 1,
-                  stream())
+        if self.fused:
+            self.lay.epi_cg_pass(self.p, self.op._tmp, self.ap, self.epi_partials, self.ticket, self.scal)
+        else:
+            self.op.apply(self.p, self.ap)
+            _lib.call("sme_dot", dt, self.op.n, ptr(self.p), ptr(self.ap), ptr(self.partial), None, ptr(self.scal),
+                      1, stream())
         _lib.call("sme_cg_update", dt, self.op.n, ptr(self.x), ptr(self.r), ptr(self.p), ptr(self.ap),
                   ptr(self.scal), ptr(self.partial), stream())
 

@@ -116,6 +116,25 @@ class SegLayout:
                   stream())
         self._window(None, None)
 
+    def epi_cg_pass(self, p: torch.Tensor, y: torch.Tensor, out: torch.Tensor, partials: torch.Tensor,
+                    ticket: torch.Tensor, scal: torch.Tensor) -> None:
+        """out = A p with p.Ap reduced in the last pass and alpha = scal[0] / p.Ap -> scal[1]
+        (sme_spmv_seg_epi_cg)."""
+        if not self.full_last:
+            raise ValueError("the fused epilogue needs a layout built with full_last=True")
+        P = self.n_panels
+        for q in range(P - 1):
+            self._window(q, p)
+            self._pass(q, p, y)
+        self._window(P - 1, p)
+        vb = self.val.element_size()
+        o = int(self.offsets[P - 1])
+        _lib.call("sme_spmv_seg_epi_cg", _cuda.sme_dtype(self.val), self.n_warps, ptr(self.pk) + 4 * o,
+                  ptr(self.val) + vb * o, ptr(self.hdr) + 4 * (o // CHUNK),
+                  ptr(self.plans) + 4 * (P - 1) * (self.n_warps + 1), ptr(p) + vb * int(self.bounds_host[P - 1]),
+                  ptr(p), ptr(y), int(P > 1), ptr(out), ptr(partials), ptr(ticket), ptr(scal), stream())
+        self._window(None, None)
+
     def _window(self, p: int | None, xd: torch.Tensor | None) -> None:
         if not self.persist:
             return

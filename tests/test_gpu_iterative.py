@@ -125,3 +125,26 @@ def test_fused_power_iteration_graph_is_bitwise_eager_and_deterministic():
     assert eager.eigenvalue == graphed.eigenvalue == again.eigenvalue
     with pytest.raises(ValueError, match="even"):
         PowerIteration(op, x0, fused=True).capture(3)
+
+
+@pytest.mark.parametrize("panels", [1, 3])
+def test_fused_cg_matches_oracle_and_unfused(panels):
+    """sme_spmv_seg_epi_cg: p.Ap and alpha from the SpMV's last pass."""
+    g = 30
+    A = synth.laplacian5(g)
+    n = A.n_rows
+    p = P.random_permutation(n, 9)
+    op = _seg_op(A, p, P.random_permutation(n, 11), panels)  # folded: symmetric by p
+    b = O.input_vector(1, n)
+    fused = ConjugateGradient(op, b, fused=True)
+    assert fused.fused and fused.lay.n_panels == panels
+    fused.capture(6)
+    fused.run(198)
+    unfused = ConjugateGradient(op, b, fused=False)
+    unfused.run(199)
+    ptr, col, val = O.laplacian5(g)
+    x_ref, rr_ref = O.conjugate_gradient(ptr, col, val, b, 201)
+    x = fused.solution().cpu().numpy()
+    assert O.relative_error(x, x_ref) <= 1e-8
+    assert O.relative_error(x, unfused.solution().cpu().numpy()) <= 1e-10
+    assert O.relative_error(O.spmv_csr(ptr, col, val, x), b) <= 1e-6
