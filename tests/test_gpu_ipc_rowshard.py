@@ -37,7 +37,6 @@ def _worker(rank, world, port, out_dir, panels):
         A = synth.laplacian5(G)
         n = A.n_rows
         p = P.random_permutation(n, 3)
-        A._cache  # noqa: B018
         x0 = O.input_vector(0, n)
         from paper_2308_00106_b200 import seg as S
 
