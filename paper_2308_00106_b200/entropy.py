@@ -90,6 +90,7 @@ def _zeros(n: int) -> torch.Tensor:
     return torch.zeros(n, dtype=torch.int64, device=_cuda.require_cuda())
 
 
+@_cuda.nvtx("histogram_2d")
 def histogram_2d(m, bins_r: int, bins_c: int) -> BinnedHistogram:
     """Count nonzeros on a bins_r x bins_c grid (entropy.py:91-101).
 
@@ -134,6 +135,7 @@ def _csr_of(m: CooMatrix) -> CsrMatrix:
     return coo_to_csr(m)
 
 
+@_cuda.nvtx("shannon_entropy")
 def shannon_entropy(h: BinnedHistogram, base: float = 2.0) -> float:
     """-sum p_i log(p_i) over nonzero bins, p_i = count_i / total (entropy.py:104-119)."""
     if base <= 1.0:

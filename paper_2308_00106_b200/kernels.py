@@ -252,6 +252,7 @@ def spmv_into(m: CsrMatrix, xd: torch.Tensor, y: torch.Tensor, kernel: str = "ve
         raise ValueError(f"unknown kernel {kernel!r}; expected one of {KERNELS}")
 
 
+@_cuda.nvtx("spmv_csr")
 def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None = None):
     """y[i] = sum over row i of values[k] * x[col_idx[k]] (kernels.py:73-78).
 
@@ -285,6 +286,7 @@ def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None 
 PIPELINE_BUFFERS = 2  # device x/y buffers of spmv_csr_pipelined (steps in flight)
 
 
+@_cuda.nvtx("spmv_csr_pipelined")
 def spmv_csr_pipelined(m: CsrMatrix, xs, ys=None, kernel: str = "auto") -> list:
     """y_k = A x_k for a sequence of host vectors, with the PCIe copies of neighbouring
     steps overlapped: step k+1's x crosses host->device while step k computes and step
@@ -369,6 +371,7 @@ def spmv_csr_pipelined(m: CsrMatrix, xs, ys=None, kernel: str = "auto") -> list:
     return ys
 
 
+@_cuda.nvtx("spmv_csr_parallel")
 def spmv_csr_parallel(m: CsrMatrix, x, workers: int, reuse_pool: bool = True, kernel: str = "vector"):
     """Row-partitioned CSR SpMV (kernels.py:102-128): each of `workers` even row
     ranges (make_row_partition) is one CSR-vector launch over its rows; every
@@ -398,6 +401,7 @@ def spmv_csr_parallel(m: CsrMatrix, x, workers: int, reuse_pool: bool = True, ke
     return _y_out(y, mode)
 
 
+@_cuda.nvtx("spmv_coo")
 def spmv_coo(m: CooMatrix, x):
     """y = 0; y[row_idx[k]] += values[k] * x[col_idx[k]] (kernels.py:81-86), with device atomics."""
     if not isinstance(m, CooMatrix):

@@ -281,6 +281,7 @@ def _raise_range(m: CooMatrix) -> None:
     raise ValueError("index outside the matrix")
 
 
+@_cuda.nvtx("coo_to_csr")
 def coo_to_csr(m: CooMatrix) -> CsrMatrix:
     """Convert COO to CSR; values reordered (row-major, columns ascending) but
     otherwise bit-identical.  Duplicates are an error (reference: matio.py:281-294)."""

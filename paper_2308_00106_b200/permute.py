@@ -210,6 +210,7 @@ def permute_cols(m: CooMatrix, p: Permutation) -> CooMatrix:
     return _permute_coo(m, None, p)
 
 
+@_cuda.nvtx("permute_matrix")
 def permute_matrix(m: CooMatrix, p_r: Permutation, p_c: Permutation) -> CooMatrix:
     """Apply a (row, column) permutation pair in one pass (permute.py:98-102).
 
@@ -244,6 +245,7 @@ def _permute_coo(m: CooMatrix, p_r: Permutation | None, p_c: Permutation | None)
     return CooMatrix._from_device(m.n_rows, m.n_cols, row, col, m.d_values.clone(), csr_thunk=thunk)
 
 
+@_cuda.nvtx("permute_csr")
 def permute_csr(m: CsrMatrix, p_r: Permutation | None, p_c: Permutation | None) -> CsrMatrix:
     """P_r A P_c directly on CSR (K4): row gather through inverse(p_r), column remap
     through p_c, segmented sort inside each row.  Bit-identical to
