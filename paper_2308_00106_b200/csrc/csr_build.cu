@@ -80,15 +80,40 @@ __device__ __forceinline__ uint32_t map_col(const int32_t* __restrict__ cmap, in
 // ---------------------------------------------------------------------------
 // rows with len <= 32: sub-warp bitonic sort in registers
 // ---------------------------------------------------------------------------
-template <typename T, class Src>
+// Keys: 64-bit (mapped col << 32 | slot) in general; 32-bit (mapped col << 5 |
+// slot) when every mapped column is < 2^27 (KEY32: one shuffle per exchange
+// instead of two).  The column map (p_c, a random gather from an n_cols table) is
+// read with an L2 evict-last hint and the streams (old rows in, new rows out)
+// with evict-first, so the table keeps as much of L2 as it can.
+template <bool KEY32>
+struct SortKey {
+  using K = uint64_t;
+  static constexpr K NONE = ~0ull;
+  __device__ static K make(uint32_t col, int slot) { return ((uint64_t)col << 32) | (uint32_t)slot; }
+  __device__ static uint32_t col(K k) { return (uint32_t)(k >> 32); }
+  __device__ static int slot(K k) { return (int)(uint32_t)k; }
+};
+template <>
+struct SortKey<true> {
+  using K = uint32_t;
+  static constexpr K NONE = ~0u;
+  __device__ static K make(uint32_t col, int slot) { return (col << 5) | (uint32_t)slot; }
+  __device__ static uint32_t col(K k) { return k >> 5; }
+  __device__ static int slot(K k) { return (int)(k & 31u); }
+};
+
+template <typename T, class Src, bool KEY32 = false>
 __global__ void __launch_bounds__(SORT_NT) k_sort_rows_warp(
     int32_t n_rows, const int32_t* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
     const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
     T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key) {
+  using SK = SortKey<KEY32>;
+  using K = typename SK::K;
   const int lane = threadIdx.x & 31;
   const int64_t n_groups = ((int64_t)n_rows + 31) / 32;
   const int64_t warp_global = ((int64_t)blockIdx.x * SORT_NT + threadIdx.x) >> 5;
   const int64_t warps_total = ((int64_t)gridDim.x * SORT_NT) >> 5;
+  const uint64_t keep = policy_evict_last(), once = policy_evict_first();
   for (int64_t g = warp_global; g < n_groups; g += warps_total) {
     const int32_t r = (int32_t)(g * 32 + lane);
     int32_t dst = 0, len = 0;
@@ -123,25 +148,28 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_rows_warp(
       const int32_t my_len = __shfl_sync(0xffffffffu, len, rr);
       const int32_t my_dst = __shfl_sync(0xffffffffu, dst, rr);
       const int64_t my_from = __shfl_sync(0xffffffffu, from, rr);
-      uint64_t v = ~0ull;
-      if (li < my_len) v = ((uint64_t)map_col(cmap, src_col[my_from + li]) << 32) | (uint32_t)li;
+      K v = SK::NONE;
+      if (li < my_len) {
+        const int32_t c = ld_stream_i1(src_col + my_from + li, once);
+        v = SK::make(cmap ? (uint32_t)ld_l1(cmap + c, keep) : (uint32_t)c, li);
+      }
       for (int k = 2; k <= G; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
-          uint64_t o = __shfl_xor_sync(0xffffffffu, v, j);
-          bool asc = (li & k) == 0;
-          bool lower = (li & j) == 0;
-          uint64_t mn = v < o ? v : o, mx = v < o ? o : v;
+          const K o = __shfl_xor_sync(0xffffffffu, v, j);
+          const bool asc = (li & k) == 0;
+          const bool lower = (li & j) == 0;
+          const K mn = v < o ? v : o, mx = v < o ? o : v;
           v = (lower == asc) ? mn : mx;
         }
       }
-      uint64_t prev = __shfl_up_sync(0xffffffffu, v, 1);
+      const K prev = __shfl_up_sync(0xffffffffu, v, 1);
       if (li < my_len) {
-        uint32_t key = (uint32_t)(v >> 32);
-        uint32_t idx = (uint32_t)v;
-        const bool dup = li > 0 && (uint32_t)(prev >> 32) == key;
+        const uint32_t key = SK::col(v);
+        const int idx = SK::slot(v);
+        const bool dup = li > 0 && SK::col(prev) == key;
         if (dup && !L.mark_dups) report_dup((int32_t)(g * 32 + rr), key, flag, dup_key);
         out_col[my_dst + li] = (dup && L.mark_dups) ? -1 : (int32_t)key;
-        out_val[my_dst + li] = src_val[my_from + idx];
+        st_stream(out_val + my_dst + li, ld_stream(src_val + my_from + idx, once));
       }
     }
   }
@@ -390,11 +418,17 @@ __global__ void k_csr_expand_rows(int64_t n_rows, const int32_t* __restrict__ pt
 template <typename T, class Src>
 int launch_sorts(int64_t n_rows, const int32_t* new_ptr, Src src, const int32_t* src_col, const T* src_val,
                  const int32_t* cmap, int32_t* out_col, T* out_val, SortLists L, int32_t* flag,
-                 uint64_t* dup_key, cudaStream_t s) {
+                 uint64_t* dup_key, cudaStream_t s, int64_t n_cols = INT32_MAX) {
   int64_t groups = (n_rows + 31) / 32;
   int blocks = grid_for(groups * 32, SORT_NT, 8);
-  k_sort_rows_warp<T, Src><<<blocks, SORT_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val, cmap,
-                                                      out_col, out_val, L, flag, (unsigned long long*)dup_key);
+  if (n_cols <= ((int64_t)1 << 27))  // mapped columns < 2^27: 32-bit keys (col << 5 | slot)
+    k_sort_rows_warp<T, Src, true><<<blocks, SORT_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
+                                                               cmap, out_col, out_val, L, flag,
+                                                               (unsigned long long*)dup_key);
+  else
+    k_sort_rows_warp<T, Src, false><<<blocks, SORT_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
+                                                                cmap, out_col, out_val, L, flag,
+                                                                (unsigned long long*)dup_key);
   SME_CHECK_LAUNCH("k_sort_rows_warp");
   k_sort_rows_block<T, Src><<<sm_count() * 4, SORT_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
                                                                 out_val, L, flag, (unsigned long long*)dup_key);
@@ -511,13 +545,13 @@ static int coo_to_csr_impl(int dtype, int64_t n_rows, int64_t n_cols, int64_t nn
                                                             row_map, cursor, st_col, (double*)st_val);
     SME_CHECK_LAUNCH("k_coo_scatter");
     return launch_sorts<double>(n_rows, row_ptr, SrcStaged{}, st_col, (const double*)st_val, col_map, col_out,
-                                (double*)val_out, L, flag, dup_key, s);
+                                (double*)val_out, L, flag, dup_key, s, n_cols);
   } else {
     k_coo_scatter<float><<<grid_for(nnz, 256), 256, 0, s>>>(nnz, n_rows, n_cols, row, col, (const float*)val,
                                                            row_map, cursor, st_col, (float*)st_val);
     SME_CHECK_LAUNCH("k_coo_scatter");
     return launch_sorts<float>(n_rows, row_ptr, SrcStaged{}, st_col, (const float*)st_val, col_map, col_out,
-                               (float*)val_out, L, flag, dup_key, s);
+                               (float*)val_out, L, flag, dup_key, s, n_cols);
   }
 }
 
@@ -543,9 +577,9 @@ SME_API int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t n
   SrcGather src{row_ptr, inv_row};
   if (dtype == SME_F64)
     return launch_sorts<double>(n_rows, row_ptr_out, src, col, (const double*)val, col_map, col_out,
-                                (double*)val_out, L, flag, dup_key, s);
+                                (double*)val_out, L, flag, dup_key, s, n_cols);
   return launch_sorts<float>(n_rows, row_ptr_out, src, col, (const float*)val, col_map, col_out,
-                             (float*)val_out, L, flag, dup_key, s);
+                             (float*)val_out, L, flag, dup_key, s, n_cols);
 }
 
 SME_API int sme_row_stats(int64_t n_rows, const int32_t* row_ptr, int64_t* out, sme_stream_t stream) {
