@@ -426,6 +426,20 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         total_ms, per = timed(B, xp, args.kernel, args.steps, args.warmup, preload_s=1.0)
         clk = clocks.stop()
         un_total, un_per = timed(A, x, args.kernel, args.steps, args.warmup)
+        # the same comparison with the two matrices alternating step by step (no clock/thermal drift
+        # between two separate loops): medians of per-step events
+        yb_, ya_ = torch.empty(n, dtype=B.dtype, device=dev), torch.empty(n, dtype=A.dtype, device=dev)
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        for e0, e1, e2 in ev:
+            e0.record()
+            spmv_into(B, xp, yb_, args.kernel)
+            e1.record()
+            spmv_into(A, x, ya_, args.kernel)
+            e2.record()
+        torch.cuda.synchronize()
+        inter = (statistics.median(e0.elapsed_time(e1) for e0, e1, _ in ev),
+                 statistics.median(e1.elapsed_time(e2) for _, e1, e2 in ev))
+        del yb_, ya_
         others = {}
         for other in ("panel", "stream", "vector", "merge"):
             if other != resolved:
@@ -456,7 +470,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
                               preload_s=1.0)
         clk = clocks.stop()
         un_total = ot_total = None
-        un_per = None
+        un_per = inter = None
         nnz_total = nnz
         bytes_step = spmv_bytes(shard.local.n_rows, plan.world * plan.pad, shard.nnz, 8, 4)
 
@@ -605,6 +619,10 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
             "permuted_gflops": round(gflops, 3),
             "unpermuted_gflops": round(2 * nnz / (un_total / args.steps * 1e-3) / 1e9, 3),
             "ratio": round((un_total / args.steps) / ms_per_step, 4),
+            "interleaved": {"permuted_ms": round(inter[0], 4), "unpermuted_ms": round(inter[1], 4),
+                            "ratio": round(inter[1] / inter[0], 4),
+                            "how": "permuted and unpermuted SpMV alternating step by step, medians of per-step "
+                                   "CUDA events (ratio = unpermuted time / permuted time)"},
         },
         "other_kernels_gflops": others if world == 1 else None,
         "gather_roofline": gather_roof,
