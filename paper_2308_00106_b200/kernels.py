@@ -284,6 +284,7 @@ def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None 
 
 
 PIPELINE_BUFFERS = 2  # device x/y buffers of spmv_csr_pipelined (steps in flight)
+PIPELINE_H2D_COPIES = 0  # H2D copies per x (0: one per column panel)
 
 
 @_cuda.nvtx("spmv_csr_pipelined")
@@ -338,12 +339,15 @@ def spmv_csr_pipelined(m: CsrMatrix, xs, ys=None, kernel: str = "auto") -> list:
         with torch.cuda.stream(h2d):
             if computed[b] is not None:
                 h2d.wait_event(computed[b])  # x buffer b is free once step k-2 computed
-            for p in range(P):
-                lo, hi = int(bounds[p]), int(bounds[p + 1])
+            # x crosses in `groups` copies; pass p waits for the copy holding its slice
+            groups = max(1, min(P, PIPELINE_H2D_COPIES or P))
+            for gi in range(groups):
+                p0, p1 = gi * P // groups, (gi + 1) * P // groups
+                lo, hi = int(bounds[p0]), int(bounds[p1])
                 xb[b][lo:hi].copy_(xk[lo:hi], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(h2d)
-                slice_ev.append(ev)
+                slice_ev.extend([ev] * (p1 - p0))
         if copied_out[b] is not None:
             main.wait_event(copied_out[b])  # y buffer b is free once step k-2's y left
         if lay is None:

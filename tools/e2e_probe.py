@@ -34,10 +34,19 @@ def run(label):
 
 import paper_2308_00106_b200.kernels as K
 
+orig_pass = SegLayout._pass
+
 for nb in (2, 3):
     K.PIPELINE_BUFFERS = nb
     run(f"pipelined e2e, {nb} buffers")
 K.PIPELINE_BUFFERS = 2
+for g in (1, 2, 4):
+    K.PIPELINE_H2D_COPIES = g
+    run(f"pipelined e2e, 2 buffers, {g} H2D copies per x")
+    SegLayout._pass = lambda self, p, xd, y: None
+    run(f"copies only, {g} H2D copies per x")
+    SegLayout._pass = orig_pass
+K.PIPELINE_H2D_COPIES = 0
 orig = SegLayout._pass
 SegLayout._pass = lambda self, p, xd, y: None
 for nb in (2, 3):
