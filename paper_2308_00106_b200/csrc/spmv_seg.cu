@@ -60,6 +60,10 @@ constexpr uint32_t SEG_END = 1u << SEG_DBITS;
 constexpr int SEG_CSHIFT = SEG_DBITS + 1;
 constexpr uint32_t SEG_MARK = (1u << (32 - SEG_CSHIFT)) - 1;  // col field of an explicit zero
 constexpr int SEG_GAP = 2;                                    // padding stride of empty rows (p > 0)
+// row-total staging (CMP, see seg_warp_body) pays for f64 (C4 -3.8 %, C5 -3 %) but not for
+// f32 (C3 +7 %: 4-byte y words already share lines, and the scan's instructions dominate)
+template <typename T>
+constexpr bool kStageRows = sizeof(T) == 8;
 
 // ---------------------------------------------------------------------------
 // layout build
@@ -248,11 +252,16 @@ __device__ __forceinline__ void seg_epi_finish_impl(const SegEpi<T>& epi, int32_
   }
 }
 
-template <typename T, bool ACC, bool EPI, bool RED = false>
+// CMP: the chunk's row totals are staged in shared memory in row order (an
+// exclusive warp scan of each lane's row ends gives the slots) and written with
+// one instruction per 32 rows, so consecutive lanes hit consecutive y words: ~4 y
+// requests per chunk instead of ~16 (four predicated instructions each spanning the
+// chunk's ~50 rows).  Applies to the writing pass and to RED accumulation.
+template <typename T, bool ACC, bool EPI, bool RED = false, bool CMP = false>
 __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk, const T* __restrict__ val,
                                                 const int32_t* __restrict__ hdr, const int32_t* __restrict__ plan,
                                                 int warp, const T* __restrict__ xs, T* __restrict__ y,
-                                                const SegEpi<T>& epi) {
+                                                const SegEpi<T>& epi, T* s_val = nullptr, int* s_row = nullptr) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   double ss = 0.0;
@@ -320,6 +329,25 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
     carry = __shfl_sync(FULL, lane_out, 31);
     // row totals: entries up to the lane's first end get the incoming chain
     bool first = true;
+    int slot = 0, n_ends = 0;
+    if (CMP) {
+      unsigned emitm = endm;
+      if (ACC && !EPI) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if ((cur.w[k] >> SEG_CSHIFT) == SEG_MARK) emitm &= ~(1u << k);
+      }
+      const int cnt = __popc(emitm);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      slot = incl - cnt;
+      n_ends = __shfl_sync(FULL, incl, 31);
+      __syncwarp();  // the previous chunk's staged rows have been written out
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const T fin = run[k] + (first ? in_v : T(0));
@@ -330,16 +358,44 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
           // every row ends exactly once in the epilogue pass (explicit zeros included)
           const int r = cur.h + (int)(cur.w[k] & SEG_DMASK);
           const T v = sc * (ACC ? yv[k] + fin : fin);
+          if (CMP) {  // stores (and the dot) happen row-ordered after the loop
+            s_row[slot] = r;
+            s_val[slot] = v;
+            ++slot;
+          } else {
+            const int64_t g = (int64_t)(epi.qinv ? epi.qinv[r] : r) + epi.row_offset;
+            epi.out[g] = v;
+            for (int d = 0; d < epi.n_peers; ++d) epi.peers[d][g] = v;  // the exchange, row by row
+            ss += (double)v * (double)(epi.dotv ? epi.dotv[g] : v);
+          }
+        } else if (!(ACC && lc == SEG_MARK)) {
+          const int r = cur.h + (int)(cur.w[k] & SEG_DMASK);
+          if (CMP) {
+            s_row[slot] = r;
+            s_val[slot] = fin;
+            ++slot;
+          } else if (ACC && RED) {
+            atomicAdd(y + r, fin);  // RED.ADD at L2: one add per row per pass, passes ordered: deterministic
+          } else {
+            y[r] = ACC ? yv[k] + fin : fin;
+          }
+        }
+      }
+    }
+    if (CMP) {
+      __syncwarp();
+      for (int q = lane; q < n_ends; q += 32) {
+        if (EPI) {
+          const int r = s_row[q];
+          const T v = s_val[q];
           const int64_t g = (int64_t)(epi.qinv ? epi.qinv[r] : r) + epi.row_offset;
           epi.out[g] = v;
           for (int d = 0; d < epi.n_peers; ++d) epi.peers[d][g] = v;  // the exchange, row by row
           ss += (double)v * (double)(epi.dotv ? epi.dotv[g] : v);
-        } else if (!(ACC && lc == SEG_MARK)) {
-          const int r = cur.h + (int)(cur.w[k] & SEG_DMASK);
-          if (ACC && RED)
-            atomicAdd(y + r, fin);  // RED.ADD at L2: one add per row per pass, passes ordered: deterministic
-          else
-            y[r] = ACC ? yv[k] + fin : fin;
+        } else if (ACC) {
+          atomicAdd(y + s_row[q], s_val[q]);
+        } else {
+          y[s_row[q]] = s_val[q];
         }
       }
     }
@@ -350,7 +406,7 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
   return ss;
 }
 
-template <typename T, bool ACC, bool EPI, bool RED = false>
+template <typename T, bool ACC, bool EPI, bool RED = false, bool CMP = false>
 __global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict__ pk, const T* __restrict__ val,
                                                    const int32_t* __restrict__ hdr, const int32_t* __restrict__ plan,
                                                    int32_t n_warps, const T* __restrict__ xs, T* __restrict__ y,
@@ -359,8 +415,12 @@ __global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict_
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * SEG_NT + threadIdx.x) >> 5;
   if (EPI) {
+    __shared__ T e_val[SEG_NT / 32][SEG_CH];
+    __shared__ int e_row[SEG_NT / 32][SEG_CH];
     double ss = 0.0;
-    if (warp < n_warps) ss = seg_warp_body<T, ACC, true>(pk, val, hdr, plan, warp, xs, y, epi);
+    if (warp < n_warps)
+      ss = seg_warp_body<T, ACC, true, false, kStageRows<T>>(pk, val, hdr, plan, warp, xs, y, epi,
+                                                             e_val[threadIdx.x >> 5], e_row[threadIdx.x >> 5]);
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
     if (lane == 0 && warp < n_warps) epi.partials[warp] = ss;
     if (epi.n_peers > 0) __threadfence_system();  // peer stores performed before this launch completes
@@ -368,7 +428,14 @@ __global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict_
     return;
   }
   if (warp >= n_warps) return;
-  seg_warp_body<T, ACC, false, RED>(pk, val, hdr, plan, warp, xs, y, epi);
+  if (CMP) {
+    __shared__ T s_val[SEG_NT / 32][SEG_CH];
+    __shared__ int s_row[SEG_NT / 32][SEG_CH];
+    seg_warp_body<T, ACC, false, RED, true>(pk, val, hdr, plan, warp, xs, y, epi, s_val[threadIdx.x >> 5],
+                                            s_row[threadIdx.x >> 5]);
+  } else {
+    seg_warp_body<T, ACC, false, RED>(pk, val, hdr, plan, warp, xs, y, epi);
+  }
 }
 
 
@@ -404,8 +471,9 @@ __global__ void __launch_bounds__(SEG_NT) k_seg_probe(const uint32_t* __restrict
   }
 }
 
-// 0 = SpMV (default: accumulating passes add with RED.ADD.F64 at L2, C4 -3.8 %),
-// 3 = bound probe, 5 = accumulating passes load y, add, store (the previous default)
+// 0 = SpMV (default: row totals staged and written in row order; accumulating passes
+// add with RED.ADD.F64 at L2), 3 = bound probe, 5 = accumulating passes load y, add,
+// store, 6 = RED accumulation without the staging (one write per (lane, k) row end)
 static int s_seg_mode = 0;
 
 template <typename T>
@@ -422,10 +490,14 @@ int launch_seg(int32_t n_warps, const uint32_t* pk, const T* val, const int32_t*
     k_seg_probe<T><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y);
   else if (accumulate && s_seg_mode == 5)
     k_spmv_seg<T, true, false><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
-  else if (accumulate)
+  else if (accumulate && (s_seg_mode == 6 || !kStageRows<T>))
     k_spmv_seg<T, true, false, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
-  else
+  else if (accumulate)
+    k_spmv_seg<T, true, false, true, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
+  else if (s_seg_mode == 6 || !kStageRows<T>)
     k_spmv_seg<T, false, false><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
+  else
+    k_spmv_seg<T, false, false, false, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
   SME_CHECK_LAUNCH("k_spmv_seg");
   return SME_OK;
 }
@@ -500,8 +572,8 @@ SME_API int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* row_ptr, cons
 // Kernel variant (process-wide; experiments): 0 = the SpMV, 3 = bound probe (the
 // chunk stream and gathers without the row reduction; timing only, not y = A x).
 SME_API int sme_spmv_seg_set_mode(int mode) {
-  SME_REQUIRE(mode == 0 || mode == 3 || mode == 5,
-              "mode must be 0 (SpMV), 3 (bound probe) or 5 (accumulating passes with load + store)");
+  SME_REQUIRE(mode == 0 || mode == 3 || mode == 5 || mode == 6,
+              "mode must be 0 (SpMV), 3 (bound probe), 5 (accumulate with load + store) or 6 (no staging)");
   s_seg_mode = mode;
   return SME_OK;
 }
@@ -520,6 +592,8 @@ SME_API int sme_spmv_seg_warps(int32_t* n_warps) {
   occ((const void*)k_spmv_seg<float, true, false>);
   occ((const void*)k_spmv_seg<double, false, true>);
   occ((const void*)k_spmv_seg<double, true, true>);
+  occ((const void*)k_spmv_seg<double, false, false, false, true>);
+  occ((const void*)k_spmv_seg<double, true, false, true, true>);
   per_sm = std::max(1, per_sm);
   *n_warps = sm_count() * per_sm * (SEG_NT / 32);
   return SME_OK;
