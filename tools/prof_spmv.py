@@ -28,6 +28,7 @@ ap.add_argument("--time", action="store_true")
 ap.add_argument("--panels", type=int, default=0)
 ap.add_argument("--seg-panels", type=int, default=0)
 ap.add_argument("--seg-mode", type=int, default=-1)
+ap.add_argument("--seg-warps", type=int, default=0, help="persistent warps of the seg grid (default: occupancy)")
 ap.add_argument("--seg-hit", type=float, default=-1.0, help="x-slice L2 window hit ratio (0 = no persistence)")
 ap.add_argument("--check", action="store_true", help="compare with the stream kernel")
 ap.add_argument("--persist", action="store_true")
@@ -78,6 +79,14 @@ if a.panels:
         pc.enable_persistence(True)
 if a.seg_panels:
     B._cache["seg_panels"] = a.seg_panels
+if a.seg_warps:
+    from paper_2308_00106_b200.seg import SegLayout, auto_seg_panels
+
+    P_ = a.seg_panels or auto_seg_panels(B)
+    lay_ = SegLayout(B, P_, a.seg_warps)
+    if P_ > 1:
+        lay_.enable_persistence(True)
+    B._cache[("seg", P_, False)] = lay_
 if a.seg_hit >= 0:
     from paper_2308_00106_b200.seg import seg_of
 
