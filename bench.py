@@ -746,7 +746,8 @@ def run_iterative(args, cfg) -> dict:
                    "folded": bool(op.folded),
                    "folded_note": "the per-iteration gather by q = p_r o p_c^-1 is folded into the matrix once: "
                                   "the iterated operator is permute_csr(A, p_r, p_r) (iterative.py docstring)",
-                   "unpermuted_step": ("fused seg" if pi_u.fused else "SpMV + dot + scale (unfused)")},
+                   "unpermuted_step": (f"fused {type(pi_u.lay).__name__} epilogue" if pi_u.fused
+                                       else "SpMV + dot + scale (unfused)")},
         "eigenvalue": {"permuted": lam_p, "unpermuted": lam_u, "rel_diff": abs(lam_p - lam_u) / lam_u},
         "amortisation": {"permutation_setup_ms": round(perm_s * 1e3, 2),
                          "of_which_host_generation_ms": round(HOST_PERM_S.get("native", 0.0) * 1e3, 2),
@@ -758,8 +759,9 @@ def run_iterative(args, cfg) -> dict:
         "x_norm_check": float(torch.linalg.vector_norm(x_p).item()),
         "cg": {"permuted_ms_per_iteration": round(cg_p_ms, 5), "unpermuted_ms_per_iteration": round(cg_u_ms, 5),
                "residual_norm2_permuted": cg_p_rr, "residual_norm2_unpermuted": cg_u_rr,
-               "step": "permuted: seg passes with p.Ap fused into the last (sme_spmv_seg_epi_cg) + x,r update + "
-                       "p update; unpermuted: vector SpMV + dot + x,r update + p update; CUDA graphs",
+               "step": "permuted: seg passes with p.Ap fused into the last (sme_spmv_seg_epi_cg); unpermuted: "
+                       "CSR-vector SpMV with p.Ap fused (sme_spmv_vector_epi); both + x,r update + p update; "
+                       "CUDA graphs",
                "iterations": iters, "rhs": "input_vector(1, n)"},
         "iterations_total": 1 + args.warmup * graph_steps + iters,
         "clocks": clk, "gpu_launches": launches(pi_p) * iters,

@@ -349,6 +349,19 @@ int sme_spmv_seg_epi_cg(int dtype, int32_t n_warps, const uint32_t* d_pk, const 
                         const int32_t* d_plan, const void* d_xs, const void* d_p, void* d_y, int accumulate,
                         void* d_out, double* d_partials, uint32_t* d_ticket, double* d_scal, sme_stream_t stream);
 
+/* The CSR-vector twin of the fused iteration epilogue (banded / unpermuted operators):
+ * d_out = scale[0] * (A x) (scale NULL: 1) with sum d_out * (d_dotv ? d_dotv : d_out)
+ * reduced deterministically over a fixed grid of sme_spmv_vector_epi_blocks() blocks
+ * (d_partials holds one double per block; d_ticket one uint32, zero-initialised once);
+ * finish 0: d_result = {1/sqrt(sum), sum} (power iteration), finish 1: d_result[1] =
+ * d_result[0] / sum (CG alpha).  f64.  Replaces spmv_csr + the oracle loop's norm / dot
+ * (kernels.py:73-78). */
+int sme_spmv_vector_epi_blocks(int64_t n_rows, int lanes, int64_t* blocks);
+int sme_spmv_vector_epi(int lanes, int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_col,
+                        const double* d_val, const double* d_x, double* d_out, const double* d_scale,
+                        const double* d_dotv, double* d_partials, uint32_t* d_ticket, double* d_result,
+                        int finish, sme_stream_t stream);
+
 /* CUDA IPC buffers for the fused exchange (ipc.cu): whole cudaMalloc allocations
  * whose handles (SME_IPC_HANDLE_BYTES bytes) are exchanged between the ranks of a
  * node (torch.distributed all_gather_object) and opened by the peers. */

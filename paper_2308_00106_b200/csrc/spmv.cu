@@ -351,6 +351,87 @@ __global__ void __launch_bounds__(256) k_spmv_vector(int64_t n_rows, const int32
   }
 }
 
+// CSR-vector SpMV with the power-iteration / CG epilogue fused in (the unpermuted,
+// banded operators of the iterative drivers; the seg twin is sme_spmv_seg_epi):
+// v_r = scale * (A x)_r -> out[r]; sum of v_r * (dotv ? dotv[r] : v_r) accumulated
+// per thread in the fixed grid-stride order, per block in a fixed tree, and by the
+// last block (ticket) in block order: finish 0 -> result = {1/sqrt(sum), sum},
+// finish 1 -> result[1] = result[0] / sum (CG alpha).  Deterministic.
+constexpr int VE_NT = 256;
+
+template <typename T, int L>
+__global__ void __launch_bounds__(VE_NT) k_spmv_vector_epi(int64_t n_rows, const int32_t* __restrict__ row_ptr,
+                                                         const int32_t* __restrict__ col, const T* __restrict__ val,
+                                                         const T* __restrict__ x, T* __restrict__ out,
+                                                         const double* __restrict__ scale, const T* __restrict__ dotv,
+                                                         double* __restrict__ partials, unsigned* ticket,
+                                                         double* result, int finish) {
+  constexpr int RPW = 32 / L;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / L, li = lane % L;
+  const int64_t warp = ((int64_t)blockIdx.x * VE_NT + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * VE_NT) >> 5;
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();
+  const T sc = scale ? (T)*scale : T(1);
+  double ss = 0.0;
+  for (int64_t base = warp * RPW; base < n_rows; base += n_warps * RPW) {
+    const int64_t r = base + sub;
+    T s = T(0);
+    if (r < n_rows) {
+      const int32_t a = row_ptr[r], b = row_ptr[r + 1];
+      for (int32_t k = a + li; k < b; k += L)
+        if (L >= 8)
+          s += ld_stream(val + k, pol_stream) * ld_keep(x + ld_stream_i1(col + k, pol_stream), pol_keep);
+        else
+          s += ld_l1(val + k, pol_stream) * ld_keep(x + ld_l1(col + k, pol_stream), pol_keep);
+    }
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (r < n_rows && li == 0) {
+      const T v = sc * s;
+      out[r] = v;
+      ss += (double)v * (double)(dotv ? dotv[r] : v);
+    }
+  }
+  // block partial (fixed tree), then the last block folds the partials in block order
+  __shared__ double red[VE_NT / 32];
+  __shared__ bool last;
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < VE_NT / 32; ++w) t += red[w];
+    partials[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // every thread folds a fixed stride of the partials, then a fixed tree (deterministic)
+  __shared__ double fold[VE_NT];
+  double acc = 0.0;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += VE_NT) acc += __ldcg(partials + b);
+  fold[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = VE_NT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) fold[threadIdx.x] += fold[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double tot = fold[0];
+    if (finish == 1) {
+      result[1] = result[0] / tot;
+    } else {
+      result[1] = tot;
+      result[0] = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+    }
+    *ticket = 0u;
+  }
+}
+
 // numpy's pairwise summation (loops_utils.h.src: pairwise_sum) over the
 // products of positions [s, s+n), each product separately rounded.  Leaves:
 __device__ double pw_leaf(const int32_t* __restrict__ col, const double* __restrict__ val,
@@ -573,3 +654,50 @@ SME_API int sme_spmv_merge_set_mode(int mode) {
   return SME_OK;
 }
 
+
+// Blocks of sme_spmv_vector_epi's fixed grid (= the length of its partials scratch):
+// exactly one resident wave of the kernel (its occupancy at 40 registers is 6 CTAs
+// of 256 per SM), never more than the rows need — a partial second wave would idle
+// most SMs at the tail (measured: the 8-per-SM grid of k_spmv_vector ran 36 % slower).
+static int64_t vector_epi_blocks(int64_t n_rows, int lanes) {
+  int occ = 0;
+  const void* fn = lanes == 1 ? (const void*)k_spmv_vector_epi<double, 1>
+                 : lanes == 2 ? (const void*)k_spmv_vector_epi<double, 2>
+                 : lanes == 4 ? (const void*)k_spmv_vector_epi<double, 4>
+                 : lanes == 8 ? (const void*)k_spmv_vector_epi<double, 8>
+                 : lanes == 16 ? (const void*)k_spmv_vector_epi<double, 16>
+                               : (const void*)k_spmv_vector_epi<double, 32>;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, VE_NT, 0) != cudaSuccess || occ < 1) occ = 4;
+  return grid_for(std::max<int64_t>(1, n_rows) * lanes, VE_NT, occ);
+}
+
+SME_API int sme_spmv_vector_epi_blocks(int64_t n_rows, int lanes, int64_t* blocks) {
+  SME_REQUIRE(blocks && n_rows >= 0 && lanes >= 1 && lanes <= 32, "bad arguments");
+  *blocks = vector_epi_blocks(n_rows, lanes);
+  return SME_OK;
+}
+
+// out = scale[0] * (A x) with the iterative drivers' reduction fused (see k_spmv_vector_epi);
+// f64; scale may be null (1); dotv null -> sum of squares (power iteration), else
+// sum out * dotv (CG's p.Ap, finish = 1 writes alpha = result[0] / sum into result[1]).
+SME_API int sme_spmv_vector_epi(int lanes, int64_t n_rows, const int32_t* row_ptr, const int32_t* col,
+                                const double* val, const double* x, double* out, const double* scale,
+                                const double* dotv, double* partials, uint32_t* ticket, double* result, int finish,
+                                sme_stream_t stream) {
+  SME_REQUIRE(n_rows >= 1 && n_rows < INT32_MAX && out && partials && ticket && result && (finish == 0 || finish == 1),
+              "bad arguments");
+  cudaStream_t s = as_stream(stream);
+  const int blocks = (int)vector_epi_blocks(n_rows, lanes);
+#define VE_CASE(LN)                                                                                             \
+  case LN:                                                                                                      \
+    k_spmv_vector_epi<double, LN><<<blocks, VE_NT, 0, s>>>(n_rows, row_ptr, col, val, x, out, scale, dotv,     \
+                                                           partials, ticket, result, finish);                  \
+    break;
+  switch (lanes) {
+    VE_CASE(1) VE_CASE(2) VE_CASE(4) VE_CASE(8) VE_CASE(16) VE_CASE(32)
+    default: SME_REQUIRE(false, "lanes must be one of 1,2,4,8,16,32 (got %d)", lanes);
+  }
+#undef VE_CASE
+  SME_CHECK_LAUNCH("k_spmv_vector_epi");
+  return SME_OK;
+}

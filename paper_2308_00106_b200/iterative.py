@@ -84,17 +84,22 @@ class PermutedOperator:
         return out
 
     def fused_layout(self):
-        """The seg layout (with the full last panel) for the fused power-iteration
-        epilogue, or None when the operator's kernel is not 'seg' or values are not f64."""
-        from .kernels import auto_kernel
+        """The fused-epilogue SpMV of this operator: the seg layout (with the full last
+        panel) for 'seg', VectorEpi for 'vector' (no gather by q); None otherwise or
+        when values are not f64."""
+        from .kernels import auto_kernel, default_lanes
         from .seg import seg_of
 
         kern = auto_kernel(self.B) if self.kernel == "auto" else self.kernel
-        if kern != "seg" or self.dtype != torch.float64:
+        if self.dtype != torch.float64:
             return None
         if not hasattr(self, "_qinv"):
             self._qinv = Permutation(self.q, _trusted=True).d_inverse if self.q is not None else None
-        return seg_of(self.B, full_last=True)
+        if kern == "seg":
+            return seg_of(self.B, full_last=True)
+        if kern == "vector" and self.q is None:
+            return VectorEpi(self.B, default_lanes(self.B))
+        return None
 
     def apply(self, z: torch.Tensor, out: torch.Tensor) -> None:
         """out = P_c^-1 A P_c z (stream-ordered; no allocation: graph-capturable)."""
@@ -103,6 +108,31 @@ class PermutedOperator:
         else:
             spmv_into(self.B, z, self._tmp, self.kernel)
             _lib.call("sme_gather", _cuda.sme_dtype(out), self.n, ptr(self.q), ptr(self._tmp), ptr(out), stream())
+
+
+class VectorEpi:
+    """The CSR-vector twin of the seg fused epilogue (sme_spmv_vector_epi): one launch
+    computes out = s * (A x) and the iteration's reduction (same interface as
+    SegLayout.epi_pass / epi_cg_pass)."""
+
+    n_panels = 1
+    full_last = True
+
+    def __init__(self, B: CsrMatrix, lanes: int):
+        self.B, self.lanes = B, int(lanes)
+        self.n_warps = _lib.query_i64("sme_spmv_vector_epi_blocks", B.n_rows, self.lanes)  # partials length
+
+    def epi_pass(self, xd, y, out, qinv, scal, partials, ticket, result) -> None:
+        if qinv is not None:
+            raise ValueError("the CSR-vector epilogue does not scatter: fold the operator")
+        B = self.B
+        _lib.call("sme_spmv_vector_epi", self.lanes, B.n_rows, ptr(B.d_row_ptr), ptr(B.d_col_idx), ptr(B.d_values),
+                  ptr(xd), ptr(out), ptr(scal), None, ptr(partials), ptr(ticket), ptr(result), 0, stream())
+
+    def epi_cg_pass(self, p, y, out, partials, ticket, scal) -> None:
+        B = self.B
+        _lib.call("sme_spmv_vector_epi", self.lanes, B.n_rows, ptr(B.d_row_ptr), ptr(B.d_col_idx), ptr(B.d_values),
+                  ptr(p), ptr(out), None, ptr(p), ptr(partials), ptr(ticket), ptr(scal), 1, stream())
 
 
 def _ident(n: int) -> Permutation:
@@ -114,7 +144,7 @@ def _ident(n: int) -> Permutation:
 class PowerIteration:
     """x_{k+1} = A x_k / ||A x_k|| (2-norm); eigenvalue estimate ||A x_k||.
 
-    Fused mode (seg operators, f64): one step is the operator's panel passes with
+    Fused mode (seg or CSR-vector operators, f64): one step is the operator's passes with
     the BLAS-1 work folded into the last pass (sme_spmv_seg_epi): the iterate is
     kept unnormalised, w_{k+1} = (B w_k) / ||w_k|| scattered straight into
     permuted coordinates, and ||w_{k+1}||^2 (the eigenvalue estimate squared) and
@@ -136,7 +166,7 @@ class PowerIteration:
         _lib.call("sme_scale", dt, op.n, ptr(self.z), ptr(self.z), ptr(self.scal), 3, s)
         self.lay = op.fused_layout() if fused is not False else None
         if fused and self.lay is None:
-            raise ValueError("the fused power iteration needs a 'seg' operator with f64 values")
+            raise ValueError("the fused power iteration needs a 'seg' or 'vector' operator with f64 values")
         self.fused = self.lay is not None
         if self.fused:
             self.w = [self.z, self.y]  # iterate ping-pongs between the two
@@ -195,7 +225,7 @@ class PowerIteration:
 class ConjugateGradient:
     """CG for SPD A (use a symmetric permutation p_c = p_r so that B = P A P^T is SPD).
 
-    Fused mode (seg operators, f64): p.Ap is reduced inside the SpMV's last pass
+    Fused mode (seg or CSR-vector operators, f64): p.Ap is reduced inside the SpMV's last pass
     and alpha written by its last CTA (sme_spmv_seg_epi_cg), so a step is the
     panel passes + the x/r update + the p update."""
 
@@ -221,7 +251,7 @@ class ConjugateGradient:
         del dt
         self.lay = op.fused_layout() if fused is not False else None
         if fused and self.lay is None:
-            raise ValueError("the fused CG needs a 'seg' operator with f64 values")
+            raise ValueError("the fused CG needs a 'seg' or 'vector' operator with f64 values")
         self.fused = self.lay is not None
         if self.fused:
             self.epi_partials = torch.zeros(self.lay.n_warps, dtype=torch.float64, device=dev)

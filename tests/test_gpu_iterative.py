@@ -148,3 +148,28 @@ def test_fused_cg_matches_oracle_and_unfused(panels):
     assert O.relative_error(x, x_ref) <= 1e-8
     assert O.relative_error(x, unfused.solution().cpu().numpy()) <= 1e-10
     assert O.relative_error(O.spmv_csr(ptr, col, val, x), b) <= 1e-6
+
+
+@pytest.mark.parametrize("perm", ["none", "symmetric"])
+def test_fused_vector_epilogue_power_and_cg(perm):
+    """sme_spmv_vector_epi: the CSR-vector operator (banded / unpermuted) fused like seg."""
+    g = 26
+    A = synth.laplacian5(g)
+    n = A.n_rows
+    p = P.random_permutation(n, 4) if perm == "symmetric" else None
+    op = PermutedOperator(A, p, p, kernel="vector")
+    x0 = O.input_vector(0, n)
+    pi = PowerIteration(op, x0, fused=True)
+    assert pi.fused and pi.lay.n_panels == 1
+    pi.capture(10)  # one eager step + a 10-step graph
+    pi.run(50)
+    ptr, col, val = O.laplacian5(g)
+    x_ref, lam_ref = O.power_iteration(ptr, col, val, x0, 51)
+    assert abs(pi.eigenvalue - lam_ref) <= 1e-10 * lam_ref
+    assert O.relative_error(pi.x().cpu().numpy(), x_ref) <= 1e-9
+    b = O.input_vector(1, n)
+    cg = ConjugateGradient(op, b, fused=True)
+    assert cg.fused
+    cg.run(150)
+    x_cg, _ = O.conjugate_gradient(ptr, col, val, b, 151)
+    assert O.relative_error(cg.solution().cpu().numpy(), x_cg) <= 1e-8
