@@ -1,0 +1,63 @@
+"""Property-based GPU parity (hypothesis): random shapes, densities, strategies and
+seeds through the whole path — build_strategy -> permute_matrix -> coo_to_csr (bit-exact
+vs the oracle's restatement of the reference), the 2-D histogram (bit-exact), and
+every SpMV kernel (normwise <= 1e-12, reference CORRECTNESS_RTOL)."""
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+import oracle as O
+import paper_2308_00106_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+KINDS = [P.StrategyKind.REGULAR, P.StrategyKind.ROW_PERMUTE, P.StrategyKind.ROW_COLUMN_PERMUTE,
+         P.StrategyKind.ROW_GRADIENT, P.StrategyKind.COLUMN_GRADIENT]
+
+
+@st.composite
+def matrices(draw):
+    n_rows = draw(st.integers(1, 400))
+    n_cols = draw(st.integers(1, 400))
+    dens = draw(st.sampled_from([0.0, 0.002, 0.02, 0.1, 0.5]))
+    seed = draw(st.integers(0, 2**31 - 1))
+    rng = np.random.default_rng(seed)
+    mask = rng.random((n_rows, n_cols)) < dens
+    if draw(st.booleans()) and n_rows > 1:  # one long row and a block of empty rows
+        mask[rng.integers(0, n_rows)] = rng.random(n_cols) < 0.9
+        lo = rng.integers(0, n_rows)
+        mask[lo : lo + n_rows // 3] = False
+    rows, cols = np.nonzero(mask)
+    order = rng.permutation(rows.size)  # arbitrary COO order
+    vals = rng.random(rows.size) * 2 - 1
+    return n_rows, n_cols, rows[order], cols[order], vals[order], seed
+
+
+@given(matrices(), st.sampled_from(KINDS), st.integers(0, 1000))
+@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+def test_pipeline_properties(mat, kind, strat_seed):
+    n_rows, n_cols, rows, cols, vals, seed = mat
+    m = P.CooMatrix(n_rows, n_cols, rows, cols, vals)
+    if kind in (P.StrategyKind.ROW_GRADIENT, P.StrategyKind.COLUMN_GRADIENT) and (n_rows < 3 or n_cols < 3):
+        return  # the reference needs >= 2 histogram bins and a pivot inside the range
+    try:
+        p_r, p_c = P.build_strategy(m, kind, strat_seed)
+    except ValueError:
+        return  # the reference raises too (e.g. a pivot at the edge); error parity has its own tests
+    csr = P.coo_to_csr(P.permute_matrix(m, p_r, p_c))
+    fr, fc = p_r.forward, p_c.forward
+    pr, pc = O.permute_coo(rows, cols, fr, fc)
+    optr, ocol, oval = O.coo_to_csr(n_rows, pr, pc, vals)
+    assert np.array_equal(csr.row_ptr, optr) and np.array_equal(csr.col_idx, ocol)
+    assert np.array_equal(csr.values.view(np.uint64), oval.view(np.uint64))
+    br, bc = min(128, n_rows), min(128, n_cols)
+    assert np.array_equal(P.histogram_2d(csr, br, bc).counts, O.histogram_2d_counts(pr, pc, n_rows, n_cols, br, bc))
+    x = np.random.default_rng(seed + 1).random(n_cols)
+    xp = O.permute_vector(x, fc)
+    want = O.spmv_csr(optr, ocol, oval, xp)
+    for kernel in ("seg", "vector", "stream", "merge", "panel"):
+        got = P.spmv_csr(csr, xp, kernel)
+        assert O.relative_error(got, want) <= 1e-12, kernel
+    assert np.array_equal(P.spmv_csr(csr, xp, "exact").view(np.uint64), want.view(np.uint64))
