@@ -211,6 +211,9 @@ int sme_hist2d_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d
  * 0 = lane-private u16 counters when bins_c <= 128 (default), 1 = the
  * shared-memory window with warp-aggregated atomics, 2 = lane counters on one CTA. */
 int sme_hist2d_set_mode(int mode);
+/* Row-sort keys of the CSR builds (process-wide; tests): 1 = 32-bit (mapped col << 5 |
+ * slot) whenever n_cols <= 2^27 (default), 0 = always 64-bit (col << 32 | slot). */
+int sme_sort_rows_set_key32(int enable);
 /* Tiling of the lane-counter kernel (experiments): 0 = 864 threads x 4 int4 loads per
  * lane (default; 768 x 4 when bins_r > ~1500), 1 = 768 x 4, 2 = 512 x 4 + next-iteration
  * prefetch, 3 = 768 x 2 + prefetch, 4 = 640 x 4 + prefetch, 5 = 864 x 4, 6 = 864 x 2,

@@ -80,6 +80,9 @@ __device__ __forceinline__ uint32_t map_col(const int32_t* __restrict__ cmap, in
 // ---------------------------------------------------------------------------
 // rows with len <= 32: sub-warp bitonic sort in registers
 // ---------------------------------------------------------------------------
+// 1: 32-bit keys whenever n_cols <= 2^27 (default); 0: always 64-bit keys (tests of that path)
+static int g_sort_key32 = 1;
+
 // Keys: 64-bit (mapped col << 32 | slot) in general; 32-bit (mapped col << 5 |
 // slot) when every mapped column is < 2^27 (KEY32: one shuffle per exchange
 // instead of two).  The column map (p_c, a random gather from an n_cols table) is
@@ -421,7 +424,7 @@ int launch_sorts(int64_t n_rows, const int32_t* new_ptr, Src src, const int32_t*
                  uint64_t* dup_key, cudaStream_t s, int64_t n_cols = INT32_MAX) {
   int64_t groups = (n_rows + 31) / 32;
   int blocks = grid_for(groups * 32, SORT_NT, 8);
-  if (n_cols <= ((int64_t)1 << 27))  // mapped columns < 2^27: 32-bit keys (col << 5 | slot)
+  if (n_cols <= ((int64_t)1 << 27) && g_sort_key32)  // mapped columns < 2^27: 32-bit keys (col << 5 | slot)
     k_sort_rows_warp<T, Src, true><<<blocks, SORT_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
                                                                cmap, out_col, out_val, L, flag,
                                                                (unsigned long long*)dup_key);
@@ -658,5 +661,12 @@ SME_API int sme_csr_compact(int dtype, int64_t n_rows, const int32_t* row_ptr, c
   else
     SME_REQUIRE(false, "unknown dtype %d", dtype);
   SME_CHECK_LAUNCH("k_csr_compact");
+  return SME_OK;
+}
+
+// Test hook: 0 forces the 64-bit sort keys of k_sort_rows_warp (the path of n_cols > 2^27).
+SME_API int sme_sort_rows_set_key32(int enable) {
+  SME_REQUIRE(enable == 0 || enable == 1, "enable must be 0 or 1");
+  g_sort_key32 = enable;
   return SME_OK;
 }

@@ -61,3 +61,30 @@ def test_pipeline_properties(mat, kind, strat_seed):
         got = P.spmv_csr(csr, xp, kernel)
         assert O.relative_error(got, want) <= 1e-12, kernel
     assert np.array_equal(P.spmv_csr(csr, xp, "exact").view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("key32", [0, 1])
+def test_row_sort_key_widths_agree(key32):
+    """The 64-bit sort keys (n_cols > 2^27 path, forced here) and the 32-bit ones build the
+    same permuted CSR, bit for bit, as the oracle."""
+    from paper_2308_00106_b200 import _lib
+
+    rng = np.random.default_rng(17)
+    n = 3000
+    mask = rng.random((n, n)) < 0.004
+    mask[5] = rng.random(n) < 0.5  # a long row (block / long sort paths)
+    rows, cols = np.nonzero(mask)
+    vals = rng.random(rows.size)
+    m = P.CooMatrix(n, n, rows, cols, vals)
+    p_r, p_c = P.build_strategy(m, P.StrategyKind.ROW_COLUMN_PERMUTE, 3)
+    _lib.call("sme_sort_rows_set_key32", key32)
+    try:
+        csr = P.coo_to_csr(P.permute_matrix(m, p_r, p_c))
+        csr2 = P.permute_csr(P.CsrMatrix(n, n, *O.coo_to_csr(n, rows, cols, vals)), p_r, p_c)
+    finally:
+        _lib.call("sme_sort_rows_set_key32", 1)
+    pr, pc = O.permute_coo(rows, cols, p_r.forward, p_c.forward)
+    optr, ocol, oval = O.coo_to_csr(n, pr, pc, vals)
+    for c in (csr, csr2):
+        assert np.array_equal(c.row_ptr, optr) and np.array_equal(c.col_idx, ocol)
+        assert np.array_equal(c.values.view(np.uint64), oval.view(np.uint64))
