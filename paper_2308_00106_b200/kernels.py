@@ -256,9 +256,11 @@ def spmv_into(m: CsrMatrix, xd: torch.Tensor, y: torch.Tensor, kernel: str = "ve
 def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None = None):
     """y[i] = sum over row i of values[k] * x[col_idx[k]] (kernels.py:73-78).
 
-    kernel="auto" picks the CSR-vector kernel when x fits in half of L2 (then
-    spmv_csr_parallel is bitwise equal, as in the reference) and the column-panel
-    stream kernel otherwise."""
+    kernel="auto" (auto_kernel): the segmented-chunk column panels ('seg') when x is
+    large (> 60 % of L2) or medium-sized and the matrix is not banded; the
+    nnz-balanced 'stream' kernel for other ragged matrices; else the CSR-vector
+    kernel (then spmv_csr_parallel is bitwise equal, as in the reference).  A pinned
+    host x of a panel layout streams in slice by slice while the passes run."""
     if not isinstance(m, CsrMatrix):
         raise TypeError("spmv_csr expects a CsrMatrix of this package (see matio.from_reference)")
     dev = m.d_row_ptr.device
