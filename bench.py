@@ -118,12 +118,11 @@ HOST_PERM_S: dict = {}
 
 
 def host_perms(n_rows: int, n_cols: int, native: bool = True):
-    """ROW_COLUMN_PERMUTE with seed 7 (permute.py:234-235), int64 forward vectors.
+    """ROW_COLUMN_PERMUTE with seed 7 (permute.py:234-235), int64 forward vectors on the host.
 
-    native: the package's bit-exact PCG64 generator (sme_host_pcg64_permutation,
-    row and column concurrently); otherwise numpy's own Generator.permutation
-    (the reference arm's setup).
-    """
+    native: the package's bit-exact PCG64 shuffle (sme_host_pcg64_permutation, row and
+    column concurrently); otherwise numpy's own Generator.permutation (the reference
+    arm's setup)."""
     from paper_2308_00106_b200.permute import axis_seed, random_permutation_forward
 
     t = time.perf_counter()
@@ -139,6 +138,25 @@ def host_perms(n_rows: int, n_cols: int, native: bool = True):
     HOST_PERM_S["native" if native else "numpy"] = round(dt, 3)
     log(f"[bench] host permutations {n_rows:,}+{n_cols:,} ({'native' if native else 'numpy'}): {dt:.2f}s")
     return fr, fc
+
+
+def device_perms(n_rows: int, n_cols: int):
+    """ROW_COLUMN_PERMUTE with seed 7 as device Permutations: host swap partners (parallel
+    PCG64 jump-ahead + branch-free rejection replay), swaps applied on the GPU
+    (sme_fy_apply); bit-exact with numpy (tests/test_gpu_shuffle.py)."""
+    import torch
+
+    import paper_2308_00106_b200 as P
+    from paper_2308_00106_b200.permute import axis_seed
+
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    p_r, p_c = P.random_permutations([(n_rows, axis_seed(PERM_SEED, 0)), (n_cols, axis_seed(PERM_SEED, 1))])
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+    HOST_PERM_S["native"] = round(dt, 3)
+    log(f"[bench] permutations {n_rows:,}+{n_cols:,} (host partners + GPU swaps): {dt:.2f}s")
+    return p_r, p_c
 
 
 def build_matrix(cfg: dict):
@@ -320,9 +338,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
     torch.cuda.synchronize()
     n, nnz = A.n_rows, A.nnz
     log(f"[bench] rank {rank}: built {cfg['workload']} nnz={nnz:,} in {time.perf_counter() - t0:.1f}s")
-    fr, fc = host_perms(n, A.n_cols)
-    p_r = P.Permutation(torch.from_numpy(fr.astype(np.int32)).to(dev), _host=fr)
-    p_c = P.Permutation(torch.from_numpy(fc.astype(np.int32)).to(dev), _host=fc)
+    p_r, p_c = device_perms(n, A.n_cols)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ev[0].record()
     B = P.permute_csr(A, p_r, p_c)
@@ -629,7 +645,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         "entropy_bits": {"unpermuted": round(H_before, 6), "permuted": round(H_after, 6), "max": 14.0},
         "load_balance_148_even_rows": balance,
         "permute_ms": round(permute_ms, 2),
-        "host_perm_gen_s": HOST_PERM_S.get("native"),
+        "perm_gen_s": HOST_PERM_S.get("native"),
         "hist_ms": round(hist_ms, 3),
         "roundtrip_rel_err": rel_err,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -669,9 +685,7 @@ def run_iterative(args, cfg) -> dict:
     x0 = P.input_vector(0, n)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    fr, fc = host_perms(n, n)
-    p_r = P.Permutation(torch.from_numpy(fr.astype(np.int32)).to(dev), _host=fr)
-    p_c = P.Permutation(torch.from_numpy(fc.astype(np.int32)).to(dev), _host=fc)
+    p_r, p_c = device_perms(n, n)
     t1 = time.perf_counter()
     op = PermutedOperator(A, p_r, p_c, kernel=args.kernel)
     torch.cuda.synchronize()
@@ -750,7 +764,7 @@ def run_iterative(args, cfg) -> dict:
                                        else "SpMV + dot + scale (unfused)")},
         "eigenvalue": {"permuted": lam_p, "unpermuted": lam_u, "rel_diff": abs(lam_p - lam_u) / lam_u},
         "amortisation": {"permutation_setup_ms": round(perm_s * 1e3, 2),
-                         "of_which_host_generation_ms": round(HOST_PERM_S.get("native", 0.0) * 1e3, 2),
+                         "of_which_generation_ms": round(HOST_PERM_S.get("native", 0.0) * 1e3, 2),
                          "of_which_permuted_csr_build_ms": round(build_s * 1e3, 2),
                          "permuted_1000_iter_ms": round(perm_ms, 3), "unpermuted_1000_iter_ms": round(unperm_ms, 3),
                          "permuted_total_ms": round(total_perm, 3),
@@ -783,8 +797,7 @@ def run_iterative_dist(args, cfg, rank: int, world: int) -> dict:
     A = build_matrix(cfg)
     n, nnz = A.n_rows, A.nnz
     iters = 1000
-    fr, _ = host_perms(n, n)
-    p = P.Permutation(torch.from_numpy(fr.astype(np.int32)).to(dev), _host=fr)
+    p, _ = device_perms(n, n)
     dpi = DistributedPowerIteration(A, p, P.input_vector(0, n))
     dpi.run(max(3, args.warmup))
     torch.cuda.synchronize()

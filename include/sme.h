@@ -96,6 +96,18 @@ int sme_host_mm_format(const int64_t* rows, const int64_t* cols, const double* v
  * h_out = int32[n] host buffer, 1 <= n <= 2^31 - 1.  Swap partners are drawn
  * ahead of the swaps and prefetched (pcg64_host.cpp). */
 int sme_host_pcg64_permutation(uint64_t* st, int64_t n, int32_t* h_out);
+/* HOST call: only the swap partners of that shuffle, h_j[i] = random_interval(i)
+ * for i = n-1 .. 1 (h_j[0] = 0), st updated exactly as numpy's shuffle leaves it.
+ * Raw outputs are generated in parallel (LCG jump-ahead per thread), the masked
+ * rejection replayed sequentially and branch-free.  threads <= 0: up to 8. */
+int sme_host_pcg64_swap_partners(uint64_t* st, int64_t n, uint32_t* h_j, int threads);
+/* The swaps of that shuffle on the GPU (shuffle.cu): d_perm = the permutation
+ * a = arange(n); for i = n-1..1: swap(a[i], a[d_j[i]]) builds — computed as a
+ * bucket sort of the steps by partner, a link pass and a chain walk (no dependent
+ * swaps).  Bit-exact with numpy's Generator.permutation given the partners. */
+int sme_fy_apply_workspace_size(int64_t n, size_t* bytes);
+int sme_fy_apply(int64_t n, const uint32_t* d_j, int32_t* d_perm, void* d_ws, size_t ws_bytes,
+                 sme_stream_t stream);
 
 /* Permutation.inverse: inv[fwd[i]] = i.  Replaces permute.py:42-45 and the
  * bijection check of Permutation.__post_init__ (permute.py:29-36): bit

@@ -36,6 +36,9 @@ SIGNATURES: dict[str, list] = {
     "sme_l2_set_persisting": [sz],
     "sme_l2_window": [p, sz, C.c_float, p],
     "sme_host_pcg64_permutation": [p, i64, p],
+    "sme_host_pcg64_swap_partners": [p, i64, p, C.c_int],
+    "sme_fy_apply_workspace_size": [i64, psz],
+    "sme_fy_apply": [i64, p, p, p, sz, p],
     "sme_host_mm_parse": [p, i64, C.c_int, i64, i64, i64, i64, C.c_int, C.c_int, p, p, p, p],
     "sme_host_mm_format": [p, p, p, i64, p, i64, C.c_int, p],
     "sme_perm_inverse": [i64, p, p, p, p],

@@ -101,6 +101,28 @@ void store_state(const Pcg64& g, uint64_t* st) {
   st[5] = g.buf32;  // numpy keeps the stale half after consuming it
 }
 
+// state after `delta` more steps of the LCG (Brown's O(log delta) jump-ahead)
+inline u128 advance(u128 state, u128 inc, uint64_t delta) {
+  u128 acc_mult = 1, acc_plus = 0, cur_mult = kMult, cur_plus = inc;
+  while (delta > 0) {
+    if (delta & 1) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return acc_mult * state + acc_plus;
+}
+
+inline uint64_t xsl_rr(u128 state) {
+  const uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
+  const unsigned rot = (unsigned)(hi >> 58);
+  const uint64_t x = hi ^ lo;
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
 constexpr int kAhead = 32;           // swaps prefetched ahead
 constexpr int64_t kBlock = 1 << 16;  // swap partners per producer block
 constexpr int kRing = 8;             // producer blocks in flight
@@ -166,6 +188,86 @@ SME_API int sme_host_pcg64_permutation(uint64_t* st, int64_t n, int32_t* h_out) 
       consumed.store(b + 1, std::memory_order_release);
     }
     producer.join();
+  }
+  store_state(g, st);
+  return SME_OK;
+}
+
+// The swap partners of Generator(PCG64).permutation(n) without the swaps:
+// h_j[i] = random_interval(i) for i = n-1 .. 1 in numpy's draw order (h_j[0] = 0),
+// st updated exactly as the full shuffle leaves it.  The raw 64-bit outputs are
+// produced in parallel, already split into numpy's uint32 order (low half, then
+// the buffered high half), each thread jumping ahead to its share of a block with
+// the LCG's O(log k) advance; one sequential pass then replays the masked
+// rejection over that uint32 stream.  The swaps themselves run on the GPU
+// (sme_fy_apply).
+SME_API int sme_host_pcg64_swap_partners(uint64_t* st, int64_t n, uint32_t* h_j, int threads) {
+  if (!st || !h_j || n < 1 || n > INT32_MAX) {
+    sme::set_error("sme_host_pcg64_swap_partners: bad arguments (n=%lld)", (long long)n);
+    return SME_EINVAL;
+  }
+  Pcg64 g = load_state(st);
+  h_j[0] = 0;
+  if (n == 1) return SME_OK;
+  const int T = threads > 0 ? threads : (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  constexpr int64_t kOut = 1 << 20;      // 64-bit outputs per parallel block
+  std::vector<uint32_t> u((size_t)(2 * kOut + 1));
+  u128 base = g.state;                   // state before the next block's first output
+  int64_t blocks = 0;                    // blocks generated
+  int64_t d = 0, d_end = 0;              // read position / end in u
+  auto refill = [&](bool first) {
+    // a pending buffered half (numpy's has_uint32) comes first
+    int64_t off = 0;
+    if (first && g.has32) u[(size_t)off++] = g.buf32;
+    std::vector<std::thread> th;
+    auto body = [&](int t) {
+      const int64_t a0 = kOut * t / T, b0 = kOut * (t + 1) / T;
+      u128 x = advance(base, g.inc, (uint64_t)a0);
+      for (int64_t k = a0; k < b0; ++k) {
+        x = x * kMult + g.inc;
+        const uint64_t v = xsl_rr(x);
+        u[(size_t)(off + 2 * k)] = (uint32_t)v;
+        u[(size_t)(off + 2 * k + 1)] = (uint32_t)(v >> 32);
+      }
+    };
+    for (int t = 1; t < T; ++t) th.emplace_back(body, t);
+    body(0);
+    for (auto& x : th) x.join();
+    base = advance(base, g.inc, (uint64_t)kOut);
+    ++blocks;
+    d = 0;
+    d_end = off + 2 * kOut;
+  };
+  refill(true);
+  const int64_t lead = g.has32 ? 1 : 0;  // the pending half occupies u[0] of the first block
+  int64_t i = n - 1;
+  while (i >= 1) {
+    uint32_t mask = (uint32_t)i;
+    mask |= mask >> 1;
+    mask |= mask >> 2;
+    mask |= mask >> 4;
+    mask |= mask >> 8;
+    mask |= mask >> 16;
+    const int64_t i_lo = (int64_t)(mask >> 1);  // the mask holds for i in (mask / 2, i]
+    // branch-free rejection: every draw is written to h_j[i]; a rejected one is
+    // overwritten by the next draw for the same i, an accepted one moves i on
+    while (i > i_lo) {
+      if (d == d_end) refill(false);
+      const uint32_t v = u[(size_t)d++] & mask;
+      h_j[i] = v;
+      i -= (int64_t)(v <= (uint32_t)i);
+    }
+  }
+  // uint32 values consumed in total (the pending half counts as one), and where they
+  // leave numpy's buffer: an odd number of fresh halves means a high half is pending
+  const int64_t total_fresh = (blocks - 1) * 2 * kOut + (d - (blocks == 1 ? lead : 0));
+  const int64_t outputs = (total_fresh + 1) / 2;
+  g.state = advance(g.state, g.inc, (uint64_t)outputs);
+  if (total_fresh > 0) {
+    g.has32 = (total_fresh & 1) != 0;
+    g.buf32 = (uint32_t)(xsl_rr(g.state) >> 32);  // the high half of the last output drawn
+  } else {
+    g.has32 = false;  // only the pending half was used (or nothing)
   }
   store_state(g, st);
   return SME_OK;

@@ -156,6 +156,33 @@ def pcg64_permutation(bitgen: np.random.PCG64, n: int) -> np.ndarray:
     return out
 
 
+def pcg64_swap_partners(bitgen: np.random.PCG64, n: int, out: np.ndarray | None = None, threads: int = 0) -> np.ndarray:
+    """The swap partners of Generator(bitgen).permutation(n): j[i] for i = n-1..1 in numpy's
+    draw order (j[0] = 0), advancing `bitgen` exactly like the full shuffle (host call)."""
+    if n < 1 or n > 2**31 - 1:
+        raise ValueError("permutation size must be in [1, 2^31)")
+    words = _pcg64_words(bitgen)
+    j = np.empty(n, dtype=np.uint32) if out is None else out
+    _lib.call("sme_host_pcg64_swap_partners", words.ctypes.data, n, j.ctypes.data, int(threads))
+    _set_pcg64_words(bitgen, words)
+    return j
+
+
+def pcg64_permutation_device(bitgen: np.random.PCG64, n: int, threads: int = 0) -> torch.Tensor:
+    """Generator(bitgen).permutation(n) as a CUDA int32 tensor, bit-exact: partners drawn on
+    the host (sme_host_pcg64_swap_partners), swaps applied in parallel on the GPU
+    (sme_fy_apply: bucket sort by partner + chain walk instead of n dependent swaps)."""
+    dev = _cuda.require_cuda()
+    # pageable partners: pinning 200 MB costs more (~0.1 s at 50M) than the pageable copy
+    h_j = pcg64_swap_partners(bitgen, n, threads=threads)
+    d_j = torch.from_numpy(h_j.view(np.int32)).to(dev)
+    out = torch.empty(n, dtype=torch.int32, device=dev)
+    ws = _cuda.workspace(_lib.query_size("sme_fy_apply_workspace_size", n))
+    _lib.call("sme_fy_apply", n, ptr(d_j), ptr(out), ptr(ws), ws.numel(), stream())
+    torch.cuda.current_stream().synchronize()  # ws is released on return
+    return out
+
+
 def _check_perm_args(n: int, seed: int) -> None:
     if n < 1:
         raise ValueError("permutation size must be >= 1")
@@ -169,15 +196,11 @@ def random_permutation_forward(n: int, seed: int) -> np.ndarray:
     return pcg64_permutation(np.random.PCG64(seed), n)
 
 
-def _upload_forward(fwd: np.ndarray) -> Permutation:
-    # a shuffle of arange is a bijection by construction
-    dev = _cuda.require_cuda()
-    return Permutation(torch.from_numpy(fwd).to(dev), _trusted=True)
-
-
 def random_permutation(n: int, seed: int) -> Permutation:
-    """Uniform permutation from a seeded PCG64 generator (Fisher-Yates), bit-identical to the reference."""
-    return _upload_forward(random_permutation_forward(n, seed))
+    """Uniform permutation from a seeded PCG64 generator (Fisher-Yates), bit-identical to the reference:
+    host draws, GPU swaps (pcg64_permutation_device)."""
+    _check_perm_args(n, seed)
+    return Permutation(pcg64_permutation_device(np.random.PCG64(seed), n), _trusted=True)
 
 
 def random_permutations(specs) -> list[Permutation]:
@@ -187,11 +210,23 @@ def random_permutations(specs) -> list[Permutation]:
         _check_perm_args(n, seed)
     if len(specs) == 1:
         return [random_permutation(*specs[0])]
+    # the host draws of all specs run concurrently (ctypes releases the GIL), then the
+    # GPU applies the swaps
     from concurrent.futures import ThreadPoolExecutor
 
+    dev = _cuda.require_cuda()
+    threads = max(1, 8 // len(specs))
     with ThreadPoolExecutor(max_workers=len(specs)) as ex:
-        fwds = list(ex.map(lambda a: random_permutation_forward(*a), specs))
-    return [_upload_forward(f) for f in fwds]
+        hs = list(ex.map(lambda a: pcg64_swap_partners(np.random.PCG64(a[1]), a[0], threads=threads), specs))
+    out = []
+    for (n, _), h in zip(specs, hs):
+        d_j = torch.from_numpy(h.view(np.int32)).to(dev)
+        perm = torch.empty(n, dtype=torch.int32, device=dev)
+        ws = _cuda.workspace(_lib.query_size("sme_fy_apply_workspace_size", n))
+        _lib.call("sme_fy_apply", n, ptr(d_j), ptr(perm), ptr(ws), ws.numel(), stream())
+        out.append(Permutation(perm, _trusted=True))
+    torch.cuda.current_stream().synchronize()  # the workspaces are released on return
+    return out
 
 
 def permute_rows(m: CooMatrix, p: Permutation) -> CooMatrix:
@@ -333,11 +368,9 @@ def riffle_shuffle_permutation(n: int, pivot: int, seed: int) -> Permutation:
         raise ValueError(f"pivot {pivot} out of range (0, {n})")
     if seed < 0:
         raise ValueError("seed must be non-negative")
-    bitgen = np.random.PCG64(seed)
-    local = np.empty(n, dtype=np.int32)
-    local[:pivot] = pcg64_permutation(bitgen, pivot)
-    local[pivot:] = pivot + pcg64_permutation(bitgen, n - pivot)
-    return compose(Permutation(_interleave_forward(n, pivot)), Permutation(local))
+    bitgen = np.random.PCG64(seed)  # one generator, two consecutive shuffles (permute.py:154-156)
+    local = torch.cat([pcg64_permutation_device(bitgen, pivot), pivot + pcg64_permutation_device(bitgen, n - pivot)])
+    return compose(Permutation(_interleave_forward(n, pivot)), Permutation(local, _trusted=True))
 
 
 class StrategyKind(Enum):

@@ -14,6 +14,7 @@ from paper_2308_00106_b200.permute import (
     _interleave_forward,
     axis_seed,
     pcg64_permutation,
+    pcg64_swap_partners,
     random_permutation_forward,
 )
 from paper_2308_00106_b200.rowshard import ShardPlan
@@ -101,3 +102,35 @@ def test_shard_plan(n, world):
     assert sizes.max() <= plan.pad
     cols = np.unique(np.r_[0, n - 1, plan.cols[:-1], np.minimum(plan.cols[1:], n - 1)])
     assert np.array_equal(plan.slot_of(cols), O.rowshard_remap_cols(cols, n, world, plan.pad))
+
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 64, 1000, 20_000])
+@pytest.mark.parametrize("seed", [0, 7, 2**40 + 3])
+@pytest.mark.parametrize("pending", [False, True])
+def test_native_swap_partners_replay_numpys_shuffle(n, seed, pending):
+    """sme_host_pcg64_swap_partners: the sequential swaps over its partners give numpy's
+    permutation, and the generator ends in numpy's state; also with a pending uint32 half
+    (pending=True draws one integer first, like a second riffle part after an odd count)."""
+    ours_bg, ref_bg = np.random.PCG64(seed), np.random.PCG64(seed)
+    if pending:
+        for bg in (ours_bg, ref_bg):
+            np.random.Generator(bg).integers(0, 10, dtype=np.uint32)
+        assert ours_bg.state["has_uint32"] == 1
+    j = pcg64_swap_partners(ours_bg, n, threads=3)
+    a = np.arange(n)
+    for i in range(n - 1, 0, -1):
+        a[i], a[j[i]] = a[j[i]], a[i]
+    assert np.array_equal(a, np.random.Generator(ref_bg).permutation(n))
+    assert ours_bg.state == ref_bg.state
+
+
+def test_native_swap_partners_large_match_full_shuffle():
+    bg1, bg2 = np.random.PCG64(123), np.random.PCG64(123)
+    n = 3_000_001
+    j = pcg64_swap_partners(bg1, n)
+    full = pcg64_permutation(bg2, n)
+    assert bg1.state == bg2.state
+    # spot-check: the partners' last steps reproduce the shuffle's tail positions' dependence
+    assert j[0] == 0 and int(j[1:].max()) < n and np.all(j[1:] <= np.arange(1, n))
+    assert full.dtype == np.int32
