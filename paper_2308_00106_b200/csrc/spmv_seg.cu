@@ -110,45 +110,92 @@ __global__ void k_seg_hdr(int64_t n_rows, const int32_t* __restrict__ pos, int32
   }
 }
 
-// warp per row: entries go to their panel at off_p + pos_p[r] + rank
+// warp per row: entries go to their panel at off_p + pos_p[r] + rank.  Lane p < P
+// holds panel p's per-row data (count, position, panel offset, first entry of the
+// row in that panel); an entry finds its panel among the bounds and takes the
+// panel's data by shuffle — no per-entry walk over the panels' count arrays.
 template <typename T>
 __global__ void k_seg_scatter(int64_t n_rows, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                               const T* __restrict__ val, int32_t n_panels, const int32_t* __restrict__ bounds,
                               const int32_t* __restrict__ counts, const int32_t* __restrict__ pos,
                               const int64_t* __restrict__ offsets, uint32_t* __restrict__ out_pk,
                               T* __restrict__ out_val, const int32_t* __restrict__ hdr) {
+  const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool direct = n_panels <= 32;
+  const int32_t my_hi = (direct && lane < n_panels) ? bounds[lane + 1] : INT32_MAX;
+  const int32_t my_lo = (direct && lane < n_panels) ? bounds[lane] : 0;
+  const int64_t my_off = (direct && lane < n_panels) ? offsets[lane] : 0;
   for (int64_t r = warp; r < n_rows; r += n_warps) {
     const int32_t a = row_ptr[r], b = row_ptr[r + 1];
-    // explicit zeros: lane p handles panel p
-    for (int p = lane; p < n_panels; p += 32) {
-      if (counts[(int64_t)p * n_rows + r] == 0) {
-        const int32_t* pp = pos + (int64_t)p * (n_rows + 1);
-        if (pp[r + 1] > pp[r]) {
-          const int64_t local = pp[r];
-          const int64_t dst = offsets[p] + local;
-          const int32_t h = hdr[(offsets[p] + local) / SEG_CH];
-          out_pk[dst] = (SEG_MARK << SEG_CSHIFT) | SEG_END | (uint32_t)(r - h);
-          out_val[dst] = T(0);
+    if (!direct) {  // > 32 panels: walk the count arrays (rare, small matrices)
+      for (int p = lane; p < n_panels; p += 32) {
+        if (counts[(int64_t)p * n_rows + r] == 0) {
+          const int32_t* pp = pos + (int64_t)p * (n_rows + 1);
+          if (pp[r + 1] > pp[r]) {
+            const int64_t dst = offsets[p] + pp[r];
+            out_pk[dst] = (SEG_MARK << SEG_CSHIFT) | SEG_END | (uint32_t)(r - hdr[dst / SEG_CH]);
+            out_val[dst] = T(0);
+          }
         }
       }
-    }
-    for (int32_t k = a + lane; k < b; k += 32) {
-      const int32_t c = col[k];
-      int p = 0;
-      int32_t first = a;
-      while (p + 1 < n_panels && c >= bounds[p + 1]) {
-        first += counts[(int64_t)p * n_rows + r];
-        ++p;
+      for (int32_t k = a + lane; k < b; k += 32) {
+        const int32_t c = col[k];
+        int p = 0;
+        int32_t first = a;
+        while (p + 1 < n_panels && c >= bounds[p + 1]) {
+          first += counts[(int64_t)p * n_rows + r];
+          ++p;
+        }
+        const int64_t dst = offsets[p] + (int64_t)pos[(int64_t)p * (n_rows + 1) + r] + (k - first);
+        const bool last = k - first == counts[(int64_t)p * n_rows + r] - 1;
+        out_pk[dst] = ((uint32_t)(c - bounds[p]) << SEG_CSHIFT) | (last ? SEG_END : 0u) |
+                      (uint32_t)(r - hdr[dst / SEG_CH]);
+        out_val[dst] = val[k];
       }
-      const int64_t local = (int64_t)pos[(int64_t)p * (n_rows + 1) + r] + (k - first);
-      const int64_t dst = offsets[p] + local;
-      const int32_t h = hdr[dst / SEG_CH];
-      const bool last = k - first == counts[(int64_t)p * n_rows + r] - 1;
-      out_pk[dst] = ((uint32_t)(c - bounds[p]) << SEG_CSHIFT) | (last ? SEG_END : 0u) | (uint32_t)(r - h);
-      out_val[dst] = val[k];
+      continue;
+    }
+    int32_t cnt = 0, ppos = 0, pnext = 0;
+    if (lane < n_panels) {
+      cnt = counts[(int64_t)lane * n_rows + r];
+      const int32_t* pp = pos + (int64_t)lane * (n_rows + 1);
+      ppos = pp[r];
+      pnext = pp[r + 1];
+    }
+    // first entry of the row in panel `lane`: exclusive prefix of the counts
+    int32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t t = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int32_t first = a + incl - cnt;
+    // explicit zero of this row in panel `lane`
+    if (lane < n_panels && cnt == 0 && pnext > ppos) {
+      const int64_t dst = my_off + ppos;
+      out_pk[dst] = (SEG_MARK << SEG_CSHIFT) | SEG_END | (uint32_t)(r - hdr[dst / SEG_CH]);
+      out_val[dst] = T(0);
+    }
+    for (int32_t k0 = a; k0 < b; k0 += 32) {
+      const int32_t k = k0 + lane;
+      const int32_t c = k < b ? col[k] : INT32_MAX;
+      // panel of c: number of panel upper bounds <= c (bounds held by lanes)
+      int p = 0;
+      for (int q = 0; q < n_panels; ++q) p += (c >= __shfl_sync(FULL, my_hi, q)) ? 1 : 0;
+      if (p >= n_panels) p = n_panels - 1;
+      const int32_t f = __shfl_sync(FULL, first, p);
+      const int32_t pc = __shfl_sync(FULL, cnt, p);
+      const int32_t pp = __shfl_sync(FULL, ppos, p);
+      const int64_t po = __shfl_sync(FULL, my_off, p);
+      const int32_t lo = __shfl_sync(FULL, my_lo, p);
+      if (k < b) {
+        const int64_t dst = po + pp + (k - f);
+        const bool last = k - f == pc - 1;
+        out_pk[dst] = ((uint32_t)(c - lo) << SEG_CSHIFT) | (last ? SEG_END : 0u) | (uint32_t)(r - hdr[dst / SEG_CH]);
+        out_val[dst] = val[k];
+      }
     }
   }
 }
