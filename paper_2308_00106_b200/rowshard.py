@@ -141,7 +141,12 @@ class RowShardedSpMV:
 
     @property
     def pipelined(self) -> bool:
-        return self.seg is not None and self.plan.world > 1
+        """Per-slot broadcasts pipelined with the panel passes (seg shards); the env
+        SME_PIPELINED_EXCHANGE=0 falls back to one all-gather before the passes."""
+        import os
+
+        return (self.seg is not None and self.plan.world > 1
+                and os.environ.get("SME_PIPELINED_EXCHANGE", "1") != "0")
 
     def step(self, x_chunk: torch.Tensor, group=None) -> torch.Tensor:
         """Exchange the padded x chunks of every rank, then y_local = A_local x.
