@@ -60,6 +60,9 @@ int sme_device_info(int64_t* out);
  * L2 (device-wide) and set/clear the access-policy window of a stream. */
 int sme_l2_set_persisting(size_t bytes);
 int sme_l2_window(const void* d_ptr, size_t bytes, float hit_ratio, sme_stream_t stream);
+/* Sequential L2 prefetch (evict-last) of a device range: warms a panel's x slice
+ * before its random gathers (stream-ordered). */
+int sme_l2_prefetch(const void* d_ptr, size_t bytes, sme_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* Matrix Market I/O — matio.py (HOST calls: host buffers, no stream)        */

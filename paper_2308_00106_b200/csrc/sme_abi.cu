@@ -76,3 +76,23 @@ SME_API int sme_l2_window(const void* ptr, size_t bytes, float hit_ratio, sme_st
   if (!bytes) SME_CUDA(cudaCtxResetPersistingL2Cache());
   return SME_OK;
 }
+
+namespace sme {
+// one prefetch per 128-B line of [p, p + bytes) into L2 (evict-last): a sequential
+// sweep that fills a column panel's x slice before the random gathers start
+__global__ void k_l2_prefetch(const char* __restrict__ p, size_t bytes) {
+  for (size_t off = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 128; off < bytes;
+       off += (size_t)gridDim.x * blockDim.x * 128)
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p + off));
+}
+}  // namespace sme
+
+// Prefetch a device range into L2 (stream-ordered; no data returned).
+SME_API int sme_l2_prefetch(const void* d_ptr, size_t bytes, sme_stream_t stream) {
+  if (bytes == 0) return SME_OK;
+  SME_REQUIRE(d_ptr, "null pointer");
+  sme::k_l2_prefetch<<<sme::grid_for((int64_t)((bytes + 127) / 128), 256, 4), 256, 0, sme::as_stream(stream)>>>(
+      (const char*)d_ptr, bytes);
+  SME_CHECK_LAUNCH("k_l2_prefetch");
+  return SME_OK;
+}

@@ -87,11 +87,15 @@ class SegLayout:
         self.nnz = m.nnz
         self.persist = False
         self.hit_ratio = 1.0  # access-policy window hit ratio of the pinned x slice
+        self.warm = False  # L2 prefetch sweep of each pass's x slice (experiment knob)
 
     # -- passes --------------------------------------------------------------
     def _pass(self, p: int, xd: torch.Tensor, y: torch.Tensor) -> None:
         vb = self.val.element_size()
         o = int(self.offsets[p])
+        if self.warm:  # sweep the pass's x slice into L2 before its random gathers
+            lo, hi = int(self.bounds_host[p]), int(self.bounds_host[p + 1])
+            _lib.call("sme_l2_prefetch", ptr(xd) + vb * lo, (hi - lo) * vb, stream())
         _lib.call("sme_spmv_seg", _cuda.sme_dtype(self.val), self.n_warps, ptr(self.pk) + 4 * o, ptr(self.val) + vb * o,
                   ptr(self.hdr) + 4 * (o // CHUNK), ptr(self.plans) + 4 * p * (self.n_warps + 1),
                   ptr(xd) + vb * int(self.bounds_host[p]), ptr(y), int(p > 0), stream())

@@ -29,6 +29,7 @@ ap.add_argument("--panels", type=int, default=0)
 ap.add_argument("--seg-panels", type=int, default=0)
 ap.add_argument("--seg-mode", type=int, default=-1)
 ap.add_argument("--seg-warps", type=int, default=0, help="persistent warps of the seg grid (default: occupancy)")
+ap.add_argument("--seg-warm", action="store_true", help="L2 prefetch sweep of each pass's x slice")
 ap.add_argument("--seg-hit", type=float, default=-1.0, help="x-slice L2 window hit ratio (0 = no persistence)")
 ap.add_argument("--check", action="store_true", help="compare with the stream kernel")
 ap.add_argument("--persist", action="store_true")
@@ -101,6 +102,10 @@ if a.seg_mode >= 0:
 
     _lib.call("sme_spmv_seg_set_mode", a.seg_mode)
 y = torch.empty(n, dtype=B.dtype, device=dev)
+if a.seg_warm:
+    from paper_2308_00106_b200.seg import seg_of
+
+    seg_of(B).warm = True
 t_setup = time.perf_counter()
 spmv_into(B, xp, y, a.kernel)
 torch.cuda.synchronize()
