@@ -321,6 +321,19 @@ __global__ void k_spmv_plan(int64_t n_tiles, int32_t n_rows, int32_t nnz, const 
 }
 
 // CSR-vector: L lanes per row; warp-uniform loop over blocks of 32/L rows.
+// x gathers of the CSR-vector kernels: L1::no_allocate + L2 evict-last.  Measured on
+// C2: permuted 0.1066 -> 0.1007 ms, unpermuted (banded) 0.0589 -> 0.0576 ms.
+__device__ __forceinline__ double ld_x_na(const double* p, uint64_t pol) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_x_na(const float* p, uint64_t pol) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
 template <typename T, int L>
 __global__ void __launch_bounds__(256) k_spmv_vector(int64_t n_rows, const int32_t* __restrict__ row_ptr,
                                                      const int32_t* __restrict__ col, const T* __restrict__ val,
@@ -339,10 +352,10 @@ __global__ void __launch_bounds__(256) k_spmv_vector(int64_t n_rows, const int32
       const int32_t a = row_ptr[r], b = row_ptr[r + 1];
       for (int32_t k = a + li; k < b; k += L)
         if (L >= 8) {
-          s += ld_stream(val + k, pol_stream) * ld_keep(x + ld_stream_i1(col + k, pol_stream), pol_keep);
+          s += ld_stream(val + k, pol_stream) * ld_x_na(x + ld_stream_i1(col + k, pol_stream), pol_keep);
         } else {
           // narrow groups touch each line several times: let L1 keep it (evict-first in L2)
-          s += ld_l1(val + k, pol_stream) * ld_keep(x + ld_l1(col + k, pol_stream), pol_keep);
+          s += ld_l1(val + k, pol_stream) * ld_x_na(x + ld_l1(col + k, pol_stream), pol_keep);
         }
     }
 #pragma unroll
@@ -382,9 +395,9 @@ __global__ void __launch_bounds__(VE_NT) k_spmv_vector_epi(int64_t n_rows, const
       const int32_t a = row_ptr[r], b = row_ptr[r + 1];
       for (int32_t k = a + li; k < b; k += L)
         if (L >= 8)
-          s += ld_stream(val + k, pol_stream) * ld_keep(x + ld_stream_i1(col + k, pol_stream), pol_keep);
+          s += ld_stream(val + k, pol_stream) * ld_x_na(x + ld_stream_i1(col + k, pol_stream), pol_keep);
         else
-          s += ld_l1(val + k, pol_stream) * ld_keep(x + ld_l1(col + k, pol_stream), pol_keep);
+          s += ld_l1(val + k, pol_stream) * ld_x_na(x + ld_l1(col + k, pol_stream), pol_keep);
     }
 #pragma unroll
     for (int o = L / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
