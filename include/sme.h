@@ -330,6 +330,15 @@ int sme_spmv_seg_warps(int32_t* n_warps);
 int sme_spmv_seg_set_mode(int mode);
 int sme_seg_plan(int64_t n_rows, const int32_t* d_pos_panel, int32_t n_warps, int32_t* d_plan,
                  sme_stream_t stream);
+/* Split-row plan (power-law rows): plan[w] = w * total / n_warps, ranges may start and
+ * end mid-row; passes over it use sme_spmv_seg_split. */
+int sme_seg_plan_split(int64_t total_entries, int32_t n_warps, int32_t* d_plan, sme_stream_t stream);
+/* One pass over a split-row plan: the pass, then the open row partials at the range ends
+ * (d_carry_val[n_warps] of the value type, d_carry_row[n_warps] int32 scratch) added to
+ * their rows in warp order (deterministic). */
+int sme_spmv_seg_split(int dtype, int32_t n_warps, const uint32_t* d_pk, const void* d_val, const int32_t* d_hdr,
+                       const int32_t* d_plan, const void* d_xs, void* d_y, int accumulate, void* d_carry_val,
+                       int32_t* d_carry_row, sme_stream_t stream);
 /* y (+)= A_p x_p for one panel: d_xs = x + bounds[p]; accumulate = 0 for panel 0. */
 int sme_spmv_seg(int dtype, int32_t n_warps, const uint32_t* d_pk, const void* d_val, const int32_t* d_hdr,
                  const int32_t* d_plan, const void* d_xs, void* d_y, int accumulate, sme_stream_t stream);

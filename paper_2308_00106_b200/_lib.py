@@ -78,6 +78,8 @@ SIGNATURES: dict[str, list] = {
     "sme_spmv_seg_warps": [C.POINTER(C.c_int32)],
     "sme_spmv_seg_set_mode": [C.c_int],
     "sme_seg_plan": [i64, p, i32, p, p],
+    "sme_seg_plan_split": [i64, i32, p, p],
+    "sme_spmv_seg_split": [C.c_int, i32, p, p, p, p, p, p, C.c_int, p, p, p],
     "sme_spmv_seg": [C.c_int, i32, p, p, p, p, p, p, C.c_int, p],
     "sme_spmv_seg_epi": [C.c_int, i32, p, p, p, p, p, p, C.c_int, p, p, p, p, p, p, p],
     "sme_spmv_vector_epi_blocks": [i64, C.c_int, pi64],

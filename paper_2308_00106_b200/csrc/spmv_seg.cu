@@ -264,6 +264,10 @@ struct SegEpi {
   int64_t row_offset;  // global index of this shard's row 0 in out / peers
   const T* dotv;       // null: reduce v*v; else reduce v * dotv[g] (CG's p.Ap)
   int finish;          // 0: result = {1/sqrt(sum), sum}; 1 (CG alpha): result[1] = result[0] / sum
+  // split-row plans (non-epilogue passes): the open row partial at the end of a warp's
+  // range -> carry_val[warp], its row -> carry_row[warp] (-1: the range ends on a row end)
+  T* carry_val;
+  int32_t* carry_row;
 };
 
 // last-CTA reduction of the warp partials (fixed order) -> result, next scale
@@ -341,7 +345,10 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
   const int lane = threadIdx.x & 31;
   double ss = 0.0;
   const int P0 = plan[warp], P1 = plan[warp + 1];
-  if (P0 >= P1) return ss;
+  if (P0 >= P1) {
+    if (!EPI && epi.carry_row && lane == 0) epi.carry_row[warp] = -1;
+    return ss;
+  }
   const T sc = (EPI && epi.scale) ? (T)*epi.scale : T(1);
 
   int c = P0 & ~(SEG_CH - 1);
@@ -470,11 +477,40 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
         }
       }
     }
-    if (!more) break;
+    if (!more) {
+      if (!EPI && epi.carry_row) {
+        // a split-row plan may end this range mid-row: keep the open partial for the
+        // ordered fix-up (k_seg_carry_fixup); explicit zeros always end their row
+        const int last = P1 - 1 - c, kk = last & 3;
+        const uint32_t wsel = kk == 0 ? cur.w[0] : kk == 1 ? cur.w[1] : kk == 2 ? cur.w[2] : cur.w[3];
+        const uint32_t wl = __shfl_sync(FULL, wsel, last >> 2);
+        if (lane == 0) {
+          const bool open = !(wl & SEG_END);
+          epi.carry_row[warp] = open ? cur.h + (int)(wl & SEG_DMASK) : -1;
+          epi.carry_val[warp] = open ? carry : T(0);
+        }
+      }
+      break;
+    }
     cur = nxt;
     c += SEG_CH;
   }
   return ss;
+}
+
+// Fix-up of a split-row pass: each row that ended in a later warp than it started
+// gets the open partials of its earlier warps, summed in warp order (deterministic),
+// after the pass has written / accumulated the row's tail.
+template <typename T>
+__global__ void k_seg_carry_fixup(int32_t n_warps, const int32_t* __restrict__ carry_row,
+                                  const T* __restrict__ carry_val, T* __restrict__ y) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < n_warps; w += gridDim.x * blockDim.x) {
+    const int32_t r = carry_row[w];
+    if (r < 0 || (w > 0 && carry_row[w - 1] == r)) continue;
+    T sum = carry_val[w];
+    for (int v = w + 1; v < n_warps && carry_row[v] == r; ++v) sum += carry_val[v];
+    y[r] += sum;
+  }
 }
 
 template <typename T, bool ACC, bool EPI, bool RED = false, bool CMP = false>
@@ -552,6 +588,20 @@ int launch_seg(int32_t n_warps, const uint32_t* pk, const T* val, const int32_t*
                const T* xs, T* y, int accumulate, cudaStream_t s, const SegEpi<T>* epi = nullptr) {
   const int grid = (int)(((int64_t)n_warps * 32 + SEG_NT - 1) / SEG_NT);
   const SegEpi<T> e = epi ? *epi : SegEpi<T>{};
+  if (epi && e.carry_row) {  // split-row plan: the pass, then the ordered fix-up of the open partials
+    SegEpi<T> plain = e;
+    const bool stage = kStageRows<T> && s_seg_mode != 6;
+    if (accumulate)
+      stage ? k_spmv_seg<T, true, false, true, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, plain)
+            : k_spmv_seg<T, true, false, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, plain);
+    else
+      stage ? k_spmv_seg<T, false, false, false, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, plain)
+            : k_spmv_seg<T, false, false><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, plain);
+    SME_CHECK_LAUNCH("k_spmv_seg");
+    k_seg_carry_fixup<T><<<(n_warps + 255) / 256, 256, 0, s>>>(n_warps, e.carry_row, e.carry_val, y);
+    SME_CHECK_LAUNCH("k_seg_carry_fixup");
+    return SME_OK;
+  }
   if (epi) {
     if (accumulate)
       k_spmv_seg<T, true, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
@@ -705,7 +755,8 @@ SME_API int sme_spmv_seg_epi(int dtype, int32_t n_warps, const uint32_t* pk, con
   SME_REQUIRE(n_warps >= 1 && pk && val && hdr && plan && out && scale && partials && ticket && result,
               "bad arguments");
   SME_REQUIRE((((uintptr_t)pk | (uintptr_t)val) & 15) == 0, "pk/val must be 16-byte aligned");
-  const SegEpi<double> e{(double*)out, qinv, scale, partials, ticket, result, nullptr, 0, 0, nullptr, 0};
+  const SegEpi<double> e{(double*)out, qinv, scale, partials, ticket, result, nullptr, 0, 0, nullptr, 0, nullptr,
+                         nullptr};
   return launch_seg<double>(n_warps, pk, (const double*)val, hdr, plan, (const double*)xs, (double*)y, accumulate,
                             as_stream(stream), &e);
 }
@@ -727,7 +778,7 @@ SME_API int sme_spmv_seg_epi_peers(int dtype, int32_t n_warps, const uint32_t* p
               "bad arguments");
   SME_REQUIRE((((uintptr_t)pk | (uintptr_t)val) & 15) == 0, "pk/val must be 16-byte aligned");
   const SegEpi<double> e{(double*)out, nullptr, scale, partials, ticket, result, (double* const*)d_peers, n_peers,
-                         row_offset, nullptr, 0};
+                         row_offset, nullptr, 0, nullptr, nullptr};
   return launch_seg<double>(n_warps, pk, (const double*)val, hdr, plan, (const double*)xs, (double*)y, accumulate,
                             as_stream(stream), &e);
 }
@@ -742,7 +793,46 @@ SME_API int sme_spmv_seg_epi_cg(int dtype, int32_t n_warps, const uint32_t* pk, 
   SME_REQUIRE(dtype == SME_F64, "the fused epilogue is f64 only");
   SME_REQUIRE(n_warps >= 1 && pk && val && hdr && plan && p && out && partials && ticket && scal, "bad arguments");
   SME_REQUIRE((((uintptr_t)pk | (uintptr_t)val) & 15) == 0, "pk/val must be 16-byte aligned");
-  const SegEpi<double> e{(double*)out, nullptr, nullptr, partials, ticket, scal, nullptr, 0, 0, (const double*)p, 1};
+  const SegEpi<double> e{(double*)out, nullptr, nullptr, partials, ticket, scal, nullptr, 0, 0, (const double*)p, 1,
+                         nullptr, nullptr};
   return launch_seg<double>(n_warps, pk, (const double*)val, hdr, plan, (const double*)xs, (double*)y, accumulate,
                             as_stream(stream), &e);
+}
+
+// Split-row plan: plan[w] = w * total / n_warps entry positions (ranges may start and end
+// mid-row, so one long row no longer lands on a single warp).
+__global__ void k_seg_plan_split(int64_t total, int32_t n_warps, int32_t* __restrict__ plan) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= n_warps; w += gridDim.x * blockDim.x)
+    plan[w] = (int32_t)((int64_t)w * total / n_warps);
+}
+
+SME_API int sme_seg_plan_split(int64_t total_entries, int32_t n_warps, int32_t* plan, sme_stream_t stream) {
+  SME_REQUIRE(n_warps >= 1 && total_entries >= 0 && total_entries < INT32_MAX && plan, "bad arguments");
+  k_seg_plan_split<<<grid_for((int64_t)n_warps + 1, 256), 256, 0, as_stream(stream)>>>(total_entries, n_warps, plan);
+  SME_CHECK_LAUNCH("k_seg_plan_split");
+  return SME_OK;
+}
+
+// One panel pass over a split-row plan (not the fused epilogue): like sme_spmv_seg, then
+// the open partials at the warp-range ends (carry_val[n_warps], carry_row[n_warps]
+// scratch) are added to their rows in warp order by k_seg_carry_fixup.
+SME_API int sme_spmv_seg_split(int dtype, int32_t n_warps, const uint32_t* pk, const void* val, const int32_t* hdr,
+                               const int32_t* plan, const void* xs, void* y, int accumulate, void* carry_val,
+                               int32_t* carry_row, sme_stream_t stream) {
+  SME_REQUIRE(dtype == SME_F64 || dtype == SME_F32, "unknown dtype %d", dtype);
+  SME_REQUIRE(n_warps >= 1 && pk && val && hdr && plan && carry_val && carry_row, "bad arguments");
+  SME_REQUIRE((((uintptr_t)pk | (uintptr_t)val) & 15) == 0, "pk/val must be 16-byte aligned");
+  cudaStream_t s = as_stream(stream);
+  if (dtype == SME_F64) {
+    SegEpi<double> e{};
+    e.carry_val = (double*)carry_val;
+    e.carry_row = carry_row;
+    return launch_seg<double>(n_warps, pk, (const double*)val, hdr, plan, (const double*)xs, (double*)y, accumulate,
+                              s, &e);
+  }
+  SegEpi<float> e{};
+  e.carry_val = (float*)carry_val;
+  e.carry_row = carry_row;
+  return launch_seg<float>(n_warps, pk, (const float*)val, hdr, plan, (const float*)xs, (float*)y, accumulate, s,
+                           &e);
 }

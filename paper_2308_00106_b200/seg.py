@@ -44,7 +44,8 @@ def auto_seg_panels(m: CsrMatrix, l2_fraction: float = 0.38) -> int:
 class SegLayout:
     """P column panels of a CsrMatrix in the segmented-chunk layout."""
 
-    def __init__(self, m: CsrMatrix, n_panels: int, n_warps: int | None = None, full_last: bool = False):
+    def __init__(self, m: CsrMatrix, n_panels: int, n_warps: int | None = None, full_last: bool = False,
+                 split_rows: bool | None = None):
         P, n = int(n_panels), m.n_rows
         if P < 1 or P > max(1, m.n_cols):
             raise ValueError("panel count must lie in [1, n_cols]")
@@ -80,9 +81,25 @@ class SegLayout:
                   ptr(self.pk), ptr(self.val), ptr(self.hdr), ptr(ws), s)
         self.n_warps = int(n_warps or seg_warps())
         self.plans = torch.empty(P * (self.n_warps + 1), dtype=torch.int32, device=dev)
+        # split-row plans when one row would dominate a warp's share (power-law rows): ranges
+        # then end mid-row and an ordered fix-up adds the open partials (not for the fused
+        # epilogue layouts, whose last pass needs whole rows)
+        if split_rows is None:
+            from .kernels import row_stats
+
+            max_len, _ = row_stats(m)
+            split_rows = (not full_last) and max_len > max(256, 0.25 * m.nnz / max(1, self.n_warps))
+        self.split_rows = bool(split_rows) and not full_last
         for p in range(P):
-            _lib.call("sme_seg_plan", n, ptr(pos) + p * (n + 1) * 4, self.n_warps,
-                      ptr(self.plans) + p * (self.n_warps + 1) * 4, s)
+            if self.split_rows:
+                _lib.call("sme_seg_plan_split", int(ent[p]), self.n_warps, ptr(self.plans) + p * (self.n_warps + 1) * 4,
+                          s)
+            else:
+                _lib.call("sme_seg_plan", n, ptr(pos) + p * (n + 1) * 4, self.n_warps,
+                          ptr(self.plans) + p * (self.n_warps + 1) * 4, s)
+        if self.split_rows:
+            self.carry_val = torch.empty(self.n_warps, dtype=m.dtype, device=dev)
+            self.carry_row = torch.empty(self.n_warps, dtype=torch.int32, device=dev)
         torch.cuda.current_stream().synchronize()  # pos / ws are freed on return
         self.nnz = m.nnz
         self.persist = False
@@ -96,6 +113,12 @@ class SegLayout:
         if self.warm:  # sweep the pass's x slice into L2 before its random gathers
             lo, hi = int(self.bounds_host[p]), int(self.bounds_host[p + 1])
             _lib.call("sme_l2_prefetch", ptr(xd) + vb * lo, (hi - lo) * vb, stream())
+        if self.split_rows:
+            _lib.call("sme_spmv_seg_split", _cuda.sme_dtype(self.val), self.n_warps, ptr(self.pk) + 4 * o,
+                      ptr(self.val) + vb * o, ptr(self.hdr) + 4 * (o // CHUNK),
+                      ptr(self.plans) + 4 * p * (self.n_warps + 1), ptr(xd) + vb * int(self.bounds_host[p]), ptr(y),
+                      int(p > 0), ptr(self.carry_val), ptr(self.carry_row), stream())
+            return
         _lib.call("sme_spmv_seg", _cuda.sme_dtype(self.val), self.n_warps, ptr(self.pk) + 4 * o, ptr(self.val) + vb * o,
                   ptr(self.hdr) + 4 * (o // CHUNK), ptr(self.plans) + 4 * p * (self.n_warps + 1),
                   ptr(xd) + vb * int(self.bounds_host[p]), ptr(y), int(p > 0), stream())

@@ -239,3 +239,46 @@ def test_very_long_rows(dev, rng, n_panels):
         lay, y = run_seg(m, x, n_panels, n_warps)
         check_layout(lay, ptr, col, val)
         assert O.relative_error(y, O.spmv_csr(ptr, col, val, x)) <= F64_TOL
+
+
+@pytest.mark.parametrize("n_panels", [1, 3])
+@pytest.mark.parametrize("n_warps", [7, 37, 300])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_split_row_plans(dev, rng, n_panels, n_warps, dtype):
+    """Split-row plans: warp ranges end mid-row (a 150k-entry row spans many warps) and the
+    ordered fix-up adds the open partials; same result as whole-row plans and the oracle."""
+    n_rows, n_cols = 600, 200_000
+    lens = rng.integers(0, 6, n_rows)
+    lens[11], lens[400], lens[599] = 150_000, 40_000, 9_000
+    ptr, col, val = csr_from_lens(rng, lens, n_cols, dtype)
+    m = P.CsrMatrix(n_rows, n_cols, ptr, col, val, dtype=dtype)
+    x = (rng.random(n_cols) * 2 - 1).astype(dtype)
+    want = O.spmv_csr(ptr, col, val.astype(np.float64), x.astype(np.float64))
+    tol = F64_TOL if dtype == np.float64 else F32_TOL
+    split = SegLayout(m, n_panels, n_warps, split_rows=True)
+    whole = SegLayout(m, n_panels, n_warps, split_rows=False)
+    assert split.split_rows and not whole.split_rows
+    for lay in (split, whole):
+        xd = torch.as_tensor(x).to(dev)
+        y = torch.full((n_rows,), float("nan"), dtype=m.dtype, device=dev)
+        lay.spmv_into(xd, y)
+        assert O.relative_error(y.double().cpu().numpy(), want) <= tol
+    # repeated calls are deterministic
+    y1 = torch.empty(n_rows, dtype=m.dtype, device=dev)
+    y2 = torch.empty(n_rows, dtype=m.dtype, device=dev)
+    split.spmv_into(torch.as_tensor(x).to(dev), y1)
+    split.spmv_into(torch.as_tensor(x).to(dev), y2)
+    assert torch.equal(y1, y2)
+
+
+def test_split_rows_chosen_automatically_for_dominant_rows(dev, rng):
+    n_rows, n_cols = 2000, 50_000
+    lens = rng.integers(0, 4, n_rows)
+    lens[5] = 45_000
+    ptr, col, val = csr_from_lens(rng, lens, n_cols)
+    m = P.CsrMatrix(n_rows, n_cols, ptr, col, val)
+    assert SegLayout(m, 1, 64).split_rows
+    assert not SegLayout(m, 1, 64, full_last=True).split_rows  # fused-epilogue layouts keep whole rows
+    lens[5] = 3
+    ptr, col, val = csr_from_lens(rng, lens, n_cols)
+    assert not SegLayout(P.CsrMatrix(n_rows, n_cols, ptr, col, val), 1, 64).split_rows

@@ -30,6 +30,7 @@ ap.add_argument("--seg-panels", type=int, default=0)
 ap.add_argument("--seg-mode", type=int, default=-1)
 ap.add_argument("--seg-warps", type=int, default=0, help="persistent warps of the seg grid (default: occupancy)")
 ap.add_argument("--seg-warm", action="store_true", help="L2 prefetch sweep of each pass's x slice")
+ap.add_argument("--seg-split", type=int, default=-1, help="split-row plans: 1 on, 0 off, -1 auto")
 ap.add_argument("--seg-hit", type=float, default=-1.0, help="x-slice L2 window hit ratio (0 = no persistence)")
 ap.add_argument("--check", action="store_true", help="compare with the stream kernel")
 ap.add_argument("--persist", action="store_true")
@@ -50,6 +51,8 @@ elif a.config == "c4s":
     A = synth.random_rows(10_000_000, 10_000_000, 20)
 elif a.config == "c3":
     A = synth.rmat(24, 16, cap=1024)
+elif a.config == "c3u":  # R-MAT scale 24 without the degree cap (dense rows), f64 (x 134 MB > L2)
+    A = synth.rmat(24, 16, cap=1 << 30, dtype=np.float64)
 elif a.config == "c5":
     A = synth.laplacian5(2828)
 else:
@@ -102,6 +105,17 @@ if a.seg_mode >= 0:
 
     _lib.call("sme_spmv_seg_set_mode", a.seg_mode)
 y = torch.empty(n, dtype=B.dtype, device=dev)
+if a.seg_split >= 0:
+    from paper_2308_00106_b200.seg import SegLayout, auto_seg_panels
+
+    P_ = a.seg_panels or auto_seg_panels(B)
+    lay_ = SegLayout(B, P_, a.seg_warps or None, split_rows=bool(a.seg_split))
+    if P_ > 1:
+        lay_.enable_persistence(True)
+    B._cache[("seg", P_, False)] = lay_
+    from paper_2308_00106_b200.kernels import row_stats
+
+    print(f"max row {row_stats(B)[0]}, nnz {B.nnz}, split={lay_.split_rows}, panels {P_}", flush=True)
 if a.seg_warm:
     from paper_2308_00106_b200.seg import seg_of
 
