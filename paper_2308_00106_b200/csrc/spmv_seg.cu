@@ -504,11 +504,22 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
 template <typename T>
 __global__ void k_seg_carry_fixup(int32_t n_warps, const int32_t* __restrict__ carry_row,
                                   const T* __restrict__ carry_val, T* __restrict__ y) {
+  // Only empty ranges (-1) can sit between two carries of the same row (a non-empty range
+  // inside the row carries it, one ending on the row's end owns its tail), so -1 entries
+  // are skipped: exactly one thread per row sums the row's run of carries.
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < n_warps; w += gridDim.x * blockDim.x) {
     const int32_t r = carry_row[w];
-    if (r < 0 || (w > 0 && carry_row[w - 1] == r)) continue;
+    if (r < 0) continue;
+    int pw = w - 1;
+    while (pw >= 0 && carry_row[pw] < 0) --pw;
+    if (pw >= 0 && carry_row[pw] == r) continue;  // not the first carry of this row
     T sum = carry_val[w];
-    for (int v = w + 1; v < n_warps && carry_row[v] == r; ++v) sum += carry_val[v];
+    for (int v = w + 1; v < n_warps; ++v) {
+      const int32_t rv = carry_row[v];
+      if (rv < 0) continue;
+      if (rv != r) break;
+      sum += carry_val[v];
+    }
     y[r] += sum;
   }
 }

@@ -241,6 +241,21 @@ def test_very_long_rows(dev, rng, n_panels):
         assert O.relative_error(y, O.spmv_csr(ptr, col, val, x)) <= F64_TOL
 
 
+def test_split_row_plans_with_empty_ranges(dev, rng):
+    """More warps than entries: most split ranges are empty and sit between carries of the
+    same row (the property test's 2 x 281 case)."""
+    n_rows, n_cols = 2, 281
+    lens = np.array([270, 0])
+    ptr, col, val = csr_from_lens(rng, lens, n_cols)
+    m = P.CsrMatrix(n_rows, n_cols, ptr, col, val)
+    x = rng.random(n_cols) * 2 - 1
+    for n_warps in (4736, 1000, 300):
+        lay = SegLayout(m, 1, n_warps, split_rows=True)
+        y = torch.full((n_rows,), float("nan"), dtype=m.dtype, device=dev)
+        lay.spmv_into(torch.as_tensor(x).to(dev), y)
+        assert O.relative_error(y.cpu().numpy(), O.spmv_csr(ptr, col, val, x)) <= F64_TOL, n_warps
+
+
 @pytest.mark.parametrize("n_panels", [1, 3])
 @pytest.mark.parametrize("n_warps", [7, 37, 300])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
