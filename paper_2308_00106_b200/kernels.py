@@ -80,9 +80,9 @@ def auto_kernel(m: CsrMatrix) -> str:
       60 % of L2 — random gathers would miss to DRAM (62 G gathers/s at 400 MB vs
       287 G/s L2-resident, tools/gather_roofline.py); C4: 5.9 ms vs 6.4-7.0 ms for
       the CSR column panels ('panel');
-    * 'seg' also when x exceeds 30 % of L2 and no row is longer than SEG_MAX_ROW
-      (a warp's range holds whole rows): C3 R-MAT 447 vs 409 GFLOP/s ('stream'),
-      C5 307 vs 299 ('vector');
+    * 'seg' also when x exceeds 30 % of L2 and the matrix is not banded: C3 R-MAT 447
+      vs 409 GFLOP/s ('stream'), C5 307 vs 299 ('vector'); dominant rows get split-row
+      plans (uncapped R-MAT: 1.42 ms vs 4.64 'stream', 3.62 'merge');
     * 'stream' for other ragged rows (max row > 8 x mean + 32: C3 405 GFLOP/s vs
       214 for CSR-vector);
     * else 'vector' (partition-invariant; fastest on regular rows: C2 0.113 ms vs
@@ -96,14 +96,11 @@ def auto_kernel(m: CsrMatrix) -> str:
         else:
             max_len, _ = row_stats(m)
             mean = m.nnz / max(1, m.n_rows)
-            if xb > 0.3 * l2_bytes() and max_len <= SEG_MAX_ROW and not banded(m):
+            if xb > 0.3 * l2_bytes() and not banded(m):
                 m._cache["auto"] = "seg"
             else:
                 m._cache["auto"] = "stream" if max_len > 8 * mean + 32 else "vector"
     return m._cache["auto"]
-
-
-SEG_MAX_ROW = 4096
 
 
 def banded(m: CsrMatrix, samples: int = 4096) -> bool:
