@@ -75,18 +75,17 @@ def default_lanes(m: CsrMatrix) -> int:
 
 
 def auto_kernel(m: CsrMatrix) -> str:
-    """Kernel policy (measured on B200, profiles/round1/kernel_compare.txt):
+    """Kernel policy (measured on B200, profiles/round1/kernel_compare.txt, DESIGN.md §5-6):
     * 'seg' (column panels in the segmented-chunk layout, seg.py) when x exceeds
       60 % of L2 — random gathers would miss to DRAM (62 G gathers/s at 400 MB vs
-      287 G/s L2-resident, tools/gather_roofline.py); C4: 5.9 ms vs 6.4-7.0 ms for
+      287 G/s L2-resident, tools/gather_roofline.py); C4: 5.5-5.7 ms vs 6.4-7.0 ms for
       the CSR column panels ('panel');
-    * 'seg' also when x exceeds 30 % of L2 and the matrix is not banded: C3 R-MAT 447
-      vs 409 GFLOP/s ('stream'), C5 307 vs 299 ('vector'); dominant rows get split-row
-      plans (uncapped R-MAT: 1.42 ms vs 4.64 'stream', 3.62 'merge');
-    * 'stream' for other ragged rows (max row > 8 x mean + 32: C3 405 GFLOP/s vs
-      214 for CSR-vector);
-    * else 'vector' (partition-invariant; fastest on regular rows: C2 0.113 ms vs
-      0.115 for 'seg')."""
+    * 'seg' for ragged rows (max row > 8 x mean + 32), whose dominant rows get
+      split-row plans: uncapped R-MAT scale 22 (f32) 0.256 ms vs 1.24 'stream', 0.72
+      'merge', 3.5 'vector'; scale 24 (f64) 1.42 ms vs 4.64 / 3.62;
+    * 'seg' when x exceeds 30 % of L2 and the matrix is not banded: C3 R-MAT 447 vs 409
+      GFLOP/s ('stream'), C5 307 vs 299 ('vector');
+    * else 'vector' (partition-invariant; banded / regular rows: C2 0.107 ms, ties 'seg')."""
     if "auto" not in m._cache:
         from .panels import l2_bytes
 
@@ -96,10 +95,11 @@ def auto_kernel(m: CsrMatrix) -> str:
         else:
             max_len, _ = row_stats(m)
             mean = m.nnz / max(1, m.n_rows)
-            if xb > 0.3 * l2_bytes() and not banded(m):
+            ragged = max_len > 8 * mean + 32
+            if ragged or (xb > 0.3 * l2_bytes() and not banded(m)):
                 m._cache["auto"] = "seg"
             else:
-                m._cache["auto"] = "stream" if max_len > 8 * mean + 32 else "vector"
+                m._cache["auto"] = "vector"
     return m._cache["auto"]
 
 

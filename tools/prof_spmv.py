@@ -51,6 +51,8 @@ elif a.config == "c4s":
     A = synth.random_rows(10_000_000, 10_000_000, 20)
 elif a.config == "c3":
     A = synth.rmat(24, 16, cap=1024)
+elif a.config == "c3s":  # R-MAT scale 22 uncapped, f32 (x 16 MB: L2-resident, ragged rows)
+    A = synth.rmat(22, 16, cap=1 << 30)
 elif a.config == "c3u":  # R-MAT scale 24 without the degree cap (dense rows), f64 (x 134 MB > L2)
     A = synth.rmat(24, 16, cap=1 << 30, dtype=np.float64)
 elif a.config == "c5":
