@@ -389,6 +389,14 @@ int sme_spmv_vector_epi(int lanes, int64_t n_rows, const int32_t* d_row_ptr, con
                         const double* d_dotv, double* d_partials, uint32_t* d_ticket, double* d_result,
                         int finish, sme_stream_t stream);
 
+/* The epilogue alone (split-row seg layouts, whose passes end mid-row): d_out[qinv[r]] =
+ * scale[0] * d_y[r] with the same deterministic reduction and d_result semantics as
+ * sme_spmv_vector_epi; d_partials holds sme_rows_epi_blocks() doubles. */
+int sme_rows_epi_blocks(int64_t n_rows, int64_t* blocks);
+int sme_rows_epi(int64_t n_rows, const double* d_y, double* d_out, const int32_t* d_qinv, const double* d_scale,
+                 const double* d_dotv, double* d_partials, uint32_t* d_ticket, double* d_result, int finish,
+                 sme_stream_t stream);
+
 /* CUDA IPC buffers for the fused exchange (ipc.cu): whole cudaMalloc allocations
  * whose handles (SME_IPC_HANDLE_BYTES bytes) are exchanged between the ranks of a
  * node (torch.distributed all_gather_object) and opened by the peers. */

@@ -83,6 +83,8 @@ SIGNATURES: dict[str, list] = {
     "sme_spmv_seg": [C.c_int, i32, p, p, p, p, p, p, C.c_int, p],
     "sme_spmv_seg_epi": [C.c_int, i32, p, p, p, p, p, p, C.c_int, p, p, p, p, p, p, p],
     "sme_spmv_vector_epi_blocks": [i64, C.c_int, pi64],
+    "sme_rows_epi_blocks": [i64, pi64],
+    "sme_rows_epi": [i64, p, p, p, p, p, p, p, p, C.c_int, p],
     "sme_spmv_vector_epi": [C.c_int, i64, p, p, p, p, p, p, p, p, p, p, C.c_int, p],
     "sme_spmv_seg_epi_cg": [C.c_int, i32, p, p, p, p, p, p, p, C.c_int, p, p, p, p, p],
     "sme_spmv_seg_epi_peers": [C.c_int, i32, p, p, p, p, p, p, C.c_int, p, i64, p, i32, p, p, p, p, p],

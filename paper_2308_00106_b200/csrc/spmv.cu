@@ -714,3 +714,79 @@ SME_API int sme_spmv_vector_epi(int lanes, int64_t n_rows, const int32_t* row_pt
   SME_CHECK_LAUNCH("k_spmv_vector_epi");
   return SME_OK;
 }
+
+namespace sme {
+// The fused epilogue on its own, for layouts whose passes cannot carry it (split-row seg
+// plans): v_r = scale * y[r] -> out[qinv ? qinv[r] : r], reduction as k_spmv_vector_epi.
+__global__ void __launch_bounds__(VE_NT) k_rows_epi(int64_t n_rows, const double* __restrict__ y,
+                                                  double* __restrict__ out, const int32_t* __restrict__ qinv,
+                                                  const double* __restrict__ scale, const double* __restrict__ dotv,
+                                                  double* __restrict__ partials, unsigned* ticket, double* result,
+                                                  int finish) {
+  const double sc = scale ? *scale : 1.0;
+  double ss = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * VE_NT + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * VE_NT) {
+    const double v = sc * y[r];
+    const int64_t g = qinv ? qinv[r] : r;
+    out[g] = v;
+    ss += v * (dotv ? dotv[g] : v);
+  }
+  __shared__ double red[VE_NT / 32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31;
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < VE_NT / 32; ++w) t += red[w];
+    partials[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double fold[VE_NT];
+  double acc = 0.0;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += VE_NT) acc += __ldcg(partials + b);
+  fold[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = VE_NT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) fold[threadIdx.x] += fold[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double tot = fold[0];
+    if (finish == 1) {
+      result[1] = result[0] / tot;
+    } else {
+      result[1] = tot;
+      result[0] = tot > 0.0 ? 1.0 / sqrt(tot) : 0.0;
+    }
+    *ticket = 0u;
+  }
+}
+}  // namespace sme
+
+// Blocks of sme_rows_epi's fixed grid (the length of its partials scratch).
+SME_API int sme_rows_epi_blocks(int64_t n_rows, int64_t* blocks) {
+  SME_REQUIRE(blocks && n_rows >= 0, "bad arguments");
+  *blocks = grid_for(std::max<int64_t>(1, n_rows), VE_NT, 8);
+  return SME_OK;
+}
+
+// out = scale[0] * y (scale NULL: 1), scattered through qinv (NULL: identity), with the
+// iteration's reduction (dotv NULL: sum out^2 -> result {1/sqrt, sum}; else sum out * dotv,
+// finish 1 -> result[1] = result[0] / sum).  f64.
+SME_API int sme_rows_epi(int64_t n_rows, const double* y, double* out, const int32_t* qinv, const double* scale,
+                         const double* dotv, double* partials, uint32_t* ticket, double* result, int finish,
+                         sme_stream_t stream) {
+  SME_REQUIRE(n_rows >= 1 && y && out && partials && ticket && result && (finish == 0 || finish == 1),
+              "bad arguments");
+  const int blocks = grid_for(n_rows, VE_NT, 8);
+  k_rows_epi<<<blocks, VE_NT, 0, as_stream(stream)>>>(n_rows, y, out, qinv, scale, dotv, partials, ticket, result,
+                                                      finish);
+  SME_CHECK_LAUNCH("k_rows_epi");
+  return SME_OK;
+}

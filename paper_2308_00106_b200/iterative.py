@@ -172,7 +172,8 @@ class PowerIteration:
             self.w = [self.z, self.y]  # iterate ping-pongs between the two
             self.cur = 0
             self.res = torch.tensor([1.0, 0.0], dtype=torch.float64, device=op.dev)  # {scale, ||w||^2}
-            self.epi_partials = torch.zeros(self.lay.n_warps, dtype=torch.float64, device=op.dev)
+            self.epi_partials = torch.zeros(getattr(self.lay, "epi_partials_len", self.lay.n_warps),
+                                            dtype=torch.float64, device=op.dev)
             self.ticket = torch.zeros(1, dtype=torch.int32, device=op.dev)
 
     def _step(self) -> None:
@@ -254,7 +255,8 @@ class ConjugateGradient:
             raise ValueError("the fused CG needs a 'seg' or 'vector' operator with f64 values")
         self.fused = self.lay is not None
         if self.fused:
-            self.epi_partials = torch.zeros(self.lay.n_warps, dtype=torch.float64, device=dev)
+            self.epi_partials = torch.zeros(getattr(self.lay, "epi_partials_len", self.lay.n_warps),
+                                            dtype=torch.float64, device=dev)
             self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
 
     def _step(self) -> None:

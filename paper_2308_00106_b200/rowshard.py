@@ -276,7 +276,7 @@ class DistributedPowerIteration:
         local = CsrMatrix._from_device(hi - lo, self.n, (Cm.d_row_ptr[lo : hi + 1] - p0).contiguous(),
                                        Cm.d_col_idx[p0:p1].clone(), Cm.d_values[p0:p1].clone())
         self.local = local
-        self.lay = seg_of(local, full_last=True)
+        self.lay = seg_of(local, full_last=True, split_rows=False)  # its epilogue pass stores to peers
         self.bufs = [IpcBuffer(self.n, dev), IpcBuffer(self.n, dev)]
         handles = [b.handle() for b in self.bufs]
         everyone = [None] * self.world

@@ -82,14 +82,14 @@ class SegLayout:
         self.n_warps = int(n_warps or seg_warps())
         self.plans = torch.empty(P * (self.n_warps + 1), dtype=torch.int32, device=dev)
         # split-row plans when one row would dominate a warp's share (power-law rows): ranges
-        # then end mid-row and an ordered fix-up adds the open partials (not for the fused
-        # epilogue layouts, whose last pass needs whole rows)
+        # then end mid-row and an ordered fix-up adds the open partials; the fused epilogue
+        # then runs as its own row pass (sme_rows_epi) after the passes
         if split_rows is None:
             from .kernels import row_stats
 
             max_len, _ = row_stats(m)
-            split_rows = (not full_last) and max_len > max(256, 0.25 * m.nnz / max(1, self.n_warps))
-        self.split_rows = bool(split_rows) and not full_last
+            split_rows = max_len > max(256, 0.25 * m.nnz / max(1, self.n_warps))
+        self.split_rows = bool(split_rows)
         for p in range(P):
             if self.split_rows:
                 _lib.call("sme_seg_plan_split", int(ent[p]), self.n_warps, ptr(self.plans) + p * (self.n_warps + 1) * 4,
@@ -100,6 +100,9 @@ class SegLayout:
         if self.split_rows:
             self.carry_val = torch.empty(self.n_warps, dtype=m.dtype, device=dev)
             self.carry_row = torch.empty(self.n_warps, dtype=torch.int32, device=dev)
+        # partials scratch of the fused epilogue: per warp (in-pass) or per block (row pass)
+        self.epi_partials_len = (max(self.n_warps, _lib.query_i64("sme_rows_epi_blocks", n)) if self.split_rows
+                                 else self.n_warps)
         torch.cuda.current_stream().synchronize()  # pos / ws are freed on return
         self.nnz = m.nnz
         self.persist = False
@@ -130,6 +133,11 @@ class SegLayout:
         if not self.full_last:
             raise ValueError("the fused epilogue needs a layout built with full_last=True")
         P = self.n_panels
+        if self.split_rows:  # passes end mid-row: all passes into y, then the epilogue as a row pass
+            self.spmv_into(xd, y)
+            _lib.call("sme_rows_epi", self.n_rows, ptr(y), ptr(out), ptr(qinv), ptr(scal), None, ptr(partials),
+                      ptr(ticket), ptr(result), 0, stream())
+            return
         for p in range(P - 1):
             self._window(p, xd)
             self._pass(p, xd, y)
@@ -150,6 +158,11 @@ class SegLayout:
         if not self.full_last:
             raise ValueError("the fused epilogue needs a layout built with full_last=True")
         P = self.n_panels
+        if self.split_rows:
+            self.spmv_into(p, y)
+            _lib.call("sme_rows_epi", self.n_rows, ptr(y), ptr(out), None, None, ptr(p), ptr(partials), ptr(ticket),
+                      ptr(scal), 1, stream())
+            return
         for q in range(P - 1):
             self._window(q, p)
             self._pass(q, p, y)
@@ -224,12 +237,13 @@ class SegLayout:
         return self.n_panels
 
 
-def seg_of(m: CsrMatrix, n_panels: int | None = None, full_last: bool = False) -> SegLayout:
+def seg_of(m: CsrMatrix, n_panels: int | None = None, full_last: bool = False,
+           split_rows: bool | None = None) -> SegLayout:
     """The cached segmented-chunk layout of m (built on first use)."""
     P = n_panels or m._cache.get("seg_panels") or auto_seg_panels(m)
-    key = ("seg", P, bool(full_last))
+    key = ("seg", P, bool(full_last)) if split_rows is None else ("seg", P, bool(full_last), bool(split_rows))
     if key not in m._cache:
-        lay = SegLayout(m, P, full_last=full_last)
+        lay = SegLayout(m, P, full_last=full_last, split_rows=split_rows)
         from .panels import device_info
 
         slice_bytes = int(max(np.diff(lay.bounds_host))) * m.d_values.element_size()

@@ -173,3 +173,43 @@ def test_fused_vector_epilogue_power_and_cg(perm):
     cg.run(150)
     x_cg, _ = O.conjugate_gradient(ptr, col, val, b, 151)
     assert O.relative_error(cg.solution().cpu().numpy(), x_cg) <= 1e-8
+
+
+def _hub_spd(n=3000):
+    """SPD: 1-D Laplacian plus a hub (row/column 0 coupled to every node), diagonally dominant."""
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        for j in (i - 1, i + 1):
+            if 0 <= j < n:
+                rows.append(i); cols.append(j); vals.append(-1.0)
+    for j in range(2, n):  # hub couplings (0, j) and (j, 0), skipping the existing (0, 1)
+        rows += [0, j]; cols += [j, 0]; vals += [-0.01, -0.01]
+    rows, cols, vals = np.array(rows), np.array(cols), np.array(vals)
+    diag = np.zeros(n)
+    np.add.at(diag, rows, np.abs(vals))
+    rows = np.concatenate([rows, np.arange(n)])
+    cols = np.concatenate([cols, np.arange(n)])
+    vals = np.concatenate([vals, diag + 1.0])
+    return O.coo_to_csr(n, rows, cols, vals)
+
+
+def test_fused_iterations_on_split_row_layouts():
+    """A dominant (hub) row makes the seg layout split rows; the fused power iteration and CG
+    then run their epilogue as a row pass (sme_rows_epi) and still match the oracle."""
+    ptr, col, val = _hub_spd()
+    n = ptr.size - 1
+    A = P.CsrMatrix(n, n, ptr, col, val)
+    p = P.random_permutation(n, 21)
+    op = PermutedOperator(A, p, p, kernel="seg")
+    x0 = O.input_vector(0, n)
+    pi = PowerIteration(op, x0, fused=True)
+    assert pi.fused and pi.lay.split_rows
+    pi.run(40)
+    x_ref, lam_ref = O.power_iteration(ptr, col, val, x0, 40)
+    assert abs(pi.eigenvalue - lam_ref) <= 1e-10 * lam_ref
+    assert O.relative_error(pi.x().cpu().numpy(), x_ref) <= 1e-9
+    b = O.input_vector(1, n)
+    cg = ConjugateGradient(op, b, fused=True)
+    cg.run(60)
+    x_cg, _ = O.conjugate_gradient(ptr, col, val, b, 61)
+    assert O.relative_error(cg.solution().cpu().numpy(), x_cg) <= 1e-8
