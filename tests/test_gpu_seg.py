@@ -293,7 +293,8 @@ def test_split_rows_chosen_automatically_for_dominant_rows(dev, rng):
     ptr, col, val = csr_from_lens(rng, lens, n_cols)
     m = P.CsrMatrix(n_rows, n_cols, ptr, col, val)
     assert SegLayout(m, 1, 64).split_rows
-    assert not SegLayout(m, 1, 64, full_last=True).split_rows  # fused-epilogue layouts keep whole rows
+    assert SegLayout(m, 1, 64, full_last=True).split_rows  # fused layouts too (epilogue as a row pass)
+    assert not SegLayout(m, 1, 64, split_rows=False).split_rows
     lens[5] = 3
     ptr, col, val = csr_from_lens(rng, lens, n_cols)
     assert not SegLayout(P.CsrMatrix(n_rows, n_cols, ptr, col, val), 1, 64).split_rows
