@@ -60,6 +60,10 @@ int sme_device_info(int64_t* out);
  * L2 (device-wide) and set/clear the access-policy window of a stream. */
 int sme_l2_set_persisting(size_t bytes);
 int sme_l2_window(const void* d_ptr, size_t bytes, float hit_ratio, sme_stream_t stream);
+/* Demote every persisting L2 line to normal (cudaCtxResetPersistingL2Cache).  Not
+ * stream-ordered: it waits for the whole device, so pipelines call it once at the end,
+ * not per step.  sme_l2_window(bytes = 0) only clears the stream's window. */
+int sme_l2_reset_persisting(void);
 /* Sequential L2 prefetch (evict-last) of a device range: warms a panel's x slice
  * before its random gathers (stream-ordered). */
 int sme_l2_prefetch(const void* d_ptr, size_t bytes, sme_stream_t stream);

@@ -35,6 +35,7 @@ SIGNATURES: dict[str, list] = {
     "sme_device_info": [p],
     "sme_l2_set_persisting": [sz],
     "sme_l2_window": [p, sz, C.c_float, p],
+    "sme_l2_reset_persisting": [],
     "sme_l2_prefetch": [p, sz, p],
     "sme_host_pcg64_permutation": [p, i64, p],
     "sme_host_pcg64_swap_partners": [p, i64, p, C.c_int],

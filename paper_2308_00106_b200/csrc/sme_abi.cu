@@ -60,7 +60,8 @@ SME_API int sme_l2_set_persisting(size_t bytes) {
 }
 
 // Access-policy window on `stream`: [ptr, ptr + bytes) persists with probability hit_ratio
-// (bytes = 0 clears the window and resets persisting lines to normal).
+// (bytes = 0 clears the window; lines already persisting stay so until
+// sme_l2_reset_persisting or until later persisting lines replace them).
 SME_API int sme_l2_window(const void* ptr, size_t bytes, float hit_ratio, sme_stream_t stream) {
   cudaStreamAttrValue attr = {};
   if (bytes) {
@@ -73,7 +74,12 @@ SME_API int sme_l2_window(const void* ptr, size_t bytes, float hit_ratio, sme_st
     attr.accessPolicyWindow.num_bytes = 0;
   }
   SME_CUDA(cudaStreamSetAttribute(sme::as_stream(stream), cudaStreamAttributeAccessPolicyWindow, &attr));
-  if (!bytes) SME_CUDA(cudaCtxResetPersistingL2Cache());
+  return SME_OK;
+}
+
+// Demote all persisting lines to normal.  Device-synchronising (not stream-ordered).
+SME_API int sme_l2_reset_persisting(void) {
+  SME_CUDA(cudaCtxResetPersistingL2Cache());
   return SME_OK;
 }
 

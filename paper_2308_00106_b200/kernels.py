@@ -358,7 +358,7 @@ def spmv_csr_pipelined(m: CsrMatrix, xs, ys=None, kernel: str = "auto") -> list:
                 lay._window(p, xb[b])
                 lay._pass(p, xb[b], yb[b]) if kern == "seg" else spmv_into(
                     lay.panels[p], xb[b], yb[b], lay.inner, accumulate=p > 0, lanes=lay.lanes)
-            lay._window(None, None)
+            lay._window(None, None, reset=False)  # a device-wide reset here would serialise the pipeline
         done = torch.cuda.Event()
         done.record(main)
         computed[b] = done
@@ -369,6 +369,8 @@ def spmv_csr_pipelined(m: CsrMatrix, xs, ys=None, kernel: str = "auto") -> list:
             out.record(d2h)
             copied_out[b] = out
     d2h.synchronize()
+    if lay is not None:
+        lay._window(None, None)  # demote the last slice's persisting lines once, at the end
     main.wait_stream(d2h)
     main.wait_stream(h2d)
     return ys

@@ -82,12 +82,15 @@ class PanelCsr:
     inner: str = "stream"  # kernel of each pass
     lanes: int | None = None  # CSR-vector lanes when inner == "vector"
 
-    def _window(self, p: int | None, xd: torch.Tensor | None) -> None:
-        """Pin x slice p in L2 (access-policy window) or clear the window (p None)."""
+    def _window(self, p: int | None, xd: torch.Tensor | None, reset: bool = True) -> None:
+        """Pin x slice p in L2 (access-policy window) or clear the window (p None; with
+        `reset` also demote the persisting lines, which waits for the device)."""
         if not self.persist:
             return
         if p is None:
             _lib.call("sme_l2_window", None, 0, 0.0, stream())
+            if reset:
+                _lib.call("sme_l2_reset_persisting")
             return
         vb = xd.element_size()
         lo, hi = int(self.bounds_host[p]), int(self.bounds_host[p + 1])
@@ -105,6 +108,7 @@ class PanelCsr:
             spmv_into(a, xd, y, kernel, accumulate=p > 0, lanes=self.lanes)
         if self.persist:
             _lib.call("sme_l2_window", None, 0, 0.0, stream())
+            _lib.call("sme_l2_reset_persisting")
 
     def spmv_host(self, x_host: torch.Tensor, y_host: torch.Tensor, x_dev: torch.Tensor, y_dev: torch.Tensor,
                   kernel: str | None = None) -> None:
@@ -134,6 +138,7 @@ class PanelCsr:
             spmv_into(a, x_dev, y_dev, kernel, accumulate=p > 0, lanes=self.lanes)
         if self.persist:
             _lib.call("sme_l2_window", None, 0, 0.0, stream())
+            _lib.call("sme_l2_reset_persisting")
         y_host.copy_(y_dev, non_blocking=True)
         main.synchronize()
 

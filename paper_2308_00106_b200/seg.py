@@ -175,11 +175,16 @@ class SegLayout:
                   ptr(p), ptr(y), int(P > 1), ptr(out), ptr(partials), ptr(ticket), ptr(scal), stream())
         self._window(None, None)
 
-    def _window(self, p: int | None, xd: torch.Tensor | None) -> None:
+    def _window(self, p: int | None, xd: torch.Tensor | None, reset: bool = True) -> None:
+        """Pin x slice p in L2 (access-policy window), or clear the window (p None) and,
+        with `reset`, demote the persisting lines.  The reset waits for the whole device,
+        so a pipeline of steps (spmv_csr_pipelined) clears without it and resets once."""
         if not self.persist:
             return
         if p is None:
             _lib.call("sme_l2_window", None, 0, 0.0, stream())
+            if reset:
+                _lib.call("sme_l2_reset_persisting")
             return
         vb = xd.element_size()
         lo, hi = int(self.bounds_host[p]), int(self.bounds_host[p + 1])

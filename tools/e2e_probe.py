@@ -18,8 +18,9 @@ B = P.permute_csr(A, P.random_permutation(n, 1), P.random_permutation(n, 2))
 del A
 lay = seg_of(B)
 xs = [torch.rand(n, dtype=torch.float64).pin_memory() for _ in range(2)]
-steps = 12
-ys = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(steps)]
+steps = 20
+yr = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(2)]
+ys = [yr[k & 1] for k in range(steps)]
 
 
 def run(label):
@@ -40,7 +41,7 @@ for nb in (2, 3):
     K.PIPELINE_BUFFERS = nb
     run(f"pipelined e2e, {nb} buffers")
 K.PIPELINE_BUFFERS = 2
-for g in (1, 2, 4):
+for g in (1, 2, 4, 8):
     K.PIPELINE_H2D_COPIES = g
     run(f"pipelined e2e, 2 buffers, {g} H2D copies per x")
     SegLayout._pass = lambda self, p, xd, y: None
