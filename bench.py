@@ -351,6 +351,21 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
     ev[1].record()
     torch.cuda.synchronize()
     hist_ms = ev[0].elapsed_time(ev[1])
+    # the same two calls again, warm (allocator pools and kernel attributes set up):
+    # the first-call numbers above include cudaMalloc of the new matrix
+    B2 = P.permute_csr(A, p_r, p_c)  # fills the allocator pool with a matrix's worth of blocks
+    del B2
+    ev[0].record()
+    B2 = P.permute_csr(A, p_r, p_c)
+    ev[1].record()
+    torch.cuda.synchronize()
+    permute_warm_ms = ev[0].elapsed_time(ev[1])
+    del B2
+    ev[0].record()
+    P.histogram_2d(B, 128, 128)
+    ev[1].record()
+    torch.cuda.synchronize()
+    hist_warm_ms = ev[0].elapsed_time(ev[1])
     H_before, H_after = P.shannon_entropy(P.histogram_2d(A, 128, 128)), P.shannon_entropy(hB)
     x = torch.from_numpy(P.input_vector(0, n)).to(dev, B.dtype)
     xp = P.permute_vector(x, p_c)
@@ -647,9 +662,9 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         "gather_roofline": gather_roof,
         "entropy_bits": {"unpermuted": round(H_before, 6), "permuted": round(H_after, 6), "max": 14.0},
         "load_balance_148_even_rows": balance,
-        "permute_ms": round(permute_ms, 2),
+        "permute_ms": round(permute_ms, 2), "permute_warm_ms": round(permute_warm_ms, 2),
         "perm_gen_s": HOST_PERM_S.get("native"),
-        "hist_ms": round(hist_ms, 3),
+        "hist_ms": round(hist_ms, 3), "hist_warm_ms": round(hist_warm_ms, 3),
         "roundtrip_rel_err": rel_err,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,

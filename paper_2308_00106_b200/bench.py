@@ -184,6 +184,10 @@ class _LazyHost:
 def gpu_kernels(max_workers: int = 1) -> list[KernelSpec]:
     """GPU KernelSpecs for the reference protocol (ids recognised by the report as raw ids)."""
     specs = [
+        # "auto": the kernel bench.py measures (seg column panels for large permuted
+        # matrices, CSR-vector for banded ones; kernels.auto_kernel)
+        KernelSpec("gpu_csr_auto", _host_call("auto")),
+        KernelSpec("gpu_csr_auto_resident", _resident_call("auto")),
         KernelSpec("gpu_csr_vector", _host_call("vector")),
         KernelSpec("gpu_csr_merge", _host_call("merge")),
         KernelSpec("gpu_csr_merge_resident", _resident_call("merge")),
@@ -195,6 +199,8 @@ def gpu_kernels(max_workers: int = 1) -> list[KernelSpec]:
 
 
 KERNEL_LABELS = {
+    "gpu_csr_auto": "GPU AUTO",
+    "gpu_csr_auto_resident": "GPU AUTO-RES",
     "gpu_csr_vector": "GPU CSR",
     "gpu_csr_merge": "GPU CSR-MRG",
     "gpu_csr_merge_resident": "GPU MRG-RES",
