@@ -210,36 +210,54 @@ SME_API int sme_host_pcg64_swap_partners(uint64_t* st, int64_t n, uint32_t* h_j,
   h_j[0] = 0;
   if (n == 1) return SME_OK;
   const int T = threads > 0 ? threads : (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-  constexpr int64_t kOut = 1 << 20;      // 64-bit outputs per parallel block
-  std::vector<uint32_t> u((size_t)(2 * kOut + 1));
-  u128 base = g.state;                   // state before the next block's first output
-  int64_t blocks = 0;                    // blocks generated
-  int64_t d = 0, d_end = 0;              // read position / end in u
-  auto refill = [&](bool first) {
-    // a pending buffered half (numpy's has_uint32) comes first
-    int64_t off = 0;
-    if (first && g.has32) u[(size_t)off++] = g.buf32;
-    std::vector<std::thread> th;
-    auto body = [&](int t) {
-      const int64_t a0 = kOut * t / T, b0 = kOut * (t + 1) / T;
-      u128 x = advance(base, g.inc, (uint64_t)a0);
-      for (int64_t k = a0; k < b0; ++k) {
+  // 64-bit outputs per block (the draws consume about 1.3 n uint32, so small n get a small block)
+  const int64_t kOut = std::min<int64_t>(1 << 20, std::max<int64_t>(1024, n));
+  // two blocks: the workers fill the next while this thread replays the current one
+  std::vector<uint32_t> ubuf[2] = {std::vector<uint32_t>((size_t)(2 * kOut + 1)),
+                                   std::vector<uint32_t>((size_t)(2 * kOut + 1))};
+  auto gen_block = [&](uint32_t* out, u128 b0, int64_t off) {
+    auto body = [&, out, b0, off](int t) {
+      const int64_t a0 = kOut * t / T, e0 = kOut * (t + 1) / T;
+      u128 x = advance(b0, g.inc, (uint64_t)a0);
+      for (int64_t k = a0; k < e0; ++k) {
         x = x * kMult + g.inc;
         const uint64_t v = xsl_rr(x);
-        u[(size_t)(off + 2 * k)] = (uint32_t)v;
-        u[(size_t)(off + 2 * k + 1)] = (uint32_t)(v >> 32);
+        out[off + 2 * k] = (uint32_t)v;
+        out[off + 2 * k + 1] = (uint32_t)(v >> 32);
       }
     };
+    std::vector<std::thread> th;
     for (int t = 1; t < T; ++t) th.emplace_back(body, t);
     body(0);
     for (auto& x : th) x.join();
-    base = advance(base, g.inc, (uint64_t)kOut);
-    ++blocks;
-    d = 0;
-    d_end = off + 2 * kOut;
   };
-  refill(true);
-  const int64_t lead = g.has32 ? 1 : 0;  // the pending half occupies u[0] of the first block
+  u128 next_base = g.state;              // state before the next block's first output
+  int cur = 0;
+  std::thread bg;                        // generates block `blocks` into ubuf[cur ^ 1]
+  auto prefetch = [&]() {
+    const u128 b0 = next_base;
+    uint32_t* out = ubuf[cur ^ 1].data();
+    bg = std::thread([&gen_block, out, b0] { gen_block(out, b0, 0); });
+    next_base = advance(next_base, g.inc, (uint64_t)kOut);
+  };
+  // the first block, with a pending buffered half (numpy's has_uint32) in front
+  const int64_t lead = g.has32 ? 1 : 0;
+  if (lead) ubuf[0][0] = g.buf32;
+  gen_block(ubuf[0].data(), next_base, lead);
+  next_base = advance(next_base, g.inc, (uint64_t)kOut);
+  int64_t blocks = 1;                    // blocks replayed so far (the current one included)
+  const uint32_t* u = ubuf[0].data();
+  int64_t d = 0, d_end = lead + 2 * kOut;  // read position / end in u
+  prefetch();
+  auto refill = [&]() {
+    bg.join();
+    cur ^= 1;
+    u = ubuf[cur].data();
+    d = 0;
+    d_end = 2 * kOut;
+    ++blocks;
+    prefetch();
+  };
   int64_t i = n - 1;
   while (i >= 1) {
     uint32_t mask = (uint32_t)i;
@@ -252,12 +270,13 @@ SME_API int sme_host_pcg64_swap_partners(uint64_t* st, int64_t n, uint32_t* h_j,
     // branch-free rejection: every draw is written to h_j[i]; a rejected one is
     // overwritten by the next draw for the same i, an accepted one moves i on
     while (i > i_lo) {
-      if (d == d_end) refill(false);
-      const uint32_t v = u[(size_t)d++] & mask;
+      if (d == d_end) refill();
+      const uint32_t v = u[d++] & mask;
       h_j[i] = v;
       i -= (int64_t)(v <= (uint32_t)i);
     }
   }
+  bg.join();  // the block prefetched last is not needed
   // uint32 values consumed in total (the pending half counts as one), and where they
   // leave numpy's buffer: an odd number of fresh halves means a high half is pending
   const int64_t total_fresh = (blocks - 1) * 2 * kOut + (d - (blocks == 1 ? lead : 0));
