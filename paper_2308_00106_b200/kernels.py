@@ -26,7 +26,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _cuda, _lib
+from . import _cuda, _lib, hostio
 from ._cuda import ptr, stream
 from .matio import CooMatrix, CsrMatrix
 
@@ -168,43 +168,51 @@ def merge_plan(m: CsrMatrix) -> MergePlan:
     return m._cache["merge"]
 
 
-def _x_device(x, n: int, dtype: torch.dtype, dev) -> tuple[torch.Tensor, str]:
-    """x on the device plus the caller's mode: 'device' (CUDA tensor in/out), 'host'
-    (CPU torch tensor in/out; async copies when pinned), 'numpy' (numpy in/out)."""
+def _host_src(x, n: int) -> tuple[torch.Tensor, str]:
+    """A host input vector as a CPU tensor (numpy wrapped without a copy) and the
+    caller's mode: 'host' (CPU torch tensor in / out) or 'numpy' (numpy in / out)."""
     if isinstance(x, torch.Tensor):
         if x.dim() != 1 or x.numel() != n:
             raise ValueError(f"input vector length {tuple(x.shape)} does not match n_cols {n}")
-        if x.is_cuda:
-            return x.to(dtype).contiguous(), "device"
-        return x.to(dev, dtype, non_blocking=x.is_pinned()), "host"
+        return x.contiguous(), "host"
     xa = np.asarray(x, dtype=np.float64)
     if xa.shape != (n,):
         raise ValueError(f"input vector length {xa.shape} does not match n_cols {n}")
-    return torch.from_numpy(np.ascontiguousarray(xa)).to(dev, dtype), "numpy"
+    return torch.from_numpy(np.ascontiguousarray(xa)), "numpy"
 
 
-_PINNED: dict[tuple, torch.Tensor] = {}
-
-
-def _pinned(shape, dtype) -> torch.Tensor:
-    """A reusable pinned host buffer (page-locking 400 MB costs tens of ms per call)."""
-    key = (tuple(shape), dtype)
-    buf = _PINNED.get(key)
-    if buf is None:
-        buf = _PINNED[key] = torch.empty(shape, dtype=dtype, pin_memory=True)
-    return buf
+def _x_device(x, n: int, dtype: torch.dtype, dev) -> tuple[torch.Tensor, str]:
+    """x on the device plus the caller's mode: 'device' (CUDA tensor in/out), 'host'
+    (CPU torch tensor in/out), 'numpy' (numpy in/out).  Host vectors cross through
+    hostio.stage_in (pinned staging, host-parallel copies overlapped with the DMA)."""
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        if x.dim() != 1 or x.numel() != n:
+            raise ValueError(f"input vector length {tuple(x.shape)} does not match n_cols {n}")
+        return x.to(dtype).contiguous(), "device"
+    src, mode = _host_src(x, n)
+    xd = torch.empty(n, dtype=dtype, device=dev)
+    ev = None
+    for _, ev in hostio.stage_in(src, xd, hostio.slices(n, xd.element_size())):
+        pass
+    torch.cuda.current_stream(dev).wait_event(ev)
+    return xd, mode
 
 
 def _y_out(y: torch.Tensor, mode: str):
+    """The result in the caller's mode; host results are fresh arrays (never a buffer
+    a later call reuses), as the reference's are."""
     if mode == "device":
         return y
-    if mode == "host":
-        # the returned pinned tensor is reused by the next host-mode call of the same shape
-        yh = _pinned(y.shape, y.dtype)
-        yh.copy_(y, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return yh
-    return y.to("cpu").numpy().astype(np.float64, copy=False)
+    return hostio.to_host(y, np.float64, as_numpy=(mode == "numpy"))
+
+
+def _layout_pass(lay, kern: str, p: int, xd: torch.Tensor, y: torch.Tensor) -> None:
+    """Pass p of a column-panel layout ('seg' or 'panel') with x slice p pinned in L2."""
+    lay._window(p, xd)
+    if kern == "seg":
+        lay._pass(p, xd, y)
+    else:
+        spmv_into(lay.panels[p], xd, y, lay.inner, accumulate=p > 0, lanes=lay.lanes)
 
 
 def spmv_into(m: CsrMatrix, xd: torch.Tensor, y: torch.Tensor, kernel: str = "vector", *, lanes: int | None = None,
@@ -261,24 +269,37 @@ def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None 
     if not isinstance(m, CsrMatrix):
         raise TypeError("spmv_csr expects a CsrMatrix of this package (see matio.from_reference)")
     dev = m.d_row_ptr.device
-    if (isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.dtype == m.dtype and x.dim() == 1
-            and x.numel() == m.n_cols and out is None
-            and (auto_kernel(m) if kernel == "auto" else kernel) in ("panel", "seg")):
-        # host vectors + column panels: x slice p+1 crosses PCIe while pass p runs
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        xd, mode = _x_device(x, m.n_cols, m.dtype, dev)
+        y = out if out is not None else torch.empty(m.n_rows, dtype=m.dtype, device=dev)
+        spmv_into(m, xd, y, kernel)
+        return y
+    # host x: it crosses PCIe slice by slice; with column panels pass p starts as soon
+    # as slice p has landed
+    src, mode = _host_src(x, m.n_cols)
+    bufs = m._cache.get("host_bufs")
+    if bufs is None:
+        bufs = m._cache["host_bufs"] = (torch.empty(m.n_cols, dtype=m.dtype, device=dev),
+                                        torch.empty(m.n_rows, dtype=m.dtype, device=dev))
+    xd = bufs[0]
+    y = out if out is not None else bufs[1]
+    main = torch.cuda.current_stream(dev)
+    kern = auto_kernel(m) if kernel == "auto" else kernel
+    if kern in ("seg", "panel"):
         from .panels import panels_of
         from .seg import seg_of
 
-        bufs = m._cache.get("host_bufs")
-        if bufs is None:
-            bufs = m._cache["host_bufs"] = (torch.empty(m.n_cols, dtype=m.dtype, device=dev),
-                                            torch.empty(m.n_rows, dtype=m.dtype, device=dev))
-        yh = _pinned((m.n_rows,), m.dtype)
-        lay = seg_of(m) if (auto_kernel(m) if kernel == "auto" else kernel) == "seg" else panels_of(m)
-        lay.spmv_host(x, yh, bufs[0], bufs[1])
-        return yh
-    xd, mode = _x_device(x, m.n_cols, m.dtype, dev)
-    y = out if out is not None else torch.empty(m.n_rows, dtype=m.dtype, device=dev)
-    spmv_into(m, xd, y, kernel)
+        lay = seg_of(m) if kern == "seg" else panels_of(m)
+        for p, ev in hostio.stage_in(src, xd, lay.bounds_host):
+            main.wait_event(ev)
+            _layout_pass(lay, kern, p, xd, y)
+        lay._window(None, None)
+    else:
+        ev = None
+        for _, ev in hostio.stage_in(src, xd, hostio.slices(m.n_cols, xd.element_size())):
+            pass
+        main.wait_event(ev)
+        spmv_into(m, xd, y, kern)
     return _y_out(y, mode)
 
 
@@ -355,9 +376,7 @@ def spmv_csr_pipelined(m: CsrMatrix, xs, ys=None, kernel: str = "auto") -> list:
         else:
             for p in range(P):
                 main.wait_event(slice_ev[p])
-                lay._window(p, xb[b])
-                lay._pass(p, xb[b], yb[b]) if kern == "seg" else spmv_into(
-                    lay.panels[p], xb[b], yb[b], lay.inner, accumulate=p > 0, lanes=lay.lanes)
+                _layout_pass(lay, kern, p, xb[b], yb[b])
             lay._window(None, None, reset=False)  # a device-wide reset here would serialise the pipeline
         done = torch.cuda.Event()
         done.record(main)

@@ -221,6 +221,10 @@ def test_pipelined_host_stream_equals_per_vector_calls(dev, rng, kernel):
         want = P.spmv_csr(m, x.cuda(), kernel).cpu()
         assert torch.equal(y, want)
         assert O.relative_error(y.numpy(), O.spmv_csr(ptr, col, val, x.numpy())) <= F64_TOL
+    # outputs in a ring of two host buffers (bench.py's e2e): the last two survive
+    ring = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(2)]
+    P.spmv_csr_pipelined(m, xs, [ring[k & 1] for k in range(len(xs))], kernel=kernel)
+    assert torch.equal(ring[(len(xs) - 1) & 1], ys[-1]) and torch.equal(ring[(len(xs) - 2) & 1], ys[-2])
     with pytest.raises(ValueError):
         P.spmv_csr_pipelined(m, [torch.zeros(n + 1)])
 
