@@ -302,3 +302,45 @@ def test_split_rows_chosen_automatically_for_dominant_rows(dev, rng):
     lens[5] = 3
     ptr, col, val = csr_from_lens(rng, lens, n_cols)
     assert not SegLayout(P.CsrMatrix(n_rows, n_cols, ptr, col, val), 1, 64).split_rows
+
+
+@pytest.mark.parametrize("kernel,dtype", [("seg", np.float64), ("vector", np.float64), ("seg", np.float32)])
+def test_host_vectors_large_fresh_results(dev, rng, kernel, dtype):
+    """numpy / CPU-tensor x above the staging threshold (hostio): slices staged through
+    pinned memory, results in fresh pooled page-locked memory that never aliases a live
+    result (the reference returns a new array per call, kernels.py:73-78)."""
+    import gc
+
+    from paper_2308_00106_b200 import hostio
+
+    n = (hostio.CHUNK_MIN_BYTES // 8) + 12345  # x and y above the chunking threshold
+    rows = np.repeat(np.arange(n), rng.integers(0, 4, n))
+    cols = rng.integers(0, n, rows.size)
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    keep = np.ones(rows.size, dtype=bool)
+    keep[1:] = (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])
+    rows, col = rows[keep], cols[keep]
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=ptr[1:])
+    val = (rng.random(col.size) * 2 - 1).astype(dtype)
+    m = P.CsrMatrix(n, n, ptr, col, val)
+    m._cache["seg_panels"] = 3
+    x1, x2 = rng.random(n), rng.random(n)
+    want1 = O.spmv_csr(ptr, col, val.astype(np.float64), x1)
+    want2 = O.spmv_csr(ptr, col, val.astype(np.float64), x2)
+    tol = F64_TOL if dtype == np.float64 else F32_TOL
+    for rep in range(3):  # the pool recycles released results
+        y1 = P.spmv_csr(m, x1, kernel)
+        y2 = P.spmv_csr(m, x2, kernel)
+        assert isinstance(y1, np.ndarray) and y1.dtype == np.float64 and y1.shape == (n,)
+        assert not np.shares_memory(y1, y2)
+        assert O.relative_error(y1, want1) <= tol and O.relative_error(y2, want2) <= tol
+        del y1
+        gc.collect()
+        yt = P.spmv_csr(m, torch.from_numpy(x1).to(torch.float64 if dtype == np.float64 else torch.float32), kernel)
+        assert isinstance(yt, torch.Tensor) and not yt.is_cuda and yt.dtype == m.dtype
+        assert O.relative_error(yt.double().numpy(), want1) <= tol
+        assert O.relative_error(y2, want2) <= tol  # untouched by the later calls
+        del y2, yt
+        gc.collect()
