@@ -85,16 +85,18 @@ def test_hist2d_unaligned_col_idx(mode, hist_mode):
     assert np.array_equal(got, O.histogram_2d_counts(rows, cols, 4000, 5000, 50, 128))
 
 
-def test_hist2d_u16_counters_flush_before_overflow(hist_mode):
+@pytest.mark.parametrize("target", [0, 1])
+def test_hist2d_u16_counters_flush_before_overflow(hist_mode, target):
     """40M nonzeros in ONE bin on one CTA: every lane's u16 counter would overflow ~20
-    times without the periodic flush."""
+    times without the periodic flush.  Bins 0 and 1 share a counter word (low / high
+    half), so an overflow of either would show in the other or be lost."""
     dev = torch.device("cuda")
-    n_rows, k, n_cols = 40_000, 1000, 128_000  # width 1000: every column lies in bin 0
+    n_rows, k, n_cols = 40_000, 1000, 128_000  # width 1000: every column lies in bin `target`
     row_ptr = (torch.arange(n_rows + 1, device=dev, dtype=torch.int64) * k).to(torch.int32)
-    col = torch.arange(k, device=dev, dtype=torch.int32).repeat(n_rows)
+    col = (torch.arange(k, device=dev, dtype=torch.int32) + target * k).repeat(n_rows)
     m = CsrMatrix._from_device(n_rows, n_cols, row_ptr, col, torch.ones(n_rows * k, dtype=torch.float64,
                                                                           device=dev))
     for mode in (2, 0):
         hist_mode(mode)
         got = P.histogram_2d(m, 1, 128).counts
-        assert int(got[0, 0]) == n_rows * k and int(got.sum()) == n_rows * k
+        assert int(got[0, target]) == n_rows * k and int(got.sum()) == n_rows * k

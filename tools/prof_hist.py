@@ -19,8 +19,10 @@ A = {"c4": lambda: synth.random_rows(50_000_000, 50_000_000, 20), "c2": lambda: 
 n = A.n_rows
 B = P.permute_csr(A, P.random_permutation(n, 1), P.random_permutation(n, 2))
 ref = None
-for mode, var, name in ((1, 0, "shared-atomic window"), (0, 0, "lanes default (864x4)"), (0, 7, "lanes 512x8"), (0, 1, "lanes 768x4"),
-                        (0, 2, "lanes 512x4+pf"), (0, 3, "lanes 768x2+pf"), (0, 4, "lanes 640x4+pf"), (0, 5, "lanes 864x4"), (0, 6, "lanes 864x2")):
+for mode, var, name in ((1, 0, "shared-atomic window"), (0, 0, "lanes default (864x4, CL 2)"), (0, 7, "lanes 512x8"), (0, 1, "lanes 768x4"),
+                        (0, 2, "lanes 512x4+pf"), (0, 3, "lanes 768x2+pf"), (0, 4, "lanes 640x4+pf"), (0, 5, "lanes 864x4 (CL 0, previous default)"), (0, 6, "lanes 864x2"),
+                        (0, 8, "lanes 864x4 conflict-free words"), (0, 9, "lanes 864x4 conflict-free words, shared atomics"),
+                        (0, 10, "lanes 864x2 CL 2"), (0, 11, "lanes 640x4+pf CL 2"), (0, 12, "lanes 512x8 CL 2")):
     _lib.call("sme_hist2d_set_mode", mode)
     _lib.call("sme_hist2d_set_variant", var)
     h = P.histogram_2d(B, 128, 128).counts  # warm
