@@ -270,6 +270,18 @@ SME_API int sme_host_pcg64_swap_partners(uint64_t* st, int64_t n, uint32_t* h_j,
     // branch-free rejection: every draw is written to h_j[i]; a rejected one is
     // overwritten by the next draw for the same i, an accepted one moves i on
     while (i > i_lo) {
+      if (d_end - d >= 8 && i - 8 > i_lo) {
+        // 8 draws with no bounds checks: at most 8 acceptances keep i above i_lo
+        // (the mask holds) and the block holds 8 more values
+#pragma GCC unroll 8
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t v = u[d + k] & mask;
+          h_j[i] = v;
+          i -= (int64_t)(v <= (uint32_t)i);
+        }
+        d += 8;
+        continue;
+      }
       if (d == d_end) refill();
       const uint32_t v = u[d++] & mask;
       h_j[i] = v;
