@@ -108,6 +108,12 @@ int sme_host_pcg64_permutation(uint64_t* st, int64_t n, int32_t* h_out);
  * Raw outputs are generated in parallel (LCG jump-ahead per thread), the masked
  * rejection replayed sequentially and branch-free.  threads <= 0: up to 8. */
 int sme_host_pcg64_swap_partners(uint64_t* st, int64_t n, uint32_t* h_j, int threads);
+/* The same partners written straight to DEVICE memory d_j (int32[n]): the replay
+ * fills a small pinned ring (4 x 4 MB) and each slot is copied with cudaMemcpyAsync on
+ * `stream` as soon as the replay has moved below it, so the upload hides behind the
+ * draws and no n-sized host buffer is touched.  HOST call; returns after the copies
+ * have completed (it synchronises `stream`). */
+int sme_pcg64_swap_partners_to_device(uint64_t* st, int64_t n, int32_t* d_j, int threads, sme_stream_t stream);
 /* The swaps of that shuffle on the GPU (shuffle.cu): d_perm = the permutation
  * a = arange(n); for i = n-1..1: swap(a[i], a[d_j[i]]) builds — computed as a
  * bucket sort of the steps by partner, a link pass and a chain walk (no dependent

@@ -29,8 +29,11 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <thread>
 #include <vector>
+
+#include <cuda_runtime.h>
 
 #include "../../include/sme.h"
 
@@ -193,72 +196,103 @@ SME_API int sme_host_pcg64_permutation(uint64_t* st, int64_t n, int32_t* h_out) 
   return SME_OK;
 }
 
-// The swap partners of Generator(PCG64).permutation(n) without the swaps:
-// h_j[i] = random_interval(i) for i = n-1 .. 1 in numpy's draw order (h_j[0] = 0),
-// st updated exactly as the full shuffle leaves it.  The raw 64-bit outputs are
-// produced in parallel, already split into numpy's uint32 order (low half, then
-// the buffered high half), each thread jumping ahead to its share of a block with
-// the LCG's O(log k) advance; one sequential pass then replays the masked
-// rejection over that uint32 stream.  The swaps themselves run on the GPU
-// (sme_fy_apply).
-SME_API int sme_host_pcg64_swap_partners(uint64_t* st, int64_t n, uint32_t* h_j, int threads) {
-  if (!st || !h_j || n < 1 || n > INT32_MAX) {
-    sme::set_error("sme_host_pcg64_swap_partners: bad arguments (n=%lld)", (long long)n);
-    return SME_EINVAL;
+namespace {
+
+// numpy's uint32 stream of one PCG64 (low half of each 64-bit output, then the
+// buffered high half), produced in blocks by T threads that each jump ahead to their
+// share with the LCG's O(log k) advance; double-buffered, so the workers fill the
+// next block while the caller consumes the current one.
+class U32Stream {
+ public:
+  U32Stream(const Pcg64& g, int64_t n, int threads) : g_(g) {
+    T_ = threads > 0 ? threads : (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    // 64-bit outputs per block (the draws consume about 1.3 n uint32: small n, small block)
+    kOut_ = std::min<int64_t>(1 << 20, std::max<int64_t>(1024, n));
+    for (auto& b : buf_) b.resize((size_t)(2 * kOut_ + 1));
+    next_base_ = g.state;
+    lead_ = g.has32 ? 1 : 0;  // a pending buffered half (numpy's has_uint32) comes first
+    if (lead_) buf_[0][0] = g.buf32;
+    gen_block(buf_[0].data(), next_base_, lead_);
+    next_base_ = advance(next_base_, g.inc, (uint64_t)kOut_);
+    u = buf_[0].data();
+    d = 0;
+    d_end = lead_ + 2 * kOut_;
+    prefetch();
   }
-  Pcg64 g = load_state(st);
-  h_j[0] = 0;
-  if (n == 1) return SME_OK;
-  const int T = threads > 0 ? threads : (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-  // 64-bit outputs per block (the draws consume about 1.3 n uint32, so small n get a small block)
-  const int64_t kOut = std::min<int64_t>(1 << 20, std::max<int64_t>(1024, n));
-  // two blocks: the workers fill the next while this thread replays the current one
-  std::vector<uint32_t> ubuf[2] = {std::vector<uint32_t>((size_t)(2 * kOut + 1)),
-                                   std::vector<uint32_t>((size_t)(2 * kOut + 1))};
-  auto gen_block = [&](uint32_t* out, u128 b0, int64_t off) {
+  ~U32Stream() {
+    if (bg_.joinable()) bg_.join();
+  }
+  const uint32_t* u;  // current block
+  int64_t d, d_end;   // read position / end in u
+
+  void refill() {
+    bg_.join();
+    cur_ ^= 1;
+    u = buf_[cur_].data();
+    d = 0;
+    d_end = 2 * kOut_;
+    ++blocks_;
+    prefetch();
+  }
+  // the generator state after the values consumed so far (numpy's, exactly)
+  void final_state(Pcg64& g) {
+    if (bg_.joinable()) bg_.join();  // the block prefetched last is not needed
+    // uint32 values consumed in total (the pending half counts as one), and where they
+    // leave numpy's buffer: an odd number of fresh halves means a high half is pending
+    const int64_t total_fresh = (blocks_ - 1) * 2 * kOut_ + (d - (blocks_ == 1 ? lead_ : 0));
+    const int64_t outputs = (total_fresh + 1) / 2;
+    g.state = advance(g_.state, g_.inc, (uint64_t)outputs);
+    if (total_fresh > 0) {
+      g.has32 = (total_fresh & 1) != 0;
+      g.buf32 = (uint32_t)(xsl_rr(g.state) >> 32);  // the high half of the last output drawn
+    } else {
+      g.has32 = g_.has32 && d == 0;  // only the pending half was used (or nothing)
+    }
+  }
+
+ private:
+  void gen_block(uint32_t* out, u128 b0, int64_t off) {
     auto body = [&, out, b0, off](int t) {
-      const int64_t a0 = kOut * t / T, e0 = kOut * (t + 1) / T;
-      u128 x = advance(b0, g.inc, (uint64_t)a0);
+      const int64_t a0 = kOut_ * t / T_, e0 = kOut_ * (t + 1) / T_;
+      u128 x = advance(b0, g_.inc, (uint64_t)a0);
       for (int64_t k = a0; k < e0; ++k) {
-        x = x * kMult + g.inc;
+        x = x * kMult + g_.inc;
         const uint64_t v = xsl_rr(x);
         out[off + 2 * k] = (uint32_t)v;
         out[off + 2 * k + 1] = (uint32_t)(v >> 32);
       }
     };
     std::vector<std::thread> th;
-    for (int t = 1; t < T; ++t) th.emplace_back(body, t);
+    for (int t = 1; t < T_; ++t) th.emplace_back(body, t);
     body(0);
     for (auto& x : th) x.join();
-  };
-  u128 next_base = g.state;              // state before the next block's first output
-  int cur = 0;
-  std::thread bg;                        // generates block `blocks` into ubuf[cur ^ 1]
-  auto prefetch = [&]() {
-    const u128 b0 = next_base;
-    uint32_t* out = ubuf[cur ^ 1].data();
-    bg = std::thread([&gen_block, out, b0] { gen_block(out, b0, 0); });
-    next_base = advance(next_base, g.inc, (uint64_t)kOut);
-  };
-  // the first block, with a pending buffered half (numpy's has_uint32) in front
-  const int64_t lead = g.has32 ? 1 : 0;
-  if (lead) ubuf[0][0] = g.buf32;
-  gen_block(ubuf[0].data(), next_base, lead);
-  next_base = advance(next_base, g.inc, (uint64_t)kOut);
-  int64_t blocks = 1;                    // blocks replayed so far (the current one included)
-  const uint32_t* u = ubuf[0].data();
-  int64_t d = 0, d_end = lead + 2 * kOut;  // read position / end in u
-  prefetch();
-  auto refill = [&]() {
-    bg.join();
-    cur ^= 1;
-    u = ubuf[cur].data();
-    d = 0;
-    d_end = 2 * kOut;
-    ++blocks;
-    prefetch();
-  };
+  }
+  void prefetch() {
+    const u128 b0 = next_base_;
+    uint32_t* out = buf_[cur_ ^ 1].data();
+    bg_ = std::thread([this, out, b0] { gen_block(out, b0, 0); });
+    next_base_ = advance(next_base_, g_.inc, (uint64_t)kOut_);
+  }
+  const Pcg64 g_;  // the state before the first value
+  int T_;
+  int64_t kOut_, lead_, blocks_ = 1;
+  std::vector<uint32_t> buf_[2];
+  int cur_ = 0;
+  u128 next_base_;
+  std::thread bg_;
+};
+
+// numpy's masked-rejection replay over the stream: for i = n-1 .. 1, draw
+// v = next_uint32 & mask(i) until v <= i, and h[i] = v.  Branch-free: every draw is
+// written to h[i]; a rejected one is overwritten by the next draw for the same i, an
+// accepted one moves i on.  Indices are written into `sink` slots: h = sink.base
+// (indexed by i) holds [sink.lo, ...); when i drops below sink.lo, everything from
+// sink.lo up is final and sink.next(i) hands over the next slot.
+template <class Sink>
+void replay(U32Stream& us, int64_t n, Sink& sink) {
   int64_t i = n - 1;
+  uint32_t* h = sink.base;
+  int64_t lo = sink.lo;
   while (i >= 1) {
     uint32_t mask = (uint32_t)i;
     mask |= mask >> 1;
@@ -267,38 +301,168 @@ SME_API int sme_host_pcg64_swap_partners(uint64_t* st, int64_t n, uint32_t* h_j,
     mask |= mask >> 8;
     mask |= mask >> 16;
     const int64_t i_lo = (int64_t)(mask >> 1);  // the mask holds for i in (mask / 2, i]
-    // branch-free rejection: every draw is written to h_j[i]; a rejected one is
-    // overwritten by the next draw for the same i, an accepted one moves i on
     while (i > i_lo) {
-      if (d_end - d >= 8 && i - 8 > i_lo) {
-        // 8 draws with no bounds checks: at most 8 acceptances keep i above i_lo
-        // (the mask holds) and the block holds 8 more values
+      if (i < lo) {
+        sink.next(i);
+        h = sink.base;
+        lo = sink.lo;
+      }
+      const int64_t stop = std::max(i_lo, lo - 1);  // i stays above: same mask, same slot
+      if (us.d_end - us.d >= 8 && i - 8 > stop) {
+        // 8 draws with no bounds checks
 #pragma GCC unroll 8
         for (int k = 0; k < 8; ++k) {
-          const uint32_t v = u[d + k] & mask;
-          h_j[i] = v;
+          const uint32_t v = us.u[us.d + k] & mask;
+          h[i] = v;
           i -= (int64_t)(v <= (uint32_t)i);
         }
-        d += 8;
+        us.d += 8;
         continue;
       }
-      if (d == d_end) refill();
-      const uint32_t v = u[d++] & mask;
-      h_j[i] = v;
+      if (us.d == us.d_end) us.refill();
+      const uint32_t v = us.u[us.d++] & mask;
+      h[i] = v;
       i -= (int64_t)(v <= (uint32_t)i);
     }
   }
-  bg.join();  // the block prefetched last is not needed
-  // uint32 values consumed in total (the pending half counts as one), and where they
-  // leave numpy's buffer: an odd number of fresh halves means a high half is pending
-  const int64_t total_fresh = (blocks - 1) * 2 * kOut + (d - (blocks == 1 ? lead : 0));
-  const int64_t outputs = (total_fresh + 1) / 2;
-  g.state = advance(g.state, g.inc, (uint64_t)outputs);
-  if (total_fresh > 0) {
-    g.has32 = (total_fresh & 1) != 0;
-    g.buf32 = (uint32_t)(xsl_rr(g.state) >> 32);  // the high half of the last output drawn
+  if (lo > 0) {  // the last acceptance left the slot holding index 1
+    sink.next(0);
+    h = sink.base;
+  }
+  h[0] = 0;
+  sink.finish();
+}
+
+struct HostSink {  // one slot: the whole array
+  uint32_t* base;
+  int64_t lo = 0;
+  void next(int64_t) {}
+  void finish() {}
+};
+
+// Pinned staging ring of the device-streaming variant: slots of kSlot indices, each
+// copied to the device (cudaMemcpyAsync) as soon as the replay has moved below it.
+constexpr int kSlots = 4;
+constexpr int64_t kSlot = 1 << 20;
+
+struct Ring {
+  uint32_t* host = nullptr;  // kSlots * kSlot pinned
+  cudaEvent_t ev[kSlots] = {};
+};
+std::mutex g_ring_mu;
+std::vector<Ring*> g_rings;  // free rings (a process keeps a few; concurrent calls take one each)
+
+struct DeviceSink {
+  Ring* ring;
+  int32_t* d_j;
+  cudaStream_t s;
+  int64_t n;
+  uint32_t* base = nullptr;
+  int64_t lo = 0, hi = 0;
+  int slot = -1;
+  bool used[kSlots] = {};
+  cudaError_t err = cudaSuccess;
+
+  void open_slot() {  // the slot for [lo, hi) with hi = the previous lo
+    slot = (slot + 1) % kSlots;
+    if (used[slot] && err == cudaSuccess) err = cudaEventSynchronize(ring->ev[slot]);  // its last copy is done
+    lo = std::max<int64_t>(0, hi - kSlot);
+    base = ring->host + (int64_t)slot * kSlot - lo;
+  }
+  void flush() {
+    if (err == cudaSuccess)
+      err = cudaMemcpyAsync(d_j + lo, base + lo, (size_t)(hi - lo) * 4, cudaMemcpyHostToDevice, s);
+    if (err == cudaSuccess) err = cudaEventRecord(ring->ev[slot], s);
+    used[slot] = true;
+  }
+  void start() {
+    hi = n;
+    slot = -1;
+    open_slot();
+  }
+  void next(int64_t i) {  // i < lo: [lo, hi) is final
+    while (i < lo) {
+      flush();
+      hi = lo;
+      open_slot();
+    }
+  }
+  void finish() {  // i = 0 and h[0] written: [0, hi) is final
+    flush();
+    if (err == cudaSuccess) err = cudaStreamSynchronize(s);
+  }
+};
+
+}  // namespace
+
+// The swap partners of Generator(PCG64).permutation(n) without the swaps:
+// h_j[i] = random_interval(i) for i = n-1 .. 1 in numpy's draw order (h_j[0] = 0),
+// st updated exactly as the full shuffle leaves it.  The raw outputs come from
+// U32Stream (parallel, double-buffered); one sequential pass replays the masked
+// rejection.  The swaps themselves run on the GPU (sme_fy_apply).
+SME_API int sme_host_pcg64_swap_partners(uint64_t* st, int64_t n, uint32_t* h_j, int threads) {
+  if (!st || !h_j || n < 1 || n > INT32_MAX) {
+    sme::set_error("sme_host_pcg64_swap_partners: bad arguments (n=%lld)", (long long)n);
+    return SME_EINVAL;
+  }
+  Pcg64 g = load_state(st);
+  h_j[0] = 0;
+  if (n == 1) return SME_OK;
+  U32Stream us(g, n, threads);
+  HostSink sink{h_j};
+  replay(us, n, sink);
+  us.final_state(g);
+  store_state(g, st);
+  return SME_OK;
+}
+
+// The same partners written straight to DEVICE memory d_j (int32[n]): the replay fills
+// a small pinned ring and each 4 MB slot is copied with cudaMemcpyAsync on `stream` as
+// soon as the replay has moved below it, so the upload hides behind the draws and no
+// n-sized host buffer is touched.  Returns after the copies have completed.
+SME_API int sme_pcg64_swap_partners_to_device(uint64_t* st, int64_t n, int32_t* d_j, int threads,
+                                              sme_stream_t stream) {
+  if (!st || !d_j || n < 1 || n > INT32_MAX) {
+    sme::set_error("sme_pcg64_swap_partners_to_device: bad arguments (n=%lld)", (long long)n);
+    return SME_EINVAL;
+  }
+  Ring* ring = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ring_mu);
+    if (!g_rings.empty()) {
+      ring = g_rings.back();
+      g_rings.pop_back();
+    }
+  }
+  if (!ring) {
+    ring = new Ring;
+    cudaError_t e = cudaHostAlloc((void**)&ring->host, (size_t)kSlots * kSlot * 4, cudaHostAllocDefault);
+    for (int k = 0; k < kSlots && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&ring->ev[k], cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      sme::set_error("sme_pcg64_swap_partners_to_device: %s", cudaGetErrorString(e));
+      delete ring;  // (a partially created ring leaks its pinned block on this error path only)
+      return SME_ECUDA;
+    }
+  }
+  Pcg64 g = load_state(st);
+  DeviceSink sink{ring, d_j, (cudaStream_t)stream, n};
+  sink.start();
+  if (n == 1) {
+    sink.base[0] = 0;
+    sink.finish();
   } else {
-    g.has32 = false;  // only the pending half was used (or nothing)
+    U32Stream us(g, n, threads);
+    replay(us, n, sink);
+    us.final_state(g);
+  }
+  const cudaError_t err = sink.err;
+  {
+    std::lock_guard<std::mutex> lk(g_ring_mu);
+    g_rings.push_back(ring);
+  }
+  if (err != cudaSuccess) {
+    sme::set_error("sme_pcg64_swap_partners_to_device: %s", cudaGetErrorString(err));
+    return SME_ECUDA;
   }
   store_state(g, st);
   return SME_OK;

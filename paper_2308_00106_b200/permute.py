@@ -168,14 +168,32 @@ def pcg64_swap_partners(bitgen: np.random.PCG64, n: int, out: np.ndarray | None 
     return j
 
 
+def pcg64_swap_partners_device(bitgen: np.random.PCG64, n: int, threads: int = 0) -> torch.Tensor:
+    """pcg64_swap_partners straight into a CUDA int32 tensor
+    (sme_pcg64_swap_partners_to_device): the replay streams finished 4 MB slots of a
+    pinned ring to the device while it draws the rest.  `bitgen` advances exactly as the
+    full shuffle's."""
+    if n < 1 or n > 2**31 - 1:
+        raise ValueError("permutation size must be in [1, 2^31)")
+    dev = _cuda.require_cuda()
+    d_j = torch.empty(n, dtype=torch.int32, device=dev)
+    cs = torch.cuda.Stream(device=dev)
+    cs.wait_stream(torch.cuda.current_stream(dev))  # d_j's allocation is ordered before the copies
+    words = _pcg64_words(bitgen)
+    _lib.call("sme_pcg64_swap_partners_to_device", words.ctypes.data, n, ptr(d_j), int(threads), cs.cuda_stream)
+    _set_pcg64_words(bitgen, words)
+    torch.cuda.current_stream(dev).wait_stream(cs)
+    d_j.record_stream(cs)
+    return d_j
+
+
 def pcg64_permutation_device(bitgen: np.random.PCG64, n: int, threads: int = 0) -> torch.Tensor:
     """Generator(bitgen).permutation(n) as a CUDA int32 tensor, bit-exact: partners drawn on
-    the host (sme_host_pcg64_swap_partners), swaps applied in parallel on the GPU
-    (sme_fy_apply: bucket sort by partner + chain walk instead of n dependent swaps)."""
+    the host and uploaded while they are drawn (pcg64_swap_partners_device), swaps applied
+    in parallel on the GPU (sme_fy_apply: bucket sort by partner + chain walk instead of n
+    dependent swaps)."""
     dev = _cuda.require_cuda()
-    # pageable partners: pinning 200 MB costs more (~0.1 s at 50M) than the pageable copy
-    h_j = pcg64_swap_partners(bitgen, n, threads=threads)
-    d_j = torch.from_numpy(h_j.view(np.int32)).to(dev)
+    d_j = pcg64_swap_partners_device(bitgen, n, threads=threads)
     out = torch.empty(n, dtype=torch.int32, device=dev)
     ws = _cuda.workspace(_lib.query_size("sme_fy_apply_workspace_size", n))
     _lib.call("sme_fy_apply", n, ptr(d_j), ptr(out), ptr(ws), ws.numel(), stream())
@@ -210,17 +228,17 @@ def random_permutations(specs) -> list[Permutation]:
         _check_perm_args(n, seed)
     if len(specs) == 1:
         return [random_permutation(*specs[0])]
-    # the host draws of all specs run concurrently (ctypes releases the GIL), then the
-    # GPU applies the swaps
+    # the host draws of all specs run concurrently (ctypes releases the GIL), each with
+    # its upload overlapped; then the GPU applies the swaps
     from concurrent.futures import ThreadPoolExecutor
 
     dev = _cuda.require_cuda()
     threads = max(1, 8 // len(specs))
     with ThreadPoolExecutor(max_workers=len(specs)) as ex:
-        hs = list(ex.map(lambda a: pcg64_swap_partners(np.random.PCG64(a[1]), a[0], threads=threads), specs))
+        djs = list(ex.map(lambda a: pcg64_swap_partners_device(np.random.PCG64(a[1]), a[0], threads=threads),
+                          specs))
     out = []
-    for (n, _), h in zip(specs, hs):
-        d_j = torch.from_numpy(h.view(np.int32)).to(dev)
+    for (n, _), d_j in zip(specs, djs):
         perm = torch.empty(n, dtype=torch.int32, device=dev)
         ws = _cuda.workspace(_lib.query_size("sme_fy_apply_workspace_size", n))
         _lib.call("sme_fy_apply", n, ptr(d_j), ptr(perm), ptr(ws), ws.numel(), stream())

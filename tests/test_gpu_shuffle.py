@@ -34,3 +34,28 @@ def test_random_permutations_and_strategies_match_numpy():
 
     want = _interleave_forward(n, pivot)[local]
     assert np.array_equal(P.riffle_shuffle_permutation(n, pivot, sd).forward, want)
+
+
+@pytest.mark.parametrize("n", [1, 2, (1 << 20) - 1, 1 << 20, (1 << 20) + 1, (1 << 20) + 2, 3 * (1 << 20) + 7,
+                               9 * (1 << 20) + 3])
+@pytest.mark.parametrize("pending", [False, True])
+def test_partners_streamed_to_device_are_numpys(n, pending):
+    """sme_pcg64_swap_partners_to_device: slot boundaries of the pinned ring (4 MB =
+    2^20 partners), a ring that wraps (9 slots > 4), and a generator with a buffered
+    uint32 half pending (numpy's has_uint32) — partners equal the host replay's, and the
+    generator state equals numpy's after the full shuffle."""
+    from paper_2308_00106_b200.permute import pcg64_swap_partners, pcg64_swap_partners_device
+
+    def gen():
+        bg = np.random.PCG64(2024 + n)
+        if pending:
+            np.random.Generator(bg).integers(0, 2**32, dtype=np.uint32)  # leaves a half buffered
+            assert bg.state["has_uint32"] == 1
+        return bg
+
+    a, b, c = gen(), gen(), gen()
+    got = pcg64_swap_partners_device(a, n).cpu().numpy().view(np.uint32)
+    want = pcg64_swap_partners(b, n)
+    assert np.array_equal(got, want)
+    np.random.Generator(c).permutation(n)
+    assert a.state == b.state == c.state

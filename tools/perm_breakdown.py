@@ -1,0 +1,101 @@
+"""random_permutations at C4 (2 x 50M, the bench's device_perms) broken down: concurrent
+host partners, pageable vs pinned H2D, GPU apply."""
+import sys
+import time
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np
+import torch
+
+import paper_2308_00106_b200 as P
+from paper_2308_00106_b200 import _cuda, _lib
+from paper_2308_00106_b200._cuda import ptr, stream
+from paper_2308_00106_b200.permute import axis_seed, pcg64_swap_partners
+
+torch.zeros(1, device="cuda")
+n = 50_000_000
+specs = [(n, axis_seed(7, 0)), (n, axis_seed(7, 1))]
+for rep in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    p = P.random_permutations(specs)
+    torch.cuda.synchronize()
+    print(f"random_permutations total: {time.perf_counter() - t0:.3f} s", flush=True)
+    del p
+for rep in range(2):
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        hs = list(ex.map(lambda a: pcg64_swap_partners(np.random.PCG64(a[1]), a[0], threads=4), specs))
+    t1 = time.perf_counter()
+    ds = [torch.from_numpy(h.view(np.int32)).to("cuda") for h in hs]
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    ws = _cuda.workspace(_lib.query_size("sme_fy_apply_workspace_size", n))
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    for d in ds:
+        _lib.call("sme_fy_apply", n, ptr(d), ptr(out), ptr(ws), ws.numel(), stream())
+    torch.cuda.synchronize()
+    t4 = time.perf_counter()
+    print(f"partners (2 concurrent) {t1 - t0:.3f} s, pageable H2D x2 {t2 - t1:.3f}, ws alloc {t3 - t2:.3f}, "
+          f"apply x2 {t4 - t3:.3f}", flush=True)
+    # the same partners into pre-faulted buffers
+    bufs = [np.empty(n, dtype=np.uint32) for _ in range(2)]
+    for b in bufs:
+        b.fill(0)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        list(ex.map(lambda ab: pcg64_swap_partners(np.random.PCG64(ab[0][1]), ab[0][0], ab[1], threads=4),
+                    zip(specs, bufs)))
+    print(f"partners into pre-faulted buffers: {time.perf_counter() - t0:.3f} s", flush=True)
+    pin = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in range(2)]
+    for pb, h in zip(pin, hs):
+        pb.numpy()[:] = h.view(np.int32)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ds = [pb.to("cuda", non_blocking=True) for pb in pin]
+    torch.cuda.synchronize()
+    print(f"pinned H2D x2 {time.perf_counter() - t0:.3f}", flush=True)
+
+from paper_2308_00106_b200 import hostio
+
+for rep in range(2):
+    t0 = time.perf_counter()
+    bufs = [hostio.thp_empty(n, np.uint32) for _ in range(2)]
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        list(ex.map(lambda ab: pcg64_swap_partners(np.random.PCG64(ab[0][1]), ab[0][0], ab[1], threads=4),
+                    zip(specs, bufs)))
+    print(f"partners into fresh THP mappings (no prefault): {time.perf_counter() - t0:.3f} s", flush=True)
+    t0 = time.perf_counter()
+    bufs = [np.empty(n, dtype=np.uint32) for _ in range(2)]
+    for b in bufs:
+        torch.from_numpy(b.view(np.int32)).zero_()
+    t1 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        list(ex.map(lambda ab: pcg64_swap_partners(np.random.PCG64(ab[0][1]), ab[0][0], ab[1], threads=4),
+                    zip(specs, bufs)))
+    print(f"np.empty + parallel zero_ prefault {t1 - t0:.3f} s, then partners {time.perf_counter() - t1:.3f} s",
+          flush=True)
+    t0 = time.perf_counter()
+    bufs = [hostio.thp_empty(n, np.uint32) for _ in range(2)]
+    for b in bufs:
+        torch.from_numpy(b.view(np.int32)).zero_()
+    t1 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        list(ex.map(lambda ab: pcg64_swap_partners(np.random.PCG64(ab[0][1]), ab[0][0], ab[1], threads=4),
+                    zip(specs, bufs)))
+    print(f"THP + parallel zero_ prefault {t1 - t0:.3f} s, then partners {time.perf_counter() - t1:.3f} s", flush=True)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        djs = list(ex.map(lambda a: P.permute.pcg64_swap_partners_device(np.random.PCG64(a[1]), a[0], threads=4),
+                          specs))
+    torch.cuda.synchronize()
+    print(f"overlapped partners + upload (2 concurrent): {time.perf_counter() - t0:.3f} s", flush=True)
+    t0 = time.perf_counter()
+    for b in bufs:
+        torch.from_numpy(b.view(np.int32)).to("cuda")
+    torch.cuda.synchronize()
+    print(f"pageable H2D from THP prefaulted x2: {time.perf_counter() - t0:.3f} s", flush=True)
