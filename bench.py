@@ -552,12 +552,16 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         e_steps = max(4, args.steps)
         ys_pin = [torch.empty(n, dtype=B.dtype, pin_memory=True) for _ in range(2)]
         # single-call API (synchronous per vector): the reference-shaped spmv_csr
-        P.spmv_csr(B, xs_pin[0], args.kernel)
+        # warm as a caller's loop runs (each result alive until the next call returns):
+        # the result pool then holds the two page-locked host mappings such a loop uses
+        yh = P.spmv_csr(B, xs_pin[0], args.kernel)
+        yh = P.spmv_csr(B, xs_pin[1], args.kernel)
         torch.cuda.synchronize()
         w0 = time.perf_counter()
         for k in range(3):
             yh = P.spmv_csr(B, xs_pin[k & 1], args.kernel)
         single_ms = (time.perf_counter() - w0) / 3 * 1e3
+        del yh
         # pipelined API over a stream of vectors: copies of neighbouring steps overlap
         P.spmv_csr_pipelined(B, xs_pin[:2], ys_pin[:2], args.kernel)
         torch.cuda.synchronize()
