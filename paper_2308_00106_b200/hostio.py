@@ -116,21 +116,6 @@ def _fresh(n: int, dtype) -> tuple[np.ndarray, bool]:
     return np.frombuffer(_PooledMapping(m), dtype=dt, count=n), m.registered
 
 
-def thp_empty(n: int, dtype) -> np.ndarray:
-    """An uninitialised host array on its own anonymous mapping with MADV_HUGEPAGE (not
-    pooled, not page-locked): first touch costs one fault per 2 MB instead of per 4 KB."""
-    dt = np.dtype(dtype)
-    nbytes = n * dt.itemsize
-    if nbytes < CHUNK_MIN_BYTES:
-        return np.empty(n, dtype=dt)
-    mm = mmap.mmap(-1, nbytes)
-    try:
-        mm.madvise(mmap.MADV_HUGEPAGE)
-    except (AttributeError, OSError, ValueError):
-        pass
-    return np.frombuffer(mm, dtype=dt, count=n)
-
-
 def fresh_host(n: int, dtype) -> np.ndarray:
     return _fresh(n, dtype)[0]
 

@@ -60,42 +60,10 @@ for rep in range(2):
     torch.cuda.synchronize()
     print(f"pinned H2D x2 {time.perf_counter() - t0:.3f}", flush=True)
 
-from paper_2308_00106_b200 import hostio
-
 for rep in range(2):
-    t0 = time.perf_counter()
-    bufs = [hostio.thp_empty(n, np.uint32) for _ in range(2)]
-    with ThreadPoolExecutor(max_workers=2) as ex:
-        list(ex.map(lambda ab: pcg64_swap_partners(np.random.PCG64(ab[0][1]), ab[0][0], ab[1], threads=4),
-                    zip(specs, bufs)))
-    print(f"partners into fresh THP mappings (no prefault): {time.perf_counter() - t0:.3f} s", flush=True)
-    t0 = time.perf_counter()
-    bufs = [np.empty(n, dtype=np.uint32) for _ in range(2)]
-    for b in bufs:
-        torch.from_numpy(b.view(np.int32)).zero_()
-    t1 = time.perf_counter()
-    with ThreadPoolExecutor(max_workers=2) as ex:
-        list(ex.map(lambda ab: pcg64_swap_partners(np.random.PCG64(ab[0][1]), ab[0][0], ab[1], threads=4),
-                    zip(specs, bufs)))
-    print(f"np.empty + parallel zero_ prefault {t1 - t0:.3f} s, then partners {time.perf_counter() - t1:.3f} s",
-          flush=True)
-    t0 = time.perf_counter()
-    bufs = [hostio.thp_empty(n, np.uint32) for _ in range(2)]
-    for b in bufs:
-        torch.from_numpy(b.view(np.int32)).zero_()
-    t1 = time.perf_counter()
-    with ThreadPoolExecutor(max_workers=2) as ex:
-        list(ex.map(lambda ab: pcg64_swap_partners(np.random.PCG64(ab[0][1]), ab[0][0], ab[1], threads=4),
-                    zip(specs, bufs)))
-    print(f"THP + parallel zero_ prefault {t1 - t0:.3f} s, then partners {time.perf_counter() - t1:.3f} s", flush=True)
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=2) as ex:
         djs = list(ex.map(lambda a: P.permute.pcg64_swap_partners_device(np.random.PCG64(a[1]), a[0], threads=4),
                           specs))
     torch.cuda.synchronize()
-    print(f"overlapped partners + upload (2 concurrent): {time.perf_counter() - t0:.3f} s", flush=True)
-    t0 = time.perf_counter()
-    for b in bufs:
-        torch.from_numpy(b.view(np.int32)).to("cuda")
-    torch.cuda.synchronize()
-    print(f"pageable H2D from THP prefaulted x2: {time.perf_counter() - t0:.3f} s", flush=True)
+    print(f"partners streamed to the device (2 concurrent): {time.perf_counter() - t0:.3f} s", flush=True)
