@@ -149,6 +149,7 @@ def device_perms(n_rows: int, n_cols: int):
     import paper_2308_00106_b200 as P
     from paper_2308_00106_b200.permute import axis_seed
 
+    torch.cuda.Stream()  # torch's lazy stream-pool init (~60 ms once per process) is not permutation work
     torch.cuda.synchronize()
     t = time.perf_counter()
     p_r, p_c = P.random_permutations([(n_rows, axis_seed(PERM_SEED, 0)), (n_cols, axis_seed(PERM_SEED, 1))])

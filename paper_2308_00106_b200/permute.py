@@ -168,7 +168,8 @@ def pcg64_swap_partners(bitgen: np.random.PCG64, n: int, out: np.ndarray | None 
     return j
 
 
-def pcg64_swap_partners_device(bitgen: np.random.PCG64, n: int, threads: int = 0) -> torch.Tensor:
+def pcg64_swap_partners_device(bitgen: np.random.PCG64, n: int, threads: int = 0,
+                               out: torch.Tensor | None = None) -> torch.Tensor:
     """pcg64_swap_partners straight into a CUDA int32 tensor
     (sme_pcg64_swap_partners_to_device): the replay streams finished 4 MB slots of a
     pinned ring to the device while it draws the rest.  `bitgen` advances exactly as the
@@ -176,7 +177,7 @@ def pcg64_swap_partners_device(bitgen: np.random.PCG64, n: int, threads: int = 0
     if n < 1 or n > 2**31 - 1:
         raise ValueError("permutation size must be in [1, 2^31)")
     dev = _cuda.require_cuda()
-    d_j = torch.empty(n, dtype=torch.int32, device=dev)
+    d_j = torch.empty(n, dtype=torch.int32, device=dev) if out is None else out
     cs = torch.cuda.Stream(device=dev)
     cs.wait_stream(torch.cuda.current_stream(dev))  # d_j's allocation is ordered before the copies
     words = _pcg64_words(bitgen)
@@ -229,22 +230,29 @@ def random_permutations(specs) -> list[Permutation]:
     if len(specs) == 1:
         return [random_permutation(*specs[0])]
     # the host draws of all specs run concurrently (ctypes releases the GIL), each with
-    # its upload overlapped; then the GPU applies the swaps
+    # its upload overlapped and its GPU shuffle started as soon as its partners are in
     from concurrent.futures import ThreadPoolExecutor
 
     dev = _cuda.require_cuda()
     threads = max(1, 8 // len(specs))
+    main = torch.cuda.current_stream(dev)
+    # buffers come from the caller's stream (its allocator pool); each spec's shuffle then
+    # runs on its own stream as soon as its partners are in, overlapping the others' draws
+    bufs = [(torch.empty(n, dtype=torch.int32, device=dev), torch.empty(n, dtype=torch.int32, device=dev),
+             _cuda.workspace(_lib.query_size("sme_fy_apply_workspace_size", n))) for n, _ in specs]
+
+    def one(k):
+        (n, seed), (d_j, perm, ws) = specs[k], bufs[k]
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(main)
+        with torch.cuda.stream(s):
+            pcg64_swap_partners_device(np.random.PCG64(seed), n, threads=threads, out=d_j)
+            _lib.call("sme_fy_apply", n, ptr(d_j), ptr(perm), ptr(ws), ws.numel(), stream())
+        s.synchronize()
+
     with ThreadPoolExecutor(max_workers=len(specs)) as ex:
-        djs = list(ex.map(lambda a: pcg64_swap_partners_device(np.random.PCG64(a[1]), a[0], threads=threads),
-                          specs))
-    out = []
-    for (n, _), d_j in zip(specs, djs):
-        perm = torch.empty(n, dtype=torch.int32, device=dev)
-        ws = _cuda.workspace(_lib.query_size("sme_fy_apply_workspace_size", n))
-        _lib.call("sme_fy_apply", n, ptr(d_j), ptr(perm), ptr(ws), ws.numel(), stream())
-        out.append(Permutation(perm, _trusted=True))
-    torch.cuda.current_stream().synchronize()  # the workspaces are released on return
-    return out
+        list(ex.map(one, range(len(specs))))
+    return [Permutation(perm, _trusted=True) for _, perm, _ in bufs]
 
 
 def permute_rows(m: CooMatrix, p: Permutation) -> CooMatrix:

@@ -17,6 +17,36 @@ from paper_2308_00106_b200.permute import axis_seed, pcg64_swap_partners
 torch.zeros(1, device="cuda")
 n = 50_000_000
 specs = [(n, axis_seed(7, 0)), (n, axis_seed(7, 1))]
+# first call, piece by piece (what bench.py's perm_gen_s sees once)
+from paper_2308_00106_b200.permute import pcg64_swap_partners_device
+
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+bufs = [(torch.empty(n, dtype=torch.int32, device="cuda"), torch.empty(n, dtype=torch.int32, device="cuda"),
+         _cuda.workspace(_lib.query_size("sme_fy_apply_workspace_size", n))) for _ in specs]
+torch.cuda.synchronize()
+t1 = time.perf_counter()
+ss = [torch.cuda.Stream() for _ in specs]
+t2 = time.perf_counter()
+tt = {}
+
+
+def one(k):
+    a = time.perf_counter()
+    with torch.cuda.stream(ss[k]):
+        pcg64_swap_partners_device(np.random.PCG64(specs[k][1]), n, threads=4, out=bufs[k][0])
+        b = time.perf_counter()
+        _lib.call("sme_fy_apply", n, ptr(bufs[k][0]), ptr(bufs[k][1]), ptr(bufs[k][2]), bufs[k][2].numel(), stream())
+    ss[k].synchronize()
+    tt[k] = (b - a, time.perf_counter() - b)
+
+
+with ThreadPoolExecutor(max_workers=2) as ex:
+    list(ex.map(one, range(2)))
+t3 = time.perf_counter()
+print(f"first call: buffers {t1 - t0:.3f} s (ws {bufs[0][2].numel() / 1e6:.0f} MB each), streams {t2 - t1:.3f}, "
+      f"partners+apply {t3 - t2:.3f} (per axis partners/apply: {tt})", flush=True)
+del bufs
 for rep in range(3):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
