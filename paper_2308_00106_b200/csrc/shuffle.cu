@@ -76,8 +76,8 @@ __global__ void k_fy_final(int64_t n, const uint32_t* __restrict__ j, const int3
   }
 }
 
-inline size_t fy_ws_bytes(int64_t n) {
-  return align_up((size_t)n * 4) * 4 + align_up((size_t)(n + 1) * 4) + scan_workspace_bytes(n);
+inline size_t fy_ws_bytes(int64_t n) {  // counts (later succ), bucket, nxt, off, scan scratch
+  return align_up((size_t)n * 4) * 3 + align_up((size_t)(n + 1) * 4) + scan_workspace_bytes(n);
 }
 
 }  // namespace sme
@@ -100,8 +100,8 @@ SME_API int sme_fy_apply(int64_t n, const uint32_t* d_j, int32_t* d_perm, void* 
   cudaStream_t s = as_stream(stream);
   char* p = (char*)ws;
   int32_t* counts = (int32_t*)p;  p += align_up((size_t)n * 4);
+  int32_t* succ = counts;         // the counts / fill cursors are dead once the buckets are filled
   int32_t* bucket = (int32_t*)p;  p += align_up((size_t)n * 4);
-  int32_t* succ = (int32_t*)p;    p += align_up((size_t)n * 4);
   int32_t* nxt = (int32_t*)p;     p += align_up((size_t)n * 4);
   int32_t* off = (int32_t*)p;     p += align_up((size_t)(n + 1) * 4);
   void* scan_ws = p;
