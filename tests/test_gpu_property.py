@@ -3,6 +3,8 @@ seeds through the whole path — build_strategy -> permute_matrix -> coo_to_csr 
 vs the oracle's restatement of the reference), the 2-D histogram (bit-exact), and
 every SpMV kernel (normwise <= 1e-12, reference CORRECTNESS_RTOL)."""
 
+import os
+
 import numpy as np
 import pytest
 from hypothesis import HealthCheck, given, settings
@@ -36,7 +38,8 @@ def matrices(draw):
 
 
 @given(matrices(), st.sampled_from(KINDS), st.integers(0, 1000))
-@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@settings(max_examples=int(os.environ.get("SME_PROPERTY_EXAMPLES", "40")), deadline=None,
+          suppress_health_check=[HealthCheck.too_slow])
 def test_pipeline_properties(mat, kind, strat_seed):
     n_rows, n_cols, rows, cols, vals, seed = mat
     m = P.CooMatrix(n_rows, n_cols, rows, cols, vals)
