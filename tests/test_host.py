@@ -134,3 +134,37 @@ def test_native_swap_partners_large_match_full_shuffle():
     # spot-check: the partners' last steps reproduce the shuffle's tail positions' dependence
     assert j[0] == 0 and int(j[1:].max()) < n and np.all(j[1:] <= np.arange(1, n))
     assert full.dtype == np.int32
+
+
+def test_hostio_fresh_results_never_alias_and_recycle():
+    """hostio.fresh_host: large results are pooled mappings handed out again only after
+    every array (and tensor) viewing them has been released; small ones are np.empty."""
+    import gc
+
+    import torch
+
+    from paper_2308_00106_b200 import hostio
+
+    n = hostio.CHUNK_MIN_BYTES // 8 + 7
+    key = n * 8
+    hostio._POOL.pop(key, None)
+    a = hostio.fresh_host(n, np.float64)
+    b = hostio.fresh_host(n, np.float64)
+    assert a.flags.writeable and a.shape == (n,) and not np.shares_memory(a, b)
+    a[:] = 1.0
+    view = a[5:9]
+    t = torch.from_numpy(a)
+    del a
+    gc.collect()
+    assert len(hostio._POOL.get(key, [])) == 0  # a view and a tensor still hold the mapping
+    del view
+    gc.collect()
+    assert len(hostio._POOL.get(key, [])) == 0
+    del t
+    gc.collect()
+    assert len(hostio._POOL[key]) == 1
+    c = hostio.fresh_host(n, np.float64)  # the released mapping comes back
+    assert len(hostio._POOL[key]) == 0 and c[0] == 1.0 and not np.shares_memory(c, b)
+    small = hostio.fresh_host(10, np.float32)
+    assert small.dtype == np.float32 and small.shape == (10,)
+    assert hostio.slices(10, 8) == [0, 10] and hostio.slices(n, 8, 4)[-1] == n
