@@ -114,6 +114,13 @@ int sme_host_pcg64_swap_partners(uint64_t* st, int64_t n, uint32_t* h_j, int thr
  * draws and no n-sized host buffer is touched.  HOST call; returns after the copies
  * have completed (it synchronises `stream`). */
 int sme_pcg64_swap_partners_to_device(uint64_t* st, int64_t n, int32_t* d_j, int threads, sme_stream_t stream);
+/* The same partners drawn on the GPU (shuffle_gen.cu): the PCG64 stream is generated in
+ * parallel, every draw whose step provably lies in a narrow statistical window is
+ * decided in parallel, the few others in order on the host, and a final pass checks
+ * the windows and writes d_j.  n >= 2.  Returns SME_OK, or 1 if a window check failed
+ * (odds ~1e-30; st untouched, replay on the host instead).  HOST call that
+ * synchronises `stream`. */
+int sme_pcg64_swap_partners_gpu(uint64_t* st, int64_t n, int32_t* d_j, sme_stream_t stream);
 /* The swaps of that shuffle on the GPU (shuffle.cu): d_perm = the permutation
  * a = arange(n); for i = n-1..1: swap(a[i], a[d_j[i]]) builds — computed as a
  * bucket sort of the steps by partner, a link pass and a chain walk (no dependent

@@ -168,12 +168,18 @@ def pcg64_swap_partners(bitgen: np.random.PCG64, n: int, out: np.ndarray | None 
     return j
 
 
+#: sizes from which the partners are drawn on the GPU (sme_pcg64_swap_partners_gpu)
+GPU_PARTNERS_MIN = 1 << 20
+
+
 def pcg64_swap_partners_device(bitgen: np.random.PCG64, n: int, threads: int = 0,
-                               out: torch.Tensor | None = None) -> torch.Tensor:
-    """pcg64_swap_partners straight into a CUDA int32 tensor
-    (sme_pcg64_swap_partners_to_device): the replay streams finished 4 MB slots of a
-    pinned ring to the device while it draws the rest.  `bitgen` advances exactly as the
-    full shuffle's."""
+                               out: torch.Tensor | None = None, gpu_min: int | None = None) -> torch.Tensor:
+    """pcg64_swap_partners straight into a CUDA int32 tensor.  From GPU_PARTNERS_MIN on
+    they are drawn on the GPU (sme_pcg64_swap_partners_gpu: parallel PCG64 stream, draws
+    decided in parallel inside statistical step windows, the few ambiguous ones in order
+    on the host); below it, or if a window check fails, the host replay streams finished
+    4 MB slots of a pinned ring to the device while it draws the rest
+    (sme_pcg64_swap_partners_to_device).  `bitgen` advances exactly as the full shuffle's."""
     if n < 1 or n > 2**31 - 1:
         raise ValueError("permutation size must be in [1, 2^31)")
     dev = _cuda.require_cuda()
@@ -181,6 +187,16 @@ def pcg64_swap_partners_device(bitgen: np.random.PCG64, n: int, threads: int = 0
     cs = torch.cuda.Stream(device=dev)
     cs.wait_stream(torch.cuda.current_stream(dev))  # d_j's allocation is ordered before the copies
     words = _pcg64_words(bitgen)
+    if n >= (GPU_PARTNERS_MIN if gpu_min is None else gpu_min) and n >= 2:
+        rc = _lib.load().sme_pcg64_swap_partners_gpu(words.ctypes.data, n, ptr(d_j), cs.cuda_stream)
+        if rc == _lib.SME_OK:
+            _set_pcg64_words(bitgen, words)
+            torch.cuda.current_stream(dev).wait_stream(cs)
+            d_j.record_stream(cs)
+            return d_j
+        if rc != 1:  # 1: a window check failed -> the host replay below
+            raise RuntimeError(f"sme_pcg64_swap_partners_gpu: {_lib.last_error()}")
+        words = _pcg64_words(bitgen)
     _lib.call("sme_pcg64_swap_partners_to_device", words.ctypes.data, n, ptr(d_j), int(threads), cs.cuda_stream)
     _set_pcg64_words(bitgen, words)
     torch.cuda.current_stream(dev).wait_stream(cs)

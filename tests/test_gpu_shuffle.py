@@ -59,3 +59,24 @@ def test_partners_streamed_to_device_are_numpys(n, pending):
     assert np.array_equal(got, want)
     np.random.Generator(c).permutation(n)
     assert a.state == b.state == c.state
+
+
+@pytest.mark.parametrize("n", [2, 3, 1000, 65_537, 300_001, 2_000_003])
+@pytest.mark.parametrize("seed", [0, 7])
+@pytest.mark.parametrize("pending", [False, True])
+def test_partners_drawn_on_gpu_are_numpys(n, seed, pending):
+    """sme_pcg64_swap_partners_gpu (forced at every size): the same partners and the same
+    generator state as numpy's shuffle, with and without a buffered uint32 half."""
+    from paper_2308_00106_b200.permute import pcg64_swap_partners, pcg64_swap_partners_device
+
+    def gen():
+        bg = np.random.PCG64(seed * 1000 + n)
+        if pending:
+            np.random.Generator(bg).integers(0, 2**32, dtype=np.uint32)
+        return bg
+
+    a, b, c = gen(), gen(), gen()
+    got = pcg64_swap_partners_device(a, n, gpu_min=2).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, pcg64_swap_partners(b, n))
+    np.random.Generator(c).permutation(n)
+    assert a.state == b.state == c.state
