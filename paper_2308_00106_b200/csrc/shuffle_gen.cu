@@ -14,10 +14,11 @@
 // whole window).  Only the rest ("ambiguous": values inside the window, windows that
 // straddle a power of two, and every draw for steps below 2^16) need the exact count,
 // and the host resolves those in order with the certain rejections before each of them
-// (a few 10^5 of ~1.4 n draws).  A final pass recomputes every R_t, checks that each
+// (~2 % of the ~1.47 n draws).  A final pass recomputes every R_t, checks that each
 // certain draw's step really lay inside its window (if not — odds ~1e-30 — the caller
 // falls back to the sequential host replay), and writes j[i_t] for the accepted draws.
-// Measured at n = 50M: ~2.8 % of the ~73M draws are ambiguous with a 12-sigma window.
+// Measured at n = 50M: 1.3M of the 73M draws are ambiguous (7-sigma windows); 20-25 ms
+// per axis warm, against 50 ms for the sequential host replay.
 #include "common.cuh"
 #include "scan.cuh"
 
