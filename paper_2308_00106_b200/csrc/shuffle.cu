@@ -28,11 +28,13 @@ __global__ void k_fy_count(int64_t n, const uint32_t* __restrict__ j, int32_t* _
     atomicAdd(&counts[j[s]], 1);
 }
 
-__global__ void k_fy_fill(int64_t n, const uint32_t* __restrict__ j, const int32_t* __restrict__ off,
-                          int32_t* __restrict__ cursor, int32_t* __restrict__ bucket) {
+// cursor[p] starts at off[p]: one random atomic per step instead of a read of off[p] plus an
+// atomic on a zeroed counter
+__global__ void k_fy_fill(int64_t n, const uint32_t* __restrict__ j, int32_t* __restrict__ cursor,
+                          int32_t* __restrict__ bucket) {
   for (int64_t s = 1 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t p = j[s];
-    bucket[off[p] + atomicAdd(&cursor[p], 1)] = (int32_t)s;
+    bucket[atomicAdd(&cursor[p], 1)] = (int32_t)s;
   }
 }
 
@@ -111,8 +113,8 @@ SME_API int sme_fy_apply(int64_t n, const uint32_t* d_j, int32_t* d_perm, void* 
   SME_CHECK_LAUNCH("k_fy_count");
   int rc = exclusive_scan_lengths(n, LenFromArray{counts}, off, scan_ws, nullptr, s);
   if (rc != SME_OK) return rc;
-  SME_CUDA(cudaMemsetAsync(counts, 0, (size_t)n * 4, s));  // reused as the fill cursor
-  k_fy_fill<<<grid, 256, 0, s>>>(n, d_j, off, counts, bucket);
+  SME_CUDA(cudaMemcpyAsync(counts, off, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));  // the fill cursors
+  k_fy_fill<<<grid, 256, 0, s>>>(n, d_j, counts, bucket);
   SME_CHECK_LAUNCH("k_fy_fill");
   k_fy_links<<<grid, 256, 0, s>>>(n, off, bucket, succ, nxt);
   SME_CHECK_LAUNCH("k_fy_links");
