@@ -71,9 +71,20 @@ class SegLayout:
         total = max(int(offs[-1]), CHUNK)
         self.entries = ent
         self.offsets = offs
-        self.pk = torch.full((total,), -1, dtype=torch.int32, device=dev)  # tail padding = explicit zeros
-        self.val = torch.zeros(total, dtype=m.dtype, device=dev)
-        self.hdr = torch.zeros(total // CHUNK, dtype=torch.int32, device=dev)
+        # the fill writes every entry slot and every chunk header; only each panel's tail
+        # padding (< CHUNK slots) is set here, as explicit zeros
+        self.pk = torch.empty(total, dtype=torch.int32, device=dev)
+        self.val = torch.empty(total, dtype=m.dtype, device=dev)
+        self.hdr = torch.zeros(total // CHUNK, dtype=torch.int32, device=dev) if total == CHUNK else \
+            torch.empty(total // CHUNK, dtype=torch.int32, device=dev)
+        for p in range(P):
+            lo, hi = int(offs[p] + ent[p]), int(offs[p + 1])
+            if hi > lo:
+                self.pk[lo:hi] = -1
+                self.val[lo:hi] = 0
+        if total > int(offs[-1]):  # an all-empty layout: one chunk of explicit zeros
+            self.pk[int(offs[-1]):] = -1
+            self.val[int(offs[-1]):] = 0
         h_offs = (ctypes.c_int64 * P)(*[int(o) for o in offs[:P]])
         d_offs = torch.from_numpy(offs[:P].copy()).to(dev)
         _lib.call("sme_seg_fill", _cuda.sme_dtype(m.d_values), n, ptr(m.d_row_ptr), ptr(m.d_col_idx),
