@@ -339,6 +339,9 @@ int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const int3
                  const void* d_val, int32_t n_panels, const int32_t* d_bounds, const int32_t* d_pos,
                  const int64_t* d_offsets, const int64_t* h_offsets, uint32_t* d_pk, void* d_out_val,
                  int32_t* d_hdr, const void* d_ws, sme_stream_t stream);
+/* Test hook: 1 (default) fills the layout with a warp per 32-row group through a
+ * shared-memory image of the group's panel ranges (coalesced writes); 0 = warp per row. */
+int sme_seg_set_scatter_groups(int on);
 int sme_spmv_seg_warps(int32_t* n_warps);
 /* Kernel variant (process-wide): 0 = the SpMV (default; accumulating passes add
  * with RED.ADD at L2), 3 = bound probe (the chunk stream and gathers without the

@@ -53,6 +53,7 @@
 namespace sme {
 
 constexpr int SEG_NT = 256;
+static bool s_seg_scatter_groups = true;  // sme_seg_set_scatter_groups
 constexpr int SEG_CH = 128;
 constexpr int SEG_DBITS = 8;
 constexpr uint32_t SEG_DMASK = (1u << SEG_DBITS) - 1;
@@ -195,6 +196,194 @@ __global__ void k_seg_scatter(int64_t n_rows, const int32_t* __restrict__ row_pt
         const bool last = k - f == pc - 1;
         out_pk[dst] = ((uint32_t)(c - lo) << SEG_CSHIFT) | (last ? SEG_END : 0u) | (uint32_t)(r - hdr[dst / SEG_CH]);
         out_val[dst] = val[k];
+      }
+    }
+  }
+}
+
+// Warp per group of 32 consecutive rows (panels <= 32): a panel's slots for those rows
+// are one contiguous range (positions are row-ordered), so the group's entries are
+// placed in a shared-memory image of the group's panel ranges (lane per row) and written
+// out per panel with consecutive lanes on consecutive slots — ~2 write requests per row
+// instead of one per (row, panel) piece and array.  A group whose ranges exceed SG_CAP
+// slots (long rows) takes the per-row path of k_seg_scatter.  C4 layout build: 26 ->
+// 22.8 ms (an entry-parallel placement with a row search measured 30 ms; 768 slots x 8
+// warps 23.6-25.5 ms).
+constexpr int SG_CAP = 1024;
+constexpr int SG_WARPS = 4;
+
+inline size_t sg_warp_bytes(int n_panels, size_t val_bytes) {
+  return align_up((size_t)SG_CAP * (4 + val_bytes) + (size_t)3 * n_panels * 32 * 4 + 40 * 4 + 4 * 32 * 4, 16);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
+    int64_t n_rows, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col, const T* __restrict__ val,
+    int32_t n_panels, const int32_t* __restrict__ bounds, const int32_t* __restrict__ counts,
+    const int32_t* __restrict__ pos, const int64_t* __restrict__ offsets, uint32_t* __restrict__ out_pk,
+    T* __restrict__ out_val, const int32_t* __restrict__ hdr, size_t warp_bytes) {
+  extern __shared__ __align__(16) unsigned char sg_smem[];
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int P = n_panels;
+  unsigned char* wb = sg_smem + (size_t)wib * warp_bytes;
+  T* s_val = reinterpret_cast<T*>(wb);
+  uint32_t* s_pk = reinterpret_cast<uint32_t*>(wb + (size_t)SG_CAP * sizeof(T));
+  int32_t* s_first = reinterpret_cast<int32_t*>(s_pk + SG_CAP);  // [P][32]
+  int32_t* s_cnt = s_first + P * 32;                             // [P][32]
+  int32_t* s_ppos = s_cnt + P * 32;                              // [P][32]
+  int32_t* s_rp = s_ppos + P * 32;                               // [33] row starts
+  int32_t* s_gs = s_rp + 40;                                     // [32] group range start per panel
+  int32_t* s_sb = s_gs + 32;                                     // [32] staging base per panel
+  int32_t* s_len = s_sb + 32;                                    // [32]
+  __shared__ int32_t c_hi[32], c_lo[32];  // panel column bounds and slot offsets (CTA-wide)
+  __shared__ int64_t c_off[32];
+  const int32_t my_hi = lane < P ? bounds[lane + 1] : INT32_MAX;
+  const int32_t my_lo = lane < P ? bounds[lane] : 0;
+  const int64_t my_off = lane < P ? offsets[lane] : 0;
+  if (wib == 0) {
+    c_hi[lane] = my_hi;
+    c_lo[lane] = my_lo;
+    c_off[lane] = my_off;
+  }
+  __syncthreads();
+  const int64_t n_groups = (n_rows + 31) / 32;
+  const int64_t warp = (int64_t)blockIdx.x * SG_WARPS + wib, n_warps = (int64_t)gridDim.x * SG_WARPS;
+  for (int64_t g = warp; g < n_groups; g += n_warps) {
+    const int64_t r0 = g * 32;
+    const int nr = (int)min((int64_t)32, n_rows - r0);
+    __syncwarp();
+    if (lane < nr) s_rp[lane] = row_ptr[r0 + lane];
+    if (lane == 0) s_rp[nr] = row_ptr[r0 + nr];
+    // the group's range in each panel and its place in the staging image
+    int32_t gs = 0, len = 0;
+    if (lane < P) {
+      const int32_t* pp = pos + (int64_t)lane * (n_rows + 1);
+      gs = pp[r0];
+      len = pp[r0 + nr] - gs;
+    }
+    int32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t t = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int32_t total = __shfl_sync(FULL, incl, 31);
+    if (total > SG_CAP) {  // long rows: the per-row path
+      for (int i = 0; i < nr; ++i) {
+        const int64_t r = r0 + i;
+        const int32_t a = row_ptr[r], b = row_ptr[r + 1];
+        int32_t cnt = 0, ppos = 0, pnext = 0;
+        if (lane < P) {
+          cnt = counts[(int64_t)lane * n_rows + r];
+          const int32_t* pp = pos + (int64_t)lane * (n_rows + 1);
+          ppos = pp[r];
+          pnext = pp[r + 1];
+        }
+        int32_t ic = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t t = __shfl_up_sync(FULL, ic, o);
+          if (lane >= o) ic += t;
+        }
+        const int32_t first = a + ic - cnt;
+        if (lane < P && cnt == 0 && pnext > ppos) {
+          const int64_t dst = my_off + ppos;
+          out_pk[dst] = (SEG_MARK << SEG_CSHIFT) | SEG_END | (uint32_t)(r - hdr[dst / SEG_CH]);
+          out_val[dst] = T(0);
+        }
+        for (int32_t k0 = a; k0 < b; k0 += 32) {
+          const int32_t k = k0 + lane;
+          const int32_t c = k < b ? col[k] : INT32_MAX;
+          int p = 0;
+          for (int q = 0; q < P; ++q) p += (c >= __shfl_sync(FULL, my_hi, q)) ? 1 : 0;
+          if (p >= P) p = P - 1;
+          const int32_t f = __shfl_sync(FULL, first, p);
+          const int32_t pc = __shfl_sync(FULL, cnt, p);
+          const int32_t pq = __shfl_sync(FULL, ppos, p);
+          const int64_t po = __shfl_sync(FULL, my_off, p);
+          const int32_t lo = __shfl_sync(FULL, my_lo, p);
+          if (k < b) {
+            const int64_t dst = po + pq + (k - f);
+            out_pk[dst] = ((uint32_t)(c - lo) << SEG_CSHIFT) | (k - f == pc - 1 ? SEG_END : 0u) |
+                          (uint32_t)(r - hdr[dst / SEG_CH]);
+            out_val[dst] = val[k];
+          }
+        }
+      }
+      continue;
+    }
+    if (lane < P) {
+      s_gs[lane] = gs;
+      s_sb[lane] = incl - len;
+      s_len[lane] = len;
+    }
+    // per (panel, row): first entry, count, slot; explicit zeros go straight to the image
+    if (lane < nr) {
+      const int64_t r = r0 + lane;
+      int32_t run = s_rp[lane];
+      for (int p = 0; p < P; ++p) {
+        const int32_t c = counts[(int64_t)p * n_rows + r];
+        const int32_t* pp = pos + (int64_t)p * (n_rows + 1);
+        const int32_t ppos = pp[r];
+        s_first[p * 32 + lane] = run;
+        s_cnt[p * 32 + lane] = c;
+        s_ppos[p * 32 + lane] = ppos;
+        run += c;
+      }
+    }
+    __syncwarp();
+    if (lane < nr) {
+      const int64_t r = r0 + lane;
+      for (int p = 0; p < P; ++p) {
+        if (s_cnt[p * 32 + lane] != 0) continue;
+        const int32_t ppos = s_ppos[p * 32 + lane];
+        const int32_t pnext = (lane + 1 < nr) ? s_ppos[p * 32 + lane + 1] : s_gs[p] + s_len[p];
+        if (pnext > ppos) {
+          const int32_t sidx = s_sb[p] + (ppos - s_gs[p]);
+          const int64_t dst = c_off[p] + ppos;
+          s_pk[sidx] = (SEG_MARK << SEG_CSHIFT) | SEG_END | (uint32_t)(r - hdr[dst / SEG_CH]);
+          s_val[sidx] = T(0);
+        }
+      }
+    }
+    // the entries into the image: lane per row (columns ascend along a row, so the panel
+    // only moves forward and its table entries are reloaded only when it changes)
+    if (lane < nr) {
+      const int32_t r_rel = r0 + lane;
+      const int32_t kend = s_rp[lane + 1];
+      int p = 0;
+      int32_t f = s_first[lane], pc = s_cnt[lane], pq = s_ppos[lane], sb = s_sb[0] - s_gs[0];
+      int64_t po = c_off[0];
+      uint32_t clo = (uint32_t)c_lo[0];
+      for (int32_t k = s_rp[lane]; k < kend; ++k) {
+        const int32_t c = col[k];
+        const T v = val[k];
+        if (p < P - 1 && c >= c_hi[p]) {
+          do ++p;
+          while (p < P - 1 && c >= c_hi[p]);
+          f = s_first[p * 32 + lane];
+          pc = s_cnt[p * 32 + lane];
+          pq = s_ppos[p * 32 + lane];
+          sb = s_sb[p] - s_gs[p];
+          po = c_off[p];
+          clo = (uint32_t)c_lo[p];
+        }
+        const int32_t dip = pq + (k - f);  // slot within the panel
+        const int32_t sidx = sb + dip;
+        s_pk[sidx] = (((uint32_t)c - clo) << SEG_CSHIFT) | (k - f == pc - 1 ? SEG_END : 0u) |
+                     (uint32_t)(r_rel - hdr[(po + dip) / SEG_CH]);
+        s_val[sidx] = v;
+      }
+    }
+    __syncwarp();
+    // out, panel by panel, consecutive lanes on consecutive slots
+    for (int p = 0; p < P; ++p) {
+      const int32_t n_p = s_len[p], sb = s_sb[p];
+      const int64_t base = c_off[p] + s_gs[p];
+      for (int q = lane; q < n_p; q += 32) {
+        out_pk[base + q] = s_pk[sb + q];
+        out_val[base + q] = s_val[sb + q];
       }
     }
   }
@@ -689,6 +878,24 @@ SME_API int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* row_ptr, cons
     k_seg_hdr<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, pos + (int64_t)p * (n_rows + 1), hdr + h_offsets[p] / SEG_CH);
     SME_CHECK_LAUNCH("k_seg_hdr");
   }
+  if (n_panels <= 32 && s_seg_scatter_groups) {
+    auto launch = [&](auto kern, size_t vb, auto* v, auto* ov) {
+      const size_t wbytes = sg_warp_bytes(n_panels, vb), smem = wbytes * SG_WARPS;
+      SME_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const int64_t groups = (n_rows + 31) / 32;
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((groups + SG_WARPS - 1) / SG_WARPS,
+                                                                 (int64_t)sm_count() * 16));
+      kern<<<grid, SG_WARPS * 32, smem, s>>>(n_rows, row_ptr, col, v, n_panels, bounds, counts, pos, offsets, pk, ov,
+                                             hdr, wbytes);
+      return SME_OK;
+    };
+    if (dtype == SME_F64)
+      launch(k_seg_scatter_groups<double>, 8, (const double*)val, (double*)out_val);
+    else
+      launch(k_seg_scatter_groups<float>, 4, (const float*)val, (float*)out_val);
+    SME_CHECK_LAUNCH("k_seg_scatter_groups");
+    return SME_OK;
+  }
   if (dtype == SME_F64)
     k_seg_scatter<double><<<grid_for(n_rows * 32, 256), 256, 0, s>>>(n_rows, row_ptr, col, (const double*)val, n_panels,
                                                                       bounds, counts, pos, offsets, pk,
@@ -698,6 +905,13 @@ SME_API int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* row_ptr, cons
                                                                      bounds, counts, pos, offsets, pk, (float*)out_val,
                                                                      hdr);
   SME_CHECK_LAUNCH("k_seg_scatter");
+  return SME_OK;
+}
+
+// Layout fill: 1 = warp per 32-row group through a shared-memory image (default),
+// 0 = warp per row (k_seg_scatter).  Process-wide; for A/B tests.
+SME_API int sme_seg_set_scatter_groups(int on) {
+  s_seg_scatter_groups = on != 0;
   return SME_OK;
 }
 
