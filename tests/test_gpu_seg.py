@@ -344,3 +344,27 @@ def test_host_vectors_large_fresh_results(dev, rng, kernel, dtype):
         assert O.relative_error(y2, want2) <= tol  # untouched by the later calls
         del y2, yt
         gc.collect()
+
+
+@pytest.mark.parametrize("n_panels", [1, 3, 8])
+def test_grouped_fill_equals_per_row_fill(dev, rng, n_panels):
+    """The grouped layout fill (warp per 32 rows through shared memory, with the per-row
+    path for groups too long for the image) builds the same layout, bit for bit, as the
+    per-row fill."""
+    from paper_2308_00106_b200 import _lib
+
+    n = 5000
+    lens = rng.integers(0, 40, n)
+    lens[[7, 8, 900]] = [3000, 1500, 2500]  # groups over the image capacity
+    lens[100:180] = 0  # empty rows: explicit zeros
+    ptr, col, val = csr_from_lens(rng, lens, n)
+    m = P.CsrMatrix(n, n, ptr, col, val)
+    layouts = []
+    for on in (1, 0):
+        _lib.call("sme_seg_set_scatter_groups", on)
+        try:
+            layouts.append(SegLayout(m, n_panels))
+        finally:
+            _lib.call("sme_seg_set_scatter_groups", 1)
+    a, b = layouts
+    assert torch.equal(a.pk, b.pk) and torch.equal(a.val, b.val) and torch.equal(a.hdr, b.hdr)
