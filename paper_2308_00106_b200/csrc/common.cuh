@@ -179,6 +179,9 @@ __device__ __forceinline__ void st_stream(double* p, double v) {
 __device__ __forceinline__ void st_stream(float* p, float v) {
   asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v));
 }
+__device__ __forceinline__ void st_stream(int32_t* p, int32_t v) {
+  asm volatile("st.global.cs.s32 [%0], %1;" ::"l"(p), "r"(v));
+}
 
 // ---------------------------------------------------------------------------
 // exact division by an invariant divisor: q = (n * m) >> s, exact for

@@ -171,7 +171,8 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_rows_warp(
         const int idx = SK::slot(v);
         const bool dup = li > 0 && SK::col(prev) == key;
         if (dup && !L.mark_dups) report_dup((int32_t)(g * 32 + rr), key, flag, dup_key);
-        out_col[my_dst + li] = (dup && L.mark_dups) ? -1 : (int32_t)key;
+        // streaming stores: the outputs must not push the column map (cmap) out of L2
+        st_stream(out_col + my_dst + li, (dup && L.mark_dups) ? -1 : (int32_t)key);
         st_stream(out_val + my_dst + li, ld_stream(src_val + my_from + idx, once));
       }
     }
