@@ -586,6 +586,57 @@ SME_API int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t n
                              (float*)val_out, L, flag, dup_key, s, n_cols);
 }
 
+namespace sme {
+// out[k] = cmap[col[k]] for the entries whose column lies in [lo, hi): one pass of the
+// column-sliced pre-map (the slice of cmap stays L2-resident during its pass)
+__global__ void k_map_cols_slice(int64_t nnz, const int32_t* __restrict__ col, const int32_t* __restrict__ cmap,
+                                 int32_t* __restrict__ out, int32_t lo, int32_t hi) {
+  const uint64_t once = policy_evict_first();
+  const int64_t n4 = nnz / 4;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
+    const int4 c = ld_stream_i4(reinterpret_cast<const int4*>(col) + q, once);
+    const int64_t k = q * 4;
+    if (c.x >= lo && c.x < hi) st_stream(out + k, __ldg(cmap + c.x));
+    if (c.y >= lo && c.y < hi) st_stream(out + k + 1, __ldg(cmap + c.y));
+    if (c.z >= lo && c.z < hi) st_stream(out + k + 2, __ldg(cmap + c.z));
+    if (c.w >= lo && c.w < hi) st_stream(out + k + 3, __ldg(cmap + c.w));
+  }
+  if (blockIdx.x == 0)
+    for (int64_t k = n4 * 4 + threadIdx.x; k < nnz; k += blockDim.x) {
+      const int32_t c = col[k];
+      if (c >= lo && c < hi) out[k] = cmap[c];
+    }
+}
+}  // namespace sme
+
+// mapped[k] = cmap[col[k]] (the column relabelling of permute_matrix, permute.py:98-102)
+// in n_slices passes over col, pass s mapping the columns of slice s with that slice of
+// cmap pinned in L2 (access-policy window on `stream`): the random cmap reads hit L2
+// instead of DRAM.  col must be 16-byte aligned.
+SME_API int sme_map_cols_sliced(int64_t nnz, int64_t n_cols, const int32_t* col, const int32_t* cmap,
+                                int32_t* mapped, int32_t n_slices, sme_stream_t stream) {
+  SME_REQUIRE(nnz >= 0 && n_cols >= 1 && n_slices >= 1 && col && cmap && mapped, "bad arguments");
+  SME_REQUIRE(((uintptr_t)col & 15) == 0, "col must be 16-byte aligned");
+  if (nnz == 0) return SME_OK;
+  cudaStream_t s = as_stream(stream);
+  const int grid = sm_count() * 8;
+  for (int32_t q = 0; q < n_slices; ++q) {
+    const int64_t lo = n_cols * q / n_slices, hi = n_cols * (q + 1) / n_slices;
+    cudaStreamAttrValue attr = {};
+    attr.accessPolicyWindow.base_ptr = const_cast<int32_t*>(cmap + lo);
+    attr.accessPolicyWindow.num_bytes = (size_t)(hi - lo) * 4;
+    attr.accessPolicyWindow.hitRatio = 1.0f;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    SME_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &attr));
+    k_map_cols_slice<<<grid, 256, 0, s>>>(nnz, col, cmap, mapped, (int32_t)lo, (int32_t)hi);
+    SME_CHECK_LAUNCH("k_map_cols_slice");
+  }
+  cudaStreamAttrValue clear = {};
+  SME_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &clear));
+  return SME_OK;
+}
+
 SME_API int sme_row_stats(int64_t n_rows, const int32_t* row_ptr, int64_t* out, sme_stream_t stream) {
   cudaStream_t s = as_stream(stream);
   SME_CUDA(cudaMemsetAsync(out, 0, 16, s));

@@ -322,6 +322,31 @@ def _permute_coo(m: CooMatrix, p_r: Permutation | None, p_c: Permutation | None)
     return CooMatrix._from_device(m.n_rows, m.n_cols, row, col, m.d_values.clone(), csr_thunk=thunk)
 
 
+#: K4 pre-maps the columns in L2-resident slices of p_c when p_c exceeds this share of L2
+#: and the matrix has at least PREMAP_MIN_NNZ entries (0 disables the pre-map).  Off: at
+#: C4 it measured 31.6 ms against 22.4 ms for the in-sort gather (tools/k4_premap_ab.py;
+#: four full passes over col plus scattered 4-byte writes cost more than the DRAM misses
+#: they remove).  Results are bit-identical either way.
+PREMAP_L2_SHARE = 0.0
+PREMAP_MIN_NNZ = 1 << 26
+
+
+def _premap_slices(m: CsrMatrix) -> int:
+    """Number of column slices for the pre-map (0: gather p_c inside the row sort)."""
+    if not PREMAP_L2_SHARE or m.nnz < PREMAP_MIN_NNZ or m.d_col_idx.data_ptr() % 16:
+        return 0
+    from .panels import device_info
+
+    info = device_info()
+    table = m.n_cols * 4
+    if table <= PREMAP_L2_SHARE * info["l2"]:
+        return 0
+    slice_cap = min(info["max_persisting_l2"], info["l2"] // 2)
+    n = -(-table // slice_cap)
+    _lib.call("sme_l2_set_persisting", min(info["max_persisting_l2"], -(-table // n)))
+    return int(n)
+
+
 @_cuda.nvtx("permute_csr")
 def permute_csr(m: CsrMatrix, p_r: Permutation | None, p_c: Permutation | None) -> CsrMatrix:
     """P_r A P_c directly on CSR (K4): row gather through inverse(p_r), column remap
@@ -346,10 +371,21 @@ def permute_csr(m: CsrMatrix, p_r: Permutation | None, p_c: Permutation | None) 
     col = torch.empty_like(m.d_col_idx)
     val = torch.empty_like(m.d_values)
     fl = DeviceFlags()
+    src_col, cmap = m.d_col_idx, (p_c.d_forward if p_c is not None else None)
+    n_slices = _premap_slices(m) if cmap is not None else 0
+    if n_slices:
+        # p_c larger than L2: relabel the columns first in L2-resident slices of p_c, so
+        # the row sort reads new column ids instead of gathering p_c from DRAM
+        src_col = torch.empty_like(m.d_col_idx)
+        _lib.call("sme_map_cols_sliced", m.nnz, m.n_cols, ptr(m.d_col_idx), ptr(cmap), ptr(src_col), n_slices,
+                  stream())
+        _lib.call("sme_l2_reset_persisting")
+        cmap = None
     _lib.call("sme_permute_csr", _cuda.sme_dtype(m.d_values), m.n_rows, m.n_cols, m.nnz, ptr(m.d_row_ptr),
-              ptr(m.d_col_idx), ptr(m.d_values), ptr(inv_r), ptr(p_c.d_forward if p_c is not None else None),
+              ptr(src_col), ptr(m.d_values), ptr(inv_r), ptr(cmap),
               ptr(row_ptr), ptr(col), ptr(val), ptr(ws2), ws2.numel(), long_nnz, fl.flag_ptr, fl.dup_ptr,
               stream())
+    del src_col
     out = CsrMatrix._from_device(m.n_rows, m.n_cols, row_ptr, col, val)
     out._cache["long_nnz"] = long_nnz
     return out
