@@ -401,3 +401,25 @@ def test_panel_layout_matches_oracle(dev, rng, n_panels):
     m._cache["n_panels"] = n_panels
     want = O.spmv_csr(ptr, col, val, x)
     assert O.relative_error(P.spmv_csr(m, x, "panel"), want) <= F64_TOL
+
+
+def test_permute_csr_premap_path_is_bit_identical(dev, rng):
+    """K4 with the column-sliced pre-map forced on (sme_map_cols_sliced, off by default)
+    builds the same permuted CSR, bit for bit, as the in-sort gather."""
+    import paper_2308_00106_b200.permute as PM
+
+    n = 20_000
+    mask = rng.random((400, n)) < 0.01
+    rows, cols = np.nonzero(mask)
+    m = P.coo_to_csr(P.CooMatrix(400, n, rows, cols, rng.random(rows.size)))
+    p_r, p_c = P.random_permutation(400, 3), P.random_permutation(n, 4)
+    saved = PM.PREMAP_L2_SHARE, PM.PREMAP_MIN_NNZ
+    try:
+        PM.PREMAP_L2_SHARE, PM.PREMAP_MIN_NNZ = 1e-9, 0
+        a = P.permute_csr(m, p_r, p_c)
+        PM.PREMAP_L2_SHARE = 0.0
+        b = P.permute_csr(m, p_r, p_c)
+    finally:
+        PM.PREMAP_L2_SHARE, PM.PREMAP_MIN_NNZ = saved
+    assert np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.col_idx, b.col_idx)
+    assert np.array_equal(a.values.view(np.uint64), b.values.view(np.uint64))
