@@ -120,7 +120,11 @@ int sme_pcg64_swap_partners_to_device(uint64_t* st, int64_t n, int32_t* d_j, int
  * the windows and writes d_j.  n >= 2.  Returns SME_OK, or 1 if a window check failed
  * (odds ~1e-30; st untouched, replay on the host instead).  HOST call that
  * synchronises `stream`. */
-int sme_pcg64_swap_partners_gpu(uint64_t* st, int64_t n, int32_t* d_j, sme_stream_t stream);
+int sme_pcg64_swap_partners_gpu_workspace_size(int64_t n, size_t* bytes);
+/* d_ws: optional caller scratch of sme_pcg64_swap_partners_gpu_workspace_size bytes (NULL:
+ * allocated stream-ordered inside). */
+int sme_pcg64_swap_partners_gpu(uint64_t* st, int64_t n, int32_t* d_j, void* d_ws, size_t ws_bytes,
+                                sme_stream_t stream);
 /* The swaps of that shuffle on the GPU (shuffle.cu): d_perm = the permutation
  * a = arange(n); for i = n-1..1: swap(a[i], a[d_j[i]]) builds — computed as a
  * bucket sort of the steps by partner, a link pass and a chain walk (no dependent

@@ -40,7 +40,8 @@ SIGNATURES: dict[str, list] = {
     "sme_host_pcg64_permutation": [p, i64, p],
     "sme_host_pcg64_swap_partners": [p, i64, p, C.c_int],
     "sme_pcg64_swap_partners_to_device": [p, i64, p, C.c_int, p],
-    "sme_pcg64_swap_partners_gpu": [p, i64, p, p],
+    "sme_pcg64_swap_partners_gpu_workspace_size": [i64, psz],
+    "sme_pcg64_swap_partners_gpu": [p, i64, p, p, sz, p],
     "sme_fy_apply_workspace_size": [i64, psz],
     "sme_fy_apply": [i64, p, p, p, sz, p],
     "sme_host_mm_parse": [p, i64, C.c_int, i64, i64, i64, i64, C.c_int, C.c_int, p, p, p, p],

@@ -330,7 +330,32 @@ using namespace sme;
 // the full shuffle leaves it.  Returns SME_OK, or 1 when a window check failed (nothing
 // usable written; st untouched) so the caller replays on the host.  HOST call that
 // synchronises `stream` (the ambiguous draws go to the host and back).
-SME_API int sme_pcg64_swap_partners_gpu(uint64_t* st, int64_t n, int32_t* d_j, sme_stream_t stream) {
+namespace sme {
+namespace {
+// bytes of the n-dependent scratch (the draws, windows, bases, counts)
+size_t gg_scratch_bytes(int64_t n, int64_t* n_blocks_out) {
+  const StepGrid sg = step_grid(n);
+  const int64_t t_max = (int64_t)std::ceil(sg.thi.back()) + GG_BLK;
+  const int64_t n_blocks = (t_max + GG_BLK - 1) / GG_BLK;
+  if (n_blocks_out) *n_blocks_out = n_blocks;
+  const size_t b_U = align_up((size_t)(n_blocks * GG_BLK) * 4), b_w = align_up((size_t)n_blocks * 8),
+               b_c = align_up((size_t)n_blocks * 4);
+  const int64_t amb_cap = n_blocks * GG_BLK / 16;  // ambiguous draws held in the caller's scratch
+  return b_U + 4 * b_w + 2 * b_c + 256 + 3 * align_up((size_t)amb_cap * 4 + 4) + align_up((size_t)amb_cap + 1);
+}
+}  // namespace
+}  // namespace sme
+
+// Scratch of sme_pcg64_swap_partners_gpu for size n (pass a buffer this large to skip
+// the stream-ordered allocation inside; the few ambiguous draws still use one).
+SME_API int sme_pcg64_swap_partners_gpu_workspace_size(int64_t n, size_t* bytes) {
+  SME_REQUIRE(bytes && n >= 2 && n < INT32_MAX, "bad arguments (n=%lld)", (long long)n);
+  *bytes = gg_scratch_bytes(n, nullptr);
+  return SME_OK;
+}
+
+SME_API int sme_pcg64_swap_partners_gpu(uint64_t* st, int64_t n, int32_t* d_j, void* d_ws, size_t ws_bytes,
+                                        sme_stream_t stream) {
   SME_REQUIRE(st && d_j && n >= 2 && n < INT32_MAX, "bad arguments (n=%lld)", (long long)n);
   cudaStream_t s = as_stream(stream);
   const bool dbg = std::getenv("SME_GG_DEBUG") != nullptr;
@@ -355,7 +380,12 @@ SME_API int sme_pcg64_swap_partners_gpu(uint64_t* st, int64_t n, int32_t* d_j, s
   // device buffers (one allocation)
   const size_t b_U = align_up((size_t)g.T * 4), b_w = align_up((size_t)n_blocks * 8), b_c = align_up((size_t)n_blocks * 4);
   char* ws = nullptr;
-  SME_CUDA(cudaMallocAsync((void**)&ws, b_U + 4 * b_w + 2 * b_c + 256, s));
+  const size_t ws_need = b_U + 4 * b_w + 2 * b_c + 256;
+  const bool own_ws = !(d_ws && ws_bytes >= ws_need);
+  if (own_ws)
+    SME_CUDA(cudaMallocAsync((void**)&ws, ws_need, s));
+  else
+    ws = (char*)d_ws;
   uint32_t* U = (uint32_t*)ws;
   int64_t* d_wlo = (int64_t*)(ws + b_U);
   int64_t* d_whi = (int64_t*)(ws + b_U + b_w);
@@ -365,7 +395,7 @@ SME_API int sme_pcg64_swap_partners_gpu(uint64_t* st, int64_t n, int32_t* d_j, s
   int32_t* d_amb = (int32_t*)(ws + b_U + 4 * b_w + b_c);
   int* d_bad = (int*)(ws + b_U + 4 * b_w + 2 * b_c);
   auto fail = [&](int rc) {
-    cudaFreeAsync(ws, s);
+    if (own_ws) cudaFreeAsync(ws, s);
     return rc;
   };
   SME_CUDA(cudaMemcpyAsync(d_wlo, wlo.data(), (size_t)n_blocks * 8, cudaMemcpyHostToDevice, s));
@@ -388,13 +418,17 @@ SME_API int sme_pcg64_swap_partners_gpu(uint64_t* st, int64_t n, int32_t* d_j, s
   }
   char* aws = nullptr;
   const size_t b_a = align_up((size_t)n_amb * 4 + 4), b_ad = align_up((size_t)n_amb + 1);
-  SME_CUDA(cudaMallocAsync((void**)&aws, 3 * b_a + b_ad, s));
+  const bool own_aws = own_ws || ws_bytes < ws_need + 3 * b_a + b_ad;  // the caller's scratch holds them
+  if (own_aws)
+    SME_CUDA(cudaMallocAsync((void**)&aws, 3 * b_a + b_ad, s));
+  else
+    aws = ws + ws_need;
   uint32_t* d_at = (uint32_t*)aws;
   uint32_t* d_acr = (uint32_t*)(aws + b_a);
   uint32_t* d_au = (uint32_t*)(aws + 2 * b_a);
   uint8_t* d_dec = (uint8_t*)(aws + 3 * b_a);
   auto fail2 = [&](int rc) {
-    cudaFreeAsync(aws, s);
+    if (own_aws) cudaFreeAsync(aws, s);
     return fail(rc);
   };
   SME_CUDA(cudaMemcpyAsync(d_base1, cr_base.data(), (size_t)n_blocks * 8, cudaMemcpyHostToDevice, s));

@@ -188,7 +188,12 @@ def pcg64_swap_partners_device(bitgen: np.random.PCG64, n: int, threads: int = 0
     cs.wait_stream(torch.cuda.current_stream(dev))  # d_j's allocation is ordered before the copies
     words = _pcg64_words(bitgen)
     if n >= (GPU_PARTNERS_MIN if gpu_min is None else gpu_min) and n >= 2:
-        rc = _lib.load().sme_pcg64_swap_partners_gpu(words.ctypes.data, n, ptr(d_j), cs.cuda_stream)
+        # scratch from torch's caching allocator (warm after the matrix build): no
+        # driver-level allocation inside the call
+        ws = _cuda.workspace(_lib.query_size("sme_pcg64_swap_partners_gpu_workspace_size", n))
+        rc = _lib.load().sme_pcg64_swap_partners_gpu(words.ctypes.data, n, ptr(d_j), ptr(ws), ws.numel(),
+                                                     cs.cuda_stream)
+        ws.record_stream(cs)
         if rc == _lib.SME_OK:
             _set_pcg64_words(bitgen, words)
             torch.cuda.current_stream(dev).wait_stream(cs)
