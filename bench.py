@@ -198,23 +198,220 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline_run(ptr, col, val, x, steps: int, warmup: int) -> dict:
-    """The reference algorithm (oracle numpy port of kernels.py:59-128) on the host cores."""
+def ref_module():
+    """The UNMODIFIED reference package installed in baseline/_ref (baseline/install_ref.sh),
+    or None when it is absent.  Timed as the CPU baseline ("kind": "reference");
+    the oracle port stands in when it is missing ("kind": "port")."""
+    p = ROOT / "baseline" / "_ref"
+    if not (p / "spmv_entropy" / "__init__.py").is_file():
+        return None
+    if str(p) not in sys.path:
+        sys.path.insert(0, str(p))
+    try:
+        import spmv_entropy  # noqa: F401
+        import spmv_entropy.entropy
+        import spmv_entropy.kernels
+        import spmv_entropy.matio
+        import spmv_entropy.permute
+    except Exception as e:  # pragma: no cover - a broken install falls back to the port
+        log(f"[bench] baseline/_ref present but not importable ({e}); using the oracle port")
+        return None
+    return spmv_entropy
+
+
+def cpu_baseline_run(ptr, col, val, x, n_cols: int, steps: int, warmup: int) -> dict:
+    """The reference's CSR SpMV on the host cores over a row sample: the real
+    reference (baseline/_ref: spmv_entropy.kernels.spmv_csr_parallel on a reference
+    CsrMatrix, kernels.py:102-128) when installed, else the oracle numpy port of
+    kernels.py:59-128.  Returns the rates and the last output (a parity input)."""
     import oracle as O
 
     cores = os.cpu_count() or 1
     nnz = int(ptr[-1])
+    ref = ref_module()
+    if ref is not None:
+        m = ref.matio.CsrMatrix(int(ptr.size - 1), int(n_cols), ptr, col, val)
+        par_fn = lambda: ref.kernels.spmv_csr_parallel(m, x, cores)  # noqa: E731
+        ser_fn = lambda: ref.kernels.spmv_csr(m, x)  # noqa: E731
+        kind, impl = "reference", "baseline/_ref spmv_entropy.kernels.spmv_csr_parallel (unmodified reference)"
+    else:
+        par_fn = lambda: O.spmv_csr_parallel(ptr, col, val, x, cores)  # noqa: E731
+        ser_fn = lambda: O.spmv_csr(ptr, col, val, x)  # noqa: E731
+        kind, impl = "port", "oracle numpy port of kernels.py:59-128 (baseline/_ref not installed)"
     for _ in range(warmup):
-        O.spmv_csr_parallel(ptr, col, val, x, cores)
+        par_fn()
     t = time.perf_counter()
     for _ in range(steps):
-        O.spmv_csr_parallel(ptr, col, val, x, cores)
+        y = par_fn()
     par = (time.perf_counter() - t) / steps
     t = time.perf_counter()
-    O.spmv_csr(ptr, col, val, x)
+    ser_fn()
     ser = time.perf_counter() - t
     return {"gflops_parallel": 2 * nnz / par / 1e9, "gflops_serial": 2 * nnz / ser / 1e9, "cores": cores,
-            "sec_per_call_parallel": par, "nnz": nnz}
+            "sec_per_call_parallel": par, "nnz": nnz, "kind": kind, "impl": impl, "y": y}
+
+
+# ---------------------------------------------------------------------------
+# full-scale parity (VERDICT r1 item 1): oracle rows of the permuted matrix
+# ---------------------------------------------------------------------------
+PARITY_RANDOM_ROWS = 10_000
+PERM_SAMPLE_NNZ = 4_000_000  # the reference permute/histogram timing sample
+
+
+def sample_rows(n_rows: int, nnz: int, seed: int = 2308, target_nnz: int = CPU_SAMPLE_NNZ,
+                n_random: int = PARITY_RANDOM_ROWS) -> tuple[int, np.ndarray]:
+    """The parity / CPU-baseline row sample: the first R rows (about target_nnz
+    nonzeros) plus n_random seeded random rows from the rest, ascending."""
+    R = max(1, min(n_rows, int(n_rows * target_nnz / max(1, nnz))))
+    extra = np.empty(0, dtype=np.int64)
+    if n_rows > R:
+        rng = np.random.default_rng(seed)
+        extra = np.unique(rng.integers(R, n_rows, size=min(n_random, n_rows - R)))
+    return R, np.concatenate([np.arange(R, dtype=np.int64), extra])
+
+
+def gather_rows_host(ptr, col, val, rows):
+    """Rows `rows` of a host CSR as a new CSR (ptr int64, col, val)."""
+    ptr = np.asarray(ptr, dtype=np.int64)
+    s, e = ptr[rows], ptr[rows + 1]
+    lens = e - s
+    out = np.zeros(rows.size + 1, dtype=np.int64)
+    np.cumsum(lens, out=out[1:])
+    idx = np.repeat(s - out[:-1], lens) + np.arange(out[-1], dtype=np.int64)
+    return out, col[idx], val[idx]
+
+
+def device_rows(M, rows: np.ndarray):
+    """Rows `rows` of a device CsrMatrix, copied to the host (ptr int64, col int64, val)."""
+    import torch
+
+    dev = M.d_row_ptr.device
+    r = torch.from_numpy(rows).to(dev)
+    s = M.d_row_ptr[r].to(torch.int64)
+    lens = M.d_row_ptr[r + 1].to(torch.int64) - s
+    out = torch.zeros(rows.size + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(lens, 0, out=out[1:])
+    total = int(out[-1])
+    idx = torch.repeat_interleave(s - out[:-1], lens, output_size=total) + torch.arange(total, device=dev)
+    return (out.cpu().numpy(), M.d_col_idx[idx].to(torch.int64).cpu().numpy(), M.d_values[idx].cpu().numpy())
+
+
+def oracle_sample(cfg: dict, fr: np.ndarray, fc: np.ndarray, rows: np.ndarray, A=None):
+    """Rows `rows` of coo_to_csr(permute_matrix(A, fr, fc)) built on the host by the
+    oracle (oracle.permute_csr_rows vectorised): new row r
+    is original row inv(fr)[r], its columns mapped through fc and sorted, values
+    following.  Original rows come from the oracle's restatement of the generator
+    (C4: O.random_rows_fast; C2/C5: O.laplacian5), for C3 from the device-built A
+    (an input, not the path under test).  Returns (ptr, col int64, val) with val in
+    the matrix dtype."""
+    import oracle as O
+
+    old = O.inverse(fr)[rows]
+    if cfg["kind"] == "random_rows":
+        from paper_2308_00106_b200.synth import C4_SEED
+
+        k = cfg["k"]
+        cols, vals = O.random_rows_fast(old, cfg["n"], k, C4_SEED)
+        ptr0 = np.arange(rows.size + 1, dtype=np.int64) * k
+        col0, val0 = cols.ravel(), vals.ravel()
+    elif cfg["kind"] == "laplacian":
+        ptr_a, col_a, val_a = O.laplacian5(cfg["g"])
+        ptr0, col0, val0 = gather_rows_host(ptr_a, col_a, val_a, old)
+    else:
+        ptr0, col0, val0 = device_rows(A, old)
+    mapped = fc[col0]
+    rid = np.repeat(np.arange(rows.size, dtype=np.int64), np.diff(ptr0))
+    order = np.lexsort((mapped, rid))
+    vdt = np.float32 if cfg.get("dtype") == "f32" else np.float64
+    return ptr0, mapped[order], np.asarray(val0, dtype=vdt)[order]
+
+
+def oracle_x(n: int, fc: np.ndarray, f32: bool) -> np.ndarray:
+    """x' = permute_vector(input_vector(0, n), p_c) (bench.py:168-171, 211), f32-rounded
+    and widened for an f32 matrix (the f32 oracle sees the kernel's inputs)."""
+    import oracle as O
+
+    x = O.input_vector(0, n)
+    if f32:
+        x = x.astype(np.float32).astype(np.float64)
+    return O.permute_vector(x, fc)
+
+
+def parity_full_scale(cfg: dict, B, p_r, p_c, y_dev, fr_np, fc_np, rows, sample, x_np, tol: float,
+                      y_cpu=None, R: int = 0) -> dict:
+    """Compare the timed kernel's y and K4's permuted CSR with the oracle at full
+    scale: the permutations against numpy's Generator.permutation (all n entries),
+    the sampled rows of B bit-exact (row lengths, columns, value bits), and y on the
+    sampled rows against the oracle SpMV (relative_error, kernels.py:131-142) at
+    `tol`.  Raises SystemExit on any mismatch."""
+    import oracle as O
+    import torch
+
+    perms_ok = bool(np.array_equal(p_r.forward, fr_np) and np.array_equal(p_c.forward, fc_np))
+    ptr_o, col_o, val_o = sample
+    ptr_d, col_d, val_d = device_rows(B, rows)
+    csr_ok = bool(np.array_equal(ptr_o, ptr_d) and np.array_equal(col_o, col_d)
+                  and np.array_equal(val_o.view(np.uint8), np.ascontiguousarray(val_d).view(np.uint8)))
+    y_o = O.spmv_csr(ptr_o, col_o, val_o.astype(np.float64), x_np)
+    y_g = y_dev[torch.from_numpy(rows).to(y_dev.device)].to(torch.float64).cpu().numpy()
+    err = O.relative_error(y_g, y_o)
+    out = {"rows_checked": int(rows.size), "nnz_checked": int(ptr_o[-1]),
+           "rows": f"rows [0, {R:,}) + {rows.size - R:,} seeded random rows of the permuted matrix",
+           "perms_bitexact_vs_numpy": perms_ok, "csr_rows_bitexact": csr_ok,
+           "max_rel_err": err, "tol": tol,
+           "oracle": "oracle/ restatement: numpy Generator.permutation perms, generator rows, p_c map + sort "
+                     "(App. A item 4), numpy reduceat SpMV (kernels.py:59-70)"}
+    if y_cpu is not None:  # the cpu_baseline leg's own output on rows [0, R)
+        out["cpu_baseline_y_bitwise_vs_oracle"] = bool(np.array_equal(np.asarray(y_cpu), y_o[:R]))
+    if not (perms_ok and csr_ok and err <= tol and out.get("cpu_baseline_y_bitwise_vs_oracle", True)):
+        raise SystemExit(f"full-scale parity FAILED: {out}")
+    return out
+
+
+def cpu_permute_hist_baseline(cfg: dict, sample, n_cols: int, fc: np.ndarray) -> dict | None:
+    """the reference's permute_matrix + coo_to_csr (permute.py:98-102,
+    matio.py:281-294) and histogram_2d + shannon_entropy (entropy.py:96-119) timed on
+    the host over a bounded sample of the workload's rows (the first rows of the
+    oracle sample; a random row permutation of the sample, the full p_c)."""
+    import oracle as O
+
+    ptr, col, val = sample
+    nr = int(np.searchsorted(ptr, PERM_SAMPLE_NNZ, side="right")) - 1
+    nr = max(1, min(nr, ptr.size - 1))
+    nz = int(ptr[nr])
+    rows = np.repeat(np.arange(nr, dtype=np.int64), np.diff(ptr[: nr + 1]))
+    ref = ref_module()
+    pr = O.random_permutation(nr, O.axis_seed(PERM_SEED, 0))
+    t = {}
+    if ref is not None:
+        R = ref
+        coo = R.matio.CooMatrix(nr, n_cols, rows, col[:nz], val[:nz].astype(np.float64))
+        Pr, Pc = R.permute.Permutation(pr), R.permute.Permutation(fc)
+        t0 = time.perf_counter()
+        pm = R.permute.permute_matrix(coo, Pr, Pc)
+        csr = R.matio.coo_to_csr(pm)
+        t["permute_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        bins = (min(128, nr), min(128, n_cols))
+        H = R.entropy.shannon_entropy(R.entropy.histogram_2d(pm, *bins))
+        t["hist_s"] = time.perf_counter() - t0
+        kind = "reference"
+        del csr
+    else:
+        t0 = time.perf_counter()
+        r2, c2 = O.permute_coo(rows, col[:nz], pr, fc)
+        O.coo_to_csr(nr, r2, c2, val[:nz])
+        t["permute_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        bins = (min(128, nr), min(128, n_cols))
+        H = O.entropy_of_counts(O.histogram_2d_counts(r2, c2, nr, n_cols, *bins))
+        t["hist_s"] = time.perf_counter() - t0
+        kind = "port"
+    return {"kind": kind, "cores": 1, "sample": f"{nr:,} rows x {n_cols:,} cols, {nz:,} nnz of the workload",
+            "permute_matrix_plus_coo_to_csr_s": round(t["permute_s"], 4),
+            "permute_nnz_per_s": round(nz / t["permute_s"], 1),
+            "histogram_2d_plus_entropy_s": round(t["hist_s"], 4),
+            "hist_nnz_per_s": round(nz / t["hist_s"], 1), "entropy_bits": H}
 
 
 # ---------------------------------------------------------------------------
@@ -222,25 +419,13 @@ def cpu_baseline_run(ptr, col, val, x, steps: int, warmup: int) -> dict:
 # ---------------------------------------------------------------------------
 def run_reference(args, cfg) -> dict:
     """Bounded sample of the permuted workload, built on the host with the oracle's
-    restatements (generator, permutation, row gather + column sort), timed with the
-    reference's parallel CSR algorithm on all host cores."""
+    restatements (numpy Generator.permutation, generator rows, row gather + column
+    sort), timed with the reference's parallel CSR SpMV on all host cores: the
+    unmodified reference from baseline/_ref when installed, else the oracle port."""
     import oracle as O
 
     t0 = time.perf_counter()
-    if cfg["kind"] == "random_rows":
-        n = cfg["n"]
-        fr, fc = host_perms(n, n, native=False)
-        inv_r = O.inverse(fr)
-        R = cpu_sample_rows(n, n * cfg["k"])
-        old = inv_r[:R]
-        cols, vals = O.random_rows_fast(old, n, cfg["k"], 0x5EED_C4)
-        cols = fc[cols]
-        order = np.argsort(cols, axis=1)
-        cols = np.take_along_axis(cols, order, axis=1)
-        vals = np.take_along_axis(vals, order, axis=1)
-        ptr = np.arange(R + 1, dtype=np.int64) * cfg["k"]
-        col, val = cols.ravel(), vals.ravel()
-    elif cfg["kind"] == "rmat":
+    if cfg["kind"] == "rmat":
         # bounded sample: the same construction at scale 20 (1/16 of C3), row+col permuted
         sc = 20
         ptr0, col0, val0 = O.rmat_csr(sc, cfg["ef"], 0.57, 0.19, 0.19, 0x5EED_C3, cfg["cap"])
@@ -250,32 +435,27 @@ def run_reference(args, cfg) -> dict:
         pr, pc = O.permute_coo(O.csr_to_coo_rows(ptr0), col0, fr, fc)
         ptr, col, val = O.coo_to_csr(n, pr, pc, val0)
         R = n
+        x = oracle_x(n, fc, f32=True)
     else:
-        g = cfg["g"]
-        n = g * g
+        n = cfg["n"] if cfg["kind"] == "random_rows" else cfg["g"] ** 2
+        nnz = n * cfg["k"] if cfg["kind"] == "random_rows" else 5 * n - 4 * cfg["g"]
         fr, fc = host_perms(n, n, native=False)
-        ptr0, col0, val0 = O.laplacian5(g)
-        R = cpu_sample_rows(n, int(ptr0[-1]))
-        rows = np.arange(R)
-        got = O.permute_csr_rows(ptr0, col0, val0, fr, fc, rows)
-        lens = np.array([c.size for c, _ in got])
-        ptr = np.zeros(R + 1, dtype=np.int64)
-        np.cumsum(lens, out=ptr[1:])
-        col = np.concatenate([c for c, _ in got])
-        val = np.concatenate([v for _, v in got])
-    x = O.permute_vector(O.input_vector(0, n), fc)
+        R = cpu_sample_rows(n, nnz)
+        ptr, col, val = oracle_sample(cfg, fr, fc, np.arange(R, dtype=np.int64))
+        val = val.astype(np.float64)
+        x = oracle_x(n, fc, f32=False)
     log(f"[bench-ref] sample of {R:,} rows / {int(ptr[-1]):,} nnz built in {time.perf_counter() - t0:.1f}s")
-    res = cpu_baseline_run(ptr, col, val, x, args.steps, args.warmup)
+    res = cpu_baseline_run(ptr, col, val, x, n, args.steps, args.warmup)
     v = res["gflops_parallel"]
     sample = (f"rows [0, {R:,}) of the permuted matrix ({res['nnz']:,} nnz) with the full permuted x; "
-              f"reference algorithm (numpy reduceat, row-partitioned thread pool) on {res['cores']} threads")
+              f"{res['impl']} on {res['cores']} threads")
     return {
         "metric": METRIC, "value": round(v, 4), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(res["sec_per_call_parallel"] * 1e3, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg.get("dtype", "f64"),
         "data": "synthetic", "impl": "reference",
         "config": {"workload": cfg["workload"], "sample": sample},
-        "cpu_baseline": {"value": round(v, 4), "unit": "GFLOP/s", "cores": res["cores"], "kind": "port",
+        "cpu_baseline": {"value": round(v, 4), "unit": "GFLOP/s", "cores": res["cores"], "kind": res["kind"],
                          "cpu_model": cpu_model(),
                          "sample": sample, "serial_gflops": round(res["gflops_serial"], 4)},
         "e2e": {"value": round(v, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -380,22 +560,32 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         raise SystemExit(f"permuted SpMV failed the {tol} round-trip check: {rel_err}")
     balance = {"unpermuted": load_balance(A.d_row_ptr, n), "permuted": load_balance(B.d_row_ptr, n)}
 
+    # the oracle side of the full-scale parity check (numpy perms, oracle-built sample
+    # rows of the permuted matrix, oracle x'); the CPU baseline times the same rows
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        R = cpu_sample_rows(n, nnz)
-        p1 = int(B.d_row_ptr[R])
-        ptr_h = B.d_row_ptr[: R + 1].cpu().numpy().astype(np.int64)
-        col_h = B.d_col_idx[:p1].cpu().numpy()
-        val_h = B.d_values[:p1].cpu().numpy().astype(np.float64)
-        x_h = xp.cpu().numpy().astype(np.float64)
-        cs = cpu_baseline_run(ptr_h, col_h, val_h, x_h, steps=5, warmup=1)
-        cpu = {"value": round(cs["gflops_parallel"], 4), "unit": "GFLOP/s", "cores": cs["cores"], "kind": "port",
-               "cpu_model": cpu_model(),
-               "sample": f"rows [0, {R:,}) of the permuted matrix ({cs['nnz']:,} nnz), full permuted x, "
-                         f"5 calls; reference algorithm (numpy reduceat, row-partitioned threads)",
-               "serial_gflops": round(cs["gflops_serial"], 4)}
-        log(f"[bench] cpu baseline: {cpu}")
-        del ptr_h, col_h, val_h, x_h
+    par_in = None
+    if rank == 0 and world == 1 and not args.no_parity:
+        t_par = time.perf_counter()
+        fr_np, fc_np = host_perms(n, A.n_cols, native=False)
+        R, rows = sample_rows(n, nnz)
+        sample = oracle_sample(cfg, fr_np, fc_np, rows, A)
+        x_np = oracle_x(A.n_cols, fc_np, f32=(B.dtype == torch.float32))
+        par_in = (fr_np, fc_np, R, rows, sample, x_np)
+        log(f"[bench] oracle sample of {rows.size:,} rows built in {time.perf_counter() - t_par:.1f}s")
+        if not args.no_cpu:
+            ptr_s, col_s, val_s = sample
+            cs = cpu_baseline_run(ptr_s[: R + 1], col_s[: ptr_s[R]], val_s[: ptr_s[R]].astype(np.float64), x_np,
+                                  A.n_cols, steps=5, warmup=1)
+            cpu = {"value": round(cs["gflops_parallel"], 4), "unit": "GFLOP/s", "cores": cs["cores"],
+                   "kind": cs["kind"], "cpu_model": cpu_model(),
+                   "sample": f"rows [0, {R:,}) of the permuted matrix ({cs['nnz']:,} nnz), full permuted x, "
+                             f"5 calls; {cs['impl']}",
+                   "serial_gflops": round(cs["gflops_serial"], 4), "_y": cs["y"]}
+            try:
+                cpu["permute_and_histogram"] = cpu_permute_hist_baseline(cfg, sample, A.n_cols, fc_np)
+            except MemoryError:
+                cpu["permute_and_histogram"] = None
+            log(f"[bench] cpu baseline: { {k: v for k, v in cpu.items() if k != '_y'} }")
 
     def timed(matrix, xv, kernel: str, steps: int, warmup: int, shard=None, chunk=None, preload_s: float = 0.0):
         """Device-timed loop: per-step events on the launching stream + whole-region events."""
@@ -433,6 +623,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
             tt = torch.tensor([total], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             total = float(tt.item())
+        timed.last_y = y
         return total, per
 
     from paper_2308_00106_b200.kernels import auto_kernel
@@ -456,6 +647,13 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         clocks.start()
         total_ms, per = timed(B, xp, args.kernel, args.steps, args.warmup, preload_s=1.0)
         clk = clocks.stop()
+        parity = None
+        if par_in is not None:  # the timed loop's own output against the oracle
+            fr_np, fc_np, R, rows, sample, x_np = par_in
+            parity = parity_full_scale(cfg, B, p_r, p_c, timed.last_y, fr_np, fc_np, rows, sample, x_np, tol,
+                                       y_cpu=None if cpu is None else cpu.pop("_y"), R=R)
+            log(f"[bench] parity: {parity}")
+            del par_in, sample
         un_total, un_per = timed(A, x, args.kernel, args.steps, args.warmup)
         # the same comparison with the two matrices alternating step by step (no clock/thermal drift
         # between two separate loops): medians of per-step events
@@ -479,31 +677,6 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         ot_total = None
         nnz_total = nnz
         bytes_step = spmv_bytes(n, A.n_cols, nnz, B.d_values.element_size(), 4)
-    else:
-        plan = rowshard.ShardPlan(n, n, world)
-        shard = rowshard.RowShardedSpMV(B, plan, rank, args.kernel)
-        if shard.seg is not None:  # the shard's own panels (aligned to the ranks' x slots)
-            resolved, kernels_per_step = "seg", shard.seg.n_panels
-        c0, c1 = plan.col_range(rank)
-        chunk = plan.pad_slice(xp[c0:c1])
-        lo_r, hi_r = plan.row_range(rank)
-        y_ref_slice = y_perm[lo_r:hi_r].clone()
-        del A, B
-        torch.cuda.empty_cache()
-        # the sharded step (all-gather + local SpMV) must reproduce this rank's rows
-        shard_err = P.relative_error(shard.step(chunk), y_ref_slice)
-        if shard_err > tol:
-            raise SystemExit(f"rank {rank}: sharded SpMV differs from the 1-GPU result: {shard_err}")
-        log(f"[bench] rank {rank}: sharded rows [{lo_r}, {hi_r}) rel err vs 1-GPU {shard_err:.2e}")
-        clocks = Clocks(torch.cuda.current_device())
-        clocks.start()
-        total_ms, per = timed(shard.local, None, args.kernel, args.steps, args.warmup, shard=shard, chunk=chunk,
-                              preload_s=1.0)
-        clk = clocks.stop()
-        un_total = ot_total = None
-        un_per = inter = None
-        nnz_total = nnz
-        bytes_step = spmv_bytes(shard.local.n_rows, plan.world * plan.pad, shard.nnz, 8, 4)
 
     ms_per_step = total_ms / args.steps
     gflops = 2 * nnz_total / (ms_per_step * 1e-3) / 1e9
@@ -592,31 +765,6 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
                "single_call": {"api": "paper_2308_00106_b200.spmv_csr(CsrMatrix, pinned host tensor)",
                                "ms_per_step": round(single_ms, 4),
                                "value": round(2 * nnz / (single_ms * 1e-3) / 1e9, 4)}}
-    else:
-        # every rank: pinned host x chunk -> device, all-gather + local SpMV, y slice -> host
-        x_pin = torch.empty(plan.pad, dtype=shard.local.dtype, pin_memory=True)
-        x_pin.copy_(chunk.cpu())
-        y_pin = torch.empty(shard.local.n_rows, dtype=shard.local.dtype, pin_memory=True)
-        xc = torch.empty_like(chunk)
-        e_steps = max(3, min(args.steps, 10))
-        dist.barrier()
-        torch.cuda.synchronize()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record()
-        for _ in range(e_steps):
-            xc.copy_(x_pin, non_blocking=True)
-            yl = shard.step(xc)
-            y_pin.copy_(yl, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-        s1.record()
-        torch.cuda.synchronize()
-        et = torch.tensor([s0.elapsed_time(s1) / e_steps], device=dev)
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e_ms = float(et.item())
-        e2e = {"value": round(2 * nnz_total / (e_ms * 1e-3) / 1e9, 4), "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(x_pin.numel() * x_pin.element_size()) * world,
-               "d2h_bytes_per_step": int(nnz and n * y_pin.element_size()), "ms_per_step": round(e_ms, 4),
-               "api": "rowshard.RowShardedSpMV.step (pinned host x chunk in, y slice out, every rank)"}
 
     if rank != 0:
         return None
@@ -645,9 +793,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
             "kernel": resolved + (f" ({kernels_per_step} column panels x k_spmv_stream)" if resolved == "panel" else
                                  f" ({kernels_per_step} column panels x k_spmv_seg)" if resolved == "seg" else ""),
             "n_rows": n, "nnz": nnz,
-            "parallelism": ((f"row-shard x{world} + {dist.get_backend()} per-slot x broadcasts pipelined with the panel passes"
-                             if shard.pipelined else f"row-shard x{world} + {dist.get_backend()} all_gather of x")
-                            if world > 1 else "1 GPU"),
+            "parallelism": "1 GPU",
             "l2": "inputs (13 GB/pass for C4) far exceed the 126 MB L2; no flush needed" if cfg["kind"] == "random_rows"
                   else "x fits L2; matrix streams exceed L2",
         },
@@ -670,6 +816,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         "perm_gen_s": HOST_PERM_S.get("native"),
         "hist_ms": round(hist_ms, 3), "hist_warm_ms": round(hist_warm_ms, 3),
         "roundtrip_rel_err": rel_err,
+        "parity": parity,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_step,
@@ -684,6 +831,209 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         "gpu_launches": kernels_per_step * args.steps,
     }
     return out
+
+
+def build_shard(cfg: dict, plan, rank: int, p_r, p_c):
+    """This rank's rows [lo, hi) of the permuted matrix B = P_r A P_c, built without
+    any rank holding all of B: the original rows inverse(p_r)[lo:hi] (C4: generated
+    directly by the counter-based row generator; C2/C3/C5: gathered from A, which
+    is small for those configs), then K4 on them with the row order already final
+    (permute_csr(A_rows, None, p_c): columns through p_c, sorted within rows).
+    Bit-identical to rows [lo, hi) of permute_csr(A, p_r, p_c)."""
+    import torch
+
+    import paper_2308_00106_b200 as P
+    from paper_2308_00106_b200 import synth
+    from paper_2308_00106_b200.matio import CsrMatrix
+
+    lo, hi = plan.row_range(rank)
+    old = p_r.d_inverse[lo:hi]
+    A_full = None
+    if cfg["kind"] == "random_rows":
+        A_rows = synth.random_rows_select(old, cfg["n"], cfg["k"], seed=synth.C4_SEED)
+    else:
+        A_full = build_matrix(cfg)
+        dev = A_full.d_row_ptr.device
+        s = A_full.d_row_ptr[old.long()].long()
+        lens = A_full.d_row_ptr[old.long() + 1].long() - s
+        rp = torch.zeros(hi - lo + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(lens, 0, out=rp[1:])
+        tot = int(rp[-1])
+        idx = torch.repeat_interleave(s - rp[:-1], lens, output_size=tot) + torch.arange(tot, device=dev)
+        A_rows = CsrMatrix._from_device(hi - lo, A_full.n_cols, rp.to(torch.int32), A_full.d_col_idx[idx].contiguous(),
+                                        A_full.d_values[idx].contiguous())
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    B_loc = P.permute_csr(A_rows, None, p_c)
+    ev[1].record()
+    torch.cuda.synchronize()
+    return B_loc, ev[0].elapsed_time(ev[1]), A_full
+
+
+def run_sharded(args, cfg, rank: int, world: int) -> dict | None:
+    """N > 1: one rank per GPU (torch.distributed, NCCL), C4 strong-scaled.  Rank k
+    builds only its row shard of the permuted matrix (build_shard), checks it and
+    its SpMV rows against the oracle, then times the step of north_star (4): the x
+    exchange over NVLink (per-slot broadcasts pipelined with the seg panel passes,
+    or one all_gather) plus the local SpMV.  Time = max over ranks (device events)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2308_00106_b200 as P
+    from paper_2308_00106_b200 import rowshard
+    from paper_2308_00106_b200.bench import spmv_bytes
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n = cfg["n"] if cfg["kind"] == "random_rows" else (cfg["g"] ** 2 if cfg["kind"] == "laplacian" else 1 << cfg["scale"])
+    t0 = time.perf_counter()
+    p_r, p_c = device_perms(n, n)
+    plan = rowshard.ShardPlan(n, n, world)
+    B_loc, permute_ms, A_full = build_shard(cfg, plan, rank, p_r, p_c)
+    lo, hi = plan.row_range(rank)
+    nnz_loc = B_loc.nnz
+    log(f"[bench] rank {rank}/{world}: shard rows [{lo:,}, {hi:,}) nnz {nnz_loc:,} built in "
+        f"{time.perf_counter() - t0:.1f}s (K4 {permute_ms:.1f} ms)")
+    tol = 1e-12 if B_loc.dtype == torch.float64 else 1e-5
+    shard = rowshard.RowShardedSpMV(B_loc, plan, rank, args.kernel, local=True)
+    resolved = "seg" if shard.seg is not None else (args.kernel if args.kernel != "auto" else "vector")
+    kernels_per_step = shard.seg.n_panels if shard.seg is not None else 1
+    x = torch.from_numpy(P.input_vector(0, n)).to(dev, B_loc.dtype)
+    xp = P.permute_vector(x, p_c)
+    del x
+    c0, c1 = plan.col_range(rank)
+    chunk = plan.pad_slice(xp[c0:c1])
+    y_loc = shard.step(chunk).clone()
+    torch.cuda.synchronize()
+
+    # parity of this rank's rows against the oracle (sampled, bit-exact CSR, y at tol)
+    parity = None
+    if not args.no_parity:
+        fr_np, fc_np = host_perms(n, n, native=False)
+        R_loc, rows_loc = sample_rows(hi - lo, nnz_loc, seed=rank, target_nnz=max(1, CPU_SAMPLE_NNZ // (4 * world)),
+                                      n_random=max(1, PARITY_RANDOM_ROWS // world))
+        rows = rows_loc + lo
+        sample = oracle_sample(cfg, fr_np, fc_np, rows, A_full)
+        x_np = oracle_x(n, fc_np, f32=(B_loc.dtype == torch.float32))
+        import oracle as O
+
+        perms_ok = bool(np.array_equal(p_r.forward, fr_np) and np.array_equal(p_c.forward, fc_np))
+        ptr_d, col_d, val_d = device_rows(B_loc, rows_loc)
+        ptr_o, col_o, val_o = sample
+        csr_ok = bool(np.array_equal(ptr_o, ptr_d) and np.array_equal(col_o, col_d)
+                      and np.array_equal(val_o.view(np.uint8), np.ascontiguousarray(val_d).view(np.uint8)))
+        y_o = O.spmv_csr(ptr_o, col_o, val_o.astype(np.float64), x_np)
+        y_g = y_loc[torch.from_numpy(rows_loc).to(dev)].to(torch.float64).cpu().numpy()
+        err = O.relative_error(y_g, y_o)
+        res = torch.tensor([err, 0.0 if (perms_ok and csr_ok) else 1.0, float(rows.size)], dtype=torch.float64,
+                           device=dev)
+        dist.all_reduce(res[:2], op=dist.ReduceOp.MAX)
+        dist.all_reduce(res[2:], op=dist.ReduceOp.SUM)
+        parity = {"rows_checked": int(res[2].item()), "ranks": world, "max_rel_err": float(res[0].item()),
+                  "tol": tol, "csr_rows_bitexact": res[1].item() == 0.0, "perms_bitexact_vs_numpy": perms_ok,
+                  "rows": "per rank: the first rows of its shard + seeded random rows of its shard",
+                  "oracle": "oracle/ restatement (numpy perms, generator rows, p_c map + sort, numpy reduceat SpMV)"}
+        log(f"[bench] rank {rank}: shard parity err {err:.2e} csr {csr_ok} perms {perms_ok}")
+        if not (res[1].item() == 0.0 and res[0].item() <= tol):
+            raise SystemExit(f"rank {rank}: sharded parity FAILED: {parity}")
+        del sample, fr_np, fc_np, x_np
+    del A_full
+
+    steps, warmup = args.steps, args.warmup
+    clocks = Clocks(torch.cuda.current_device())
+    clocks.start()
+    t_end_pre = time.perf_counter() + 1.0
+    while time.perf_counter() < t_end_pre:  # keep the GPU loaded so the sampler sees the timed clocks
+        shard.step(chunk)
+        torch.cuda.synchronize()
+    for _ in range(warmup):
+        shard.step(chunk)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t_start.record()
+    for i in range(steps):
+        starts[i].record()
+        shard.step(chunk)
+        ends[i].record()
+    t_end.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    tt = torch.tensor([t_start.elapsed_time(t_end), statistics.mean(s.elapsed_time(e) for s, e in zip(starts, ends))],
+                      device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total_ms, kern_ms = float(tt[0].item()), float(tt[1].item())
+    nnz_t = torch.tensor([nnz_loc], dtype=torch.int64, device=dev)
+    dist.all_reduce(nnz_t)
+    nnz = int(nnz_t.item())
+    ms_per_step = total_ms / steps
+    gflops = 2 * nnz / (ms_per_step * 1e-3) / 1e9
+
+    # e2e: every rank copies its pinned host x chunk in and its y rows out each step
+    x_pin = torch.empty(plan.pad, dtype=B_loc.dtype, pin_memory=True)
+    x_pin.copy_(chunk.cpu())
+    y_pin = torch.empty(hi - lo, dtype=B_loc.dtype, pin_memory=True)
+    xc = torch.empty_like(chunk)
+    e_steps = max(3, min(steps, 10))
+    dist.barrier()
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(e_steps):
+        xc.copy_(x_pin, non_blocking=True)
+        yl = shard.step(xc)
+        y_pin.copy_(yl, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    s1.record()
+    torch.cuda.synchronize()
+    et = torch.tensor([s0.elapsed_time(s1) / e_steps], device=dev)
+    dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e_ms = float(et.item())
+    e2e_err = P.relative_error(y_pin, y_loc)
+    if e2e_err > tol:
+        raise SystemExit(f"rank {rank}: host-vector sharded step differs from the device result: {e2e_err}")
+    if rank != 0:
+        return None
+    bytes_loc = spmv_bytes(hi - lo, plan.world * plan.pad, nnz_loc, B_loc.d_values.element_size(), 4)
+    peak, peak_src = measured_peaks()
+    achieved = bytes_loc / (kern_ms * 1e-3) / 1e9
+    nccl_ver = ".".join(map(str, torch.cuda.nccl.version())) if dist.get_backend() == "nccl" else None
+    return {
+        "metric": METRIC, "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64" if B_dtype_is_f64(cfg) else "f32",
+        "data": "synthetic (device generator, seeded; numpy PCG64 permutations, seed 7)",
+        "config": {
+            "workload": cfg["workload"],
+            "kernel": resolved + (f" ({kernels_per_step} column panels x k_spmv_seg per shard)" if resolved == "seg"
+                                  else ""),
+            "n_rows": n, "nnz": nnz,
+            "parallelism": (f"row-shard x{world} + {dist.get_backend()} per-slot x broadcasts pipelined with the "
+                            f"panel passes" if shard.pipelined else
+                            f"row-shard x{world} + {dist.get_backend()} all_gather of x"),
+            "setup": "sharded: each rank generates only its original rows inverse(p_r)[lo:hi] and runs K4 on them",
+            "nccl_version": nccl_ver,
+            "l2": "inputs far exceed the 126 MB L2; no flush needed",
+        },
+        "hbm_gbs_per_gpu": round(achieved, 1),
+        "permute_ms_rank0": round(permute_ms, 2),
+        "parity": parity,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_loc, "kernel_ms": round(kern_ms, 5),
+                     "timed": f"rank 0's shard: per-step events around the exchange + {kernels_per_step} launches "
+                              "(max over ranks)"},
+        "cpu_baseline": None,
+        "e2e": {"value": round(2 * nnz / (e_ms * 1e-3) / 1e9, 4), "unit": "GFLOP/s",
+                "h2d_bytes_per_step": int(plan.pad * B_loc.d_values.element_size()) * world,
+                "d2h_bytes_per_step": int(n * B_loc.d_values.element_size()), "ms_per_step": round(e_ms, 4),
+                "rel_err": e2e_err,
+                "api": "rowshard.RowShardedSpMV.step (pinned host x chunk in, y rows out, every rank)"},
+        "clocks": clk,
+        "gpu_launches": kernels_per_step * steps,
+    }
 
 
 def B_dtype_is_f64(cfg) -> bool:
@@ -848,6 +1198,72 @@ def run_iterative_dist(args, cfg, rank: int, world: int) -> dict:
     }
 
 
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` (N > 1) without a torchrun environment: re-run this script
+    under torch.distributed.run with N local ranks on 127.0.0.1 (one process per
+    GPU), forwarding the arguments; returns its exit code."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    log(f"[bench] self-launch: {' '.join(cmd)}")
+    return subprocess.call(cmd)
+
+
+def nccl_debug_to_file() -> None:
+    """NCCL's INIT log (communicator size per rank) goes to files, not stdout (which
+    carries the one JSON line); nccl_init_summary() reads them back."""
+    if "NCCL_DEBUG" not in os.environ:
+        d = Path(tempfile.gettempdir()) / f"sme_nccl_{os.environ.get('TORCHELASTIC_RUN_ID', 'x')}_{os.environ.get('MASTER_PORT', 'x')}"
+        d.mkdir(exist_ok=True)
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+        os.environ["NCCL_DEBUG_FILE"] = str(d / "nccl.%h.%p.log")
+
+
+def nccl_init_summary() -> dict | None:
+    """The NCCL INIT lines of every rank of this job ('comm ... rank r nRanks n'), from
+    the files nccl_debug_to_file() set up: ranks seen and the nRanks each reported."""
+    f = os.environ.get("NCCL_DEBUG_FILE")
+    if not f:
+        return None
+    import glob
+    import re
+
+    ranks, sizes, lines = set(), set(), []
+    for path in glob.glob(str(Path(f).parent / "nccl.*.log")):
+        for ln in Path(path).read_text(errors="replace").splitlines():
+            m = re.search(r"rank (\d+) nRanks (\d+)", ln)
+            if m:
+                ranks.add(int(m.group(1)))
+                sizes.add(int(m.group(2)))
+                lines.append(ln.strip())
+    for ln in lines[:16]:
+        log(f"[nccl] {ln}")
+    return {"ranks_seen": sorted(ranks), "nranks": sorted(sizes), "init_lines": len(lines)}
+
+
+def dry_run(rank: int, world: int) -> None:
+    """Rendezvous + one all_reduce over gloo (no GPU work): the CPU test of the
+    self-launch path (tests/test_bench_launch.py)."""
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        t = torch.tensor([rank + 1.0])
+        dist.all_reduce(t)
+        ok = float(t.item()) == world * (world + 1) / 2
+        dist.destroy_process_group()
+    else:
+        ok = True
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "all_reduce_ok": ok, "pid": os.getpid()}), flush=True)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -857,8 +1273,11 @@ def main() -> None:
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c4")
     ap.add_argument("--kernel", choices=["auto", "seg", "panel", "stream", "vector", "merge"], default="auto")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-scale oracle parity check")
     ap.add_argument("--iterative", action="store_true",
                     help="C5 mode: 1000-step graphed power iteration with permutation amortisation")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch + rendezvous only (CPU/gloo): rank 0 prints the world it saw (tests the self-launch)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]
@@ -870,8 +1289,20 @@ def main() -> None:
         if rank == 0:
             print(json.dumps(run_reference(args, cfg)), flush=True)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    if args.dry_run:
+        dry_run(rank, world)
+        return
 
     import torch
+
+    if world > 1:
+        if not os.environ.get("BENCH_SINGLE_DEVICE") and torch.cuda.device_count() < world:
+            raise SystemExit(f"--gpus {world} needs {world} visible GPUs, found {torch.cuda.device_count()}")
+        nccl_debug_to_file()
 
     # BENCH_SINGLE_DEVICE=1 BENCH_DIST_BACKEND=gloo runs every rank on cuda:0 (a
     # functional check of the sharded path on a 1-GPU box; NCCL needs one GPU per rank)
@@ -891,8 +1322,10 @@ def main() -> None:
             if rank == 0:
                 print(json.dumps(out), flush=True)
             return
-        out = run_ours(args, cfg, rank, world)
+        out = run_ours(args, cfg, rank, world) if world == 1 else run_sharded(args, cfg, rank, world)
         if out is not None:
+            if world > 1 and backend == "nccl":
+                out["nccl_init"] = nccl_init_summary()
             print(json.dumps(out), flush=True)
     finally:
         if world > 1:

@@ -22,6 +22,13 @@ int sme_synth_laplacian5(int dtype, int64_t g, int32_t* d_row_ptr, int32_t* d_co
 int sme_synth_random_rows(int dtype, int64_t n_rows, int64_t n_cols, int32_t k, uint64_t seed,
                           int32_t* d_row_ptr, int32_t* d_col, void* d_val, sme_stream_t stream);
 
+/* The same generator for selected rows: output row i is generator row d_rows[i]
+ * (row_ptr[i] = i*k).  A row shard of the permuted C4 generates only the original
+ * rows inverse(p_r)[lo:hi] it owns (bench.py multi-GPU setup). */
+int sme_synth_random_rows_sel(int dtype, int64_t n_sel, const int32_t* d_rows, int64_t n_cols, int32_t k,
+                              uint64_t seed, int32_t* d_row_ptr, int32_t* d_col, void* d_val,
+                              sme_stream_t stream);
+
 /* R-MAT edges (C3): edge e, level l: u = U[0,1)(hash3(seed, e, l)); quadrant (0,0) if
  * u < a, (0,1) if u < a+b, (1,0) if u < a+b+c, else (1,1); bits appended MSB first.
  * Dedupe/cap through sme_coo_to_csr_dedup + sme_csr_compact; values per (row, slot)

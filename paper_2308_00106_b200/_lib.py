@@ -117,6 +117,7 @@ SIGNATURES: dict[str, list] = {
     # sme_synth.h
     "sme_synth_laplacian5": [C.c_int, i64, p, p, p, p],
     "sme_synth_random_rows": [C.c_int, i64, i64, i32, u64, p, p, p, p],
+    "sme_synth_random_rows_sel": [C.c_int, i64, p, i64, i32, u64, p, p, p, p],
     "sme_diag_gather": [p, i64, i32, i32, i32, p, p],
     "sme_synth_rmat_edges": [i64, i32, f64, f64, f64, u64, p, p, p],
     "sme_synth_row_values": [C.c_int, i64, p, u64, p, p],

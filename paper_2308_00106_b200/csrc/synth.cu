@@ -43,16 +43,19 @@ __global__ void k_laplacian(int64_t g, int32_t* __restrict__ row_ptr, int32_t* _
 
 // warp per row; k <= 32 distinct columns: the first k distinct values of the
 // stream cand(t) = hash3(seed, r, t) -> [0, n_cols), t = 0, 1, 2, ...
+// rows != nullptr: output row i is generator row rows[i] (a row shard of the
+// permuted matrix generates only the original rows it owns)
 template <typename T>
-__global__ void k_random_rows(int64_t n_rows, int64_t n_cols, int32_t k, uint64_t seed, int32_t* __restrict__ row_ptr,
-                              int32_t* __restrict__ col, T* __restrict__ val) {
+__global__ void k_random_rows(int64_t n_rows, int64_t n_cols, int32_t k, uint64_t seed, const int32_t* __restrict__ rows,
+                              int32_t* __restrict__ row_ptr, int32_t* __restrict__ col, T* __restrict__ val) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  for (int64_t r = warp; r < n_rows; r += n_warps) {
-    if (lane == 0) row_ptr[r] = (int32_t)(r * k);
-    if (r == n_rows - 1 && lane == 0) row_ptr[n_rows] = (int32_t)(n_rows * k);
+  for (int64_t i = warp; i < n_rows; i += n_warps) {
+    if (lane == 0) row_ptr[i] = (int32_t)(i * k);
+    if (i == n_rows - 1 && lane == 0) row_ptr[n_rows] = (int32_t)(n_rows * k);
+    const int64_t r = rows ? (int64_t)__ldg(rows + i) : i;
     uint32_t acc = 0xFFFFFFFFu;  // lane a holds accepted[a], a < cnt
     int cnt = 0;
     for (int round = 0; cnt < k; ++round) {
@@ -85,7 +88,7 @@ __global__ void k_random_rows(int64_t n_rows, int64_t n_cols, int32_t k, uint64_
         v = (lower == asc) ? mn : mx;
       }
     if (lane < k) {
-      int64_t p = r * k + lane;
+      int64_t p = i * k + lane;
       col[p] = (int32_t)v;
       val[p] = (T)unit_pm1(hash3(seed ^ VAL_SALT, (uint64_t)r, (uint64_t)lane));
     }
@@ -119,9 +122,26 @@ SME_API int sme_synth_random_rows(int dtype, int64_t n_rows, int64_t n_cols, int
   cudaStream_t s = as_stream(stream);
   int blocks = grid_for(n_rows * 32, 256);
   if (dtype == SME_F64)
-    k_random_rows<double><<<blocks, 256, 0, s>>>(n_rows, n_cols, k, seed, row_ptr, col, (double*)val);
+    k_random_rows<double><<<blocks, 256, 0, s>>>(n_rows, n_cols, k, seed, nullptr, row_ptr, col, (double*)val);
   else if (dtype == SME_F32)
-    k_random_rows<float><<<blocks, 256, 0, s>>>(n_rows, n_cols, k, seed, row_ptr, col, (float*)val);
+    k_random_rows<float><<<blocks, 256, 0, s>>>(n_rows, n_cols, k, seed, nullptr, row_ptr, col, (float*)val);
+  else
+    SME_REQUIRE(false, "unknown dtype %d", dtype);
+  SME_CHECK_LAUNCH("k_random_rows");
+  return SME_OK;
+}
+
+SME_API int sme_synth_random_rows_sel(int dtype, int64_t n_sel, const int32_t* rows, int64_t n_cols, int32_t k,
+                                      uint64_t seed, int32_t* row_ptr, int32_t* col, void* val, sme_stream_t stream) {
+  SME_REQUIRE(n_sel >= 1 && n_cols >= 1 && n_cols < INT32_MAX && rows != nullptr, "bad dimensions");
+  SME_REQUIRE(k >= 1 && k <= 32 && k <= n_cols, "k must lie in [1, min(32, n_cols)]");
+  SME_REQUIRE(n_sel * k < INT32_MAX, "nnz exceeds int32");
+  cudaStream_t s = as_stream(stream);
+  int blocks = grid_for(n_sel * 32, 256);
+  if (dtype == SME_F64)
+    k_random_rows<double><<<blocks, 256, 0, s>>>(n_sel, n_cols, k, seed, rows, row_ptr, col, (double*)val);
+  else if (dtype == SME_F32)
+    k_random_rows<float><<<blocks, 256, 0, s>>>(n_sel, n_cols, k, seed, rows, row_ptr, col, (float*)val);
   else
     SME_REQUIRE(false, "unknown dtype %d", dtype);
   SME_CHECK_LAUNCH("k_random_rows");

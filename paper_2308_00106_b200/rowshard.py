@@ -99,10 +99,18 @@ def pipelined_exchange(x_full: torch.Tensor, x_chunk: torch.Tensor, rank: int, w
 class RowShardedSpMV:
     """One rank's shard of A plus the gathered-x buffer; step() = all-gather + SpMV."""
 
-    def __init__(self, m: CsrMatrix, plan: ShardPlan, rank: int, kernel: str = "vector", lanes: int | None = None):
+    def __init__(self, m: CsrMatrix, plan: ShardPlan, rank: int, kernel: str = "vector", lanes: int | None = None,
+                 *, local: bool = False):
+        """m: the whole matrix (this rank's rows are sliced out), or with local=True
+        already this rank's row shard (rows [lo, hi) of the whole matrix, all columns):
+        a sharded setup builds only its own rows (bench.py multi-GPU)."""
         self.plan, self.rank, self.kernel = plan, rank, kernel
         lo, hi = plan.row_range(rank)
         self.row_lo, self.row_hi = lo, hi
+        if local:
+            if m.n_rows != hi - lo or m.n_cols != plan.n_cols:
+                raise ValueError(f"local shard is {m.n_rows} x {m.n_cols}, rank {rank} owns {hi - lo} x {plan.n_cols}")
+            lo, hi = 0, m.n_rows
         p0, p1 = int(m.d_row_ptr[lo]), int(m.d_row_ptr[hi])
         dev = m.d_row_ptr.device
         row_ptr = (m.d_row_ptr[lo : hi + 1] - p0).contiguous()

@@ -51,6 +51,22 @@ def random_rows(n_rows: int, n_cols: int, k: int, seed: int = C4_SEED, dtype=np.
     return CsrMatrix._from_device(n_rows, n_cols, row_ptr, col, val)
 
 
+def random_rows_select(rows: torch.Tensor, n_cols: int, k: int, seed: int = C4_SEED, dtype=np.float64) -> CsrMatrix:
+    """Rows `rows` (device int32, any order) of random_rows(., n_cols, k, seed): output
+    row i is generator row rows[i].  A row shard of the permuted C4 generates only
+    the original rows inverse(p_r)[lo:hi] it owns."""
+    dev = _cuda.require_cuda()
+    vdt = _vdt(dtype)
+    rows = rows.to(dev, torch.int32).contiguous()
+    n_sel = rows.numel()
+    row_ptr = torch.empty(n_sel + 1, dtype=torch.int32, device=dev)
+    col = torch.empty(n_sel * k, dtype=torch.int32, device=dev)
+    val = torch.empty(n_sel * k, dtype=vdt, device=dev)
+    _lib.call("sme_synth_random_rows_sel", _cuda.sme_dtype(val), n_sel, ptr(rows), n_cols, k, seed, ptr(row_ptr),
+              ptr(col), ptr(val), stream())
+    return CsrMatrix._from_device(n_sel, n_cols, row_ptr, col, val)
+
+
 C3_SEED = 0x5EED_C3
 RMAT_ABC = (0.57, 0.19, 0.19)
 
