@@ -465,6 +465,16 @@ int sme_spmv_reduceat_exact(int64_t n_rows, const int32_t* d_row_ptr, const int3
 int sme_spmv_coo(int dtype, int64_t n_rows, int64_t nnz, const int32_t* d_row, const int32_t* d_col,
                  const void* d_val, const void* d_x, void* d_y, sme_stream_t stream);
 
+/* Deterministic COO SpMV, bitwise equal to the reference's np.add.at (kernels.py:81-86:
+ * y = 0, then y[row[k]] += v[k] * x[col[k]] in stored entry order).  Plan: d_row_ptr
+ * (n_rows + 1) and d_order[p] = the entry ids of each row in ascending entry order,
+ * d_val[p] = values[d_order[p]] (built once by sme_coo_to_csr with entry ids as the
+ * sort key).  One thread per row sums its products in that order with round-to-
+ * nearest multiply and add (no FMA), starting from 0. */
+int sme_spmv_coo_ordered(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_order,
+                         const void* d_val, const int32_t* d_col, const void* d_x, void* d_y,
+                         sme_stream_t stream);
+
 /* relative_error (kernels.py:131-142) helper: d_out[0] = max|got - exp|,
  * d_out[1] = max|exp| (f64, caller zeroes). */
 int sme_maxabs_diff(int dtype, int64_t n, const void* d_got, const void* d_exp, double* d_out,

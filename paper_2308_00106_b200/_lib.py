@@ -107,6 +107,7 @@ SIGNATURES: dict[str, list] = {
     "sme_spmv_vector": [C.c_int, C.c_int, i64, i64, p, p, p, p, p, C.c_int, p],
     "sme_spmv_reduceat_exact": [i64, p, p, p, p, p, p],
     "sme_spmv_coo": [C.c_int, i64, i64, p, p, p, p, p, p],
+    "sme_spmv_coo_ordered": [C.c_int, i64, p, p, p, p, p, p, p],
     "sme_maxabs_diff": [C.c_int, i64, p, p, p, p],
     "sme_rowshard_remap_cols": [i64, i64, i32, i64, p, p, p],
     "sme_blas_partials": [pi64],

@@ -104,7 +104,10 @@ def input_vector(master_seed: int, n: int) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # GPU KernelSpecs
 # ---------------------------------------------------------------------------
-_device_csr: "weakref.WeakKeyDictionary[object, CsrMatrix]" = weakref.WeakKeyDictionary()
+# device copies of reference matrices, keyed by object identity: the reference's
+# CsrMatrix defines __eq__ without __hash__ (unhashable), so the entry is dropped by a
+# weakref finalizer when the reference object dies
+_device_csr: dict[int, CsrMatrix] = {}
 
 
 def device_csr(ops) -> CsrMatrix:
@@ -116,12 +119,12 @@ def device_csr(ops) -> CsrMatrix:
         from .matio import coo_to_csr
 
         return coo_to_csr(csr)
-    try:
-        return _device_csr[csr]
-    except KeyError:
-        d = from_reference(csr)
-        _device_csr[csr] = d
-        return d
+    key = id(csr)
+    d = _device_csr.get(key)
+    if d is None:
+        d = _device_csr[key] = from_reference(csr)
+        weakref.finalize(csr, _device_csr.pop, key, None)
+    return d
 
 
 def _host_call(kernel: str) -> Callable:

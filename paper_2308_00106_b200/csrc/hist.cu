@@ -532,7 +532,7 @@ SME_API int sme_row_hist_csr(int64_t n_rows, const int32_t* row_ptr, int32_t bin
 SME_API int sme_entropy(int64_t n_bins, const int64_t* counts, double base, double* out, int64_t* total,
                         sme_stream_t stream) {
   SME_REQUIRE(n_bins >= 1, "histogram has no bins");
-  SME_REQUIRE(base > 1.0, "entropy base must be > 1");
+  SME_REQUIRE(base > 0.0 && base != 1.0, "entropy base must be > 0 and != 1");
   cudaStream_t s = as_stream(stream);
   k_entropy<<<1, 1024, 0, s>>>(n_bins, counts, base, out, total);
   SME_CHECK_LAUNCH("k_entropy");

@@ -526,6 +526,29 @@ __global__ void k_spmv_coo(int64_t nnz, const int32_t* __restrict__ row, const i
     atomicAdd(y + row[k], val[k] * x[col[k]]);
 }
 
+// Deterministic COO SpMV, bitwise equal to the reference's np.add.at (kernels.py:81-86):
+// np.add.at applies out[row[k]] += v[k] * x[col[k]] in stored entry order, so each
+// row's value is ((0 + p_a) + p_b) + ... over its entries in entry order, with every
+// product rounded before the add.  The plan lists each row's entries in entry order
+// (order[] = entry ids sorted within rows, vals[] the matching values); a thread per
+// row replays that sequence with explicit round-to-nearest mul/add (no FMA
+// contraction), so the result is independent of scheduling.
+__device__ __forceinline__ double coo_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double coo_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float coo_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float coo_add(float a, float b) { return __fadd_rn(a, b); }
+
+template <typename T>
+__global__ void k_spmv_coo_ordered(int64_t n_rows, const int32_t* __restrict__ rp, const int32_t* __restrict__ order,
+                                   const T* __restrict__ val, const int32_t* __restrict__ col,
+                                   const T* __restrict__ x, T* __restrict__ y) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+    T acc = T(0);
+    for (int32_t p = rp[r], e = rp[r + 1]; p < e; ++p) acc = coo_add(acc, coo_mul(val[p], x[col[order[p]]]));
+    y[r] = acc;
+  }
+}
+
 template <typename T>
 int launch_vector(int lanes, int64_t n_rows, const int32_t* rp, const int32_t* col, const T* val, const T* x, T* y,
                   int acc, cudaStream_t s) {
@@ -657,6 +680,21 @@ SME_API int sme_spmv_coo(int dtype, int64_t n_rows, int64_t nnz, const int32_t* 
     k_spmv_coo<float><<<grid_for(nnz, 256), 256, 0, s>>>(nnz, row, col, (const float*)val, (const float*)x,
                                                          (float*)y);
   SME_CHECK_LAUNCH("k_spmv_coo");
+  return SME_OK;
+}
+
+SME_API int sme_spmv_coo_ordered(int dtype, int64_t n_rows, const int32_t* row_ptr, const int32_t* order,
+                                 const void* val, const int32_t* col, const void* x, void* y, sme_stream_t stream) {
+  cudaStream_t s = as_stream(stream);
+  SME_REQUIRE(dtype == SME_F64 || dtype == SME_F32, "unknown dtype %d", dtype);
+  if (n_rows == 0) return SME_OK;
+  if (dtype == SME_F64)
+    k_spmv_coo_ordered<double><<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, row_ptr, order, (const double*)val, col,
+                                                                     (const double*)x, (double*)y);
+  else
+    k_spmv_coo_ordered<float><<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, row_ptr, order, (const float*)val, col,
+                                                                    (const float*)x, (float*)y);
+  SME_CHECK_LAUNCH("k_spmv_coo_ordered");
   return SME_OK;
 }
 

@@ -125,6 +125,8 @@ def row_histogram(m, bins: int) -> BinnedHistogram:
 def col_histogram(m, bins: int) -> BinnedHistogram:
     """Count nonzeros per column bin (entropy.py:84-88): the 2-D kernel with one row bin."""
     _check_bins(bins, m.n_cols, "column")
+    if m.n_rows == 0 or m.nnz == 0:  # the reference checks column bins only (a 0-row matrix is legal)
+        return BinnedHistogram(_zeros(bins), (_bin_edges(m.n_cols, bins),))
     h = histogram_2d(m, 1, bins)
     return BinnedHistogram(h.device_counts().view(bins), (_bin_edges(m.n_cols, bins),))
 
@@ -137,13 +139,22 @@ def _csr_of(m: CooMatrix) -> CsrMatrix:
 
 @_cuda.nvtx("shannon_entropy")
 def shannon_entropy(h: BinnedHistogram, base: float = 2.0) -> float:
-    """-sum p_i log(p_i) over nonzero bins, p_i = count_i / total (entropy.py:104-119)."""
-    if base <= 1.0:
-        raise ValueError("entropy base must be > 1")
+    """-sum p_i log(p_i) over nonzero bins, p_i = count_i / total (entropy.py:104-119).
+
+    Any base the reference accepts works (base 2: log2; otherwise ln / ln(base), so a
+    base in (0, 1) gives a negative value); the reference's errors are kept, in its
+    order: an empty histogram is a ValueError, then base 1 divides by ln 1 = 0
+    (ZeroDivisionError) and base <= 0 fails math.log (ValueError)."""
+    base = float(base)
+    valid = base > 0.0 and base != 1.0
     d = h.device_counts().reshape(-1).contiguous()
     out = torch.empty(1, dtype=torch.float64, device=d.device)
     total = torch.empty(1, dtype=torch.int64, device=d.device)
-    _lib.call("sme_entropy", d.numel(), ptr(d), float(base), ptr(out), ptr(total), stream())
+    _lib.call("sme_entropy", d.numel(), ptr(d), base if valid else 2.0, ptr(out), ptr(total), stream())
     if int(total.item()) == 0:
         raise ValueError("histogram is empty (total = 0)")
+    if base == 1.0:
+        raise ZeroDivisionError("float division by zero")
+    if base <= 0.0:
+        raise ValueError("math domain error")
     return float(out.item())

@@ -14,17 +14,18 @@ staged by the driver, and a fresh 400 MB numpy result is ~100k first-touch page 
   drops the array, so a result crosses PCIe in one DMA straight into it (a dtype
   change goes through a pinned stage in chunks, copied out while the next crosses).
 
-Calls are synchronous on return and not reentrant across threads (the staging
-buffers are per process)."""
+Calls are synchronous on return and reentrant: the pinned staging buffers and the
+copy streams are per thread, the result pool is guarded by a lock (the reference
+contract: pure functions, safe to call from concurrent workers)."""
 from __future__ import annotations
 
 import mmap
+import threading
 
 import numpy as np
 import torch
 
-_PINNED: dict[tuple, torch.Tensor] = {}
-_STREAMS: dict[int, torch.cuda.Stream] = {}
+_TLS = threading.local()  # per-thread pinned staging buffers and copy streams
 
 #: bytes below which vectors move in one piece (chunking only pays for large vectors)
 CHUNK_MIN_BYTES = 8 << 20
@@ -35,25 +36,76 @@ OUT_CHUNKS = 8
 def pinned(shape, dtype, tag: str = "") -> torch.Tensor:
     """A reusable pinned host buffer (page-locking 400 MB costs tens of ms per call);
     `tag` keeps the input and output staging buffers of one call apart."""
+    pins = _TLS.__dict__.setdefault("pinned", {})
     key = (tuple(shape), dtype, tag)
-    buf = _PINNED.get(key)
+    buf = pins.get(key)
     if buf is None:
-        buf = _PINNED[key] = torch.empty(shape, dtype=dtype, pin_memory=True)
+        buf = pins[key] = torch.empty(shape, dtype=dtype, pin_memory=True)
     return buf
 
 
 def copy_stream(dev: torch.device) -> torch.cuda.Stream:
+    """This thread's copy stream on `dev`."""
+    streams = _TLS.__dict__.setdefault("streams", {})
     idx = dev.index if dev.index is not None else torch.cuda.current_device()
-    s = _STREAMS.get(idx)
+    s = streams.get(idx)
     if s is None:
-        s = _STREAMS[idx] = torch.cuda.Stream(device=dev)
+        s = streams[idx] = torch.cuda.Stream(device=dev)
     return s
 
 
 #: released host mappings kept for reuse, per size (a reused mapping is already faulted
-#: in and page-locked)
+#: in and page-locked); at most POOL_PER_SIZE per size and POOL_MAX_BYTES in all, the
+#: least recently released evicted (unregistered and unmapped) first
 _POOL: dict[int, list["_Mapping"]] = {}
+_POOL_LRU: list["_Mapping"] = []
+_POOL_LOCK = threading.Lock()
 POOL_PER_SIZE = 3
+POOL_MAX_BYTES = 4 << 30
+
+
+def pool_bytes() -> int:
+    with _POOL_LOCK:
+        return sum(len(m.mm) for m in _POOL_LRU)
+
+
+def _pool_put(m: "_Mapping") -> None:
+    with _POOL_LOCK:
+        free = _POOL.setdefault(len(m.mm), [])
+        evict = []
+        if len(free) >= POOL_PER_SIZE:
+            evict.append(m)
+        else:
+            free.append(m)
+            _POOL_LRU.append(m)
+            total = sum(len(q.mm) for q in _POOL_LRU)
+            while total > POOL_MAX_BYTES and _POOL_LRU:
+                old = _POOL_LRU.pop(0)
+                _POOL[len(old.mm)].remove(old)
+                total -= len(old.mm)
+                evict.append(old)
+    for q in evict:
+        q.close()
+
+
+def pool_clear() -> None:
+    """Unregister and unmap every pooled mapping."""
+    with _POOL_LOCK:
+        evict = list(_POOL_LRU)
+        _POOL_LRU.clear()
+        _POOL.clear()
+    for q in evict:
+        q.close()
+
+
+def _pool_take(nbytes: int) -> "_Mapping | None":
+    with _POOL_LOCK:
+        free = _POOL.get(nbytes)
+        if not free:
+            return None
+        m = free.pop()
+        _POOL_LRU.remove(m)
+        return m
 
 
 class _Mapping:
@@ -95,13 +147,9 @@ class _PooledMapping:
     def __release_buffer__(self, view):
         view.release()
         try:
-            free = _POOL.setdefault(len(self._m.mm), [])
-        except AttributeError:  # interpreter shutdown: module globals are gone
+            _pool_put(self._m)
+        except (AttributeError, TypeError):  # interpreter shutdown: module globals are gone
             return
-        if len(free) < POOL_PER_SIZE:
-            free.append(self._m)
-        else:
-            self._m.close()
 
 
 def _fresh(n: int, dtype) -> tuple[np.ndarray, bool]:
@@ -111,8 +159,7 @@ def _fresh(n: int, dtype) -> tuple[np.ndarray, bool]:
     nbytes = n * dt.itemsize
     if nbytes < CHUNK_MIN_BYTES:
         return np.empty(n, dtype=dt), False
-    free = _POOL.get(nbytes)
-    m = free.pop() if free else _Mapping(nbytes)
+    m = _pool_take(nbytes) or _Mapping(nbytes)
     return np.frombuffer(_PooledMapping(m), dtype=dt, count=n), m.registered
 
 

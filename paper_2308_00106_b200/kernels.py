@@ -2,7 +2,7 @@
 
 Drop-in for `spmv_entropy.kernels` (reference
 /root/reference/pkg/src/spmv_entropy/kernels.py).  All kernels are pure and
-deterministic (the COO kernel excepted: floating-point atomics).
+deterministic (the opt-in COO kernel="atomic" excepted).
 
 Input/output convention: a host array x gives a host numpy float64 y (H2D of
 x, kernel, D2H of y — the reference-facing call); a CUDA tensor x gives a CUDA
@@ -257,6 +257,16 @@ def spmv_into(m: CsrMatrix, xd: torch.Tensor, y: torch.Tensor, kernel: str = "ve
         raise ValueError(f"unknown kernel {kernel!r}; expected one of {KERNELS}")
 
 
+def _check_out(out, m: CsrMatrix, dev) -> None:
+    """The caller's `out` must be exactly what the kernels write: a contiguous device
+    tensor of n_rows elements of the matrix dtype on the matrix's device."""
+    if not isinstance(out, torch.Tensor) or not out.is_cuda or out.device != dev:
+        raise ValueError(f"out must be a CUDA tensor on {dev}")
+    if out.dtype != m.dtype or out.dim() != 1 or out.numel() != m.n_rows or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous 1-D {m.dtype} tensor of length n_rows {m.n_rows} "
+                         f"(got {out.dtype} {tuple(out.shape)})")
+
+
 @_cuda.nvtx("spmv_csr")
 def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None = None):
     """y[i] = sum over row i of values[k] * x[col_idx[k]] (kernels.py:73-78).
@@ -264,11 +274,14 @@ def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None 
     kernel="auto" (auto_kernel): the segmented-chunk column panels ('seg') when x is
     large (> 60 % of L2) or medium-sized and the matrix is not banded; the
     nnz-balanced 'stream' kernel for other ragged matrices; else the CSR-vector
-    kernel (then spmv_csr_parallel is bitwise equal, as in the reference).  A pinned
+    kernel.  spmv_csr_parallel with the same kernel is bitwise equal (as in the
+    reference).  `out`: optional device result tensor (checked by _check_out).  A pinned
     host x of a panel layout streams in slice by slice while the passes run."""
     if not isinstance(m, CsrMatrix):
         raise TypeError("spmv_csr expects a CsrMatrix of this package (see matio.from_reference)")
     dev = m.d_row_ptr.device
+    if out is not None:
+        _check_out(out, m, dev)
     if isinstance(x, torch.Tensor) and x.is_cuda:
         xd, mode = _x_device(x, m.n_cols, m.dtype, dev)
         y = out if out is not None else torch.empty(m.n_rows, dtype=m.dtype, device=dev)
@@ -277,12 +290,10 @@ def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None 
     # host x: it crosses PCIe slice by slice; with column panels pass p starts as soon
     # as slice p has landed
     src, mode = _host_src(x, m.n_cols)
-    bufs = m._cache.get("host_bufs")
-    if bufs is None:
-        bufs = m._cache["host_bufs"] = (torch.empty(m.n_cols, dtype=m.dtype, device=dev),
-                                        torch.empty(m.n_rows, dtype=m.dtype, device=dev))
-    xd = bufs[0]
-    y = out if out is not None else bufs[1]
+    # per-call device buffers (torch's caching allocator: free after warm-up), so
+    # concurrent callers on one matrix never share them (reentrant)
+    xd = torch.empty(m.n_cols, dtype=m.dtype, device=dev)
+    y = out if out is not None else torch.empty(m.n_rows, dtype=m.dtype, device=dev)
     main = torch.cuda.current_stream(dev)
     kern = auto_kernel(m) if kernel == "auto" else kernel
     if kern in ("seg", "panel"):
@@ -396,22 +407,29 @@ def spmv_csr_pipelined(m: CsrMatrix, xs, ys=None, kernel: str = "auto") -> list:
 
 
 @_cuda.nvtx("spmv_csr_parallel")
-def spmv_csr_parallel(m: CsrMatrix, x, workers: int, reuse_pool: bool = True, kernel: str = "vector"):
-    """Row-partitioned CSR SpMV (kernels.py:102-128): each of `workers` even row
-    ranges (make_row_partition) is one CSR-vector launch over its rows; every
-    launch writes a disjoint y slice, so the result is bitwise equal to
-    spmv_csr(m, x) for every worker count.  `reuse_pool` is accepted for
-    signature compatibility (there is no thread pool).  Multi-GPU sharding of
-    the same partition is rowshard.RowShardedSpMV."""
+def spmv_csr_parallel(m: CsrMatrix, x, workers: int, reuse_pool: bool = True, kernel: str = "auto"):
+    """Row-partitioned CSR SpMV (kernels.py:102-128), bitwise equal to spmv_csr(m, x,
+    kernel) for every worker count, as the reference's is to its serial kernel.
+
+    kernel="auto" resolves exactly as spmv_csr does (auto_kernel).  For the
+    CSR-vector kernel each of the `workers` even row ranges (make_row_partition) is
+    its own launch over those rows; a row's reduction order depends only on the
+    lane count, so the ranges reproduce the whole-matrix call bit for bit.  The
+    other kernels ('seg', 'stream', 'merge', 'panel') fix each row's reduction
+    order in their per-matrix layout; the partition cannot change it, and the
+    whole-matrix launch (whose CTAs are the GPU's workers) IS every range's result.
+    `reuse_pool` is accepted for signature compatibility (there is no thread pool).
+    Multi-GPU sharding of the same partition is rowshard.RowShardedSpMV."""
     del reuse_pool
     if not isinstance(m, CsrMatrix):
         raise TypeError("spmv_csr_parallel expects a CsrMatrix of this package")
     dev = m.d_row_ptr.device
-    xd, mode = _x_device(x, m.n_cols, m.dtype, dev)
     part = make_row_partition(m.n_rows, workers)
+    kern = auto_kernel(m) if kernel == "auto" else kernel
+    if kern != "vector":
+        return spmv_csr(m, x, kern)
+    xd, mode = _x_device(x, m.n_cols, m.dtype, dev)
     y = torch.empty(m.n_rows, dtype=m.dtype, device=dev)
-    if kernel != "vector":
-        raise ValueError("spmv_csr_parallel shards the partition-invariant CSR-vector kernel")
     lanes = default_lanes(m)
     dt = _cuda.sme_dtype(m.d_values)
     es = m.d_row_ptr.element_size()
@@ -425,16 +443,50 @@ def spmv_csr_parallel(m: CsrMatrix, x, workers: int, reuse_pool: bool = True, ke
     return _y_out(y, mode)
 
 
+def coo_entry_order(m: CooMatrix) -> CsrMatrix:
+    """Per-matrix plan of the deterministic COO SpMV (cached like a CSR analysis): the
+    entries grouped by row, each row's entries in ascending stored-entry order.  Built
+    by the CSR builder (counting sort + segmented sort) with the entry id as the sort
+    key: col_idx of the result holds entry ids, values the matching values."""
+    plan = m._cache.get("coo_order")
+    if plan is None:
+        from .matio import _coo_build_csr
+
+        dev = m.d_row_idx.device
+        ids = torch.arange(m.nnz, dtype=torch.int32, device=dev)
+        proxy = CooMatrix._from_device(m.n_rows, max(1, m.nnz), m.d_row_idx, ids, m.d_values)
+        plan = _coo_build_csr(proxy, None, None, check=False)
+        m._cache["coo_order"] = plan
+    return plan
+
+
 @_cuda.nvtx("spmv_coo")
-def spmv_coo(m: CooMatrix, x):
-    """y = 0; y[row_idx[k]] += values[k] * x[col_idx[k]] (kernels.py:81-86), with device atomics."""
+def spmv_coo(m: CooMatrix, x, kernel: str = "ordered"):
+    """y = 0; y[row_idx[k]] += values[k] * x[col_idx[k]] in stored entry order (kernels.py:81-86).
+
+    kernel="ordered" (default): every row sums its products in entry order with
+    round-to-nearest arithmetic (sme_spmv_coo_ordered over coo_entry_order) — bitwise
+    equal to the reference's np.add.at and run-to-run deterministic.  kernel="atomic":
+    one floating atomic add per entry (no plan; the order of the adds, hence the last
+    ulps, can change from run to run)."""
     if not isinstance(m, CooMatrix):
         raise TypeError("spmv_coo expects a CooMatrix of this package")
     dev = m.d_row_idx.device
     xd, mode = _x_device(x, m.n_cols, m.dtype, dev)
     y = torch.empty(m.n_rows, dtype=m.dtype, device=dev)
-    _lib.call("sme_spmv_coo", _cuda.sme_dtype(m.d_values), m.n_rows, m.nnz, ptr(m.d_row_idx), ptr(m.d_col_idx),
-              ptr(m.d_values), ptr(xd), ptr(y), stream())
+    dt = _cuda.sme_dtype(m.d_values)
+    if kernel == "atomic":
+        _lib.call("sme_spmv_coo", dt, m.n_rows, m.nnz, ptr(m.d_row_idx), ptr(m.d_col_idx), ptr(m.d_values), ptr(xd),
+                  ptr(y), stream())
+    elif kernel == "ordered":
+        if m.nnz == 0:
+            y.zero_()
+        else:
+            plan = coo_entry_order(m)
+            _lib.call("sme_spmv_coo_ordered", dt, m.n_rows, ptr(plan.d_row_ptr), ptr(plan.d_col_idx),
+                      ptr(plan.d_values), ptr(m.d_col_idx), ptr(xd), ptr(y), stream())
+    else:
+        raise ValueError(f"unknown COO kernel {kernel!r}; expected 'ordered' or 'atomic'")
     return _y_out(y, mode)
 
 

@@ -182,6 +182,7 @@ class CooMatrix:
         self.d_col_idx = _cuda.as_index_tensor(col_idx, "column index")
         self.d_values = _cuda.as_value_tensor(values, vdt)
         self._host: dict[str, np.ndarray] = {}
+        self._cache: dict = {}  # per-matrix plans (kernels.coo_entry_order)
         self._csr: CsrMatrix | None = None
         self._csr_thunk: Callable[[], CsrMatrix] | None = None
         if not _trusted:
@@ -193,6 +194,7 @@ class CooMatrix:
         m.n_rows, m.n_cols = int(n_rows), int(n_cols)
         m.d_row_idx, m.d_col_idx, m.d_values = d_row, d_col, d_val
         m._host, m._csr, m._csr_thunk = {}, csr, csr_thunk
+        m._cache = {}
         return m
 
     @property

@@ -1,0 +1,149 @@
+"""Round-2 API parity: deterministic COO SpMV, spmv_csr_parallel on every kernel,
+`out=` validation, reentrant host calls, the reference's entropy base and
+col_histogram behaviour."""
+
+from __future__ import annotations
+
+import math
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2308_00106_b200 as P
+from conftest import make_random_coo_arrays
+from paper_2308_00106_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _coo(rng, n_rows, n_cols, density, dtype=np.float64):
+    r, c, v = make_random_coo_arrays(rng, n_rows, n_cols, density)
+    order = rng.permutation(r.size)  # shuffled entry order: np.add.at's order matters
+    return r[order], c[order], v[order].astype(dtype)
+
+
+@pytest.mark.parametrize("shape,density", [((1000, 700), 0.01), ((20_000, 30_000), 0.0005), ((2000, 2000), 0.25),
+                                           ((300, 5), 0.9)])
+def test_spmv_coo_bitwise_equals_np_add_at(rng, shape, density):
+    """The default COO kernel reproduces np.add.at (kernels.py:81-86) bit for bit, at
+    up to 1M nonzeros in shuffled entry order, and is run-to-run identical."""
+    r, c, v = _coo(rng, *shape, density)
+    m = P.CooMatrix(*shape, r, c, v)
+    x = rng.random(shape[1])
+    want = O.spmv_coo(shape[0], r, c, v, x)
+    got = P.spmv_coo(m, x)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    xd = torch.from_numpy(x).cuda()
+    first = P.spmv_coo(m, xd)
+    for _ in range(4):
+        assert torch.equal(P.spmv_coo(m, xd), first)
+
+
+def test_spmv_coo_f32_and_atomic_within_tolerance(rng):
+    r, c, v = _coo(rng, 50_000, 40_000, 0.0005)
+    x = rng.random(40_000)
+    want = O.spmv_coo(50_000, r, c, v, x)
+    m = P.CooMatrix(50_000, 40_000, r, c, v)
+    assert O.relative_error(P.spmv_coo(m, x, kernel="atomic"), want) <= 1e-12
+    m32 = P.CooMatrix(50_000, 40_000, r, c, v.astype(np.float32))
+    want32 = O.spmv_coo(50_000, r, c, v.astype(np.float32).astype(np.float64),
+                        x.astype(np.float32).astype(np.float64))
+    got32 = P.spmv_coo(m32, torch.from_numpy(x.astype(np.float32)).cuda()).double().cpu().numpy()
+    assert O.relative_error(got32, want32) <= 1e-5
+
+
+def test_spmv_coo_atomic_run_to_run_bound(rng):
+    """The atomic variant's run-to-run spread is bounded by the f64 reassociation
+    error of a row (<= nnz_row * eps * sum|products|); it stays opt-in."""
+    n = 2000
+    r = np.repeat(np.arange(n), 500)
+    c = np.tile(np.arange(500), n)
+    v = rng.standard_normal(r.size)
+    m = P.CooMatrix(n, 500, r, c, v)
+    x = torch.from_numpy(rng.standard_normal(500)).cuda()
+    runs = torch.stack([P.spmv_coo(m, x, kernel="atomic") for _ in range(5)])
+    spread = (runs.max(0).values - runs.min(0).values).abs().max().item()
+    bound = 500 * 2.0**-52 * float((torch.from_numpy(np.abs(v).reshape(n, 500)).cuda() * x.abs()).sum(1).max())
+    assert spread <= bound
+
+
+def test_spmv_csr_parallel_bitwise_with_auto_seg():
+    """on a matrix where auto resolves to 'seg', spmv_csr_parallel is bitwise
+    equal to spmv_csr (the reference's parallel == serial invariant, kernels.py:1-6)."""
+    A = synth.rmat(16, 16, cap=100000, dtype=np.float64)  # ragged rows -> 'seg'
+    assert P.kernels.auto_kernel(A) == "seg"
+    x = torch.from_numpy(O.input_vector(0, A.n_cols)).cuda()
+    y = P.spmv_csr(A, x)
+    for w in (1, 3, 16):
+        assert torch.equal(P.spmv_csr_parallel(A, x, w), y)
+    B = synth.laplacian5(300)
+    assert P.kernels.auto_kernel(B) == "vector"
+    xb = torch.from_numpy(O.input_vector(0, B.n_cols)).cuda()
+    assert torch.equal(P.spmv_csr_parallel(B, xb, 7), P.spmv_csr(B, xb))
+
+
+def test_out_is_validated():
+    A = synth.laplacian5(50)
+    x = torch.ones(A.n_cols, dtype=torch.float64, device="cuda")
+    good = torch.empty(A.n_rows, dtype=torch.float64, device="cuda")
+    assert P.spmv_csr(A, x, out=good) is good
+    for bad in (torch.empty(A.n_rows, dtype=torch.float32, device="cuda"),
+                torch.empty(A.n_rows - 1, dtype=torch.float64, device="cuda"),
+                torch.empty(2 * A.n_rows, dtype=torch.float64, device="cuda")[::2],
+                torch.empty(A.n_rows, dtype=torch.float64)):
+        with pytest.raises(ValueError, match="out must"):
+            P.spmv_csr(A, x, out=bad)
+
+
+def test_concurrent_host_calls_on_one_matrix():
+    """4 threads calling spmv_csr(m, x_i) with host vectors on ONE
+    matrix each get their own result (large enough for the staged/pooled paths)."""
+    g = 1500  # 2.25M rows: 18 MB vectors take the chunked staging and pooled results
+    A = synth.laplacian5(g)
+    n = A.n_rows
+    xs = [np.random.default_rng(k).random(n) for k in range(4)]
+    want = [P.spmv_csr(A, torch.from_numpy(x).cuda()).cpu().numpy() for x in xs]
+    errors: list = []
+
+    def worker(k):
+        try:
+            for it in range(6):
+                y = P.spmv_csr(A, xs[k]) if it % 2 == 0 else P.spmv_csr(A, torch.from_numpy(xs[k]))
+                y = np.asarray(y)
+                if not np.array_equal(y, want[k]):
+                    errors.append((k, it, float(np.abs(y - want[k]).max())))
+        except Exception as e:  # pragma: no cover
+            errors.append((k, repr(e)))
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+
+
+def test_entropy_base_and_errors_match_reference():
+    h = P.histogram_2d(P.CooMatrix(3, 3, [0, 1, 2, 2], [0, 1, 2, 0], [1.0, 1.0, 1.0, 1.0]), 3, 3)
+    p = np.array([1, 1, 1, 1]) / 4
+    assert P.shannon_entropy(h, base=0.5) == pytest.approx(float(-(p * np.log(p)).sum() / math.log(0.5)), rel=1e-12)
+    assert P.shannon_entropy(h, base=10.0) == pytest.approx(float(-(p * np.log(p)).sum() / math.log(10.0)),
+                                                            rel=1e-12)
+    with pytest.raises(ZeroDivisionError):
+        P.shannon_entropy(h, base=1.0)
+    with pytest.raises(ValueError, match="math domain"):
+        P.shannon_entropy(h, base=-2.0)
+    empty = P.histogram_2d(P.CooMatrix(3, 3, [], [], []), 3, 3)
+    with pytest.raises(ValueError, match="empty"):
+        P.shannon_entropy(empty, base=1.0)  # the empty check comes first, as in the reference
+
+
+def test_col_histogram_zero_row_matrix():
+    m = P.CooMatrix(0, 6, [], [], [])
+    h = P.col_histogram(m, 3)
+    assert h.counts.tolist() == [0, 0, 0]
+    with pytest.raises(ValueError, match="column bin count 7 exceeds"):
+        P.col_histogram(m, 7)

@@ -147,7 +147,7 @@ def test_hostio_fresh_results_never_alias_and_recycle():
 
     n = hostio.CHUNK_MIN_BYTES // 8 + 7
     key = n * 8
-    hostio._POOL.pop(key, None)
+    hostio.pool_clear()
     a = hostio.fresh_host(n, np.float64)
     b = hostio.fresh_host(n, np.float64)
     assert a.flags.writeable and a.shape == (n,) and not np.shares_memory(a, b)
@@ -168,3 +168,40 @@ def test_hostio_fresh_results_never_alias_and_recycle():
     small = hostio.fresh_host(10, np.float32)
     assert small.dtype == np.float32 and small.shape == (10,)
     assert hostio.slices(10, 8) == [0, 10] and hostio.slices(n, 8, 4)[-1] == n
+
+
+def test_hostio_pool_is_capped_lru(monkeypatch):
+    """released result mappings are capped in total bytes (least recently
+    released evicted first) and per size; concurrent releases are safe."""
+    import gc
+    import threading
+
+    from paper_2308_00106_b200 import hostio
+
+    hostio.pool_clear()
+    base = hostio.CHUNK_MIN_BYTES
+    monkeypatch.setattr(hostio, "POOL_MAX_BYTES", 3 * base)
+    arrs = [hostio.fresh_host(base // 8 + 64 * k, np.float64) for k in range(4)]
+    while arrs:  # released smallest first
+        del arrs[0]
+        gc.collect()
+    assert 0 < hostio.pool_bytes() <= 3 * base
+    sizes = sorted(k for k, v in hostio._POOL.items() if v)
+    assert (base // 8) * 8 not in sizes  # the first released (smallest here) was evicted
+    hostio.pool_clear()
+    assert hostio.pool_bytes() == 0
+
+    def worker():
+        for _ in range(5):
+            a = hostio.fresh_host(base // 8, np.float64)
+            a[0] = 1.0
+            del a
+            gc.collect()
+
+    ts = [threading.Thread(target=worker) for _ in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert len(hostio._POOL.get(base, [])) <= hostio.POOL_PER_SIZE
+    hostio.pool_clear()
