@@ -507,6 +507,13 @@ int sme_axpby(int dtype, int64_t n, double a, const void* d_x, double b, void* d
 int sme_rowshard_remap_cols(int64_t nnz, int64_t n_cols, int32_t parts, int64_t pad,
                             const int32_t* d_col_in, int32_t* d_col_out, sme_stream_t stream);
 
+/* 64-bit content hash of a device array (the key of the on-disk permuted-CSR cache,
+ * cache.py; the reference persists permuted matrices through cmd_permute ->
+ * write_matrix_market, cli.py:173-230, matio.py:262-278).  Over the 32-bit words w_i:
+ * *d_out = sum_i mix64((mix64(seed ^ C) + i * G) ^ (w_i * K)) mod 2^64 — deterministic
+ * for any launch shape.  n_bytes % 4 == 0, d_data 4-byte aligned. */
+int sme_hash64(const void* d_data, int64_t n_bytes, uint64_t seed, uint64_t* d_out, sme_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -106,6 +106,7 @@ SIGNATURES: dict[str, list] = {
     "sme_spmv_stream": [C.c_int, i64, i64, i64, p, p, p, p, p, p, i32, C.c_int, i32, p],
     "sme_spmv_vector": [C.c_int, C.c_int, i64, i64, p, p, p, p, p, C.c_int, p],
     "sme_spmv_reduceat_exact": [i64, p, p, p, p, p, p],
+    "sme_hash64": [p, i64, u64, p, p],
     "sme_spmv_coo": [C.c_int, i64, i64, p, p, p, p, p, p],
     "sme_spmv_coo_ordered": [C.c_int, i64, p, p, p, p, p, p, p],
     "sme_maxabs_diff": [C.c_int, i64, p, p, p, p],

@@ -205,3 +205,20 @@ def test_hostio_pool_is_capped_lru(monkeypatch):
         t.join()
     assert len(hostio._POOL.get(base, [])) <= hostio.POOL_PER_SIZE
     hostio.pool_clear()
+
+
+def test_cache_header_rejects_foreign_and_newer_files(tmp_path):
+    import struct
+
+    from paper_2308_00106_b200 import cache
+
+    f = tmp_path / "x.smecache"
+    f.write_bytes(b"NOTACACHE" + b"\0" * 100)
+    with pytest.raises(ValueError, match="not an sme cache"):
+        cache.read_header(f)
+    f.write_bytes(cache.MAGIC + struct.pack("<II", cache.VERSION + 1, 2) + b"{}")
+    with pytest.raises(ValueError, match="cache version"):
+        cache.read_header(f)
+    f.write_bytes(cache.MAGIC + struct.pack("<II", cache.VERSION, 11) + b'{"kind": 1}')
+    head, base = cache.read_header(f)
+    assert head == {"kind": 1} and base == cache.ALIGN
