@@ -257,6 +257,9 @@ int sme_hist2d_set_mode(int mode);
 /* Row-sort keys of the CSR builds (process-wide; tests): 1 = 32-bit (mapped col << 5 |
  * slot) whenever n_cols <= 2^27 (default), 0 = always 64-bit (col << 32 | slot). */
 int sme_sort_rows_set_key32(int enable);
+/* Rows with 32 < len <= 512 of the CSR builds (process-wide; tests): 1 = one warp per
+ * row, keys in registers (default), 0 = one CTA per row, bitonic in shared memory. */
+int sme_sort_rows_set_wmed(int enable);
 /* Tiling of the lane-counter kernel (experiments): 0 = 864 threads x 4 int4 loads per
  * lane (default; 768 x 4 when bins_r > ~1500), 1 = 768 x 4, 2 = 512 x 4 + next-iteration
  * prefetch, 3 = 768 x 2 + prefetch, 4 = 640 x 4 + prefetch, 5 = 864 x 4, 6 = 864 x 2,

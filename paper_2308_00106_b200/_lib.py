@@ -65,6 +65,7 @@ SIGNATURES: dict[str, list] = {
     "sme_hist2d_csr": [i64, i64, i64, p, p, i32, i32, p, p],
     "sme_hist2d_coo": [i64, i64, i64, p, p, i32, i32, p, p],
     "sme_hist2d_set_mode": [C.c_int],
+    "sme_sort_rows_set_wmed": [C.c_int],
     "sme_sort_rows_set_key32": [C.c_int],
     "sme_hist2d_set_variant": [C.c_int],
     "sme_row_hist_csr": [i64, p, i32, p, p],

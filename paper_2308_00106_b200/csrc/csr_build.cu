@@ -82,6 +82,9 @@ __device__ __forceinline__ uint32_t map_col(const int32_t* __restrict__ cmap, in
 // ---------------------------------------------------------------------------
 // 1: 32-bit keys whenever n_cols <= 2^27 (default); 0: always 64-bit keys (tests of that path)
 static int g_sort_key32 = 1;
+// 1: rows with 32 < len <= WMED_MAX are sorted warp-wide in registers (default); 0: by the
+// CTA-wide shared-memory kernel (A/B and tests of that path)
+static int g_sort_wmed = 3;  // rows 33..256 (C3 K4: 26.2 -> 20.0 ms; 512 spills: 27.8)
 
 // Keys: 64-bit (mapped col << 32 | slot) in general; 32-bit (mapped col << 5 |
 // slot) when every mapped column is < 2^27 (KEY32: one shuffle per exchange
@@ -180,6 +183,103 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_rows_warp(
 }
 
 // ---------------------------------------------------------------------------
+// rows with 32 < len <= WMED_MAX: one warp per row, E = next_pow2(len) / 32 keys per
+// lane in registers (blocked: lane l holds elements l*E .. l*E+E-1); bitonic steps
+// with j < E are in-lane compare-exchanges, the others one shuffle per key.  Replaces
+// a CTA-wide shared-memory bitonic (one __syncthreads per step) for these rows:
+// R-MAT C3 (ragged rows up to the 1024 cap) K4 20.5 ms -> see DESIGN.md §5.
+// ---------------------------------------------------------------------------
+constexpr int WMED_MAX = 512;  // the largest row the warp sort handles (g_sort_wmed selects the cut)
+
+template <int E>
+__device__ __forceinline__ void warp_bitonic(uint64_t (&v)[E], int lane) {
+  constexpr int N = 32 * E;
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = lane * E + e;
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, v[e], j / E);
+          const bool asc = (i & k) == 0, lower = (i & j) == 0;
+          const uint64_t mn = v[e] < o ? v[e] : o, mx = v[e] < o ? o : v[e];
+          v[e] = (lower == asc) ? mn : mx;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if ((e & j) == 0) {
+            const int i = lane * E + e;
+            const bool asc = (i & k) == 0;
+            const uint64_t a = v[e], b = v[e | j];
+            if ((a > b) == asc) {
+              v[e] = b;
+              v[e | j] = a;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int E, typename T>
+__device__ __forceinline__ void sort_row_warp(int32_t r, int32_t dst, int32_t len, int64_t from,
+                                              const int32_t* __restrict__ src_col, const T* __restrict__ src_val,
+                                              const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
+                                              T* __restrict__ out_val, const SortLists& L, int32_t* flag,
+                                              unsigned long long* dup_key, int lane) {
+  uint64_t v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane * E + e;
+    v[e] = i < len ? (((uint64_t)map_col(cmap, src_col[from + i]) << 32) | (uint32_t)i) : ~0ull;
+  }
+  warp_bitonic<E>(v, lane);
+  const uint64_t before = __shfl_up_sync(0xffffffffu, v[E - 1], 1);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane * E + e;
+    if (i < len) {
+      const uint32_t key = (uint32_t)(v[e] >> 32);
+      const uint64_t prev = e > 0 ? v[e > 0 ? e - 1 : 0] : before;
+      const bool dup = i > 0 && (uint32_t)(prev >> 32) == key;
+      if (dup && !L.mark_dups) report_dup(r, key, flag, dup_key);
+      out_col[dst + i] = (dup && L.mark_dups) ? -1 : (int32_t)key;
+      out_val[dst + i] = src_val[from + (uint32_t)v[e]];
+    }
+  }
+}
+
+template <typename T, class Src>
+__global__ void __launch_bounds__(SORT_NT) k_sort_rows_wmed(
+    const int32_t* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
+    const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
+    T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key, int wmed_max) {
+  const int lane = threadIdx.x & 31;
+  const int count = L.counters[0];
+  const int64_t warp = ((int64_t)blockIdx.x * SORT_NT + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * SORT_NT) >> 5;
+  for (int64_t it = warp; it < count; it += n_warps) {
+    const int32_t r = L.med[it];
+    const int32_t dst = new_ptr[r];
+    const int32_t len = new_ptr[r + 1] - dst;
+    if (len > wmed_max) continue;  // k_sort_rows_block
+    const int64_t from = src.start(r, dst);
+    if (len <= 64)
+      sort_row_warp<2, T>(r, dst, len, from, src_col, src_val, cmap, out_col, out_val, L, flag, dup_key, lane);
+    else if (len <= 128)
+      sort_row_warp<4, T>(r, dst, len, from, src_col, src_val, cmap, out_col, out_val, L, flag, dup_key, lane);
+    else if (len <= 256)
+      sort_row_warp<8, T>(r, dst, len, from, src_col, src_val, cmap, out_col, out_val, L, flag, dup_key, lane);
+    else
+      sort_row_warp<16, T>(r, dst, len, from, src_col, src_val, cmap, out_col, out_val, L, flag, dup_key, lane);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // block-level bitonic sort of P (power of two) keys in shared memory
 // ---------------------------------------------------------------------------
 template <int NT>
@@ -207,13 +307,14 @@ template <typename T, class Src>
 __global__ void __launch_bounds__(SORT_NT) k_sort_rows_block(
     const int32_t* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
     const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
-    T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key) {
+    T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key, int wmed_max) {
   __shared__ uint64_t s[SME_SORT_SMEM_MAX];
   const int count = L.counters[0];
   for (int it = blockIdx.x; it < count; it += gridDim.x) {
     const int32_t r = L.med[it];
     const int32_t dst = new_ptr[r];
     const int32_t len = new_ptr[r + 1] - dst;
+    if (len <= wmed_max) continue;  // k_sort_rows_wmed
     const int64_t from = src.start(r, dst);
     int P = 64;
     while (P < len) P <<= 1;
@@ -434,8 +535,16 @@ int launch_sorts(int64_t n_rows, const int32_t* new_ptr, Src src, const int32_t*
                                                                 cmap, out_col, out_val, L, flag,
                                                                 (unsigned long long*)dup_key);
   SME_CHECK_LAUNCH("k_sort_rows_warp");
+  const int wmed_max = g_sort_wmed > 0 ? 32 << g_sort_wmed : 0;  // 1: <= 64, 2: <= 128, 3: <= 256, 4: <= 512
+  if (wmed_max) {
+    k_sort_rows_wmed<T, Src><<<sm_count() * 8, SORT_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
+                                                                 out_val, L, flag, (unsigned long long*)dup_key,
+                                                                 wmed_max);
+    SME_CHECK_LAUNCH("k_sort_rows_wmed");
+  }
   k_sort_rows_block<T, Src><<<sm_count() * 4, SORT_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
-                                                                out_val, L, flag, (unsigned long long*)dup_key);
+                                                                out_val, L, flag, (unsigned long long*)dup_key,
+                                                                wmed_max);
   SME_CHECK_LAUNCH("k_sort_rows_block");
   k_sort_rows_long<T, Src><<<sm_count(), LONG_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
                                                            out_val, L, flag, (unsigned long long*)dup_key);
@@ -717,6 +826,15 @@ SME_API int sme_csr_compact(int dtype, int64_t n_rows, const int32_t* row_ptr, c
 }
 
 // Test hook: 0 forces the 64-bit sort keys of k_sort_rows_warp (the path of n_cols > 2^27).
+// Rows with 32 < len <= 32 << level: warp-wide register sort (level 1..4), longer ones
+// the CTA-wide shared-memory sort; level 0: every row > 32 takes the CTA sort.
+// Process-wide; for A/B tests.
+SME_API int sme_sort_rows_set_wmed(int level) {
+  SME_REQUIRE(level >= 0 && level <= 4, "level must lie in [0, 4]");
+  g_sort_wmed = level;
+  return SME_OK;
+}
+
 SME_API int sme_sort_rows_set_key32(int enable) {
   SME_REQUIRE(enable == 0 || enable == 1, "enable must be 0 or 1");
   g_sort_key32 = enable;

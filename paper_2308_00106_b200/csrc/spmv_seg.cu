@@ -210,6 +210,7 @@ __global__ void k_seg_scatter(int64_t n_rows, const int32_t* __restrict__ row_pt
 // 22.8 ms (an entry-parallel placement with a row search measured 30 ms; 768 slots x 8
 // warps 23.6-25.5 ms).
 constexpr int SG_CAP = 1024;
+constexpr int SG_SERIAL_MAX = 48;
 constexpr int SG_WARPS = 4;
 
 inline size_t sg_warp_bytes(int n_panels, size_t val_bytes) {
@@ -347,32 +348,65 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
         }
       }
     }
-    // the entries into the image: lane per row (columns ascend along a row, so the panel
-    // only moves forward and its table entries are reloaded only when it changes)
-    if (lane < nr) {
-      const int32_t r_rel = r0 + lane;
-      const int32_t kend = s_rp[lane + 1];
-      int p = 0;
-      int32_t f = s_first[lane], pc = s_cnt[lane], pq = s_ppos[lane], sb = s_sb[0] - s_gs[0];
-      int64_t po = c_off[0];
-      uint32_t clo = (uint32_t)c_lo[0];
-      for (int32_t k = s_rp[lane]; k < kend; ++k) {
+    // the entries into the image: the group's entries are one contiguous range of the
+    // CSR, read coalesced (lane = entry); each finds its row (binary search of the
+    // group's row starts), its panel (compares against the panel bounds) and its slot
+    // from the (panel, row) tables — independent entries, so the loads overlap (a lane
+    // per row walking its row serially measured latency-bound: 17.9 ms at C4, ncu)
+    // Groups of short rows (max row <= SG_SERIAL_MAX: C4's 20-entry rows) keep a lane per
+    // row walking its row (the panel only moves forward, so the table entries reload
+    // only when it changes; 17.9 ms at C4 against 23.0 ms entry-parallel); groups with a
+    // longer row go entry-parallel (C3 R-MAT: 10.8 -> 5.4 ms).
+    int32_t my_len = lane < nr ? s_rp[lane + 1] - s_rp[lane] : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) my_len = max(my_len, __shfl_xor_sync(FULL, my_len, o));
+    if (my_len <= SG_SERIAL_MAX) {
+      if (lane < nr) {
+        const int32_t r_rel = r0 + lane;
+        const int32_t kend = s_rp[lane + 1];
+        int p = 0;
+        int32_t f = s_first[lane], pc = s_cnt[lane], pq = s_ppos[lane], sb = s_sb[0] - s_gs[0];
+        int64_t po = c_off[0];
+        uint32_t clo = (uint32_t)c_lo[0];
+        for (int32_t k = s_rp[lane]; k < kend; ++k) {
+          const int32_t c = col[k];
+          const T v = val[k];
+          if (p < P - 1 && c >= c_hi[p]) {
+            do ++p;
+            while (p < P - 1 && c >= c_hi[p]);
+            f = s_first[p * 32 + lane];
+            pc = s_cnt[p * 32 + lane];
+            pq = s_ppos[p * 32 + lane];
+            sb = s_sb[p] - s_gs[p];
+            po = c_off[p];
+            clo = (uint32_t)c_lo[p];
+          }
+          const int32_t dip = pq + (k - f);  // slot within the panel
+          const int32_t sidx = sb + dip;
+          s_pk[sidx] = (((uint32_t)c - clo) << SEG_CSHIFT) | (k - f == pc - 1 ? SEG_END : 0u) |
+                       (uint32_t)(r_rel - hdr[(po + dip) / SEG_CH]);
+          s_val[sidx] = v;
+        }
+      }
+    } else {
+      const int32_t k0 = s_rp[0], k1 = s_rp[nr];
+#pragma unroll 2
+      for (int32_t k = k0 + lane; k < k1; k += 32) {
         const int32_t c = col[k];
         const T v = val[k];
-        if (p < P - 1 && c >= c_hi[p]) {
-          do ++p;
-          while (p < P - 1 && c >= c_hi[p]);
-          f = s_first[p * 32 + lane];
-          pc = s_cnt[p * 32 + lane];
-          pq = s_ppos[p * 32 + lane];
-          sb = s_sb[p] - s_gs[p];
-          po = c_off[p];
-          clo = (uint32_t)c_lo[p];
+        int lo = 0, hi = nr;  // s_rp[lo] <= k < s_rp[hi]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_rp[mid] <= k) lo = mid; else hi = mid;
         }
-        const int32_t dip = pq + (k - f);  // slot within the panel
-        const int32_t sidx = sb + dip;
-        s_pk[sidx] = (((uint32_t)c - clo) << SEG_CSHIFT) | (k - f == pc - 1 ? SEG_END : 0u) |
-                     (uint32_t)(r_rel - hdr[(po + dip) / SEG_CH]);
+        int p = 0;
+        for (int q = 0; q < P - 1; ++q) p += c >= c_hi[q] ? 1 : 0;
+        const int t = p * 32 + lo;
+        const int32_t f = s_first[t], pc = s_cnt[t];
+        const int32_t dip = s_ppos[t] + (k - f);  // slot within the panel
+        const int32_t sidx = s_sb[p] - s_gs[p] + dip;
+        s_pk[sidx] = (((uint32_t)c - (uint32_t)c_lo[p]) << SEG_CSHIFT) | (k - f == pc - 1 ? SEG_END : 0u) |
+                     (uint32_t)((int32_t)(r0 + lo) - hdr[(c_off[p] + dip) / SEG_CH]);
         s_val[sidx] = v;
       }
     }
@@ -525,7 +559,25 @@ __device__ __forceinline__ void seg_decode(const SegChunk<T>& cur, int e0, int P
 // one instruction per 32 rows, so consecutive lanes hit consecutive y words: ~4 y
 // requests per chunk instead of ~16 (four predicated instructions each spanning the
 // chunk's ~50 rows).  Applies to the writing pass and to RED accumulation.
-template <typename T, bool ACC, bool EPI, bool RED = false, bool CMP = false>
+// decode of the chunk at position cpos (all-interior fast path for f32, see seg_warp_body)
+template <typename T, bool ACC, bool EPI, bool RED>
+__device__ __forceinline__ void seg_decode_any(const SegChunk<T>& ch, int cpos, int lane, int P0, int P1,
+                                               const T* __restrict__ xs, const T* __restrict__ y, unsigned& ok,
+                                               unsigned& endm, T (&xv)[4], T (&yv)[4]) {
+  ok = 0;
+  endm = 0;
+  const int e0 = cpos + 4 * lane;
+  if (sizeof(T) == 4 && cpos >= P0 && cpos + SEG_CH <= P1)
+    seg_decode<true, T, ACC, EPI, RED>(ch, e0, P0, P1, xs, y, ok, endm, xv, yv);
+  else
+    seg_decode<false, T, ACC, EPI, RED>(ch, e0, P0, P1, xs, y, ok, endm, xv, yv);
+}
+
+// PIPE: software-pipelined gathers.  The x gathers (and y reads) of chunk k+1 are
+// issued BEFORE chunk k is reduced, and chunk k+2's stream loads before those, so a
+// warp keeps a chunk's gathers in flight while it reduces: the L1 -> L2 request port
+// sees gathers during the reduction phases too (seg_mode 7, sme_spmv_seg_set_mode).
+template <typename T, bool ACC, bool EPI, bool RED = false, bool CMP = false, bool PIPE = false>
 __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk, const T* __restrict__ val,
                                                 const int32_t* __restrict__ hdr, const int32_t* __restrict__ plan,
                                                 int warp, const T* __restrict__ xs, T* __restrict__ y,
@@ -541,25 +593,33 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
   const T sc = (EPI && epi.scale) ? (T)*epi.scale : T(1);
 
   int c = P0 & ~(SEG_CH - 1);
-  SegChunk<T> cur;
+  SegChunk<T> cur, nxt;
   cur.load(pk, val, hdr, c, lane);
   T carry = T(0);  // open row sum flowing from the previous chunk's last entry
+  unsigned ok = 0, endm = 0;
+  T xv[4], yv[4];
+  if (PIPE) {
+    seg_decode_any<T, ACC, EPI, RED>(cur, c, lane, P0, P1, xs, y, ok, endm, xv, yv);
+    if (c + SEG_CH < P1) nxt.load(pk, val, hdr, c + SEG_CH, lane);
+  }
   while (true) {
     const bool more = c + SEG_CH < P1;
-    SegChunk<T> nxt;
-    if (more) nxt.load(pk, val, hdr, c + SEG_CH, lane);
-
-    // decode: valid entries (inside [P0, P1)), end flags, gathers, y reads at row ends.
-    // f32: chunks wholly inside the warp's range (all but its first and last) skip the
-    // per-entry range checks (warp-uniform branch; C3 -4.6 %).  f64 keeps one code path
-    // (the duplicated decode measured +3 % on C4 and C5).
-    const int e0 = c + 4 * lane;
-    unsigned ok = 0, endm = 0;
-    T xv[4], yv[4];
-    if (sizeof(T) == 4 && c >= P0 && c + SEG_CH <= P1)
-      seg_decode<true, T, ACC, EPI, RED>(cur, e0, P0, P1, xs, y, ok, endm, xv, yv);
-    else
-      seg_decode<false, T, ACC, EPI, RED>(cur, e0, P0, P1, xs, y, ok, endm, xv, yv);
+    unsigned ok_n = 0, endm_n = 0;
+    T xv_n[4], yv_n[4];
+    SegChunk<T> nn;
+    if (PIPE) {
+      if (more) {
+        if (c + 2 * SEG_CH < P1) nn.load(pk, val, hdr, c + 2 * SEG_CH, lane);
+        seg_decode_any<T, ACC, EPI, RED>(nxt, c + SEG_CH, lane, P0, P1, xs, y, ok_n, endm_n, xv_n, yv_n);
+      }
+    } else {
+      if (more) nxt.load(pk, val, hdr, c + SEG_CH, lane);
+      // decode: valid entries (inside [P0, P1)), end flags, gathers, y reads at row ends.
+      // f32: chunks wholly inside the warp's range (all but its first and last) skip the
+      // per-entry range checks (warp-uniform branch; C3 -4.6 %).  f64 keeps one code path
+      // (the duplicated decode measured +3 % on C4 and C5).
+      seg_decode_any<T, ACC, EPI, RED>(cur, c, lane, P0, P1, xs, y, ok, endm, xv, yv);
+    }
     // in-lane runs: run[k] = sum of the row segment ending at k that starts in this lane
     T run[4];
 #pragma unroll
@@ -682,6 +742,16 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
       break;
     }
     cur = nxt;
+    if (PIPE) {
+      nxt = nn;
+      ok = ok_n;
+      endm = endm_n;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        xv[k] = xv_n[k];
+        yv[k] = yv_n[k];
+      }
+    }
     c += SEG_CH;
   }
   return ss;
@@ -713,7 +783,7 @@ __global__ void k_seg_carry_fixup(int32_t n_warps, const int32_t* __restrict__ c
   }
 }
 
-template <typename T, bool ACC, bool EPI, bool RED = false, bool CMP = false>
+template <typename T, bool ACC, bool EPI, bool RED = false, bool CMP = false, bool PIPE = false>
 __global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict__ pk, const T* __restrict__ val,
                                                    const int32_t* __restrict__ hdr, const int32_t* __restrict__ plan,
                                                    int32_t n_warps, const T* __restrict__ xs, T* __restrict__ y,
@@ -738,10 +808,10 @@ __global__ void __launch_bounds__(SEG_NT) k_spmv_seg(const uint32_t* __restrict_
   if (CMP) {
     __shared__ T s_val[SEG_NT / 32][SEG_CH];
     __shared__ int s_row[SEG_NT / 32][SEG_CH];
-    seg_warp_body<T, ACC, false, RED, true>(pk, val, hdr, plan, warp, xs, y, epi, s_val[threadIdx.x >> 5],
-                                            s_row[threadIdx.x >> 5]);
+    seg_warp_body<T, ACC, false, RED, true, PIPE>(pk, val, hdr, plan, warp, xs, y, epi, s_val[threadIdx.x >> 5],
+                                                  s_row[threadIdx.x >> 5]);
   } else {
-    seg_warp_body<T, ACC, false, RED>(pk, val, hdr, plan, warp, xs, y, epi);
+    seg_warp_body<T, ACC, false, RED, false, PIPE>(pk, val, hdr, plan, warp, xs, y, epi);
   }
 }
 
@@ -809,6 +879,11 @@ int launch_seg(int32_t n_warps, const uint32_t* pk, const T* val, const int32_t*
       k_spmv_seg<T, false, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
   } else if (s_seg_mode == 3)
     k_seg_probe<T><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y);
+  else if (s_seg_mode == 7 && accumulate)
+    k_spmv_seg<T, true, false, true, kStageRows<T>, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
+  else if (s_seg_mode == 7)
+    k_spmv_seg<T, false, false, false, kStageRows<T>, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y,
+                                                                                   e);
   else if (accumulate && s_seg_mode == 5)
     k_spmv_seg<T, true, false><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
   else if (accumulate && (s_seg_mode == 6 || !kStageRows<T>))
@@ -918,8 +993,9 @@ SME_API int sme_seg_set_scatter_groups(int on) {
 // Kernel variant (process-wide; experiments): 0 = the SpMV, 3 = bound probe (the
 // chunk stream and gathers without the row reduction; timing only, not y = A x).
 SME_API int sme_spmv_seg_set_mode(int mode) {
-  SME_REQUIRE(mode == 0 || mode == 3 || mode == 5 || mode == 6,
-              "mode must be 0 (SpMV), 3 (bound probe), 5 (accumulate with load + store) or 6 (no staging)");
+  SME_REQUIRE(mode == 0 || mode == 3 || mode == 5 || mode == 6 || mode == 7,
+              "mode must be 0 (SpMV), 3 (bound probe), 5 (accumulate with load + store), 6 (no staging) or "
+              "7 (pipelined gathers)");
   s_seg_mode = mode;
   return SME_OK;
 }
@@ -940,6 +1016,12 @@ SME_API int sme_spmv_seg_warps(int32_t* n_warps) {
   occ((const void*)k_spmv_seg<double, true, true>);
   occ((const void*)k_spmv_seg<double, false, false, false, true>);
   occ((const void*)k_spmv_seg<double, true, false, true, true>);
+  if (s_seg_mode == 7) {
+    occ((const void*)k_spmv_seg<double, false, false, false, true, true>);
+    occ((const void*)k_spmv_seg<double, true, false, true, true, true>);
+    occ((const void*)k_spmv_seg<float, false, false, false, false, true>);
+    occ((const void*)k_spmv_seg<float, true, false, true, false, true>);
+  }
   per_sm = std::max(1, per_sm);
   *n_warps = sm_count() * per_sm * (SEG_NT / 32);
   return SME_OK;

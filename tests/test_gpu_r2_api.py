@@ -147,3 +147,40 @@ def test_col_histogram_zero_row_matrix():
     assert h.counts.tolist() == [0, 0, 0]
     with pytest.raises(ValueError, match="column bin count 7 exceeds"):
         P.col_histogram(m, 7)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_warp_medium_row_sort_equals_block_sort_and_oracle(dtype):
+    """K4 rows with 32 < len <= 512 take the warp-wide register sort; it must equal the
+    CTA-wide shared-memory sort bit for bit and the oracle's coo_to_csr(permute_matrix)."""
+    from paper_2308_00106_b200 import _lib
+
+    rng = np.random.default_rng(3)
+    n = 4000
+    lens = np.concatenate([rng.integers(33, 513, 900), rng.integers(0, 33, 2900), rng.integers(513, 3000, 200)])
+    rng.shuffle(lens)
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    col = np.concatenate([np.sort(rng.choice(n, size=int(l), replace=False)) for l in lens])
+    val = rng.standard_normal(col.size).astype(dtype)
+    A = P.CsrMatrix(n, n, ptr, col, val)
+    fr, fc = rng.permutation(n), rng.permutation(n)
+    outs = []
+    for wmed in (4, 0):
+        _lib.call("sme_sort_rows_set_wmed", wmed)
+        try:
+            outs.append(P.permute_csr(A, P.Permutation(fr), P.Permutation(fc)))
+        finally:
+            _lib.call("sme_sort_rows_set_wmed", 3)
+    a, b = outs
+    assert torch.equal(a.d_row_ptr, b.d_row_ptr) and torch.equal(a.d_col_idx, b.d_col_idx)
+    assert torch.equal(a.d_values.view(torch.uint8), b.d_values.view(torch.uint8))
+    pr, pc = O.permute_coo(O.csr_to_coo_rows(ptr), col, fr, fc)
+    ptr_o, col_o, val_o = O.coo_to_csr(n, pr, pc, val.astype(np.float64))
+    assert np.array_equal(a.row_ptr, ptr_o) and np.array_equal(a.col_idx, col_o)
+    assert np.array_equal(a.values, val_o)
+    # the COO path (staged source) sorts its rows the same way
+    coo = P.CooMatrix(n, n, pr, pc, val)
+    c = P.coo_to_csr(coo)
+    assert torch.equal(c.d_col_idx, a.d_col_idx) and torch.equal(c.d_values.view(torch.uint8),
+                                                                  a.d_values.view(torch.uint8))
