@@ -777,12 +777,27 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
     if rank != 0:
         return None
     traffic = None
+    req_roof = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists() and world == 1:  # the table holds 1-GPU captures (a shard moves less)
         try:
-            traffic = json.loads(tf.read_text()).get(f"{args.config}/{resolved}")
+            table = json.loads(tf.read_text())
+            traffic = table.get(f"{args.config}/{resolved}")
+            reqs = table.get("l1_to_l2_requests", {}).get(f"{args.config}/{resolved}")
         except Exception:
-            traffic = None
+            traffic, reqs = None, None
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        if reqs and clk.get("sm_mhz"):
+            # the SM's L1 -> L2 (xbar) request port takes one request per clock: with one
+            # random gather per nonzero every request is its own line
+            ceil_rps = sms * clk["sm_mhz"] * 1e6
+            ach_rps = reqs / (kern_ms * 1e-3)
+            req_roof = {"requests_per_step": int(reqs), "achieved_g_per_s": round(ach_rps / 1e9, 2),
+                        "ceiling_g_per_s": round(ceil_rps / 1e9, 2), "frac": round(ach_rps / ceil_rps, 4),
+                        "min_step_ms_at_ceiling": round(reqs / ceil_rps * 1e3, 4),
+                        "source": "requests: ncu lts__t_requests_srcunit_tex.sum over one step's launches "
+                                  "(profiles/ncu_traffic.json); ceiling: 1 request / SM / clock at the median SM "
+                                  "clock sampled during the timed region"}
     out = {
         "metric": METRIC,
         "value": round(gflops, 3),
@@ -818,6 +833,7 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         },
         "other_kernels_gflops": others if world == 1 else None,
         "gather_roofline": gather_roof,
+        "request_roofline": req_roof,
         "entropy_bits": {"unpermuted": round(H_before, 6), "permuted": round(H_after, 6), "max": 14.0},
         "load_balance_148_even_rows": balance,
         "permute_ms": round(permute_ms, 2), "permute_warm_ms": round(permute_warm_ms, 2),
@@ -982,26 +998,65 @@ def run_sharded(args, cfg, rank: int, world: int) -> dict | None:
     ms_per_step = total_ms / steps
     gflops = 2 * nnz / (ms_per_step * 1e-3) / 1e9
 
-    # e2e: every rank copies its pinned host x chunk in and its y rows out each step
-    x_pin = torch.empty(plan.pad, dtype=B_loc.dtype, pin_memory=True)
-    x_pin.copy_(chunk.cpu())
-    y_pin = torch.empty(hi - lo, dtype=B_loc.dtype, pin_memory=True)
-    xc = torch.empty_like(chunk)
-    e_steps = max(3, min(steps, 10))
+    # e2e: every rank copies its pinned host x chunk in and its y rows out each step, with
+    # the copies of neighbouring steps overlapped (x of step k+1 in and y of step k-1 out
+    # on their own streams while step k exchanges and computes), as spmv_csr_pipelined
+    # does on one GPU; two pinned x chunks (x' and 2 x') alternate
+    x_pins = [torch.empty(plan.pad, dtype=B_loc.dtype, pin_memory=True) for _ in range(2)]
+    x_pins[0].copy_(chunk.cpu())
+    x_pins[1].copy_(x_pins[0] * 2)
+    y_pins = [torch.empty(hi - lo, dtype=B_loc.dtype, pin_memory=True) for _ in range(2)]
+    xcs = [torch.empty_like(chunk) for _ in range(2)]
+    ybs = [torch.empty(hi - lo, dtype=B_loc.dtype, device=dev) for _ in range(2)]
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    e_steps = max(4, min(steps, 10))
+
+    def e2e_run(n_steps: int) -> None:
+        computed, copied = [None, None], [None, None]
+        h2d.wait_stream(main)
+        d2h.wait_stream(main)
+        for k in range(n_steps):
+            b = k & 1
+            with torch.cuda.stream(h2d):
+                if computed[b] is not None:
+                    h2d.wait_event(computed[b])
+                xcs[b].copy_(x_pins[b], non_blocking=True)
+                landed = torch.cuda.Event()
+                landed.record(h2d)
+            main.wait_event(landed)
+            if copied[b] is not None:
+                main.wait_event(copied[b])
+            ybs[b].copy_(shard.step(xcs[b]))
+            done = torch.cuda.Event()
+            done.record(main)
+            computed[b] = done
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done)
+                y_pins[b].copy_(ybs[b], non_blocking=True)
+                out_ev = torch.cuda.Event()
+                out_ev.record(d2h)
+                copied[b] = out_ev
+        d2h.synchronize()
+        main.wait_stream(d2h)
+        main.wait_stream(h2d)
+
+    e2e_run(2)
     dist.barrier()
     torch.cuda.synchronize()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
     s0.record()
-    for _ in range(e_steps):
-        xc.copy_(x_pin, non_blocking=True)
-        yl = shard.step(xc)
-        y_pin.copy_(yl, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+    e2e_run(e_steps)
     s1.record()
     torch.cuda.synchronize()
-    et = torch.tensor([s0.elapsed_time(s1) / e_steps], device=dev)
+    wall_ms = (time.perf_counter() - w0) * 1e3 / e_steps
+    et = torch.tensor([max(s0.elapsed_time(s1) / e_steps, wall_ms)], device=dev)
     dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e_ms = float(et.item())
+    y_pin = y_pins[(e_steps - 1) & 1]
+    if (e_steps - 1) & 1:
+        y_loc = y_loc * 2.0
     e2e_err = P.relative_error(y_pin, y_loc)
     if e2e_err > tol:
         raise SystemExit(f"rank {rank}: host-vector sharded step differs from the device result: {e2e_err}")
@@ -1041,7 +1096,8 @@ def run_sharded(args, cfg, rank: int, world: int) -> dict | None:
                 "h2d_bytes_per_step": int(plan.pad * B_loc.d_values.element_size()) * world,
                 "d2h_bytes_per_step": int(n * B_loc.d_values.element_size()), "ms_per_step": round(e_ms, 4),
                 "rel_err": e2e_err,
-                "api": "rowshard.RowShardedSpMV.step (pinned host x chunk in, y rows out, every rank)"},
+                "api": "rowshard.RowShardedSpMV.step per rank: pinned host x chunk in, y rows out, copies of "
+                       "neighbouring steps overlapped (2 buffers)"},
         "clocks": clk,
         "gpu_launches": kernels_per_step * steps,
     }
@@ -1268,14 +1324,15 @@ def nccl_init_summary() -> dict | None:
     ranks, sizes, lines = set(), set(), []
     for path in glob.glob(str(Path(f).parent / "nccl.*.log")):
         for ln in Path(path).read_text(errors="replace").splitlines():
-            m = re.search(r"rank (\d+) nRanks (\d+)", ln)
+            m = re.search(r"rank (\d+) nranks (\d+)", ln, re.IGNORECASE)
             if m:
                 ranks.add(int(m.group(1)))
                 sizes.add(int(m.group(2)))
                 lines.append(ln.strip())
     for ln in lines[:16]:
         log(f"[nccl] {ln}")
-    return {"ranks_seen": sorted(ranks), "nranks": sorted(sizes), "init_lines": len(lines)}
+    return {"ranks_seen": sorted(ranks), "nranks": sorted(sizes), "init_lines": len(lines),
+            "log_files": len(glob.glob(str(Path(f).parent / "nccl.*.log")))}
 
 
 def dry_run(rank: int, world: int) -> None:
@@ -1331,7 +1388,12 @@ def main() -> None:
 
     import torch
 
-    if world > 1:
+    # BENCH_FORCE_SHARDED=1 (under torchrun, any world size incl. 1) takes the sharded
+    # multi-GPU path with its process group: with one rank this still runs every NCCL call
+    # of that path (all_gather / per-slot broadcasts on the side stream with
+    # SME_PIPELINED_EXCHANGE=force, all_reduce, barrier) — the check this 1-GPU pool allows
+    dist_mode = world > 1 or bool(os.environ.get("BENCH_FORCE_SHARDED"))
+    if dist_mode:
         if not os.environ.get("BENCH_SINGLE_DEVICE") and torch.cuda.device_count() < world:
             raise SystemExit(f"--gpus {world} needs {world} visible GPUs, found {torch.cuda.device_count()}")
         nccl_debug_to_file()
@@ -1341,7 +1403,7 @@ def main() -> None:
     dev_index = 0 if os.environ.get("BENCH_SINGLE_DEVICE") else local_rank
     backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
     torch.cuda.set_device(dev_index)
-    if world > 1:
+    if dist_mode:
         import torch.distributed as dist
 
         if backend == "nccl":
@@ -1350,17 +1412,17 @@ def main() -> None:
             dist.init_process_group(backend)
     try:
         if args.iterative:
-            out = run_iterative(args, cfg) if world == 1 else run_iterative_dist(args, cfg, rank, world)
+            out = run_iterative(args, cfg) if not dist_mode else run_iterative_dist(args, cfg, rank, world)
             if rank == 0:
                 print(json.dumps(out), flush=True)
             return
-        out = run_ours(args, cfg, rank, world) if world == 1 else run_sharded(args, cfg, rank, world)
+        out = run_ours(args, cfg, rank, world) if not dist_mode else run_sharded(args, cfg, rank, world)
         if out is not None:
-            if world > 1 and backend == "nccl":
+            if dist_mode and backend == "nccl":
                 out["nccl_init"] = nccl_init_summary()
             print(json.dumps(out), flush=True)
     finally:
-        if world > 1:
+        if dist_mode:
             import torch.distributed as dist
 
             dist.destroy_process_group()

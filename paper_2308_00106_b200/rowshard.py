@@ -150,11 +150,12 @@ class RowShardedSpMV:
     @property
     def pipelined(self) -> bool:
         """Per-slot broadcasts pipelined with the panel passes (seg shards); the env
-        SME_PIPELINED_EXCHANGE=0 falls back to one all-gather before the passes."""
+        SME_PIPELINED_EXCHANGE=0 falls back to one all-gather before the passes, =force
+        pipelines even a world of one (a 1-GPU check of the NCCL broadcast path)."""
         import os
 
-        return (self.seg is not None and self.plan.world > 1
-                and os.environ.get("SME_PIPELINED_EXCHANGE", "1") != "0")
+        mode = os.environ.get("SME_PIPELINED_EXCHANGE", "1")
+        return self.seg is not None and mode != "0" and (self.plan.world > 1 or mode == "force")
 
     def step(self, x_chunk: torch.Tensor, group=None) -> torch.Tensor:
         """Exchange the padded x chunks of every rank, then y_local = A_local x.
