@@ -200,13 +200,19 @@ int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz,
                     const int32_t* d_row_ptr_out /* from sme_permute_csr_row_ptr */,
                     int32_t* d_col_out, void* d_val_out, void* d_ws, size_t ws_bytes,
                     int64_t long_nnz, int32_t* d_flag, uint64_t* d_dup_key, sme_stream_t stream);
-/* mapped[k] = cmap[col[k]] (permute.py:98-102's column relabelling) in n_slices passes
- * over col, pass s mapping slice s of the columns with that slice of cmap pinned in L2
- * (access-policy window on `stream`; the caller reserves persisting L2).  A pre-pass of
- * sme_permute_csr (then called with col = mapped and no col_map) when cmap exceeds L2.
- * col 16-byte aligned. */
+/* mapped[k] = cmap[col[k]] (permute.py:98-102's column relabelling) in n_slices passes,
+ * pass s relabelling slice s of the columns while that slice of cmap stays L2-resident
+ * (the first pass reads col and writes mapped, the others rewrite mapped in place,
+ * whole 16-byte vectors; an access-policy window pins the slice when the caller
+ * reserved persisting L2).  col and mapped 16-byte aligned, n_cols < 2^31. */
 int sme_map_cols_sliced(int64_t nnz, int64_t n_cols, const int32_t* d_col, const int32_t* d_cmap,
                         int32_t* d_mapped, int32_t n_slices, sme_stream_t stream);
+/* The first n_passes (1..n_slices) of those passes: relabelled entries carry bit 31, the
+ * others keep their old id.  The K4 pre-pass when cmap exceeds L2: sme_permute_csr, given
+ * col = mapped and the same cmap, maps the unflagged entries (the last slice, L2-resident
+ * by then) and clears the flags inside its row sort. */
+int sme_map_cols_sliced_partial(int64_t nnz, int64_t n_cols, const int32_t* d_col, const int32_t* d_cmap,
+                                int32_t* d_mapped, int32_t n_slices, int32_t n_passes, sme_stream_t stream);
 
 /* Rows longer than this are sorted through global scratch (long-row path). */
 #define SME_SORT_SMEM_MAX 4096

@@ -59,6 +59,7 @@ SIGNATURES: dict[str, list] = {
     "sme_permute_csr": [C.c_int, i64, i64, i64, p, p, p, p, p, p, p, p, p, sz, i64, p, p, p],
     "sme_long_row_nnz": [i64, p, p, p],
     "sme_map_cols_sliced": [i64, i64, p, p, p, i32, p],
+    "sme_map_cols_sliced_partial": [i64, i64, p, p, p, i32, i32, p],
     "sme_csr_validate": [i64, i64, i64, p, p, p, p],
     "sme_row_stats": [i64, p, p, p],
     "sme_csr_expand_rows": [i64, p, p, p],

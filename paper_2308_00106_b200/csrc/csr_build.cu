@@ -11,7 +11,8 @@
 //      slots (order inside a row is arbitrary here);
 //   3. segmented sort inside every row by (mapped) column, values following
 //      bit-exactly, adjacent-equal columns flagged as duplicates.  Rows are
-//      dispatched by length: <= 32 -> sub-warp bitonic network in registers
+//      dispatched by length: <= 32 -> a warp per 32 rows, transposed through shared
+//      memory so one thread sorts one row with a register bitonic network
 //      (G = next_pow2(max len in the warp's 32 rows) lanes per row);
 //      <= SME_SORT_SMEM_MAX -> one CTA, bitonic in shared memory;
 //      longer -> one CTA, shared-memory chunk sort + global merge passes.
@@ -56,14 +57,18 @@ inline SortLists carve_lists(char* p, int64_t n_rows, int64_t long_nnz) {
 }
 
 // Where the entries of output row r are read from.
+// start(r, dst) = where(r); split into the old row id (key, a coalesced load) and the
+// dependent old_ptr gather (start_of) so the warp sort can issue them a phase apart.
 struct SrcGather {  // permuted CSR: old row inv[r] of the source CSR
   const int32_t* old_ptr;
   const int32_t* inv;
-  __device__ __forceinline__ int64_t start(int32_t r, int32_t /*dst*/) const {
-    return old_ptr[inv ? inv[r] : r];
-  }
+  __device__ __forceinline__ int32_t key(int32_t r) const { return inv ? inv[r] : r; }
+  __device__ __forceinline__ int64_t start_of(int32_t k, int32_t /*dst*/) const { return old_ptr[k]; }
+  __device__ __forceinline__ int64_t start(int32_t r, int32_t dst) const { return start_of(key(r), dst); }
 };
 struct SrcStaged {  // COO path: the row's slots in the staging arrays
+  __device__ __forceinline__ int32_t key(int32_t /*r*/) const { return 0; }
+  __device__ __forceinline__ int64_t start_of(int32_t /*k*/, int32_t dst) const { return dst; }
   __device__ __forceinline__ int64_t start(int32_t /*r*/, int32_t dst) const { return dst; }
 };
 
@@ -73,12 +78,14 @@ __device__ __forceinline__ void report_dup(int32_t row, uint32_t col, int32_t* f
   atomicMin(dup_key, ((unsigned long long)(uint32_t)row << 32) | col);
 }
 
+// New column id of a source entry: cmap[c], or, for an entry the sliced pre-map
+// (sme_map_cols_sliced_partial) already relabelled, its id with the bit-31 flag cleared.
 __device__ __forceinline__ uint32_t map_col(const int32_t* __restrict__ cmap, int32_t c) {
-  return (uint32_t)(cmap ? __ldg(cmap + c) : c);
+  return (uint32_t)(cmap ? (c < 0 ? (c & 0x7fffffff) : __ldg(cmap + c)) : c);
 }
 
 // ---------------------------------------------------------------------------
-// rows with len <= 32: sub-warp bitonic sort in registers
+// rows with len <= 32: thread-per-row register networks on a transposed tile
 // ---------------------------------------------------------------------------
 // 1: 32-bit keys whenever n_cols <= 2^27 (default); 0: always 64-bit keys (tests of that path)
 static int g_sort_key32 = 1;
@@ -108,27 +115,147 @@ struct SortKey<true> {
   __device__ static int slot(K k) { return (int)(k & 31u); }
 };
 
+// Ascending bitonic network over N keys held in registers (all indices static: every
+// compare-exchange is a min and a max, no shuffles).
+template <int N, typename K>
+__device__ __forceinline__ void bitonic_regs(K (&a)[N]) {
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const K x = a[i], y = a[l];
+          const K lo = x < y ? x : y, hi = x < y ? y : x;
+          const bool up = (i & k) == 0;
+          a[i] = up ? lo : hi;
+          a[l] = up ? hi : lo;
+        }
+      }
+}
+
+constexpr int SORT_STRIDE = 33;  // row pitch of the per-warp key tile (conflict-free rows and columns)
+constexpr int SORT_UNROLL = 8;   // rows per unrolled load / store step (loads in flight per lane)
+constexpr int TILE_NT = 128;     // k_sort_rows_warp block: 4 warps, 17 KB (32-bit keys) / 34 KB of tiles
+
+// Rows of up to 32 entries, a warp per group of 32 rows, in three phases per group:
+//   A. coalesced loads: the warp walks the group's rows, lane l reading entry l of each
+//      (column id, relabelled through p_c), and writes the key (new column, entry slot)
+//      into row r of a 32 x 33 shared-memory tile;
+//   B. thread per row: lane t reads row t of the tile into registers, sorts it with an
+//      N-key bitonic network (N = 8/16/32 by the group's longest row; keys past a row's
+//      length are NONE) and writes it back;
+//   C. coalesced stores: the warp walks the rows again, lane l writing entry l of the
+//      sorted row (column, and the value its slot names, read from the source row),
+//      flagging a key equal in column to its predecessor as a duplicate.
+// About 40 warp instructions per row of 20, against ~160 for a shuffle network with a
+// lane per entry, which left the kernel issue-bound (ncu, C4: 11 ms at 64 % issue).
+template <typename T, class Src, bool KEY32, int N>
+__device__ __forceinline__ void sort_group_tile(typename SortKey<KEY32>::K* tile, int lane, int64_t g,
+                                                int32_t len, int32_t dst, int64_t from,
+                                                const int32_t* __restrict__ src_col, const T* __restrict__ src_val,
+                                                const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
+                                                T* __restrict__ out_val, const SortLists& L, int32_t* flag,
+                                                unsigned long long* dup_key, uint64_t keep, uint64_t once) {
+  using SK = SortKey<KEY32>;
+  using K = typename SK::K;
+  // A: keys into the tile, SORT_UNROLL rows per step (their loads in flight together)
+#pragma unroll 1
+  for (int r0 = 0; r0 < 32; r0 += SORT_UNROLL) {
+    int32_t c[SORT_UNROLL];
+    bool in[SORT_UNROLL];
+#pragma unroll
+    for (int u = 0; u < SORT_UNROLL; ++u) {
+      const int32_t ml = __shfl_sync(0xffffffffu, len, r0 + u);
+      const int64_t mf = __shfl_sync(0xffffffffu, from, r0 + u);
+      in[u] = lane < ml;
+      c[u] = in[u] ? ld_stream_i1(src_col + mf + lane, once) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < SORT_UNROLL; ++u) {
+      uint32_t mc = (uint32_t)c[u];
+      if (cmap && in[u]) mc = c[u] < 0 ? (uint32_t)(c[u] & 0x7fffffff) : (uint32_t)ld_l1(cmap + c[u], keep);
+      tile[(r0 + u) * SORT_STRIDE + lane] = in[u] ? SK::make(mc, lane) : SK::NONE;
+    }
+  }
+  __syncwarp();
+  // B: lane t sorts row t
+  {
+    K k[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) k[i] = tile[lane * SORT_STRIDE + i];
+    bitonic_regs<N>(k);
+#pragma unroll
+    for (int i = 0; i < N; ++i) tile[lane * SORT_STRIDE + i] = k[i];
+  }
+  __syncwarp();
+  // C: sorted rows out, values gathered by slot from the source row
+#pragma unroll 1
+  for (int r0 = 0; r0 < 32; r0 += SORT_UNROLL) {
+    K key[SORT_UNROLL];
+    T w[SORT_UNROLL];
+    int32_t md[SORT_UNROLL];
+    bool in[SORT_UNROLL];
+#pragma unroll
+    for (int u = 0; u < SORT_UNROLL; ++u) {
+      const int32_t ml = __shfl_sync(0xffffffffu, len, r0 + u);
+      const int64_t mf = __shfl_sync(0xffffffffu, from, r0 + u);
+      md[u] = __shfl_sync(0xffffffffu, dst, r0 + u);
+      in[u] = lane < ml;
+      key[u] = tile[(r0 + u) * SORT_STRIDE + lane];
+      w[u] = in[u] ? ld_stream(src_val + mf + SK::slot(key[u]), once) : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < SORT_UNROLL; ++u) {
+      if (in[u]) {
+        const uint32_t col = SK::col(key[u]);
+        const bool dup = lane > 0 && SK::col(tile[(r0 + u) * SORT_STRIDE + lane - 1]) == col;
+        if (dup && !L.mark_dups) report_dup((int32_t)(g * 32 + r0 + u), col, flag, dup_key);
+        // streaming stores: the outputs must not push the column map (cmap) out of L2
+        st_stream(out_col + md[u] + lane, (dup && L.mark_dups) ? -1 : (int32_t)col);
+        st_stream(out_val + md[u] + lane, w[u]);
+      }
+    }
+  }
+  __syncwarp();
+}
+
 template <typename T, class Src, bool KEY32 = false>
-__global__ void __launch_bounds__(SORT_NT) k_sort_rows_warp(
+__global__ void __launch_bounds__(TILE_NT) k_sort_rows_warp(
     int32_t n_rows, const int32_t* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
     const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
     T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key) {
   using SK = SortKey<KEY32>;
   using K = typename SK::K;
+  __shared__ K s_tile[TILE_NT / 32][32 * SORT_STRIDE];
+  K* tile = s_tile[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t n_groups = ((int64_t)n_rows + 31) / 32;
-  const int64_t warp_global = ((int64_t)blockIdx.x * SORT_NT + threadIdx.x) >> 5;
-  const int64_t warps_total = ((int64_t)gridDim.x * SORT_NT) >> 5;
+  const int64_t warp_global = ((int64_t)blockIdx.x * TILE_NT + threadIdx.x) >> 5;
+  const int64_t warps_total = ((int64_t)gridDim.x * TILE_NT) >> 5;
   const uint64_t keep = policy_evict_last(), once = policy_evict_first();
-  for (int64_t g = warp_global; g < n_groups; g += warps_total) {
-    const int32_t r = (int32_t)(g * 32 + lane);
-    int32_t dst = 0, len = 0;
-    int64_t from = 0;
-    if (r < n_rows) {
-      dst = new_ptr[r];
-      len = new_ptr[r + 1] - dst;
-      if (len > 0) from = src.start(r, dst);
+  // group metadata, one row per lane, fetched a group ahead: new_ptr and the old row id
+  // (coalesced), then the old row's start (a gather) once the current group is running
+  int64_t g = warp_global;
+  int32_t n0 = 0, n1 = 0, k = 0;
+  auto meta_raw = [&](int64_t gg) {
+    const int32_t r = (int32_t)(gg * 32 + lane);
+    n0 = n1 = k = 0;
+    if (gg < n_groups && r < n_rows) {
+      n0 = new_ptr[r];
+      n1 = new_ptr[r + 1];
+      k = src.key(r);
     }
+  };
+  meta_raw(g);
+  int64_t from = n1 > n0 ? src.start_of(k, n0) : 0;
+  for (; g < n_groups; g += warps_total) {
+    const int32_t r = (int32_t)(g * 32 + lane);
+    const int32_t dst = n0;
+    int32_t len = n1 - n0;
+    const int64_t my_from = from;
     if (len > 32) {
       if (len <= SME_SORT_SMEM_MAX) {
         int slot = atomicAdd(&L.counters[0], 1);
@@ -140,45 +267,21 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_rows_warp(
       }
       len = 0;
     }
+    meta_raw(g + warps_total);
     int maxlen = len;
 #pragma unroll
     for (int o = 16; o; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    from = n1 > n0 ? src.start_of(k, n0) : 0;  // next group's starts: in flight during this one
     if (maxlen == 0) continue;
-    int G = 1;
-    while (G < maxlen) G <<= 1;
-    const int per_pass = 32 / G;
-    const int li = lane & (G - 1);
-    const int sub = lane / G;
-    for (int b = 0; b < 32; b += per_pass) {
-      const int rr = b + sub;  // row of this lane's sub-group, within the group of 32
-      const int32_t my_len = __shfl_sync(0xffffffffu, len, rr);
-      const int32_t my_dst = __shfl_sync(0xffffffffu, dst, rr);
-      const int64_t my_from = __shfl_sync(0xffffffffu, from, rr);
-      K v = SK::NONE;
-      if (li < my_len) {
-        const int32_t c = ld_stream_i1(src_col + my_from + li, once);
-        v = SK::make(cmap ? (uint32_t)ld_l1(cmap + c, keep) : (uint32_t)c, li);
-      }
-      for (int k = 2; k <= G; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          const K o = __shfl_xor_sync(0xffffffffu, v, j);
-          const bool asc = (li & k) == 0;
-          const bool lower = (li & j) == 0;
-          const K mn = v < o ? v : o, mx = v < o ? o : v;
-          v = (lower == asc) ? mn : mx;
-        }
-      }
-      const K prev = __shfl_up_sync(0xffffffffu, v, 1);
-      if (li < my_len) {
-        const uint32_t key = SK::col(v);
-        const int idx = SK::slot(v);
-        const bool dup = li > 0 && SK::col(prev) == key;
-        if (dup && !L.mark_dups) report_dup((int32_t)(g * 32 + rr), key, flag, dup_key);
-        // streaming stores: the outputs must not push the column map (cmap) out of L2
-        st_stream(out_col + my_dst + li, (dup && L.mark_dups) ? -1 : (int32_t)key);
-        st_stream(out_val + my_dst + li, ld_stream(src_val + my_from + idx, once));
-      }
-    }
+    if (maxlen <= 8)
+      sort_group_tile<T, Src, KEY32, 8>(tile, lane, g, len, dst, my_from, src_col, src_val, cmap, out_col, out_val,
+                                        L, flag, dup_key, keep, once);
+    else if (maxlen <= 16)
+      sort_group_tile<T, Src, KEY32, 16>(tile, lane, g, len, dst, my_from, src_col, src_val, cmap, out_col,
+                                         out_val, L, flag, dup_key, keep, once);
+    else
+      sort_group_tile<T, Src, KEY32, 32>(tile, lane, g, len, dst, my_from, src_col, src_val, cmap, out_col,
+                                         out_val, L, flag, dup_key, keep, once);
   }
 }
 
@@ -525,13 +628,13 @@ int launch_sorts(int64_t n_rows, const int32_t* new_ptr, Src src, const int32_t*
                  const int32_t* cmap, int32_t* out_col, T* out_val, SortLists L, int32_t* flag,
                  uint64_t* dup_key, cudaStream_t s, int64_t n_cols = INT32_MAX) {
   int64_t groups = (n_rows + 31) / 32;
-  int blocks = grid_for(groups * 32, SORT_NT, 8);
+  int blocks = grid_for(groups * 32, TILE_NT, 16);
   if (n_cols <= ((int64_t)1 << 27) && g_sort_key32)  // mapped columns < 2^27: 32-bit keys (col << 5 | slot)
-    k_sort_rows_warp<T, Src, true><<<blocks, SORT_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
+    k_sort_rows_warp<T, Src, true><<<blocks, TILE_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
                                                                cmap, out_col, out_val, L, flag,
                                                                (unsigned long long*)dup_key);
   else
-    k_sort_rows_warp<T, Src, false><<<blocks, SORT_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
+    k_sort_rows_warp<T, Src, false><<<blocks, TILE_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
                                                                 cmap, out_col, out_val, L, flag,
                                                                 (unsigned long long*)dup_key);
   SME_CHECK_LAUNCH("k_sort_rows_warp");
@@ -696,40 +799,76 @@ SME_API int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t n
 }
 
 namespace sme {
-// out[k] = cmap[col[k]] for the entries whose column lies in [lo, hi): one pass of the
-// column-sliced pre-map (the slice of cmap stays L2-resident during its pass)
-__global__ void k_map_cols_slice(int64_t nnz, const int32_t* __restrict__ col, const int32_t* __restrict__ cmap,
-                                 int32_t* __restrict__ out, int32_t lo, int32_t hi) {
-  const uint64_t once = policy_evict_first();
+// One pass of the column-sliced pre-map.  A random 4-byte gather from a column map
+// larger than L2 costs a 64-byte DRAM access (tools/l2fetch_bench.cu: 73 B of DRAM and
+// 86-90 G gathers/s from a 200 MB table, 287 G/s from a 50 MB one), so the map is
+// applied in passes, pass q relabelling only the columns of slice [lo, hi) while that
+// 1/n_slices of cmap stays L2-resident.  Every pass rewrites whole 16-byte vectors (no
+// partial-sector writes): an entry already relabelled carries bit 31 (columns are
+// < 2^31), and the last pass maps what is left and clears the flags.
+//   PASS 0: first of several (read col, write out)   PASS 1: middle (out in place)
+//   PASS 2: last (out in place)                       PASS 3: single pass (col -> out)
+template <int PASS>
+__device__ __forceinline__ int32_t map_one(int32_t v, const int32_t* __restrict__ cmap, int32_t lo, int32_t hi,
+                                           uint64_t keep) {
+  constexpr int32_t FLAG = (int32_t)0x80000000;
+  if (PASS == 3) return ld_l1(cmap + v, keep);
+  if (PASS == 2) return v < 0 ? (v & 0x7fffffff) : ld_l1(cmap + v, keep);
+  // PASS 0/1: flagged (negative) entries fail the range test
+  return (v >= lo && v < hi) ? (ld_l1(cmap + v, keep) | FLAG) : v;
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(256) k_map_cols_pass(int64_t nnz, const int32_t* __restrict__ src,
+                                                       const int32_t* __restrict__ cmap, int32_t* __restrict__ out,
+                                                       int32_t lo, int32_t hi) {
+  const uint64_t once = policy_evict_first(), keep = policy_evict_last();
   const int64_t n4 = nnz / 4;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
-    const int4 c = ld_stream_i4(reinterpret_cast<const int4*>(col) + q, once);
-    const int64_t k = q * 4;
-    if (c.x >= lo && c.x < hi) st_stream(out + k, __ldg(cmap + c.x));
-    if (c.y >= lo && c.y < hi) st_stream(out + k + 1, __ldg(cmap + c.y));
-    if (c.z >= lo && c.z < hi) st_stream(out + k + 2, __ldg(cmap + c.z));
-    if (c.w >= lo && c.w < hi) st_stream(out + k + 3, __ldg(cmap + c.w));
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // two vectors per thread per iteration: 8 independent gathers in flight
+  for (; q + stride < n4; q += 2 * stride) {
+    int4 a = ld_stream_i4(reinterpret_cast<const int4*>(src) + q, once);
+    int4 b = ld_stream_i4(reinterpret_cast<const int4*>(src) + q + stride, once);
+    a.x = map_one<PASS>(a.x, cmap, lo, hi, keep); a.y = map_one<PASS>(a.y, cmap, lo, hi, keep);
+    a.z = map_one<PASS>(a.z, cmap, lo, hi, keep); a.w = map_one<PASS>(a.w, cmap, lo, hi, keep);
+    b.x = map_one<PASS>(b.x, cmap, lo, hi, keep); b.y = map_one<PASS>(b.y, cmap, lo, hi, keep);
+    b.z = map_one<PASS>(b.z, cmap, lo, hi, keep); b.w = map_one<PASS>(b.w, cmap, lo, hi, keep);
+    __stcs(reinterpret_cast<int4*>(out) + q, a);
+    __stcs(reinterpret_cast<int4*>(out) + q + stride, b);
+  }
+  for (; q < n4; q += stride) {
+    int4 a = ld_stream_i4(reinterpret_cast<const int4*>(src) + q, once);
+    a.x = map_one<PASS>(a.x, cmap, lo, hi, keep); a.y = map_one<PASS>(a.y, cmap, lo, hi, keep);
+    a.z = map_one<PASS>(a.z, cmap, lo, hi, keep); a.w = map_one<PASS>(a.w, cmap, lo, hi, keep);
+    __stcs(reinterpret_cast<int4*>(out) + q, a);
   }
   if (blockIdx.x == 0)
-    for (int64_t k = n4 * 4 + threadIdx.x; k < nnz; k += blockDim.x) {
-      const int32_t c = col[k];
-      if (c >= lo && c < hi) out[k] = cmap[c];
-    }
+    for (int64_t k = n4 * 4 + threadIdx.x; k < nnz; k += blockDim.x) out[k] = map_one<PASS>(src[k], cmap, lo, hi, keep);
 }
 }  // namespace sme
 
-// mapped[k] = cmap[col[k]] (the column relabelling of permute_matrix, permute.py:98-102)
-// in n_slices passes over col, pass s mapping the columns of slice s with that slice of
-// cmap pinned in L2 (access-policy window on `stream`): the random cmap reads hit L2
-// instead of DRAM.  col must be 16-byte aligned.
-SME_API int sme_map_cols_sliced(int64_t nnz, int64_t n_cols, const int32_t* col, const int32_t* cmap,
-                                int32_t* mapped, int32_t n_slices, sme_stream_t stream) {
+// The first n_passes of the n_slices-pass column relabelling mapped[k] = cmap[col[k]]
+// (permute.py:98-102), pass q relabelling the columns of slice q with that slice of cmap
+// L2-resident (evict-last gathers, evict-first streams, and an access-policy window on
+// `stream` that pins the slice when the caller reserved persisting L2): the random cmap
+// reads hit L2 instead of costing a 64-byte DRAM access each.  The first pass reads col
+// and writes mapped, the others rewrite mapped in place.  With n_passes == n_slices the
+// result is the plain relabelling; with fewer, relabelled entries carry bit 31 and the
+// rest keep their old id, which the row sort of sme_permute_csr (given cmap) finishes:
+// it maps unflagged entries and clears the flag of the others.  col and mapped must be
+// 16-byte aligned; mapped may alias col only when n_slices == 1.
+SME_API int sme_map_cols_sliced_partial(int64_t nnz, int64_t n_cols, const int32_t* col, const int32_t* cmap,
+                                        int32_t* mapped, int32_t n_slices, int32_t n_passes,
+                                        sme_stream_t stream) {
   SME_REQUIRE(nnz >= 0 && n_cols >= 1 && n_slices >= 1 && col && cmap && mapped, "bad arguments");
-  SME_REQUIRE(((uintptr_t)col & 15) == 0, "col must be 16-byte aligned");
+  SME_REQUIRE(n_passes >= 1 && n_passes <= n_slices, "n_passes must be in [1, n_slices]");
+  SME_REQUIRE(n_cols <= INT32_MAX, "n_cols must be < 2^31");
+  SME_REQUIRE(((uintptr_t)col & 15) == 0 && ((uintptr_t)mapped & 15) == 0, "col and mapped must be 16-byte aligned");
   if (nnz == 0) return SME_OK;
   cudaStream_t s = as_stream(stream);
-  const int grid = sm_count() * 8;
-  for (int32_t q = 0; q < n_slices; ++q) {
+  const int grid = grid_for((nnz + 3) / 4, 256, 8);
+  for (int32_t q = 0; q < n_passes; ++q) {
     const int64_t lo = n_cols * q / n_slices, hi = n_cols * (q + 1) / n_slices;
     cudaStreamAttrValue attr = {};
     attr.accessPolicyWindow.base_ptr = const_cast<int32_t*>(cmap + lo);
@@ -737,13 +876,29 @@ SME_API int sme_map_cols_sliced(int64_t nnz, int64_t n_cols, const int32_t* col,
     attr.accessPolicyWindow.hitRatio = 1.0f;
     attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    SME_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &attr));
-    k_map_cols_slice<<<grid, 256, 0, s>>>(nnz, col, cmap, mapped, (int32_t)lo, (int32_t)hi);
-    SME_CHECK_LAUNCH("k_map_cols_slice");
+    if (n_slices > 1) SME_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &attr));
+    const int32_t* in = q == 0 ? col : mapped;
+    if (n_slices == 1)
+      k_map_cols_pass<3><<<grid, 256, 0, s>>>(nnz, in, cmap, mapped, (int32_t)lo, (int32_t)hi);
+    else if (q + 1 == n_slices)
+      k_map_cols_pass<2><<<grid, 256, 0, s>>>(nnz, in, cmap, mapped, (int32_t)lo, (int32_t)hi);
+    else if (q == 0)
+      k_map_cols_pass<0><<<grid, 256, 0, s>>>(nnz, in, cmap, mapped, (int32_t)lo, (int32_t)hi);
+    else
+      k_map_cols_pass<1><<<grid, 256, 0, s>>>(nnz, in, cmap, mapped, (int32_t)lo, (int32_t)hi);
+    SME_CHECK_LAUNCH("k_map_cols_pass");
   }
-  cudaStreamAttrValue clear = {};
-  SME_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &clear));
+  if (n_slices > 1) {
+    cudaStreamAttrValue clear = {};
+    SME_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &clear));
+  }
   return SME_OK;
+}
+
+// mapped[k] = cmap[col[k]]: all n_slices passes of the above.
+SME_API int sme_map_cols_sliced(int64_t nnz, int64_t n_cols, const int32_t* col, const int32_t* cmap,
+                                int32_t* mapped, int32_t n_slices, sme_stream_t stream) {
+  return sme_map_cols_sliced_partial(nnz, n_cols, col, cmap, mapped, n_slices, n_slices, stream);
 }
 
 SME_API int sme_row_stats(int64_t n_rows, const int32_t* row_ptr, int64_t* out, sme_stream_t stream) {

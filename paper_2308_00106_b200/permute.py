@@ -327,28 +327,35 @@ def _permute_coo(m: CooMatrix, p_r: Permutation | None, p_c: Permutation | None)
     return CooMatrix._from_device(m.n_rows, m.n_cols, row, col, m.d_values.clone(), csr_thunk=thunk)
 
 
-#: K4 pre-maps the columns in L2-resident slices of p_c when p_c exceeds this share of L2
-#: and the matrix has at least PREMAP_MIN_NNZ entries (0 disables the pre-map).  Off: at
-#: C4 it measured 31.6 ms against 22.4 ms for the in-sort gather (tools/k4_premap_ab.py;
-#: four full passes over col plus scattered 4-byte writes cost more than the DRAM misses
-#: they remove).  Results are bit-identical either way.
-PREMAP_L2_SHARE = 0.0
-PREMAP_MIN_NNZ = 1 << 26
+#: K4 relabels the columns in a pre-pass (sme_map_cols_sliced) when p_c is larger than
+#: PREMAP_SLICE_BYTES and the matrix has at least PREMAP_MIN_NNZ entries: one pass per
+#: PREMAP_SLICE_BYTES slice of p_c, each slice L2-resident while its gathers run.  A random
+#: 4-byte gather from a table larger than L2 costs a 64-byte DRAM access
+#: (tools/l2fetch_bench.cu: 86-90 G/s from 200 MB, 287 G/s from 50 MB, and 148-160 G/s from
+#: 100 MB: the random-gather working set that stays in L2 is about 50-60 MB).  None: auto;
+#: True/False force it on/off (tests).  Results are bit-identical either way.
+PREMAP: bool | None = None
+PREMAP_SLICE_BYTES = 48 << 20
+PREMAP_MIN_NNZ = 1 << 24
+#: reserve persisting L2 for the slice (access-policy window) during the pre-map passes
+PREMAP_PERSIST = False
+#: leave the last slice to the row sort (one pass over col fewer)
+PREMAP_FUSE_LAST = False
 
 
 def _premap_slices(m: CsrMatrix) -> int:
     """Number of column slices for the pre-map (0: gather p_c inside the row sort)."""
-    if not PREMAP_L2_SHARE or m.nnz < PREMAP_MIN_NNZ or m.d_col_idx.data_ptr() % 16:
+    if PREMAP is False or m.d_col_idx.data_ptr() % 16:
         return 0
-    from .panels import device_info
-
-    info = device_info()
     table = m.n_cols * 4
-    if table <= PREMAP_L2_SHARE * info["l2"]:
+    if PREMAP is None and (m.nnz < PREMAP_MIN_NNZ or table <= PREMAP_SLICE_BYTES):
         return 0
-    slice_cap = min(info["max_persisting_l2"], info["l2"] // 2)
-    n = -(-table // slice_cap)
-    _lib.call("sme_l2_set_persisting", min(info["max_persisting_l2"], -(-table // n)))
+    n = max(1, -(-table // PREMAP_SLICE_BYTES))
+    if PREMAP_PERSIST:
+        from .panels import device_info
+
+        info = device_info()
+        _lib.call("sme_l2_set_persisting", min(info["max_persisting_l2"], -(-table // n)))
     return int(n)
 
 
@@ -379,13 +386,17 @@ def permute_csr(m: CsrMatrix, p_r: Permutation | None, p_c: Permutation | None) 
     src_col, cmap = m.d_col_idx, (p_c.d_forward if p_c is not None else None)
     n_slices = _premap_slices(m) if cmap is not None else 0
     if n_slices:
-        # p_c larger than L2: relabel the columns first in L2-resident slices of p_c, so
-        # the row sort reads new column ids instead of gathering p_c from DRAM
+        # p_c larger than L2: relabel the columns of all but the last slice first, each
+        # pass with its slice of p_c L2-resident; the row sort then gathers only the last
+        # slice (L2-resident after the last pass) and clears the relabelled entries' flags
         src_col = torch.empty_like(m.d_col_idx)
-        _lib.call("sme_map_cols_sliced", m.nnz, m.n_cols, ptr(m.d_col_idx), ptr(cmap), ptr(src_col), n_slices,
-                  stream())
-        _lib.call("sme_l2_reset_persisting")
-        cmap = None
+        n_passes = n_slices - 1 if (PREMAP_FUSE_LAST and n_slices > 1) else n_slices
+        _lib.call("sme_map_cols_sliced_partial", m.nnz, m.n_cols, ptr(m.d_col_idx), ptr(cmap), ptr(src_col),
+                  n_slices, n_passes, stream())
+        if PREMAP_PERSIST:
+            _lib.call("sme_l2_reset_persisting")
+        if n_passes == n_slices:
+            cmap = None
     _lib.call("sme_permute_csr", _cuda.sme_dtype(m.d_values), m.n_rows, m.n_cols, m.nnz, ptr(m.d_row_ptr),
               ptr(src_col), ptr(m.d_values), ptr(inv_r), ptr(cmap),
               ptr(row_ptr), ptr(col), ptr(val), ptr(ws2), ws2.numel(), long_nnz, fl.flag_ptr, fl.dup_ptr,

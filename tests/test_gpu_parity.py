@@ -403,9 +403,14 @@ def test_panel_layout_matches_oracle(dev, rng, n_panels):
     assert O.relative_error(P.spmv_csr(m, x, "panel"), want) <= F64_TOL
 
 
-def test_permute_csr_premap_path_is_bit_identical(dev, rng):
-    """K4 with the column-sliced pre-map forced on (sme_map_cols_sliced, off by default)
-    builds the same permuted CSR, bit for bit, as the in-sort gather."""
+@pytest.mark.parametrize("fuse_last", [False, True])
+@pytest.mark.parametrize("slice_cols", [1 << 30, 20_000, 7_001, 997])
+def test_permute_csr_premap_path_is_bit_identical(dev, rng, slice_cols, fuse_last):
+    """K4 with the column pre-map forced on (sme_map_cols_sliced_partial: 1, 1, 3 and 21
+    slices, i.e. the single pass and the first / middle / last in-place flagged passes,
+    with the last slice mapped by its own pass or by the row sort, which then also clears
+    the flags) builds the same permuted CSR, bit for bit, as the in-sort gather, and the
+    same as the oracle."""
     import paper_2308_00106_b200.permute as PM
 
     n = 20_000
@@ -413,13 +418,17 @@ def test_permute_csr_premap_path_is_bit_identical(dev, rng):
     rows, cols = np.nonzero(mask)
     m = P.coo_to_csr(P.CooMatrix(400, n, rows, cols, rng.random(rows.size)))
     p_r, p_c = P.random_permutation(400, 3), P.random_permutation(n, 4)
-    saved = PM.PREMAP_L2_SHARE, PM.PREMAP_MIN_NNZ
+    saved = PM.PREMAP, PM.PREMAP_SLICE_BYTES, PM.PREMAP_FUSE_LAST
     try:
-        PM.PREMAP_L2_SHARE, PM.PREMAP_MIN_NNZ = 1e-9, 0
+        PM.PREMAP, PM.PREMAP_SLICE_BYTES, PM.PREMAP_FUSE_LAST = True, slice_cols * 4, fuse_last
+        assert PM._premap_slices(m) == -(-n // slice_cols)
         a = P.permute_csr(m, p_r, p_c)
-        PM.PREMAP_L2_SHARE = 0.0
+        PM.PREMAP = False
         b = P.permute_csr(m, p_r, p_c)
     finally:
-        PM.PREMAP_L2_SHARE, PM.PREMAP_MIN_NNZ = saved
+        PM.PREMAP, PM.PREMAP_SLICE_BYTES, PM.PREMAP_FUSE_LAST = saved
+    pr, pc = O.permute_coo(rows, cols, p_r.forward, p_c.forward)
+    optr, ocol, _ = O.coo_to_csr(400, pr, pc, np.zeros(rows.size))  # structure only; values: a == b above
+    assert np.array_equal(a.row_ptr, optr) and np.array_equal(a.col_idx, ocol)
     assert np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.col_idx, b.col_idx)
     assert np.array_equal(a.values.view(np.uint64), b.values.view(np.uint64))
