@@ -362,6 +362,9 @@ int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const int3
 /* Test hook: 1 (default) fills the layout with a warp per 32-row group through a
  * shared-memory image of the group's panel ranges (coalesced writes); 0 = warp per row. */
 int sme_seg_set_scatter_groups(int on);
+/* Test hook: 1 (default) places the entries of groups without empty rows entry-parallel
+ * (row from a mask of the row starts in each 32-entry window); 0 = the per-row walk. */
+int sme_seg_set_fill_ballot(int on);
 int sme_spmv_seg_warps(int32_t* n_warps);
 /* Kernel variant (process-wide): 0 = the SpMV (default; accumulating passes add
  * with RED.ADD at L2), 3 = bound probe (the chunk stream and gathers without the

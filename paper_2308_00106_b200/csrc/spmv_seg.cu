@@ -54,6 +54,7 @@ namespace sme {
 
 constexpr int SEG_NT = 256;
 static bool s_seg_scatter_groups = true;  // sme_seg_set_scatter_groups
+static bool s_seg_fill_ballot = true;     // sme_seg_set_fill_ballot
 constexpr int SEG_CH = 128;
 constexpr int SEG_DBITS = 8;
 constexpr uint32_t SEG_DMASK = (1u << SEG_DBITS) - 1;
@@ -213,8 +214,14 @@ constexpr int SG_CAP = 1024;
 constexpr int SG_SERIAL_MAX = 48;
 constexpr int SG_WARPS = 4;
 
+constexpr int SG_HMAX = SG_CAP / SEG_CH + 2;  // chunks a group's range of one panel can touch
+
+// per warp: the output image, the (panel, row) table, row starts, per-panel ranges and
+// the chunk headers of those ranges
 inline size_t sg_warp_bytes(int n_panels, size_t val_bytes) {
-  return align_up((size_t)SG_CAP * (4 + val_bytes) + (size_t)3 * n_panels * 32 * 4 + 40 * 4 + 4 * 32 * 4, 16);
+  return align_up((size_t)SG_CAP * (4 + val_bytes) + (size_t)n_panels * 32 * 16 + 40 * 4 + 4 * 32 * 4 + 32 * 4 +
+                      32 * 8 + 32 * 16 + (size_t)n_panels * SG_HMAX * 4,
+                  16);
 }
 
 template <typename T>
@@ -222,7 +229,7 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
     int64_t n_rows, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col, const T* __restrict__ val,
     int32_t n_panels, const int32_t* __restrict__ bounds, const int32_t* __restrict__ counts,
     const int32_t* __restrict__ pos, const int64_t* __restrict__ offsets, uint32_t* __restrict__ out_pk,
-    T* __restrict__ out_val, const int32_t* __restrict__ hdr, size_t warp_bytes) {
+    T* __restrict__ out_val, const int32_t* __restrict__ hdr, size_t warp_bytes, int fill_ballot) {
   extern __shared__ __align__(16) unsigned char sg_smem[];
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -230,15 +237,20 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
   unsigned char* wb = sg_smem + (size_t)wib * warp_bytes;
   T* s_val = reinterpret_cast<T*>(wb);
   uint32_t* s_pk = reinterpret_cast<uint32_t*>(wb + (size_t)SG_CAP * sizeof(T));
-  int32_t* s_first = reinterpret_cast<int32_t*>(s_pk + SG_CAP);  // [P][32]
-  int32_t* s_cnt = s_first + P * 32;                             // [P][32]
-  int32_t* s_ppos = s_cnt + P * 32;                              // [P][32]
-  int32_t* s_rp = s_ppos + P * 32;                               // [33] row starts
+  // per (panel, row): {first entry, count, slot in the panel, slot - first}
+  int4* s_tab = reinterpret_cast<int4*>(s_pk + SG_CAP);          // [P][32]
+  int32_t* s_rp = reinterpret_cast<int32_t*>(s_tab + P * 32);    // [33] row starts
   int32_t* s_gs = s_rp + 40;                                     // [32] group range start per panel
   int32_t* s_sb = s_gs + 32;                                     // [32] staging base per panel
   int32_t* s_len = s_sb + 32;                                    // [32]
+  int32_t* s_nch = s_len + 32;                                   // [32] chunks of the group's range per panel
+  int64_t* s_cb = reinterpret_cast<int64_t*>(s_nch + 32);        // [32] first such chunk
+  int4* s_pp = reinterpret_cast<int4*>(s_cb + 32);               // [32] {image base - gs, chunk phase - gs, lo, 0}
+  int32_t* s_hdr = reinterpret_cast<int32_t*>(s_pp + 32);        // [P][SG_HMAX] their headers
   __shared__ int32_t c_hi[32], c_lo[32];  // panel column bounds and slot offsets (CTA-wide)
   __shared__ int64_t c_off[32];
+  int ppow = 1;  // smallest power of two >= P (steps of the panel search)
+  while (ppow < P) ppow <<= 1;
   const int32_t my_hi = lane < P ? bounds[lane + 1] : INT32_MAX;
   const int32_t my_lo = lane < P ? bounds[lane] : 0;
   const int64_t my_off = lane < P ? offsets[lane] : 0;
@@ -318,6 +330,18 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
       s_gs[lane] = gs;
       s_sb[lane] = incl - len;
       s_len[lane] = len;
+      const int64_t g0 = my_off + gs;
+      s_cb[lane] = g0 / SEG_CH;
+      s_nch[lane] = len > 0 ? (int32_t)((g0 + len - 1) / SEG_CH - g0 / SEG_CH + 1) : 0;
+      // slot dip of panel lane: image index x + dip, header chunk (y + dip) >> 7
+      s_pp[lane] = make_int4(incl - len - gs, (int32_t)(g0 & (SEG_CH - 1)) - gs, my_lo, 0);
+    }
+    __syncwarp();
+    // chunk headers of the group's range in every panel (<= SG_HMAX each), so placing an
+    // entry or an explicit zero reads its chunk's first row from shared memory
+    for (int t = lane; t < P * SG_HMAX; t += 32) {
+      const int p = t / SG_HMAX, j = t - p * SG_HMAX;
+      if (j < s_nch[p]) s_hdr[t] = hdr[s_cb[p] + j];
     }
     // per (panel, row): first entry, count, slot; explicit zeros go straight to the image
     if (lane < nr) {
@@ -327,9 +351,7 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
         const int32_t c = counts[(int64_t)p * n_rows + r];
         const int32_t* pp = pos + (int64_t)p * (n_rows + 1);
         const int32_t ppos = pp[r];
-        s_first[p * 32 + lane] = run;
-        s_cnt[p * 32 + lane] = c;
-        s_ppos[p * 32 + lane] = ppos;
+        s_tab[p * 32 + lane] = make_int4(run, c, ppos, ppos - run);
         run += c;
       }
     }
@@ -337,13 +359,14 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
     if (lane < nr) {
       const int64_t r = r0 + lane;
       for (int p = 0; p < P; ++p) {
-        if (s_cnt[p * 32 + lane] != 0) continue;
-        const int32_t ppos = s_ppos[p * 32 + lane];
-        const int32_t pnext = (lane + 1 < nr) ? s_ppos[p * 32 + lane + 1] : s_gs[p] + s_len[p];
+        if (s_tab[p * 32 + lane].y != 0) continue;
+        const int32_t ppos = s_tab[p * 32 + lane].z;
+        const int32_t pnext = (lane + 1 < nr) ? s_tab[p * 32 + lane + 1].z : s_gs[p] + s_len[p];
         if (pnext > ppos) {
           const int32_t sidx = s_sb[p] + (ppos - s_gs[p]);
           const int64_t dst = c_off[p] + ppos;
-          s_pk[sidx] = (SEG_MARK << SEG_CSHIFT) | SEG_END | (uint32_t)(r - hdr[dst / SEG_CH]);
+          s_pk[sidx] = (SEG_MARK << SEG_CSHIFT) | SEG_END |
+                       (uint32_t)(r - s_hdr[p * SG_HMAX + (int)(dst / SEG_CH - s_cb[p])]);
           s_val[sidx] = T(0);
         }
       }
@@ -358,14 +381,60 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
     // only when it changes; 17.9 ms at C4 against 23.0 ms entry-parallel); groups with a
     // longer row go entry-parallel (C3 R-MAT: 10.8 -> 5.4 ms).
     int32_t my_len = lane < nr ? s_rp[lane + 1] - s_rp[lane] : 0;
+    const bool no_empty = __all_sync(FULL, lane >= nr || my_len > 0);
 #pragma unroll
     for (int o = 16; o; o >>= 1) my_len = max(my_len, __shfl_xor_sync(FULL, my_len, o));
-    if (my_len <= SG_SERIAL_MAX) {
+    if (no_empty && fill_ballot) {
+      // entry-parallel (lane = entry, coalesced loads, four windows of 32 in flight): an
+      // entry's row comes from a bit mask of the row starts inside its 32-entry window
+      // (one OR-reduction per window, no search: every row of the group is non-empty, so
+      // starts are distinct), its panel from the panel bounds, its slot from the (panel,
+      // row) tables.  C4 (20-entry rows): see DESIGN.md §5.
+      const int32_t k0 = s_rp[0], k1 = s_rp[nr];
+      const int32_t my_start = lane < nr ? s_rp[lane] : INT32_MAX;
+      int row_at = 0;  // row (within the group) of the window's first entry
+      for (int32_t w0 = k0; w0 < k1; w0 += 128) {
+        int32_t c[4];
+        T v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int32_t k = w0 + 32 * u + lane;
+          c[u] = k < k1 ? ld_nc_na_i1(col + k) : 0;
+          v[u] = k < k1 ? val[k] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int32_t base = w0 + 32 * u;
+          if (base >= k1) break;
+          const int32_t off = my_start - base;  // rows starting strictly inside this window
+          const unsigned m = __reduce_or_sync(FULL, (off > 0 && off < 32) ? (1u << off) : 0u);
+          const int32_t k = base + lane;
+          const unsigned upto = (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u)) & ~1u;
+          const int rr = row_at + __popc(m & upto);
+          row_at += __popc(m) + (__any_sync(FULL, my_start == base + 32) ? 1 : 0);
+          if (k < k1) {
+            const int32_t cc = c[u];
+            // panel: branchless search of the (INT32_MAX-padded) upper bounds
+            int p = 0;
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1)
+              if (st < ppow && cc >= c_hi[p + st - 1]) p += st;
+            const int4 tb = s_tab[p * 32 + rr];
+            const int4 pp = s_pp[p];
+            const int32_t dip = tb.w + k;  // slot within the panel
+            s_pk[pp.x + dip] = (((uint32_t)cc - (uint32_t)pp.z) << SEG_CSHIFT) |
+                               (k - tb.x == tb.y - 1 ? SEG_END : 0u) |
+                               (uint32_t)((int32_t)(r0 + rr) - s_hdr[p * SG_HMAX + ((pp.y + dip) >> 7)]);
+            s_val[pp.x + dip] = v[u];
+          }
+        }
+      }
+    } else if (my_len <= SG_SERIAL_MAX) {
       if (lane < nr) {
         const int32_t r_rel = r0 + lane;
         const int32_t kend = s_rp[lane + 1];
         int p = 0;
-        int32_t f = s_first[lane], pc = s_cnt[lane], pq = s_ppos[lane], sb = s_sb[0] - s_gs[0];
+        int32_t f = s_tab[lane].x, pc = s_tab[lane].y, pq = s_tab[lane].z, sb = s_sb[0] - s_gs[0];
         int64_t po = c_off[0];
         uint32_t clo = (uint32_t)c_lo[0];
         for (int32_t k = s_rp[lane]; k < kend; ++k) {
@@ -374,9 +443,9 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
           if (p < P - 1 && c >= c_hi[p]) {
             do ++p;
             while (p < P - 1 && c >= c_hi[p]);
-            f = s_first[p * 32 + lane];
-            pc = s_cnt[p * 32 + lane];
-            pq = s_ppos[p * 32 + lane];
+            f = s_tab[p * 32 + lane].x;
+            pc = s_tab[p * 32 + lane].y;
+            pq = s_tab[p * 32 + lane].z;
             sb = s_sb[p] - s_gs[p];
             po = c_off[p];
             clo = (uint32_t)c_lo[p];
@@ -402,8 +471,8 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
         int p = 0;
         for (int q = 0; q < P - 1; ++q) p += c >= c_hi[q] ? 1 : 0;
         const int t = p * 32 + lo;
-        const int32_t f = s_first[t], pc = s_cnt[t];
-        const int32_t dip = s_ppos[t] + (k - f);  // slot within the panel
+        const int32_t f = s_tab[t].x, pc = s_tab[t].y;
+        const int32_t dip = s_tab[t].z + (k - f);  // slot within the panel
         const int32_t sidx = s_sb[p] - s_gs[p] + dip;
         s_pk[sidx] = (((uint32_t)c - (uint32_t)c_lo[p]) << SEG_CSHIFT) | (k - f == pc - 1 ? SEG_END : 0u) |
                      (uint32_t)((int32_t)(r0 + lo) - hdr[(c_off[p] + dip) / SEG_CH]);
@@ -961,7 +1030,7 @@ SME_API int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* row_ptr, cons
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((groups + SG_WARPS - 1) / SG_WARPS,
                                                                  (int64_t)sm_count() * 16));
       kern<<<grid, SG_WARPS * 32, smem, s>>>(n_rows, row_ptr, col, v, n_panels, bounds, counts, pos, offsets, pk, ov,
-                                             hdr, wbytes);
+                                             hdr, wbytes, (int)s_seg_fill_ballot);
       return SME_OK;
     };
     if (dtype == SME_F64)
@@ -980,6 +1049,13 @@ SME_API int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* row_ptr, cons
                                                                      bounds, counts, pos, offsets, pk, (float*)out_val,
                                                                      hdr);
   SME_CHECK_LAUNCH("k_seg_scatter");
+  return SME_OK;
+}
+
+// Groups of non-empty rows: entry-parallel placement (1, default) or the lane-per-row
+// walk / searched entry-parallel paths of earlier versions (0).  For A/B tests.
+SME_API int sme_seg_set_fill_ballot(int on) {
+  s_seg_fill_ballot = on != 0;
   return SME_OK;
 }
 

@@ -368,3 +368,42 @@ def test_grouped_fill_equals_per_row_fill(dev, rng, n_panels):
             _lib.call("sme_seg_set_scatter_groups", 1)
     a, b = layouts
     assert torch.equal(a.pk, b.pk) and torch.equal(a.val, b.val) and torch.equal(a.hdr, b.hdr)
+
+
+@pytest.mark.parametrize("n_panels", [1, 3, 8, 17])
+@pytest.mark.parametrize("shape", ["c4_like", "ragged"])
+def test_ballot_fill_equals_per_row_fill(dev, rng, n_panels, shape):
+    """The entry-parallel fill of groups without empty rows (sme_seg_set_fill_ballot: row
+    of an entry from the mask of row starts in its 32-entry window) builds the same
+    layout, bit for bit, as the lane-per-row walk and as the per-row fill — with C4-like
+    20-entry rows and with ragged rows (1..60 entries, windows holding many row starts),
+    some groups with empty rows (the other paths) and some past the image capacity."""
+    from paper_2308_00106_b200 import _lib
+
+    n = 6000
+    if shape == "c4_like":
+        lens = np.full(n, 20)
+    else:
+        lens = rng.integers(1, 61, n)
+        lens[rng.random(n) < 0.3] = 1
+        lens[[5, 2000]] = [900, 1300]  # groups over the image capacity
+        lens[3000:3010] = 0  # empty rows: those groups take the walk
+    ptr, col, val = csr_from_lens(rng, lens, n)
+    m = P.CsrMatrix(n, n, ptr, col, val)
+    layouts = []
+    for groups, ballot in ((1, 1), (1, 0), (0, 1)):
+        _lib.call("sme_seg_set_scatter_groups", groups)
+        _lib.call("sme_seg_set_fill_ballot", ballot)
+        try:
+            layouts.append(SegLayout(m, n_panels))
+        finally:
+            _lib.call("sme_seg_set_scatter_groups", 1)
+            _lib.call("sme_seg_set_fill_ballot", 1)
+    a = layouts[0]
+    for b in layouts[1:]:
+        assert torch.equal(a.pk, b.pk) and torch.equal(a.val, b.val) and torch.equal(a.hdr, b.hdr)
+    x = rng.random(n)
+    want = O.spmv_csr(ptr, col, val, x)
+    y = torch.empty(n, dtype=torch.float64, device=dev)
+    a.spmv_into(torch.from_numpy(x).to(dev), y)
+    assert O.relative_error(y.cpu().numpy(), want) <= 1e-12
