@@ -526,6 +526,53 @@ int sme_rowshard_remap_cols(int64_t nnz, int64_t n_cols, int32_t parts, int64_t 
  * for any launch shape.  n_bytes % 4 == 0, d_data 4-byte aligned. */
 int sme_hash64(const void* d_data, int64_t n_bytes, uint64_t seed, uint64_t* d_out, sme_stream_t stream);
 
+/* ------------------------------------------------------------------------ */
+/* int64 row_ptr ("wide" CSR): matrices with nnz >= 2^31 - 1                 */
+/* ------------------------------------------------------------------------ */
+/* The reference stores row_ptr as int64 at every size (matio.py:97-99); the GPU
+ * layout keeps int32 row_ptr while nnz < 2^31 - 1 and switches to int64 above
+ * (SURVEY.md §7, §8(d) s_p = 8): a 180 GB B200 holds f64 CSRs of ~10^10 nonzeros.
+ * Column ids stay int32 (n_cols < 2^31), and so do the per-panel slot positions of
+ * the seg layout (each panel < 2^31 slots: the caller picks enough panels).  Each
+ * entry point below is its int32 namesake with int64 row_ptr arguments and no
+ * nnz < 2^31 limit; semantics, flags and errors are identical. */
+int sme_coo_row_ptr_i64(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row,
+                        const int32_t* d_col, const int32_t* d_row_map, int64_t* d_row_ptr_out,
+                        void* d_ws, size_t ws_bytes, int32_t* d_flag, sme_stream_t stream);
+int sme_coo_to_csr_i64(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row,
+                       const int32_t* d_col, const void* d_val, const int32_t* d_row_map,
+                       const int32_t* d_col_map, const int64_t* d_row_ptr, int32_t* d_col_out,
+                       void* d_val_out, void* d_ws, size_t ws_bytes, int64_t long_nnz,
+                       int32_t* d_flag, uint64_t* d_dup_key, sme_stream_t stream);
+int sme_permute_csr_row_ptr_i64(int64_t n_rows, const int64_t* d_row_ptr, const int32_t* d_inv_row,
+                                int64_t* d_row_ptr_out, void* d_ws, size_t ws_bytes, sme_stream_t stream);
+int sme_permute_csr_i64(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                        const int64_t* d_row_ptr, const int32_t* d_col, const void* d_val,
+                        const int32_t* d_inv_row, const int32_t* d_col_map, const int64_t* d_row_ptr_out,
+                        int32_t* d_col_out, void* d_val_out, void* d_ws, size_t ws_bytes,
+                        int64_t long_nnz, int32_t* d_flag, uint64_t* d_dup_key, sme_stream_t stream);
+int sme_long_row_nnz_i64(int64_t n_rows, const int64_t* d_row_ptr, int64_t* d_out, sme_stream_t stream);
+int sme_row_stats_i64(int64_t n_rows, const int64_t* d_row_ptr, int64_t* d_out, sme_stream_t stream);
+int sme_csr_validate_i64(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* d_row_ptr,
+                         const int32_t* d_col, int32_t* d_flag, sme_stream_t stream);
+int sme_csr_expand_rows_i64(int64_t n_rows, const int64_t* d_row_ptr, int32_t* d_row_out,
+                            sme_stream_t stream);
+int sme_hist2d_csr_i64(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* d_row_ptr,
+                       const int32_t* d_col, int32_t bins_r, int32_t bins_c, int64_t* d_counts,
+                       sme_stream_t stream);
+int sme_row_hist_csr_i64(int64_t n_rows, const int64_t* d_row_ptr, int32_t bins, int64_t* d_counts,
+                         sme_stream_t stream);
+int sme_seg_positions_i64(int64_t n_rows, const int64_t* d_row_ptr, const int32_t* d_col, int32_t n_panels,
+                          const int32_t* d_bounds, int full_last, int32_t* d_pos, void* d_ws, size_t ws_bytes,
+                          sme_stream_t stream);
+int sme_seg_fill_i64(int dtype, int64_t n_rows, const int64_t* d_row_ptr, const int32_t* d_col,
+                     const void* d_val, int32_t n_panels, const int32_t* d_bounds, const int32_t* d_pos,
+                     const int64_t* d_offsets, const int64_t* h_offsets, uint32_t* d_pk, void* d_out_val,
+                     int32_t* d_hdr, const void* d_ws, sme_stream_t stream);
+int sme_spmv_vector_i64(int dtype, int lanes, int64_t n_rows, int64_t n_cols, const int64_t* d_row_ptr,
+                        const int32_t* d_col, const void* d_val, const void* d_x, void* d_y, int accumulate,
+                        sme_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

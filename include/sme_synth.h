@@ -18,7 +18,8 @@ int sme_synth_laplacian5(int dtype, int64_t g, int32_t* d_row_ptr, int32_t* d_co
 
 /* Random-structured rows (C4): every row has k (<= 32) distinct columns, the first
  * k distinct draws of hash3(seed, r, t) mapped to [0, n_cols), sorted ascending;
- * value of sorted slot s = U[-1,1) from hash3(seed ^ 0x5DEECE66D, r, s). */
+ * value of sorted slot s = U[-1,1) from hash3(seed ^ 0x5DEECE66D, r, s).
+ * d_row_ptr may be NULL (it is r * k; required for nnz >= 2^31, int64 row_ptr). */
 int sme_synth_random_rows(int dtype, int64_t n_rows, int64_t n_cols, int32_t k, uint64_t seed,
                           int32_t* d_row_ptr, int32_t* d_col, void* d_val, sme_stream_t stream);
 

@@ -85,6 +85,33 @@ def as_index_tensor(a, what: str, n_max: int | None = None) -> torch.Tensor:
     return torch.from_numpy(arr.astype(np.int32)).to(dev)
 
 
+# Test hook: give every CSR built from now on an int64 row_ptr, whatever its nnz, so
+# the `_i64` entry points are exercised on matrices the oracle can check.
+FORCE_WIDE_ROW_PTR = False
+
+
+def wide_row_ptr(nnz: int) -> bool:
+    """int64 row_ptr for nnz >= 2^31 - 1 (int32 offsets below that)."""
+    return int(nnz) >= INT32_MAX or FORCE_WIDE_ROW_PTR
+
+
+def row_ptr_dtype(nnz: int) -> torch.dtype:
+    return torch.int64 if wide_row_ptr(nnz) else torch.int32
+
+
+def as_row_ptr_tensor(a, nnz: int) -> torch.Tensor:
+    """1-D device row_ptr: int32 while nnz < 2^31 - 1, int64 above (or when forced)."""
+    if not wide_row_ptr(nnz):
+        return as_index_tensor(a, "row_ptr")
+    dev = require_cuda()
+    if isinstance(a, torch.Tensor):
+        return a.to(dev, torch.int64).contiguous()
+    arr = np.asarray(a, dtype=np.int64)
+    if arr.ndim != 1:
+        raise ValueError("row_ptr must be a 1-D array")
+    return torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+
+
 def as_value_tensor(a, dtype: torch.dtype) -> torch.Tensor:
     dev = require_cuda()
     if isinstance(a, torch.Tensor):

@@ -130,6 +130,14 @@ SIGNATURES: dict[str, list] = {
     "sme_csr_compact_row_ptr": [i64, p, p, i32, p, p, sz, p],
     "sme_csr_compact": [C.c_int, i64, p, p, p, i32, p, p, p, p],
 }
+# int64 row_ptr twins (nnz >= 2^31 - 1): same argument list as the int32 namesake
+WIDE_ENTRY_POINTS = (
+    "sme_coo_row_ptr", "sme_coo_to_csr", "sme_permute_csr_row_ptr", "sme_permute_csr", "sme_long_row_nnz",
+    "sme_row_stats", "sme_csr_validate", "sme_csr_expand_rows", "sme_hist2d_csr", "sme_row_hist_csr",
+    "sme_seg_positions", "sme_seg_fill", "sme_spmv_vector",
+)
+for _n in WIDE_ENTRY_POINTS:
+    SIGNATURES[_n + "_i64"] = SIGNATURES[_n]
 _RESTYPES = {"sme_last_error": C.c_char_p}
 
 _lock = threading.Lock()
@@ -169,6 +177,19 @@ def call(name: str, *args) -> None:
     if status == SME_EINVAL:
         raise ValueError(msg)
     raise RuntimeError(msg)
+
+
+def rp_name(name: str, row_ptr) -> str:
+    """The entry point for a CSR whose row_ptr is `row_ptr` (a device tensor): the
+    `_i64` twin when row_ptr is int64 (nnz >= 2^31 - 1), else `name` itself."""
+    import torch
+
+    return name + "_i64" if row_ptr.dtype == torch.int64 else name
+
+
+def call_rp(name: str, row_ptr, *args) -> None:
+    """call() of the int32 or int64 row_ptr variant of `name`, picked from row_ptr's dtype."""
+    call(rp_name(name, row_ptr), *args)
 
 
 def query_size(name: str, *args) -> int:

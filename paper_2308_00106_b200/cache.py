@@ -35,7 +35,7 @@ from .matio import CsrMatrix
 MAGIC = b"SMECACHE"
 VERSION = 1
 ALIGN = 4096
-_DT = {"int32": torch.int32, "float64": torch.float64, "float32": torch.float32}
+_DT = {"int32": torch.int32, "int64": torch.int64, "float64": torch.float64, "float32": torch.float32}
 
 
 def hash64(t: torch.Tensor, seed: int = 0) -> int:

@@ -59,17 +59,20 @@ inline SortLists carve_lists(char* p, int64_t n_rows, int64_t long_nnz) {
 // Where the entries of output row r are read from.
 // start(r, dst) = where(r); split into the old row id (key, a coalesced load) and the
 // dependent old_ptr gather (start_of) so the warp sort can issue them a phase apart.
+// IP: the row_ptr element type (int32_t, or int64_t for nnz >= 2^31; entry offsets are
+// carried as int64_t either way).
+template <typename IP>
 struct SrcGather {  // permuted CSR: old row inv[r] of the source CSR
-  const int32_t* old_ptr;
+  const IP* old_ptr;
   const int32_t* inv;
   __device__ __forceinline__ int32_t key(int32_t r) const { return inv ? inv[r] : r; }
-  __device__ __forceinline__ int64_t start_of(int32_t k, int32_t /*dst*/) const { return old_ptr[k]; }
-  __device__ __forceinline__ int64_t start(int32_t r, int32_t dst) const { return start_of(key(r), dst); }
+  __device__ __forceinline__ int64_t start_of(int32_t k, int64_t /*dst*/) const { return (int64_t)old_ptr[k]; }
+  __device__ __forceinline__ int64_t start(int32_t r, int64_t dst) const { return start_of(key(r), dst); }
 };
 struct SrcStaged {  // COO path: the row's slots in the staging arrays
   __device__ __forceinline__ int32_t key(int32_t /*r*/) const { return 0; }
-  __device__ __forceinline__ int64_t start_of(int32_t /*k*/, int32_t dst) const { return dst; }
-  __device__ __forceinline__ int64_t start(int32_t /*r*/, int32_t dst) const { return dst; }
+  __device__ __forceinline__ int64_t start_of(int32_t /*k*/, int64_t dst) const { return dst; }
+  __device__ __forceinline__ int64_t start(int32_t /*r*/, int64_t dst) const { return dst; }
 };
 
 __device__ __forceinline__ void report_dup(int32_t row, uint32_t col, int32_t* flag,
@@ -154,7 +157,7 @@ constexpr int TILE_NT = 128;     // k_sort_rows_warp block: 4 warps, 17 KB (32-b
 // lane per entry, which left the kernel issue-bound (ncu, C4: 11 ms at 64 % issue).
 template <typename T, class Src, bool KEY32, int N>
 __device__ __forceinline__ void sort_group_tile(typename SortKey<KEY32>::K* tile, int lane, int64_t g,
-                                                int32_t len, int32_t dst, int64_t from,
+                                                int32_t len, int64_t dst, int64_t from,
                                                 const int32_t* __restrict__ src_col, const T* __restrict__ src_val,
                                                 const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
                                                 T* __restrict__ out_val, const SortLists& L, int32_t* flag,
@@ -196,7 +199,7 @@ __device__ __forceinline__ void sort_group_tile(typename SortKey<KEY32>::K* tile
   for (int r0 = 0; r0 < 32; r0 += SORT_UNROLL) {
     K key[SORT_UNROLL];
     T w[SORT_UNROLL];
-    int32_t md[SORT_UNROLL];
+    int64_t md[SORT_UNROLL];
     bool in[SORT_UNROLL];
 #pragma unroll
     for (int u = 0; u < SORT_UNROLL; ++u) {
@@ -222,9 +225,9 @@ __device__ __forceinline__ void sort_group_tile(typename SortKey<KEY32>::K* tile
   __syncwarp();
 }
 
-template <typename T, class Src, bool KEY32 = false>
+template <typename T, class Src, bool KEY32, typename IP>
 __global__ void __launch_bounds__(TILE_NT) k_sort_rows_warp(
-    int32_t n_rows, const int32_t* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
+    int32_t n_rows, const IP* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
     const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
     T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key) {
   using SK = SortKey<KEY32>;
@@ -239,7 +242,8 @@ __global__ void __launch_bounds__(TILE_NT) k_sort_rows_warp(
   // group metadata, one row per lane, fetched a group ahead: new_ptr and the old row id
   // (coalesced), then the old row's start (a gather) once the current group is running
   int64_t g = warp_global;
-  int32_t n0 = 0, n1 = 0, k = 0;
+  IP n0 = 0, n1 = 0;
+  int32_t k = 0;
   auto meta_raw = [&](int64_t gg) {
     const int32_t r = (int32_t)(gg * 32 + lane);
     n0 = n1 = k = 0;
@@ -253,8 +257,8 @@ __global__ void __launch_bounds__(TILE_NT) k_sort_rows_warp(
   int64_t from = n1 > n0 ? src.start_of(k, n0) : 0;
   for (; g < n_groups; g += warps_total) {
     const int32_t r = (int32_t)(g * 32 + lane);
-    const int32_t dst = n0;
-    int32_t len = n1 - n0;
+    const int64_t dst = n0;
+    int32_t len = (int32_t)(n1 - n0);
     const int64_t my_from = from;
     if (len > 32) {
       if (len <= SME_SORT_SMEM_MAX) {
@@ -329,7 +333,7 @@ __device__ __forceinline__ void warp_bitonic(uint64_t (&v)[E], int lane) {
 }
 
 template <int E, typename T>
-__device__ __forceinline__ void sort_row_warp(int32_t r, int32_t dst, int32_t len, int64_t from,
+__device__ __forceinline__ void sort_row_warp(int32_t r, int64_t dst, int32_t len, int64_t from,
                                               const int32_t* __restrict__ src_col, const T* __restrict__ src_val,
                                               const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
                                               T* __restrict__ out_val, const SortLists& L, int32_t* flag,
@@ -356,9 +360,9 @@ __device__ __forceinline__ void sort_row_warp(int32_t r, int32_t dst, int32_t le
   }
 }
 
-template <typename T, class Src>
+template <typename T, class Src, typename IP>
 __global__ void __launch_bounds__(SORT_NT) k_sort_rows_wmed(
-    const int32_t* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
+    const IP* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
     const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
     T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key, int wmed_max) {
   const int lane = threadIdx.x & 31;
@@ -367,8 +371,8 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_rows_wmed(
   const int64_t n_warps = ((int64_t)gridDim.x * SORT_NT) >> 5;
   for (int64_t it = warp; it < count; it += n_warps) {
     const int32_t r = L.med[it];
-    const int32_t dst = new_ptr[r];
-    const int32_t len = new_ptr[r + 1] - dst;
+    const int64_t dst = new_ptr[r];
+    const int32_t len = (int32_t)(new_ptr[r + 1] - dst);
     if (len > wmed_max) continue;  // k_sort_rows_block
     const int64_t from = src.start(r, dst);
     if (len <= 64)
@@ -406,17 +410,17 @@ __device__ void smem_bitonic(uint64_t* s, int P) {
 }
 
 // rows with 32 < len <= SME_SORT_SMEM_MAX: one CTA per row
-template <typename T, class Src>
+template <typename T, class Src, typename IP>
 __global__ void __launch_bounds__(SORT_NT) k_sort_rows_block(
-    const int32_t* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
+    const IP* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
     const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
     T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key, int wmed_max) {
   __shared__ uint64_t s[SME_SORT_SMEM_MAX];
   const int count = L.counters[0];
   for (int it = blockIdx.x; it < count; it += gridDim.x) {
     const int32_t r = L.med[it];
-    const int32_t dst = new_ptr[r];
-    const int32_t len = new_ptr[r + 1] - dst;
+    const int64_t dst = new_ptr[r];
+    const int32_t len = (int32_t)(new_ptr[r + 1] - dst);
     if (len <= wmed_max) continue;  // k_sort_rows_wmed
     const int64_t from = src.start(r, dst);
     int P = 64;
@@ -439,16 +443,16 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_rows_block(
 
 // rows with len > SME_SORT_SMEM_MAX: chunk sort in smem, then merge passes
 // between two global scratch buffers; one CTA per row.
-template <typename T, class Src>
+template <typename T, class Src, typename IP>
 __global__ void __launch_bounds__(LONG_NT) k_sort_rows_long(
-    const int32_t* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
+    const IP* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
     const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
     T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key) {
   __shared__ uint64_t s[LONG_CHUNK];
   const int count = L.counters[1];
   for (int it = blockIdx.x; it < count; it += gridDim.x) {
     const int32_t r = L.lng[it];
-    const int32_t dst = new_ptr[r];
+    const int64_t dst = new_ptr[r];
     const int64_t len = new_ptr[r + 1] - dst;
     const int64_t from = src.start(r, dst);
     uint64_t* a = L.scratch_a + L.lng_off[it];
@@ -525,17 +529,22 @@ __global__ void k_coo_count(int64_t nnz, int64_t n_rows, int64_t n_cols, const i
   }
 }
 
-template <typename T>
+__device__ __forceinline__ int32_t cursor_bump(int32_t* c) { return atomicAdd(c, 1); }
+__device__ __forceinline__ int64_t cursor_bump(int64_t* c) {
+  return (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(c), 1ull);
+}
+
+template <typename T, typename IP>
 __global__ void k_coo_scatter(int64_t nnz, int64_t n_rows, int64_t n_cols, const int32_t* __restrict__ row,
                               const int32_t* __restrict__ col, const T* __restrict__ val,
-                              const int32_t* __restrict__ rmap, int32_t* __restrict__ cursor,
+                              const int32_t* __restrict__ rmap, IP* __restrict__ cursor,
                               int32_t* __restrict__ st_col, T* __restrict__ st_val) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
     int32_t r = row[k], c = col[k];
     if (r < 0 || r >= n_rows || c < 0 || c >= n_cols) continue;
     if (rmap) r = rmap[r];
-    int32_t pos = atomicAdd(&cursor[r], 1);
+    const IP pos = cursor_bump(&cursor[r]);
     st_col[pos] = c;  // column mapping is applied by the sort
     st_val[pos] = val[k];
   }
@@ -545,8 +554,9 @@ struct LenFromCounts {
   const int32_t* counts;
   __device__ __forceinline__ int64_t operator()(int64_t k) const { return counts[k]; }
 };
+template <typename IP>
 struct LenFromGather {
-  const int32_t* ptr;
+  const IP* ptr;
   const int32_t* inv;
   __device__ __forceinline__ int64_t operator()(int64_t k) const {
     int32_t o = inv ? inv[k] : (int32_t)k;
@@ -554,11 +564,12 @@ struct LenFromGather {
   }
 };
 
-__global__ void k_long_row_nnz(int64_t n_rows, const int32_t* __restrict__ ptr, unsigned long long* out) {
+template <typename IP>
+__global__ void k_long_row_nnz(int64_t n_rows, const IP* __restrict__ ptr, unsigned long long* out) {
   unsigned long long s = 0;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += stride) {
-    int32_t l = ptr[r + 1] - ptr[r];
+    const int64_t l = (int64_t)ptr[r + 1] - ptr[r];
     if (l > SME_SORT_SMEM_MAX) s += (unsigned long long)l;
   }
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -566,10 +577,11 @@ __global__ void k_long_row_nnz(int64_t n_rows, const int32_t* __restrict__ ptr, 
 }
 
 // out[0] = max row length, out[1] = number of empty rows (out zeroed by the caller)
-__global__ void k_row_stats(int64_t n_rows, const int32_t* __restrict__ ptr, unsigned long long* out) {
+template <typename IP>
+__global__ void k_row_stats(int64_t n_rows, const IP* __restrict__ ptr, unsigned long long* out) {
   unsigned long long mx = 0, empty = 0;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t l = ptr[r + 1] - ptr[r];
+    const int64_t l = (int64_t)ptr[r + 1] - ptr[r];
     mx = max(mx, (unsigned long long)l);
     empty += l == 0;
   }
@@ -583,14 +595,15 @@ __global__ void k_row_stats(int64_t n_rows, const int32_t* __restrict__ ptr, uns
   }
 }
 
-__global__ void k_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* __restrict__ ptr,
+template <typename IP>
+__global__ void k_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const IP* __restrict__ ptr,
                                const int32_t* __restrict__ col, int32_t* flag) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int bits = 0;
   int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid == 0 && (ptr[0] != 0 || ptr[n_rows] != nnz)) bits |= SME_FLAG_ROWPTR;
   for (int64_t r = tid; r < n_rows; r += stride) {
-    int32_t a = ptr[r], b = ptr[r + 1];
+    const IP a = ptr[r], b = ptr[r + 1];
     if (b < a) {
       bits |= SME_FLAG_ROWPTR;
       continue;
@@ -600,7 +613,7 @@ __global__ void k_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, cons
       continue;
     }
     int32_t prev = -1;
-    for (int32_t k = a; k < b; ++k) {
+    for (IP k = a; k < b; ++k) {
       int32_t c = col[k];
       if (c < 0 || c >= n_cols) bits |= SME_FLAG_RANGE;
       if (k > a && c <= prev) bits |= SME_FLAG_UNSORTED;
@@ -612,61 +625,69 @@ __global__ void k_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, cons
   if ((threadIdx.x & 31) == 0 && bits) atomicOr(flag, bits);
 }
 
-__global__ void k_csr_expand_rows(int64_t n_rows, const int32_t* __restrict__ ptr, int32_t* __restrict__ row_out) {
+template <typename IP>
+__global__ void k_csr_expand_rows(int64_t n_rows, const IP* __restrict__ ptr, int32_t* __restrict__ row_out) {
   // warp per row: rows are short on average, long rows are strided over lanes
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int lane = threadIdx.x & 31;
   for (int64_t r = warp; r < n_rows; r += nw) {
-    int32_t a = ptr[r], b = ptr[r + 1];
-    for (int32_t k = a + lane; k < b; k += 32) row_out[k] = (int32_t)r;
+    const IP a = ptr[r], b = ptr[r + 1];
+    for (IP k = a + lane; k < b; k += 32) row_out[k] = (int32_t)r;
   }
 }
 
-template <typename T, class Src>
-int launch_sorts(int64_t n_rows, const int32_t* new_ptr, Src src, const int32_t* src_col, const T* src_val,
+template <typename T, class Src, typename IP>
+int launch_sorts(int64_t n_rows, const IP* new_ptr, Src src, const int32_t* src_col, const T* src_val,
                  const int32_t* cmap, int32_t* out_col, T* out_val, SortLists L, int32_t* flag,
                  uint64_t* dup_key, cudaStream_t s, int64_t n_cols = INT32_MAX) {
   int64_t groups = (n_rows + 31) / 32;
   int blocks = grid_for(groups * 32, TILE_NT, 16);
   if (n_cols <= ((int64_t)1 << 27) && g_sort_key32)  // mapped columns < 2^27: 32-bit keys (col << 5 | slot)
-    k_sort_rows_warp<T, Src, true><<<blocks, TILE_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
+    k_sort_rows_warp<T, Src, true, IP><<<blocks, TILE_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
                                                                cmap, out_col, out_val, L, flag,
                                                                (unsigned long long*)dup_key);
   else
-    k_sort_rows_warp<T, Src, false><<<blocks, TILE_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
+    k_sort_rows_warp<T, Src, false, IP><<<blocks, TILE_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
                                                                 cmap, out_col, out_val, L, flag,
                                                                 (unsigned long long*)dup_key);
   SME_CHECK_LAUNCH("k_sort_rows_warp");
   const int wmed_max = g_sort_wmed > 0 ? 32 << g_sort_wmed : 0;  // 1: <= 64, 2: <= 128, 3: <= 256, 4: <= 512
   if (wmed_max) {
-    k_sort_rows_wmed<T, Src><<<sm_count() * 8, SORT_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
+    k_sort_rows_wmed<T, Src, IP><<<sm_count() * 8, SORT_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
                                                                  out_val, L, flag, (unsigned long long*)dup_key,
                                                                  wmed_max);
     SME_CHECK_LAUNCH("k_sort_rows_wmed");
   }
-  k_sort_rows_block<T, Src><<<sm_count() * 4, SORT_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
+  k_sort_rows_block<T, Src, IP><<<sm_count() * 4, SORT_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
                                                                 out_val, L, flag, (unsigned long long*)dup_key,
                                                                 wmed_max);
   SME_CHECK_LAUNCH("k_sort_rows_block");
-  k_sort_rows_long<T, Src><<<sm_count(), LONG_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
+  k_sort_rows_long<T, Src, IP><<<sm_count(), LONG_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
                                                            out_val, L, flag, (unsigned long long*)dup_key);
   SME_CHECK_LAUNCH("k_sort_rows_long");
   return SME_OK;
 }
 
-inline size_t coo_stage_bytes(int64_t n_rows, int64_t nnz) {
-  return align_up(n_rows * 4) + align_up(nnz * 4) + align_up(nnz * 8);
+inline size_t coo_stage_bytes(int64_t n_rows, int64_t nnz) {  // cursor sized for int64 row_ptr
+  return align_up(n_rows * 8) + align_up(nnz * 4) + align_up(nnz * 8);
 }
 
 }  // namespace sme
 
 using namespace sme;
 
-#define CHECK_SIZES(n_rows, n_cols, nnz)                                                         \
+#define CHECK_DIMS(n_rows, n_cols)                                                               \
   SME_REQUIRE((n_rows) >= 0 && (n_rows) < INT32_MAX && (n_cols) >= 0 && (n_cols) < INT32_MAX,   \
-              "matrix dimensions must be non-negative and < 2^31-1");                            \
-  SME_REQUIRE((nnz) >= 0 && (nnz) < INT32_MAX, "nnz %lld exceeds int32 offsets", (long long)(nnz))
+              "matrix dimensions must be non-negative and < 2^31-1")
+#define CHECK_SIZES(n_rows, n_cols, nnz)                                                         \
+  CHECK_DIMS(n_rows, n_cols);                                                                    \
+  SME_REQUIRE((nnz) >= 0 && (nnz) < INT32_MAX, "nnz %lld exceeds int32 offsets (use the _i64 entry point)", \
+              (long long)(nnz))
+// the _i64 entry points: int64 row_ptr, any nnz
+#define CHECK_SIZES_WIDE(n_rows, n_cols, nnz)                                                    \
+  CHECK_DIMS(n_rows, n_cols);                                                                    \
+  SME_REQUIRE((nnz) >= 0, "negative nnz")
 
 SME_API int sme_row_ptr_workspace_size(int64_t n_rows, size_t* bytes) {
   SME_REQUIRE(bytes, "null pointer");
@@ -674,13 +695,12 @@ SME_API int sme_row_ptr_workspace_size(int64_t n_rows, size_t* bytes) {
   return SME_OK;
 }
 
-SME_API int sme_coo_row_ptr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row, const int32_t* col,
-                            const int32_t* row_map, int32_t* row_ptr_out, void* ws, size_t ws_bytes,
-                            int32_t* flag, sme_stream_t stream) {
-  CHECK_SIZES(n_rows, n_cols, nnz);
+template <typename IP>
+static int coo_row_ptr_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row, const int32_t* col,
+                            const int32_t* row_map, IP* row_ptr_out, void* ws, size_t ws_bytes, int32_t* flag,
+                            cudaStream_t s) {
   size_t need = align_up(n_rows * 4) + scan_workspace_bytes(n_rows);
   SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
-  cudaStream_t s = as_stream(stream);
   int32_t* counts = (int32_t*)ws;
   void* scan_ws = (char*)ws + align_up(n_rows * 4);
   if (n_rows > 0) SME_CUDA(cudaMemsetAsync(counts, 0, n_rows * 4, s));
@@ -691,22 +711,58 @@ SME_API int sme_coo_row_ptr(int64_t n_rows, int64_t n_cols, int64_t nnz, const i
   return exclusive_scan_lengths(n_rows, LenFromCounts{counts}, row_ptr_out, scan_ws, flag, s);
 }
 
-SME_API int sme_permute_csr_row_ptr(int64_t n_rows, const int32_t* row_ptr, const int32_t* inv_row,
-                                    int32_t* row_ptr_out, void* ws, size_t ws_bytes, sme_stream_t stream) {
+SME_API int sme_coo_row_ptr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row, const int32_t* col,
+                            const int32_t* row_map, int32_t* row_ptr_out, void* ws, size_t ws_bytes,
+                            int32_t* flag, sme_stream_t stream) {
+  CHECK_SIZES(n_rows, n_cols, nnz);
+  return coo_row_ptr_impl(n_rows, n_cols, nnz, row, col, row_map, row_ptr_out, ws, ws_bytes, flag,
+                          as_stream(stream));
+}
+
+SME_API int sme_coo_row_ptr_i64(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row, const int32_t* col,
+                                const int32_t* row_map, int64_t* row_ptr_out, void* ws, size_t ws_bytes,
+                                int32_t* flag, sme_stream_t stream) {
+  CHECK_SIZES_WIDE(n_rows, n_cols, nnz);
+  return coo_row_ptr_impl(n_rows, n_cols, nnz, row, col, row_map, row_ptr_out, ws, ws_bytes, flag,
+                          as_stream(stream));
+}
+
+template <typename IP>
+static int permute_row_ptr_impl(int64_t n_rows, const IP* row_ptr, const int32_t* inv_row, IP* row_ptr_out,
+                                void* ws, size_t ws_bytes, sme_stream_t stream) {
   SME_REQUIRE(n_rows >= 0 && n_rows < INT32_MAX, "bad n_rows");
   size_t need = scan_workspace_bytes(n_rows);
   SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
-  return exclusive_scan_lengths(n_rows, LenFromGather{row_ptr, inv_row}, row_ptr_out, ws, nullptr,
+  return exclusive_scan_lengths(n_rows, LenFromGather<IP>{row_ptr, inv_row}, row_ptr_out, ws, nullptr,
                                 as_stream(stream));
 }
 
-SME_API int sme_long_row_nnz(int64_t n_rows, const int32_t* row_ptr, int64_t* out, sme_stream_t stream) {
+SME_API int sme_permute_csr_row_ptr(int64_t n_rows, const int32_t* row_ptr, const int32_t* inv_row,
+                                    int32_t* row_ptr_out, void* ws, size_t ws_bytes, sme_stream_t stream) {
+  return permute_row_ptr_impl(n_rows, row_ptr, inv_row, row_ptr_out, ws, ws_bytes, stream);
+}
+
+SME_API int sme_permute_csr_row_ptr_i64(int64_t n_rows, const int64_t* row_ptr, const int32_t* inv_row,
+                                        int64_t* row_ptr_out, void* ws, size_t ws_bytes, sme_stream_t stream) {
+  return permute_row_ptr_impl(n_rows, row_ptr, inv_row, row_ptr_out, ws, ws_bytes, stream);
+}
+
+template <typename IP>
+static int long_row_nnz_impl(int64_t n_rows, const IP* row_ptr, int64_t* out, sme_stream_t stream) {
   cudaStream_t s = as_stream(stream);
   SME_CUDA(cudaMemsetAsync(out, 0, 8, s));
   if (n_rows == 0) return SME_OK;
-  k_long_row_nnz<<<grid_for(n_rows, 256, 4), 256, 0, s>>>(n_rows, row_ptr, (unsigned long long*)out);
+  k_long_row_nnz<IP><<<grid_for(n_rows, 256, 4), 256, 0, s>>>(n_rows, row_ptr, (unsigned long long*)out);
   SME_CHECK_LAUNCH("k_long_row_nnz");
   return SME_OK;
+}
+
+SME_API int sme_long_row_nnz(int64_t n_rows, const int32_t* row_ptr, int64_t* out, sme_stream_t stream) {
+  return long_row_nnz_impl(n_rows, row_ptr, out, stream);
+}
+
+SME_API int sme_long_row_nnz_i64(int64_t n_rows, const int64_t* row_ptr, int64_t* out, sme_stream_t stream) {
+  return long_row_nnz_impl(n_rows, row_ptr, out, stream);
 }
 
 SME_API int sme_coo_to_csr_workspace_size(int64_t n_rows, int64_t nnz, int64_t long_nnz, size_t* bytes) {
@@ -715,15 +771,53 @@ SME_API int sme_coo_to_csr_workspace_size(int64_t n_rows, int64_t nnz, int64_t l
   return SME_OK;
 }
 
+template <typename IP>
 static int coo_to_csr_impl(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row,
                            const int32_t* col, const void* val, const int32_t* row_map, const int32_t* col_map,
-                           const int32_t* row_ptr, int32_t* col_out, void* val_out, void* ws, size_t ws_bytes,
-                           int64_t long_nnz, int32_t* flag, uint64_t* dup_key, sme_stream_t stream, int mark);
+                           const IP* row_ptr, int32_t* col_out, void* val_out, void* ws, size_t ws_bytes,
+                           int64_t long_nnz, int32_t* flag, uint64_t* dup_key, sme_stream_t stream, int mark) {
+  SME_REQUIRE(dtype == SME_F64 || dtype == SME_F32, "unknown dtype %d", dtype);
+  size_t need = coo_stage_bytes(n_rows, nnz) + lists_bytes(n_rows, long_nnz);
+  SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
+  if (nnz == 0 || n_rows == 0) return SME_OK;
+  cudaStream_t s = as_stream(stream);
+  char* p = (char*)ws;
+  IP* cursor = (IP*)p;            p += align_up(n_rows * 8);
+  int32_t* st_col = (int32_t*)p;  p += align_up(nnz * 4);
+  void* st_val = p;               p += align_up(nnz * 8);
+  SortLists L = carve_lists(p, n_rows, long_nnz);
+  L.mark_dups = mark;
+  SME_CUDA(cudaMemsetAsync(L.counters, 0, 64, s));
+  SME_CUDA(cudaMemcpyAsync(cursor, row_ptr, n_rows * sizeof(IP), cudaMemcpyDeviceToDevice, s));
+  if (dtype == SME_F64) {
+    k_coo_scatter<double, IP><<<grid_for(nnz, 256), 256, 0, s>>>(nnz, n_rows, n_cols, row, col, (const double*)val,
+                                                                row_map, cursor, st_col, (double*)st_val);
+    SME_CHECK_LAUNCH("k_coo_scatter");
+    return launch_sorts<double>(n_rows, row_ptr, SrcStaged{}, st_col, (const double*)st_val, col_map, col_out,
+                                (double*)val_out, L, flag, dup_key, s, n_cols);
+  } else {
+    k_coo_scatter<float, IP><<<grid_for(nnz, 256), 256, 0, s>>>(nnz, n_rows, n_cols, row, col, (const float*)val,
+                                                               row_map, cursor, st_col, (float*)st_val);
+    SME_CHECK_LAUNCH("k_coo_scatter");
+    return launch_sorts<float>(n_rows, row_ptr, SrcStaged{}, st_col, (const float*)st_val, col_map, col_out,
+                               (float*)val_out, L, flag, dup_key, s, n_cols);
+  }
+}
 
 SME_API int sme_coo_to_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row,
                            const int32_t* col, const void* val, const int32_t* row_map, const int32_t* col_map,
                            const int32_t* row_ptr, int32_t* col_out, void* val_out, void* ws, size_t ws_bytes,
                            int64_t long_nnz, int32_t* flag, uint64_t* dup_key, sme_stream_t stream) {
+  CHECK_SIZES(n_rows, n_cols, nnz);
+  return coo_to_csr_impl(dtype, n_rows, n_cols, nnz, row, col, val, row_map, col_map, row_ptr, col_out, val_out, ws,
+                         ws_bytes, long_nnz, flag, dup_key, stream, 0);
+}
+
+SME_API int sme_coo_to_csr_i64(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row,
+                               const int32_t* col, const void* val, const int32_t* row_map, const int32_t* col_map,
+                               const int64_t* row_ptr, int32_t* col_out, void* val_out, void* ws, size_t ws_bytes,
+                               int64_t long_nnz, int32_t* flag, uint64_t* dup_key, sme_stream_t stream) {
+  CHECK_SIZES_WIDE(n_rows, n_cols, nnz);
   return coo_to_csr_impl(dtype, n_rows, n_cols, nnz, row, col, val, row_map, col_map, row_ptr, col_out, val_out, ws,
                          ws_bytes, long_nnz, flag, dup_key, stream, 0);
 }
@@ -734,41 +828,9 @@ SME_API int sme_coo_to_csr_dedup(int dtype, int64_t n_rows, int64_t n_cols, int6
                                  const int32_t* col, const void* val, const int32_t* row_ptr, int32_t* col_out,
                                  void* val_out, void* ws, size_t ws_bytes, int64_t long_nnz, int32_t* flag,
                                  sme_stream_t stream) {
+  CHECK_SIZES(n_rows, n_cols, nnz);
   return coo_to_csr_impl(dtype, n_rows, n_cols, nnz, row, col, val, nullptr, nullptr, row_ptr, col_out, val_out, ws,
                          ws_bytes, long_nnz, flag, nullptr, stream, 1);
-}
-
-static int coo_to_csr_impl(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row,
-                           const int32_t* col, const void* val, const int32_t* row_map, const int32_t* col_map,
-                           const int32_t* row_ptr, int32_t* col_out, void* val_out, void* ws, size_t ws_bytes,
-                           int64_t long_nnz, int32_t* flag, uint64_t* dup_key, sme_stream_t stream, int mark) {
-  CHECK_SIZES(n_rows, n_cols, nnz);
-  SME_REQUIRE(dtype == SME_F64 || dtype == SME_F32, "unknown dtype %d", dtype);
-  size_t need = coo_stage_bytes(n_rows, nnz) + lists_bytes(n_rows, long_nnz);
-  SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
-  if (nnz == 0 || n_rows == 0) return SME_OK;
-  cudaStream_t s = as_stream(stream);
-  char* p = (char*)ws;
-  int32_t* cursor = (int32_t*)p;  p += align_up(n_rows * 4);
-  int32_t* st_col = (int32_t*)p;  p += align_up(nnz * 4);
-  void* st_val = p;               p += align_up(nnz * 8);
-  SortLists L = carve_lists(p, n_rows, long_nnz);
-  L.mark_dups = mark;
-  SME_CUDA(cudaMemsetAsync(L.counters, 0, 64, s));
-  SME_CUDA(cudaMemcpyAsync(cursor, row_ptr, n_rows * 4, cudaMemcpyDeviceToDevice, s));
-  if (dtype == SME_F64) {
-    k_coo_scatter<double><<<grid_for(nnz, 256), 256, 0, s>>>(nnz, n_rows, n_cols, row, col, (const double*)val,
-                                                            row_map, cursor, st_col, (double*)st_val);
-    SME_CHECK_LAUNCH("k_coo_scatter");
-    return launch_sorts<double>(n_rows, row_ptr, SrcStaged{}, st_col, (const double*)st_val, col_map, col_out,
-                                (double*)val_out, L, flag, dup_key, s, n_cols);
-  } else {
-    k_coo_scatter<float><<<grid_for(nnz, 256), 256, 0, s>>>(nnz, n_rows, n_cols, row, col, (const float*)val,
-                                                           row_map, cursor, st_col, (float*)st_val);
-    SME_CHECK_LAUNCH("k_coo_scatter");
-    return launch_sorts<float>(n_rows, row_ptr, SrcStaged{}, st_col, (const float*)st_val, col_map, col_out,
-                               (float*)val_out, L, flag, dup_key, s, n_cols);
-  }
 }
 
 SME_API int sme_permute_csr_workspace_size(int64_t n_rows, int64_t nnz, int64_t long_nnz, size_t* bytes) {
@@ -777,12 +839,11 @@ SME_API int sme_permute_csr_workspace_size(int64_t n_rows, int64_t nnz, int64_t 
   return SME_OK;
 }
 
-SME_API int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row_ptr,
+template <typename IP>
+static int permute_csr_impl(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const IP* row_ptr,
                             const int32_t* col, const void* val, const int32_t* inv_row, const int32_t* col_map,
-                            const int32_t* row_ptr_out, int32_t* col_out, void* val_out, void* ws,
-                            size_t ws_bytes, int64_t long_nnz, int32_t* flag, uint64_t* dup_key,
-                            sme_stream_t stream) {
-  CHECK_SIZES(n_rows, n_cols, nnz);
+                            const IP* row_ptr_out, int32_t* col_out, void* val_out, void* ws, size_t ws_bytes,
+                            int64_t long_nnz, int32_t* flag, uint64_t* dup_key, sme_stream_t stream) {
   SME_REQUIRE(dtype == SME_F64 || dtype == SME_F32, "unknown dtype %d", dtype);
   size_t need = lists_bytes(n_rows, long_nnz);
   SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
@@ -790,12 +851,32 @@ SME_API int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t n
   cudaStream_t s = as_stream(stream);
   SortLists L = carve_lists((char*)ws, n_rows, long_nnz);
   SME_CUDA(cudaMemsetAsync(L.counters, 0, 64, s));
-  SrcGather src{row_ptr, inv_row};
+  SrcGather<IP> src{row_ptr, inv_row};
   if (dtype == SME_F64)
     return launch_sorts<double>(n_rows, row_ptr_out, src, col, (const double*)val, col_map, col_out,
                                 (double*)val_out, L, flag, dup_key, s, n_cols);
   return launch_sorts<float>(n_rows, row_ptr_out, src, col, (const float*)val, col_map, col_out,
                              (float*)val_out, L, flag, dup_key, s, n_cols);
+}
+
+SME_API int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row_ptr,
+                            const int32_t* col, const void* val, const int32_t* inv_row, const int32_t* col_map,
+                            const int32_t* row_ptr_out, int32_t* col_out, void* val_out, void* ws,
+                            size_t ws_bytes, int64_t long_nnz, int32_t* flag, uint64_t* dup_key,
+                            sme_stream_t stream) {
+  CHECK_SIZES(n_rows, n_cols, nnz);
+  return permute_csr_impl(dtype, n_rows, n_cols, nnz, row_ptr, col, val, inv_row, col_map, row_ptr_out, col_out,
+                          val_out, ws, ws_bytes, long_nnz, flag, dup_key, stream);
+}
+
+SME_API int sme_permute_csr_i64(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                                const int32_t* col, const void* val, const int32_t* inv_row, const int32_t* col_map,
+                                const int64_t* row_ptr_out, int32_t* col_out, void* val_out, void* ws,
+                                size_t ws_bytes, int64_t long_nnz, int32_t* flag, uint64_t* dup_key,
+                                sme_stream_t stream) {
+  CHECK_SIZES_WIDE(n_rows, n_cols, nnz);
+  return permute_csr_impl(dtype, n_rows, n_cols, nnz, row_ptr, col, val, inv_row, col_map, row_ptr_out, col_out,
+                          val_out, ws, ws_bytes, long_nnz, flag, dup_key, stream);
 }
 
 namespace sme {
@@ -901,30 +982,61 @@ SME_API int sme_map_cols_sliced(int64_t nnz, int64_t n_cols, const int32_t* col,
   return sme_map_cols_sliced_partial(nnz, n_cols, col, cmap, mapped, n_slices, n_slices, stream);
 }
 
-SME_API int sme_row_stats(int64_t n_rows, const int32_t* row_ptr, int64_t* out, sme_stream_t stream) {
+template <typename IP>
+static int row_stats_impl(int64_t n_rows, const IP* row_ptr, int64_t* out, sme_stream_t stream) {
   cudaStream_t s = as_stream(stream);
   SME_CUDA(cudaMemsetAsync(out, 0, 16, s));
   if (n_rows == 0) return SME_OK;
-  k_row_stats<<<grid_for(n_rows, 256, 4), 256, 0, s>>>(n_rows, row_ptr, (unsigned long long*)out);
+  k_row_stats<IP><<<grid_for(n_rows, 256, 4), 256, 0, s>>>(n_rows, row_ptr, (unsigned long long*)out);
   SME_CHECK_LAUNCH("k_row_stats");
+  return SME_OK;
+}
+
+SME_API int sme_row_stats(int64_t n_rows, const int32_t* row_ptr, int64_t* out, sme_stream_t stream) {
+  return row_stats_impl(n_rows, row_ptr, out, stream);
+}
+
+SME_API int sme_row_stats_i64(int64_t n_rows, const int64_t* row_ptr, int64_t* out, sme_stream_t stream) {
+  return row_stats_impl(n_rows, row_ptr, out, stream);
+}
+
+template <typename IP>
+static int csr_validate_impl(int64_t n_rows, int64_t n_cols, int64_t nnz, const IP* row_ptr, const int32_t* col,
+                             int32_t* flag, sme_stream_t stream) {
+  cudaStream_t s = as_stream(stream);
+  k_csr_validate<IP><<<grid_for(n_rows + 1, 256), 256, 0, s>>>(n_rows, n_cols, nnz, row_ptr, col, flag);
+  SME_CHECK_LAUNCH("k_csr_validate");
   return SME_OK;
 }
 
 SME_API int sme_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row_ptr,
                              const int32_t* col, int32_t* flag, sme_stream_t stream) {
   CHECK_SIZES(n_rows, n_cols, nnz);
+  return csr_validate_impl(n_rows, n_cols, nnz, row_ptr, col, flag, stream);
+}
+
+SME_API int sme_csr_validate_i64(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                                 const int32_t* col, int32_t* flag, sme_stream_t stream) {
+  CHECK_SIZES_WIDE(n_rows, n_cols, nnz);
+  return csr_validate_impl(n_rows, n_cols, nnz, row_ptr, col, flag, stream);
+}
+
+template <typename IP>
+static int expand_rows_impl(int64_t n_rows, const IP* row_ptr, int32_t* row_out, sme_stream_t stream) {
+  if (n_rows == 0) return SME_OK;
   cudaStream_t s = as_stream(stream);
-  k_csr_validate<<<grid_for(n_rows + 1, 256), 256, 0, s>>>(n_rows, n_cols, nnz, row_ptr, col, flag);
-  SME_CHECK_LAUNCH("k_csr_validate");
+  k_csr_expand_rows<IP><<<grid_for(n_rows * 32, 256), 256, 0, s>>>(n_rows, row_ptr, row_out);
+  SME_CHECK_LAUNCH("k_csr_expand_rows");
   return SME_OK;
 }
 
 SME_API int sme_csr_expand_rows(int64_t n_rows, const int32_t* row_ptr, int32_t* row_out, sme_stream_t stream) {
-  if (n_rows == 0) return SME_OK;
-  cudaStream_t s = as_stream(stream);
-  k_csr_expand_rows<<<grid_for(n_rows * 32, 256), 256, 0, s>>>(n_rows, row_ptr, row_out);
-  SME_CHECK_LAUNCH("k_csr_expand_rows");
-  return SME_OK;
+  return expand_rows_impl(n_rows, row_ptr, row_out, stream);
+}
+
+SME_API int sme_csr_expand_rows_i64(int64_t n_rows, const int64_t* row_ptr, int32_t* row_out,
+                                    sme_stream_t stream) {
+  return expand_rows_impl(n_rows, row_ptr, row_out, stream);
 }
 
 // ---------------------------------------------------------------------------

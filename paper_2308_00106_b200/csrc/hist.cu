@@ -62,15 +62,17 @@ __device__ __forceinline__ int fold4(const int64_t fb[4], int64_t ob[4], int oc[
   return n;
 }
 
-template <bool SMEM_EDGES>
-__global__ void __launch_bounds__(H_NT) k_hist2d_csr(int64_t n_rows, int64_t nnz, const int32_t* __restrict__ row_ptr,
+// IP: row_ptr element type (int32_t; int64_t for nnz >= 2^31); the row-bin edges are
+// kept in that type
+template <bool SMEM_EDGES, typename IP = int32_t>
+__global__ void __launch_bounds__(H_NT) k_hist2d_csr(int64_t n_rows, int64_t nnz, const IP* __restrict__ row_ptr,
                                                      const int32_t* __restrict__ col, int32_t br, int32_t bc,
                                                      int64_t width_r, Binner cb, unsigned long long* counts,
                                                      int64_t chunk, bool vec_ok) {
   extern __shared__ uint32_t smem[];
   uint32_t* s_cnt = smem;
-  int32_t* s_edge = (int32_t*)(smem + H_WIN);
-  auto edge = [&](int32_t b) -> int32_t {
+  IP* s_edge = (IP*)(smem + H_WIN);
+  auto edge = [&](int32_t b) -> IP {
     if (SMEM_EDGES) return s_edge[b];
     return row_ptr[b < br ? (int64_t)b * width_r : n_rows];
   };
@@ -179,9 +181,9 @@ constexpr int HL_FLUSH_ENTRIES = 65000;  // per-lane entries between flushes (< 
 // words cnt[bin / 2][lane] holding bins 2j and 2j+1 in their halves (bank = lane: no
 // conflicts), u16 load / store; 2 = the same words, one shared atomic add of
 // 1 << 16 (bin & 1) per entry (no load-modify-store chain in the thread).
-template <int NT, int U, bool PF, int CL = 0>
+template <int NT, int U, bool PF, int CL = 0, typename IP = int32_t>
 __global__ void __launch_bounds__(NT) k_hist2d_csr_lanes(int64_t n_rows, int64_t nnz,
-                                                         const int32_t* __restrict__ row_ptr,
+                                                         const IP* __restrict__ row_ptr,
                                                          const int32_t* __restrict__ col, int32_t br, int32_t bc,
                                                          int64_t width_r, Binner cb, unsigned long long* counts,
                                                          bool vec_ok) {
@@ -201,7 +203,7 @@ __global__ void __launch_bounds__(NT) k_hist2d_csr_lanes(int64_t n_rows, int64_t
       atomicAdd(cnt32 + ((bin >> 1) << 5) + lane, 1u << ((bin & 1) << 4));
     }
   };
-  int32_t* s_edge = reinterpret_cast<int32_t*>(smem + WARPS * HL_MAXC * 16);
+  IP* s_edge = reinterpret_cast<IP*>(smem + WARPS * HL_MAXC * 16);
   for (int b = threadIdx.x; b <= br; b += NT) s_edge[b] = row_ptr[b < br ? (int64_t)b * width_r : n_rows];
   for (int i = lane; i < HL_MAXC * 32; i += 32) cnt[i] = 0;
   __syncthreads();
@@ -324,12 +326,12 @@ __global__ void __launch_bounds__(NT) k_hist2d_csr_lanes(int64_t n_rows, int64_t
   flush();
 }
 
-template <int NT, int U, bool PF, int CL = 0>
-static int launch_hist_lanes(int64_t n_rows, int64_t nnz, const int32_t* row_ptr, const int32_t* col, int32_t br,
+template <int NT, int U, bool PF, int CL = 0, typename IP = int32_t>
+static int launch_hist_lanes(int64_t n_rows, int64_t nnz, const IP* row_ptr, const int32_t* col, int32_t br,
                              int32_t bc, int64_t width_r, Binner cb, unsigned long long* counts, bool vec_ok,
                              bool one_cta, cudaStream_t s) {
-  auto kern = k_hist2d_csr_lanes<NT, U, PF, CL>;
-  const size_t sm = (size_t)(NT / 32) * HL_MAXC * 32 * 2 + ((size_t)br + 1) * 4;
+  auto kern = k_hist2d_csr_lanes<NT, U, PF, CL, IP>;
+  const size_t sm = (size_t)(NT / 32) * HL_MAXC * 32 * 2 + ((size_t)br + 1) * sizeof(IP);
   SME_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   const int64_t need = (nnz + 4095) / 4096;  // >= 4096 positions per CTA
   const int grid = one_cta ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), need));
@@ -360,7 +362,8 @@ __global__ void __launch_bounds__(H_NT) k_hist2d_coo(int64_t nnz, const int32_t*
     if (s_cnt[i]) atomicAdd(&counts[i], (unsigned long long)s_cnt[i]);
 }
 
-__global__ void k_row_hist_csr(int64_t n_rows, const int32_t* __restrict__ row_ptr, int32_t bins, int64_t width,
+template <typename IP>
+__global__ void k_row_hist_csr(int64_t n_rows, const IP* __restrict__ row_ptr, int32_t bins, int64_t width,
                                int64_t* counts) {
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < bins; b += gridDim.x * blockDim.x) {
     int64_t lo = (int64_t)b * width, hi = (b + 1 < bins) ? (int64_t)(b + 1) * width : n_rows;
@@ -501,6 +504,47 @@ SME_API int sme_hist2d_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const in
   return SME_OK;
 }
 
+// int64 row_ptr (nnz >= 2^31): the default lane-counter tiling (bins_c <= 128) or the
+// row-bin window kernel, edges kept as int64
+SME_API int sme_hist2d_csr_i64(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                               const int32_t* col, int32_t bins_r, int32_t bins_c, int64_t* counts,
+                               sme_stream_t stream) {
+  int rc;
+  if ((rc = check_bins(n_rows, bins_r, "row")) != SME_OK) return rc;
+  if ((rc = check_bins(n_cols, bins_c, "column")) != SME_OK) return rc;
+  SME_REQUIRE(nnz >= 0 && n_cols < INT32_MAX, "bad sizes");
+  if (nnz == 0) return SME_OK;
+  cudaStream_t s = as_stream(stream);
+  Binner cb = make_binner(n_cols, bins_c);
+  const int64_t width_r = n_rows / bins_r;
+  const bool vec_ok = ((uintptr_t)col & 15) == 0;
+  auto ull = (unsigned long long*)counts;
+  if (bins_c <= HL_MAXC && bins_r <= H_EDGE_SMEM) {
+    const bool fits864 = (size_t)27 * HL_MAXC * 64 + ((size_t)bins_r + 1) * 8 <= 227 * 1024;
+    if (fits864)
+      return launch_hist_lanes<864, 4, false, 2, int64_t>(n_rows, nnz, row_ptr, col, bins_r, bins_c, width_r, cb, ull,
+                                                           vec_ok, false, s);
+    return launch_hist_lanes<768, 4, false, 2, int64_t>(n_rows, nnz, row_ptr, col, bins_r, bins_c, width_r, cb, ull,
+                                                         vec_ok, false, s);
+  }
+  const int blocks_cap = sm_count() * 2;
+  int64_t chunk = (nnz + blocks_cap - 1) / blocks_cap;
+  chunk = ((chunk + 4095) / 4096) * 4096;
+  const int blocks = (int)((nnz + chunk - 1) / chunk);
+  const size_t smem = H_WIN * 4 + (H_EDGE_SMEM + 1) * 8;
+  if (bins_r <= H_EDGE_SMEM) {
+    SME_CUDA(cudaFuncSetAttribute(k_hist2d_csr<true, int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_hist2d_csr<true, int64_t><<<blocks, H_NT, smem, s>>>(n_rows, nnz, row_ptr, col, bins_r, bins_c, width_r, cb, ull,
+                                                           chunk, vec_ok);
+  } else {
+    SME_CUDA(cudaFuncSetAttribute(k_hist2d_csr<false, int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_hist2d_csr<false, int64_t><<<blocks, H_NT, smem, s>>>(n_rows, nnz, row_ptr, col, bins_r, bins_c, width_r, cb, ull,
+                                                            chunk, vec_ok);
+  }
+  SME_CHECK_LAUNCH("k_hist2d_csr");
+  return SME_OK;
+}
+
 SME_API int sme_hist2d_coo(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row, const int32_t* col,
                            int32_t bins_r, int32_t bins_c, int64_t* counts, sme_stream_t stream) {
   int rc;
@@ -519,14 +563,24 @@ SME_API int sme_hist2d_coo(int64_t n_rows, int64_t n_cols, int64_t nnz, const in
   return SME_OK;
 }
 
-SME_API int sme_row_hist_csr(int64_t n_rows, const int32_t* row_ptr, int32_t bins, int64_t* counts,
-                             sme_stream_t stream) {
+template <typename IP>
+static int row_hist_impl(int64_t n_rows, const IP* row_ptr, int32_t bins, int64_t* counts, sme_stream_t stream) {
   int rc;
   if ((rc = check_bins(n_rows, bins, "row")) != SME_OK) return rc;
   cudaStream_t s = as_stream(stream);
-  k_row_hist_csr<<<(bins + 255) / 256, 256, 0, s>>>(n_rows, row_ptr, bins, n_rows / bins, counts);
+  k_row_hist_csr<IP><<<(bins + 255) / 256, 256, 0, s>>>(n_rows, row_ptr, bins, n_rows / bins, counts);
   SME_CHECK_LAUNCH("k_row_hist_csr");
   return SME_OK;
+}
+
+SME_API int sme_row_hist_csr(int64_t n_rows, const int32_t* row_ptr, int32_t bins, int64_t* counts,
+                             sme_stream_t stream) {
+  return row_hist_impl(n_rows, row_ptr, bins, counts, stream);
+}
+
+SME_API int sme_row_hist_csr_i64(int64_t n_rows, const int64_t* row_ptr, int32_t bins, int64_t* counts,
+                                 sme_stream_t stream) {
+  return row_hist_impl(n_rows, row_ptr, bins, counts, stream);
 }
 
 SME_API int sme_entropy(int64_t n_bins, const int64_t* counts, double base, double* out, int64_t* total,

@@ -1,4 +1,5 @@
-// scan.cuh — exclusive prefix sum of per-row lengths into an int32 row_ptr.
+// scan.cuh — exclusive prefix sum of per-row lengths into a row_ptr (int32, or int64
+// for matrices with nnz >= 2^31).
 //
 // Reduce-then-scan in three launches (tile sums, one-block scan of tile sums,
 // tile scan + offset).  The lengths come from a functor so the permuted row
@@ -89,9 +90,10 @@ static __global__ void __launch_bounds__(1024) k_scan_tile_offsets(int64_t n_til
 // (coalesced) inside a tile: item i of thread t is k = base + i*NT + t, so the
 // scan order within the tile is item-major — handled by scanning each item
 // column across the block in turn.
-template <class LenFn>
+template <class LenFn, typename OutT>
 __global__ void __launch_bounds__(SCAN_NT) k_scan_apply(int64_t n, LenFn len, const int64_t* tile_offsets,
-                                                        int32_t* out, int32_t* flag) {
+                                                        OutT* out, int32_t* flag) {
+  constexpr bool NARROW = sizeof(OutT) == 4;
   __shared__ int64_t s_total;
   int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
   int64_t run = tile_offsets[blockIdx.x];
@@ -103,15 +105,15 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan_apply(int64_t n, LenFn len, co
     __syncthreads();
     int64_t pos = run + ex;
     if (k < n) {
-      if (pos > INT32_MAX && flag) atomicOr(flag, SME_FLAG_RANGE);
-      out[k] = (int32_t)pos;
+      if (NARROW && pos > INT32_MAX && flag) atomicOr(flag, SME_FLAG_RANGE);
+      out[k] = (OutT)pos;
     }
     run += s_total;
     __syncthreads();
   }
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-    if (run > INT32_MAX && flag) atomicOr(flag, SME_FLAG_RANGE);
-    out[n] = (int32_t)run;
+    if (NARROW && run > INT32_MAX && flag) atomicOr(flag, SME_FLAG_RANGE);
+    out[n] = (OutT)run;
   }
 }
 
@@ -121,10 +123,10 @@ struct LenFromArray {
 };
 
 // Launch the three phases.  ws must hold scan_workspace_bytes(n).
-template <class LenFn>
-int exclusive_scan_lengths(int64_t n, LenFn len, int32_t* out, void* ws, int32_t* flag, cudaStream_t s) {
+template <class LenFn, typename OutT>
+int exclusive_scan_lengths(int64_t n, LenFn len, OutT* out, void* ws, int32_t* flag, cudaStream_t s) {
   if (n == 0) {
-    SME_CUDA(cudaMemsetAsync(out, 0, sizeof(int32_t), s));
+    SME_CUDA(cudaMemsetAsync(out, 0, sizeof(OutT), s));
     return SME_OK;
   }
   int64_t tiles = scan_tiles(n);

@@ -334,8 +334,8 @@ __device__ __forceinline__ float ld_x_na(const float* p, uint64_t pol) {
   return r;
 }
 
-template <typename T, int L>
-__global__ void __launch_bounds__(256) k_spmv_vector(int64_t n_rows, const int32_t* __restrict__ row_ptr,
+template <typename T, int L, typename IP = int32_t>
+__global__ void __launch_bounds__(256) k_spmv_vector(int64_t n_rows, const IP* __restrict__ row_ptr,
                                                      const int32_t* __restrict__ col, const T* __restrict__ val,
                                                      const T* __restrict__ x, T* __restrict__ y, int accumulate) {
   constexpr int RPW = 32 / L;  // rows per warp step
@@ -349,8 +349,8 @@ __global__ void __launch_bounds__(256) k_spmv_vector(int64_t n_rows, const int32
     const int64_t r = base + sub;
     T s = T(0);
     if (r < n_rows) {
-      const int32_t a = row_ptr[r], b = row_ptr[r + 1];
-      for (int32_t k = a + li; k < b; k += L)
+      const IP a = row_ptr[r], b = row_ptr[r + 1];
+      for (IP k = a + li; k < b; k += L)
         if (L >= 8) {
           s += ld_stream(val + k, pol_stream) * ld_x_na(x + ld_stream_i1(col + k, pol_stream), pol_keep);
         } else {
@@ -549,18 +549,18 @@ __global__ void k_spmv_coo_ordered(int64_t n_rows, const int32_t* __restrict__ r
   }
 }
 
-template <typename T>
-int launch_vector(int lanes, int64_t n_rows, const int32_t* rp, const int32_t* col, const T* val, const T* x, T* y,
+template <typename T, typename IP>
+int launch_vector(int lanes, int64_t n_rows, const IP* rp, const int32_t* col, const T* val, const T* x, T* y,
                   int acc, cudaStream_t s) {
   const int64_t threads = n_rows * lanes;
   const int blocks = grid_for(threads, 256, 8);
   switch (lanes) {
-    case 1: k_spmv_vector<T, 1><<<blocks, 256, 0, s>>>(n_rows, rp, col, val, x, y, acc); break;
-    case 2: k_spmv_vector<T, 2><<<blocks, 256, 0, s>>>(n_rows, rp, col, val, x, y, acc); break;
-    case 4: k_spmv_vector<T, 4><<<blocks, 256, 0, s>>>(n_rows, rp, col, val, x, y, acc); break;
-    case 8: k_spmv_vector<T, 8><<<blocks, 256, 0, s>>>(n_rows, rp, col, val, x, y, acc); break;
-    case 16: k_spmv_vector<T, 16><<<blocks, 256, 0, s>>>(n_rows, rp, col, val, x, y, acc); break;
-    case 32: k_spmv_vector<T, 32><<<blocks, 256, 0, s>>>(n_rows, rp, col, val, x, y, acc); break;
+    case 1: k_spmv_vector<T, 1, IP><<<blocks, 256, 0, s>>>(n_rows, rp, col, val, x, y, acc); break;
+    case 2: k_spmv_vector<T, 2, IP><<<blocks, 256, 0, s>>>(n_rows, rp, col, val, x, y, acc); break;
+    case 4: k_spmv_vector<T, 4, IP><<<blocks, 256, 0, s>>>(n_rows, rp, col, val, x, y, acc); break;
+    case 8: k_spmv_vector<T, 8, IP><<<blocks, 256, 0, s>>>(n_rows, rp, col, val, x, y, acc); break;
+    case 16: k_spmv_vector<T, 16, IP><<<blocks, 256, 0, s>>>(n_rows, rp, col, val, x, y, acc); break;
+    case 32: k_spmv_vector<T, 32, IP><<<blocks, 256, 0, s>>>(n_rows, rp, col, val, x, y, acc); break;
     default: SME_REQUIRE(false, "lanes must be one of 1,2,4,8,16,32 (got %d)", lanes);
   }
   SME_CHECK_LAUNCH("k_spmv_vector");
@@ -642,9 +642,9 @@ SME_API int sme_spmv_merge(int dtype, int64_t n_rows, int64_t n_cols, int64_t nn
                              n_tiles, carry, accumulate, s);
 }
 
-SME_API int sme_spmv_vector(int dtype, int lanes, int64_t n_rows, int64_t n_cols, const int32_t* row_ptr,
-                            const int32_t* col, const void* val, const void* x, void* y, int accumulate,
-                            sme_stream_t stream) {
+template <typename IP>
+static int spmv_vector_impl(int dtype, int lanes, int64_t n_rows, const IP* row_ptr, const int32_t* col,
+                            const void* val, const void* x, void* y, int accumulate, sme_stream_t stream) {
   SME_REQUIRE(n_rows >= 0 && n_rows < INT32_MAX, "n_rows exceeds int32");
   if (n_rows == 0) return SME_OK;
   cudaStream_t s = as_stream(stream);
@@ -655,6 +655,18 @@ SME_API int sme_spmv_vector(int dtype, int lanes, int64_t n_rows, int64_t n_cols
     return launch_vector<float>(lanes, n_rows, row_ptr, col, (const float*)val, (const float*)x, (float*)y,
                                 accumulate, s);
   SME_REQUIRE(false, "unknown dtype %d", dtype);
+}
+
+SME_API int sme_spmv_vector(int dtype, int lanes, int64_t n_rows, int64_t n_cols, const int32_t* row_ptr,
+                            const int32_t* col, const void* val, const void* x, void* y, int accumulate,
+                            sme_stream_t stream) {
+  return spmv_vector_impl(dtype, lanes, n_rows, row_ptr, col, val, x, y, accumulate, stream);
+}
+
+SME_API int sme_spmv_vector_i64(int dtype, int lanes, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                                const int32_t* col, const void* val, const void* x, void* y, int accumulate,
+                                sme_stream_t stream) {
+  return spmv_vector_impl(dtype, lanes, n_rows, row_ptr, col, val, x, y, accumulate, stream);
 }
 
 SME_API int sme_spmv_reduceat_exact(int64_t n_rows, const int32_t* row_ptr, const int32_t* col, const double* val,

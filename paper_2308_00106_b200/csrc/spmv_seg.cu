@@ -72,20 +72,23 @@ constexpr bool kStageRows = sizeof(T) == 8;
 // ---------------------------------------------------------------------------
 
 // counts[p * n + r] = entries of row r in panel p (rows are column-sorted)
-__global__ void k_seg_count(int64_t n_rows, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+// IP: row_ptr element type (int32_t; int64_t for nnz >= 2^31 — the per-panel positions
+// stay int32: every panel holds < 2^31 slots)
+template <typename IP>
+__global__ void k_seg_count(int64_t n_rows, const IP* __restrict__ row_ptr, const int32_t* __restrict__ col,
                             int32_t n_panels, const int32_t* __restrict__ bounds, int32_t* __restrict__ counts) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t a = row_ptr[r], b = row_ptr[r + 1];
-    int32_t k = a;
+    const IP a = row_ptr[r], b = row_ptr[r + 1];
+    IP k = a;
     for (int p = 0; p < n_panels; ++p) {
       const int32_t hi = bounds[p + 1];
       // binary search for the first column >= hi in [k, b)
-      int32_t lo = k, up = b;
+      IP lo = k, up = b;
       while (lo < up) {
-        const int32_t mid = (lo + up) >> 1;
+        const IP mid = (lo + up) >> 1;
         if (col[mid] < hi) lo = mid + 1; else up = mid;
       }
-      counts[(int64_t)p * n_rows + r] = lo - k;
+      counts[(int64_t)p * n_rows + r] = (int32_t)(lo - k);
       k = lo;
     }
   }
@@ -116,8 +119,8 @@ __global__ void k_seg_hdr(int64_t n_rows, const int32_t* __restrict__ pos, int32
 // holds panel p's per-row data (count, position, panel offset, first entry of the
 // row in that panel); an entry finds its panel among the bounds and takes the
 // panel's data by shuffle — no per-entry walk over the panels' count arrays.
-template <typename T>
-__global__ void k_seg_scatter(int64_t n_rows, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+template <typename T, typename IP>
+__global__ void k_seg_scatter(int64_t n_rows, const IP* __restrict__ row_ptr, const int32_t* __restrict__ col,
                               const T* __restrict__ val, int32_t n_panels, const int32_t* __restrict__ bounds,
                               const int32_t* __restrict__ counts, const int32_t* __restrict__ pos,
                               const int64_t* __restrict__ offsets, uint32_t* __restrict__ out_pk,
@@ -131,7 +134,7 @@ __global__ void k_seg_scatter(int64_t n_rows, const int32_t* __restrict__ row_pt
   const int32_t my_lo = (direct && lane < n_panels) ? bounds[lane] : 0;
   const int64_t my_off = (direct && lane < n_panels) ? offsets[lane] : 0;
   for (int64_t r = warp; r < n_rows; r += n_warps) {
-    const int32_t a = row_ptr[r], b = row_ptr[r + 1];
+    const IP a = row_ptr[r], b = row_ptr[r + 1];
     if (!direct) {  // > 32 panels: walk the count arrays (rare, small matrices)
       for (int p = lane; p < n_panels; p += 32) {
         if (counts[(int64_t)p * n_rows + r] == 0) {
@@ -143,10 +146,10 @@ __global__ void k_seg_scatter(int64_t n_rows, const int32_t* __restrict__ row_pt
           }
         }
       }
-      for (int32_t k = a + lane; k < b; k += 32) {
+      for (IP k = a + lane; k < b; k += 32) {
         const int32_t c = col[k];
         int p = 0;
-        int32_t first = a;
+        IP first = a;
         while (p + 1 < n_panels && c >= bounds[p + 1]) {
           first += counts[(int64_t)p * n_rows + r];
           ++p;
@@ -173,27 +176,27 @@ __global__ void k_seg_scatter(int64_t n_rows, const int32_t* __restrict__ row_pt
       const int32_t t = __shfl_up_sync(FULL, incl, o);
       if (lane >= o) incl += t;
     }
-    const int32_t first = a + incl - cnt;
+    const IP first = a + incl - cnt;
     // explicit zero of this row in panel `lane`
     if (lane < n_panels && cnt == 0 && pnext > ppos) {
       const int64_t dst = my_off + ppos;
       out_pk[dst] = (SEG_MARK << SEG_CSHIFT) | SEG_END | (uint32_t)(r - hdr[dst / SEG_CH]);
       out_val[dst] = T(0);
     }
-    for (int32_t k0 = a; k0 < b; k0 += 32) {
-      const int32_t k = k0 + lane;
+    for (IP k0 = a; k0 < b; k0 += 32) {
+      const IP k = k0 + lane;
       const int32_t c = k < b ? col[k] : INT32_MAX;
       // panel of c: number of panel upper bounds <= c (bounds held by lanes)
       int p = 0;
       for (int q = 0; q < n_panels; ++q) p += (c >= __shfl_sync(FULL, my_hi, q)) ? 1 : 0;
       if (p >= n_panels) p = n_panels - 1;
-      const int32_t f = __shfl_sync(FULL, first, p);
+      const IP f = __shfl_sync(FULL, first, p);
       const int32_t pc = __shfl_sync(FULL, cnt, p);
       const int32_t pp = __shfl_sync(FULL, ppos, p);
       const int64_t po = __shfl_sync(FULL, my_off, p);
       const int32_t lo = __shfl_sync(FULL, my_lo, p);
       if (k < b) {
-        const int64_t dst = po + pp + (k - f);
+        const int64_t dst = po + pp + (int64_t)(k - f);
         const bool last = k - f == pc - 1;
         out_pk[dst] = ((uint32_t)(c - lo) << SEG_CSHIFT) | (last ? SEG_END : 0u) | (uint32_t)(r - hdr[dst / SEG_CH]);
         out_val[dst] = val[k];
@@ -224,9 +227,11 @@ inline size_t sg_warp_bytes(int n_panels, size_t val_bytes) {
                   16);
 }
 
-template <typename T>
+// Row starts of a group are kept relative to its first entry (int32 even when row_ptr is
+// int64): the image paths address col / val through the group's base pointers.
+template <typename T, typename IP>
 __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
-    int64_t n_rows, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col, const T* __restrict__ val,
+    int64_t n_rows, const IP* __restrict__ row_ptr, const int32_t* __restrict__ col_all, const T* __restrict__ val_all,
     int32_t n_panels, const int32_t* __restrict__ bounds, const int32_t* __restrict__ counts,
     const int32_t* __restrict__ pos, const int64_t* __restrict__ offsets, uint32_t* __restrict__ out_pk,
     T* __restrict__ out_val, const int32_t* __restrict__ hdr, size_t warp_bytes, int fill_ballot) {
@@ -265,9 +270,12 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
   for (int64_t g = warp; g < n_groups; g += n_warps) {
     const int64_t r0 = g * 32;
     const int nr = (int)min((int64_t)32, n_rows - r0);
+    const IP gbase = row_ptr[r0];  // the group's first entry: s_rp and the image paths are relative to it
+    const int32_t* __restrict__ col = col_all + gbase;
+    const T* __restrict__ val = val_all + gbase;
     __syncwarp();
-    if (lane < nr) s_rp[lane] = row_ptr[r0 + lane];
-    if (lane == 0) s_rp[nr] = row_ptr[r0 + nr];
+    if (lane < nr) s_rp[lane] = (int32_t)(row_ptr[r0 + lane] - gbase);
+    if (lane == 0) s_rp[nr] = (int32_t)(row_ptr[r0 + nr] - gbase);
     // the group's range in each panel and its place in the staging image
     int32_t gs = 0, len = 0;
     if (lane < P) {
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
     if (total > SG_CAP) {  // long rows: the per-row path
       for (int i = 0; i < nr; ++i) {
         const int64_t r = r0 + i;
-        const int32_t a = row_ptr[r], b = row_ptr[r + 1];
+        const IP a = row_ptr[r], b = row_ptr[r + 1];
         int32_t cnt = 0, ppos = 0, pnext = 0;
         if (lane < P) {
           cnt = counts[(int64_t)lane * n_rows + r];
@@ -299,28 +307,28 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
           const int32_t t = __shfl_up_sync(FULL, ic, o);
           if (lane >= o) ic += t;
         }
-        const int32_t first = a + ic - cnt;
+        const IP first = a + ic - cnt;
         if (lane < P && cnt == 0 && pnext > ppos) {
           const int64_t dst = my_off + ppos;
           out_pk[dst] = (SEG_MARK << SEG_CSHIFT) | SEG_END | (uint32_t)(r - hdr[dst / SEG_CH]);
           out_val[dst] = T(0);
         }
-        for (int32_t k0 = a; k0 < b; k0 += 32) {
-          const int32_t k = k0 + lane;
-          const int32_t c = k < b ? col[k] : INT32_MAX;
+        for (IP k0 = a; k0 < b; k0 += 32) {
+          const IP k = k0 + lane;
+          const int32_t c = k < b ? col_all[k] : INT32_MAX;
           int p = 0;
           for (int q = 0; q < P; ++q) p += (c >= __shfl_sync(FULL, my_hi, q)) ? 1 : 0;
           if (p >= P) p = P - 1;
-          const int32_t f = __shfl_sync(FULL, first, p);
+          const IP f = __shfl_sync(FULL, first, p);
           const int32_t pc = __shfl_sync(FULL, cnt, p);
           const int32_t pq = __shfl_sync(FULL, ppos, p);
           const int64_t po = __shfl_sync(FULL, my_off, p);
           const int32_t lo = __shfl_sync(FULL, my_lo, p);
           if (k < b) {
-            const int64_t dst = po + pq + (k - f);
+            const int64_t dst = po + pq + (int64_t)(k - f);
             out_pk[dst] = ((uint32_t)(c - lo) << SEG_CSHIFT) | (k - f == pc - 1 ? SEG_END : 0u) |
                           (uint32_t)(r - hdr[dst / SEG_CH]);
-            out_val[dst] = val[k];
+            out_val[dst] = val_all[k];
           }
         }
       }
@@ -980,7 +988,8 @@ SME_API int sme_seg_workspace_size(int64_t n_rows, int32_t n_panels, size_t* byt
 // Step 1: per-panel entry positions pos[p * (n_rows + 1) + r] (exclusive scan of the
 // padded row lengths; pos[p * (n_rows + 1) + n_rows] = entries of panel p).
 // ws keeps the per-panel row counts for step 2.
-SME_API int sme_seg_positions(int64_t n_rows, const int32_t* row_ptr, const int32_t* col, int32_t n_panels,
+template <typename IP>
+static int seg_positions_impl(int64_t n_rows, const IP* row_ptr, const int32_t* col, int32_t n_panels,
                               const int32_t* bounds, int full_last, int32_t* pos, void* ws, size_t ws_bytes,
                               sme_stream_t stream) {
   SME_REQUIRE(n_rows >= 0 && n_rows < INT32_MAX && n_panels >= 1 && n_panels <= 1024, "bad arguments");
@@ -993,7 +1002,7 @@ SME_API int sme_seg_positions(int64_t n_rows, const int32_t* row_ptr, const int3
   }
   int32_t* counts = (int32_t*)ws;
   void* scan_ws = (char*)ws + align_up((size_t)n_panels * n_rows * 4);
-  k_seg_count<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, row_ptr, col, n_panels, bounds, counts);
+  k_seg_count<IP><<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, row_ptr, col, n_panels, bounds, counts);
   SME_CHECK_LAUNCH("k_seg_count");
   for (int p = 0; p < n_panels; ++p) {
     const bool full = full_last && p == n_panels - 1;
@@ -1004,11 +1013,26 @@ SME_API int sme_seg_positions(int64_t n_rows, const int32_t* row_ptr, const int3
   return SME_OK;
 }
 
+SME_API int sme_seg_positions(int64_t n_rows, const int32_t* row_ptr, const int32_t* col, int32_t n_panels,
+                              const int32_t* bounds, int full_last, int32_t* pos, void* ws, size_t ws_bytes,
+                              sme_stream_t stream) {
+  return seg_positions_impl(n_rows, row_ptr, col, n_panels, bounds, full_last, pos, ws, ws_bytes, stream);
+}
+
+// int64 row_ptr (nnz >= 2^31); each panel must still hold < 2^31 slots (the caller picks
+// enough panels; pos stays int32 per panel)
+SME_API int sme_seg_positions_i64(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, int32_t n_panels,
+                                  const int32_t* bounds, int full_last, int32_t* pos, void* ws, size_t ws_bytes,
+                                  sme_stream_t stream) {
+  return seg_positions_impl(n_rows, row_ptr, col, n_panels, bounds, full_last, pos, ws, ws_bytes, stream);
+}
+
 // Step 2: chunk headers and the packed entries.  offsets[p] (int64 device) = first
 // element of panel p in pk/val (multiple of 128); pk and val must be pre-filled
 // with the tail padding (pk 0xFFFFFFFF, val 0) by the caller.  bounds[p+1]-bounds[p]
 // must be < 2^23 - 1 (SEG_MARK).
-SME_API int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* row_ptr, const int32_t* col, const void* val,
+template <typename IP>
+static int seg_fill_impl(int dtype, int64_t n_rows, const IP* row_ptr, const int32_t* col, const void* val,
                          int32_t n_panels, const int32_t* bounds, const int32_t* pos, const int64_t* offsets,
                          const int64_t* h_offsets, uint32_t* pk, void* out_val, int32_t* hdr, const void* ws,
                          sme_stream_t stream) {
@@ -1034,22 +1058,38 @@ SME_API int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* row_ptr, cons
       return SME_OK;
     };
     if (dtype == SME_F64)
-      launch(k_seg_scatter_groups<double>, 8, (const double*)val, (double*)out_val);
+      launch(k_seg_scatter_groups<double, IP>, 8, (const double*)val, (double*)out_val);
     else
-      launch(k_seg_scatter_groups<float>, 4, (const float*)val, (float*)out_val);
+      launch(k_seg_scatter_groups<float, IP>, 4, (const float*)val, (float*)out_val);
     SME_CHECK_LAUNCH("k_seg_scatter_groups");
     return SME_OK;
   }
   if (dtype == SME_F64)
-    k_seg_scatter<double><<<grid_for(n_rows * 32, 256), 256, 0, s>>>(n_rows, row_ptr, col, (const double*)val, n_panels,
+    k_seg_scatter<double, IP><<<grid_for(n_rows * 32, 256), 256, 0, s>>>(n_rows, row_ptr, col, (const double*)val, n_panels,
                                                                       bounds, counts, pos, offsets, pk,
                                                                       (double*)out_val, hdr);
   else
-    k_seg_scatter<float><<<grid_for(n_rows * 32, 256), 256, 0, s>>>(n_rows, row_ptr, col, (const float*)val, n_panels,
+    k_seg_scatter<float, IP><<<grid_for(n_rows * 32, 256), 256, 0, s>>>(n_rows, row_ptr, col, (const float*)val, n_panels,
                                                                      bounds, counts, pos, offsets, pk, (float*)out_val,
                                                                      hdr);
   SME_CHECK_LAUNCH("k_seg_scatter");
   return SME_OK;
+}
+
+SME_API int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* row_ptr, const int32_t* col, const void* val,
+                         int32_t n_panels, const int32_t* bounds, const int32_t* pos, const int64_t* offsets,
+                         const int64_t* h_offsets, uint32_t* pk, void* out_val, int32_t* hdr, const void* ws,
+                         sme_stream_t stream) {
+  return seg_fill_impl(dtype, n_rows, row_ptr, col, val, n_panels, bounds, pos, offsets, h_offsets, pk, out_val, hdr,
+                       ws, stream);
+}
+
+SME_API int sme_seg_fill_i64(int dtype, int64_t n_rows, const int64_t* row_ptr, const int32_t* col, const void* val,
+                             int32_t n_panels, const int32_t* bounds, const int32_t* pos, const int64_t* offsets,
+                             const int64_t* h_offsets, uint32_t* pk, void* out_val, int32_t* hdr, const void* ws,
+                             sme_stream_t stream) {
+  return seg_fill_impl(dtype, n_rows, row_ptr, col, val, n_panels, bounds, pos, offsets, h_offsets, pk, out_val, hdr,
+                       ws, stream);
 }
 
 // Groups of non-empty rows: entry-parallel placement (1, default) or the lane-per-row

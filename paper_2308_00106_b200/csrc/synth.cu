@@ -53,8 +53,8 @@ __global__ void k_random_rows(int64_t n_rows, int64_t n_cols, int32_t k, uint64_
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t i = warp; i < n_rows; i += n_warps) {
-    if (lane == 0) row_ptr[i] = (int32_t)(i * k);
-    if (i == n_rows - 1 && lane == 0) row_ptr[n_rows] = (int32_t)(n_rows * k);
+    if (row_ptr && lane == 0) row_ptr[i] = (int32_t)(i * k);
+    if (row_ptr && i == n_rows - 1 && lane == 0) row_ptr[n_rows] = (int32_t)(n_rows * k);
     const int64_t r = rows ? (int64_t)__ldg(rows + i) : i;
     uint32_t acc = 0xFFFFFFFFu;  // lane a holds accepted[a], a < cnt
     int cnt = 0;
@@ -118,7 +118,7 @@ SME_API int sme_synth_random_rows(int dtype, int64_t n_rows, int64_t n_cols, int
                                   int32_t* row_ptr, int32_t* col, void* val, sme_stream_t stream) {
   SME_REQUIRE(n_rows >= 1 && n_cols >= 1 && n_cols < INT32_MAX, "bad dimensions");
   SME_REQUIRE(k >= 1 && k <= 32 && k <= n_cols, "k must lie in [1, min(32, n_cols)]");
-  SME_REQUIRE(n_rows * k < INT32_MAX, "nnz exceeds int32");
+  SME_REQUIRE(!row_ptr || n_rows * k < INT32_MAX, "nnz exceeds int32 (pass row_ptr = NULL: it is r * k)");
   cudaStream_t s = as_stream(stream);
   int blocks = grid_for(n_rows * 32, 256);
   if (dtype == SME_F64)

@@ -103,8 +103,8 @@ def histogram_2d(m, bins_r: int, bins_c: int) -> BinnedHistogram:
     counts = _zeros(bins_r * bins_c)
     csr = m if isinstance(m, CsrMatrix) else getattr(m, "_csr", None)
     if csr is not None:
-        _lib.call("sme_hist2d_csr", csr.n_rows, csr.n_cols, csr.nnz, ptr(csr.d_row_ptr), ptr(csr.d_col_idx),
-                  bins_r, bins_c, ptr(counts), stream())
+        _lib.call_rp("sme_hist2d_csr", csr.d_row_ptr, csr.n_rows, csr.n_cols, csr.nnz, ptr(csr.d_row_ptr),
+                     ptr(csr.d_col_idx), bins_r, bins_c, ptr(counts), stream())
     elif isinstance(m, CooMatrix):
         _lib.call("sme_hist2d_coo", m.n_rows, m.n_cols, m.nnz, ptr(m.d_row_idx), ptr(m.d_col_idx), bins_r,
                   bins_c, ptr(counts), stream())
@@ -118,7 +118,7 @@ def row_histogram(m, bins: int) -> BinnedHistogram:
     _check_bins(bins, m.n_rows, "row")
     csr = m if isinstance(m, CsrMatrix) else _csr_of(m)
     counts = _zeros(bins)
-    _lib.call("sme_row_hist_csr", csr.n_rows, ptr(csr.d_row_ptr), bins, ptr(counts), stream())
+    _lib.call_rp("sme_row_hist_csr", csr.d_row_ptr, csr.n_rows, ptr(csr.d_row_ptr), bins, ptr(counts), stream())
     return BinnedHistogram(counts, (_bin_edges(m.n_rows, bins),))
 
 

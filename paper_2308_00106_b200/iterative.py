@@ -97,7 +97,7 @@ class PermutedOperator:
             self._qinv = Permutation(self.q, _trusted=True).d_inverse if self.q is not None else None
         if kern == "seg":
             return seg_of(self.B, full_last=True)
-        if kern == "vector" and self.q is None:
+        if kern == "vector" and self.q is None and not self.B.wide:  # VectorEpi: int32 row_ptr only
             return VectorEpi(self.B, default_lanes(self.B))
         return None
 

@@ -31,6 +31,8 @@ from ._cuda import ptr, stream
 from .matio import CooMatrix, CsrMatrix
 
 KERNELS = ("auto", "seg", "stream", "panel", "vector", "merge", "exact")
+# kernels with int64 row_ptr twins (CSRs of nnz >= 2^31 - 1; auto_kernel only picks these)
+WIDE_KERNELS = ("seg", "vector")
 
 
 @dataclass(frozen=True, eq=False)
@@ -126,7 +128,7 @@ def row_stats(m: CsrMatrix) -> tuple[int, int]:
     """(max row length, empty rows), one device reduction, cached."""
     if "row_stats" not in m._cache:
         out = torch.empty(2, dtype=torch.int64, device=m.d_row_ptr.device)
-        _lib.call("sme_row_stats", m.n_rows, ptr(m.d_row_ptr), ptr(out), stream())
+        _lib.call_rp("sme_row_stats", m.d_row_ptr, m.n_rows, ptr(m.d_row_ptr), ptr(out), stream())
         m._cache["row_stats"] = tuple(int(v) for v in out.cpu())
     return m._cache["row_stats"]
 
@@ -222,10 +224,13 @@ def spmv_into(m: CsrMatrix, xd: torch.Tensor, y: torch.Tensor, kernel: str = "ve
     if kernel == "auto":
         kernel = auto_kernel(m)
         if kernel in ("panel", "seg") and accumulate:
-            kernel = "stream"
+            kernel = "vector" if m.wide else "stream"
+    if m.wide and kernel not in WIDE_KERNELS:
+        raise ValueError(f"kernel {kernel!r} uses int32 row offsets; a CSR with int64 row_ptr "
+                         f"(nnz >= 2^31 - 1) runs one of {WIDE_KERNELS}")
     if kernel == "vector":
-        _lib.call("sme_spmv_vector", dt, lanes or default_lanes(m), m.n_rows, m.n_cols, ptr(m.d_row_ptr),
-                  ptr(m.d_col_idx), ptr(m.d_values), ptr(xd), ptr(y), int(accumulate), stream())
+        _lib.call_rp("sme_spmv_vector", m.d_row_ptr, dt, lanes or default_lanes(m), m.n_rows, m.n_cols,
+                     ptr(m.d_row_ptr), ptr(m.d_col_idx), ptr(m.d_values), ptr(xd), ptr(y), int(accumulate), stream())
     elif kernel == "seg":
         from .seg import seg_of
 
@@ -438,8 +443,8 @@ def spmv_csr_parallel(m: CsrMatrix, x, workers: int, reuse_pool: bool = True, ke
         lo, hi = int(lo), int(hi)
         if hi == lo:
             continue
-        _lib.call("sme_spmv_vector", dt, lanes, hi - lo, m.n_cols, ptr(m.d_row_ptr) + lo * es, ptr(m.d_col_idx),
-                  ptr(m.d_values), ptr(xd), ptr(y) + lo * ys, 0, stream())
+        _lib.call_rp("sme_spmv_vector", m.d_row_ptr, dt, lanes, hi - lo, m.n_cols, ptr(m.d_row_ptr) + lo * es,
+                     ptr(m.d_col_idx), ptr(m.d_values), ptr(xd), ptr(y) + lo * ys, 0, stream())
     return _y_out(y, mode)
 
 
@@ -452,10 +457,12 @@ def coo_entry_order(m: CooMatrix) -> CsrMatrix:
     if plan is None:
         from .matio import _coo_build_csr
 
+        if m.nnz >= _cuda.INT32_MAX:
+            raise ValueError("the ordered COO SpMV keys entries by int32 ids (nnz < 2^31 - 1); use kernel='atomic'")
         dev = m.d_row_idx.device
         ids = torch.arange(m.nnz, dtype=torch.int32, device=dev)
         proxy = CooMatrix._from_device(m.n_rows, max(1, m.nnz), m.d_row_idx, ids, m.d_values)
-        plan = _coo_build_csr(proxy, None, None, check=False)
+        plan = _coo_build_csr(proxy, None, None, check=False, row_ptr_dtype=torch.int32)
         m._cache["coo_order"] = plan
     return plan
 

@@ -3,7 +3,9 @@
 Drop-in for the storage half of `spmv_entropy.matio` (reference
 /root/reference/pkg/src/spmv_entropy/matio.py): same class names, constructor
 arguments, validation rules and error messages, but the arrays live in HBM as
-int32 indices and f64 (default, like the reference) or f32 values.  The
+int32 indices and f64 (default, like the reference) or f32 values.  row_ptr is
+int32 while nnz < 2^31 - 1 and int64 above (the reference's int64 everywhere,
+matio.py:97-99; those CSRs go through the `_i64` entry points of include/sme.h).  The
 reference attribute names (`row_idx`, `col_idx`, `values`, `row_ptr`) return
 host numpy copies widened to int64 / float64 (made lazily, cached), so code and
 tests written against the reference keep working; the device tensors are the
@@ -72,10 +74,8 @@ class CsrMatrix:
                 raise ValueError("row_ptr must have n_rows + 1 entries")
             if _numel(col_idx) != _numel(values):
                 raise ValueError("col_idx and values must have identical length")
-            if _numel(col_idx) >= _cuda.INT32_MAX:
-                raise ValueError("nnz exceeds the int32 offsets of the GPU layout")
         vdt = _value_dtype(values, dtype)
-        self.d_row_ptr = _cuda.as_index_tensor(row_ptr, "row_ptr")
+        self.d_row_ptr = _cuda.as_row_ptr_tensor(row_ptr, _numel(values))
         self.d_col_idx = _cuda.as_index_tensor(col_idx, "col_idx")
         self.d_values = _cuda.as_value_tensor(values, vdt)
         self._host: dict[str, np.ndarray] = {}
@@ -94,8 +94,8 @@ class CsrMatrix:
 
     def _validate(self) -> None:
         fl = DeviceFlags()
-        _lib.call("sme_csr_validate", self.n_rows, self.n_cols, self.nnz, ptr(self.d_row_ptr),
-                  ptr(self.d_col_idx), fl.flag_ptr, stream())
+        _lib.call_rp("sme_csr_validate", self.d_row_ptr, self.n_rows, self.n_cols, self.nnz, ptr(self.d_row_ptr),
+                     ptr(self.d_col_idx), fl.flag_ptr, stream())
         bits, _ = fl.read()
         if bits & _lib.FLAG_ROWPTR:
             first, last = int(self.d_row_ptr[0]), int(self.d_row_ptr[-1])
@@ -115,6 +115,11 @@ class CsrMatrix:
     @property
     def dtype(self) -> torch.dtype:
         return self.d_values.dtype
+
+    @property
+    def wide(self) -> bool:
+        """int64 row_ptr (nnz >= 2^31 - 1, or forced by _cuda.FORCE_WIDE_ROW_PTR)."""
+        return self.d_row_ptr.dtype == torch.int64
 
     def _h(self, key: str, t: torch.Tensor, dt) -> np.ndarray:
         if key not in self._host:
@@ -156,7 +161,7 @@ class CsrMatrix:
         """Sum of lengths of rows longer than SME_SORT_SMEM_MAX (scratch sizing)."""
         if "long_nnz" not in self._cache:
             out = torch.zeros(1, dtype=torch.int64, device=self.d_row_ptr.device)
-            _lib.call("sme_long_row_nnz", self.n_rows, ptr(self.d_row_ptr), ptr(out), stream())
+            _lib.call_rp("sme_long_row_nnz", self.d_row_ptr, self.n_rows, ptr(self.d_row_ptr), ptr(out), stream())
             self._cache["long_nnz"] = int(out.item())
         return self._cache["long_nnz"]
 
@@ -242,28 +247,29 @@ class CooMatrix:
         return f"CooMatrix({self.n_rows}x{self.n_cols}, nnz={self.nnz}, {self.dtype}, device)"
 
 
-def _coo_build_csr(m: CooMatrix, row_map, col_map, check: bool) -> CsrMatrix:
-    """GPU counting sort + segmented column sort (csr_build.cu)."""
+def _coo_build_csr(m: CooMatrix, row_map, col_map, check: bool, row_ptr_dtype=None) -> CsrMatrix:
+    """GPU counting sort + segmented column sort (csr_build.cu).  row_ptr is int32 while
+    nnz < 2^31 - 1, else int64 (row_ptr_dtype overrides: internal plans)."""
     dev = _cuda.require_cuda()
     n_rows, n_cols, nnz = m.n_rows, m.n_cols, m.nnz
     fl = DeviceFlags()
-    row_ptr = torch.empty(n_rows + 1, dtype=torch.int32, device=dev)
+    row_ptr = torch.empty(n_rows + 1, dtype=row_ptr_dtype or _cuda.row_ptr_dtype(nnz), device=dev)
     ws1 = _cuda.workspace(_lib.query_size("sme_row_ptr_workspace_size", n_rows))
-    _lib.call("sme_coo_row_ptr", n_rows, n_cols, nnz, ptr(m.d_row_idx), ptr(m.d_col_idx), ptr(row_map),
-              ptr(row_ptr), ptr(ws1), ws1.numel(), fl.flag_ptr, stream())
+    _lib.call_rp("sme_coo_row_ptr", row_ptr, n_rows, n_cols, nnz, ptr(m.d_row_idx), ptr(m.d_col_idx), ptr(row_map),
+                 ptr(row_ptr), ptr(ws1), ws1.numel(), fl.flag_ptr, stream())
     if check:
         bits, _ = fl.read()
         if bits & _lib.FLAG_RANGE:
             _raise_range(m)
     long_t = torch.zeros(1, dtype=torch.int64, device=dev)
-    _lib.call("sme_long_row_nnz", n_rows, ptr(row_ptr), ptr(long_t), stream())
+    _lib.call_rp("sme_long_row_nnz", row_ptr, n_rows, ptr(row_ptr), ptr(long_t), stream())
     long_nnz = int(long_t.item())
     col = torch.empty(nnz, dtype=torch.int32, device=dev)
     val = torch.empty(nnz, dtype=m.dtype, device=dev)
     ws2 = _cuda.workspace(_lib.query_size("sme_coo_to_csr_workspace_size", n_rows, nnz, long_nnz))
-    _lib.call("sme_coo_to_csr", _cuda.sme_dtype(m.d_values), n_rows, n_cols, nnz, ptr(m.d_row_idx),
-              ptr(m.d_col_idx), ptr(m.d_values), ptr(row_map), ptr(col_map), ptr(row_ptr), ptr(col), ptr(val),
-              ptr(ws2), ws2.numel(), long_nnz, fl.flag_ptr, fl.dup_ptr, stream())
+    _lib.call_rp("sme_coo_to_csr", row_ptr, _cuda.sme_dtype(m.d_values), n_rows, n_cols, nnz, ptr(m.d_row_idx),
+                 ptr(m.d_col_idx), ptr(m.d_values), ptr(row_map), ptr(col_map), ptr(row_ptr), ptr(col), ptr(val),
+                 ptr(ws2), ws2.numel(), long_nnz, fl.flag_ptr, fl.dup_ptr, stream())
     if check:
         bits, dup = fl.read()
         if bits & _lib.FLAG_DUPLICATE:
@@ -298,7 +304,7 @@ def coo_to_csr(m: CooMatrix) -> CsrMatrix:
 def csr_to_coo(m: CsrMatrix) -> CooMatrix:
     """Expand CSR back to COO; coo_to_csr(csr_to_coo(m)) reproduces m exactly (matio.py:297-300)."""
     row = torch.empty(m.nnz, dtype=torch.int32, device=m.d_row_ptr.device)
-    _lib.call("sme_csr_expand_rows", m.n_rows, ptr(m.d_row_ptr), ptr(row), stream())
+    _lib.call_rp("sme_csr_expand_rows", m.d_row_ptr, m.n_rows, ptr(m.d_row_ptr), ptr(row), stream())
     return CooMatrix._from_device(m.n_rows, m.n_cols, row, m.d_col_idx.clone(), m.d_values.clone(), csr=m)
 
 

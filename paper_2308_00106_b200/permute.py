@@ -374,10 +374,10 @@ def permute_csr(m: CsrMatrix, p_r: Permutation | None, p_c: Permutation | None) 
             raise ValueError("permutation sizes must match matrix dimensions")
     dev = m.d_row_ptr.device
     inv_r = p_r.d_inverse if p_r is not None else None
-    row_ptr = torch.empty(m.n_rows + 1, dtype=torch.int32, device=dev)
+    row_ptr = torch.empty(m.n_rows + 1, dtype=m.d_row_ptr.dtype, device=dev)  # int64 for nnz >= 2^31 - 1
     ws1 = _cuda.workspace(_lib.query_size("sme_row_ptr_workspace_size", m.n_rows))
-    _lib.call("sme_permute_csr_row_ptr", m.n_rows, ptr(m.d_row_ptr), ptr(inv_r), ptr(row_ptr), ptr(ws1),
-              ws1.numel(), stream())
+    _lib.call_rp("sme_permute_csr_row_ptr", row_ptr, m.n_rows, ptr(m.d_row_ptr), ptr(inv_r), ptr(row_ptr),
+                 ptr(ws1), ws1.numel(), stream())
     long_nnz = m.long_row_nnz()
     ws2 = _cuda.workspace(_lib.query_size("sme_permute_csr_workspace_size", m.n_rows, m.nnz, long_nnz))
     col = torch.empty_like(m.d_col_idx)
@@ -397,7 +397,7 @@ def permute_csr(m: CsrMatrix, p_r: Permutation | None, p_c: Permutation | None) 
             _lib.call("sme_l2_reset_persisting")
         if n_passes == n_slices:
             cmap = None
-    _lib.call("sme_permute_csr", _cuda.sme_dtype(m.d_values), m.n_rows, m.n_cols, m.nnz, ptr(m.d_row_ptr),
+    _lib.call_rp("sme_permute_csr", row_ptr, _cuda.sme_dtype(m.d_values), m.n_rows, m.n_cols, m.nnz, ptr(m.d_row_ptr),
               ptr(src_col), ptr(m.d_values), ptr(inv_r), ptr(cmap),
               ptr(row_ptr), ptr(col), ptr(val), ptr(ws2), ws2.numel(), long_nnz, fl.flag_ptr, fl.dup_ptr,
               stream())

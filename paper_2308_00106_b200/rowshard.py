@@ -113,7 +113,8 @@ class RowShardedSpMV:
             lo, hi = 0, m.n_rows
         p0, p1 = int(m.d_row_ptr[lo]), int(m.d_row_ptr[hi])
         dev = m.d_row_ptr.device
-        row_ptr = (m.d_row_ptr[lo : hi + 1] - p0).contiguous()
+        # a shard of a wide (int64 row_ptr) matrix goes back to int32 offsets when it fits
+        row_ptr = (m.d_row_ptr[lo : hi + 1] - p0).to(_cuda.row_ptr_dtype(p1 - p0)).contiguous()
         col = torch.empty(p1 - p0, dtype=torch.int32, device=dev)
         _lib.call("sme_rowshard_remap_cols", p1 - p0, m.n_cols, plan.world, plan.pad, ptr(m.d_col_idx) + 4 * p0,
                   ptr(col), stream())
@@ -282,7 +283,8 @@ class DistributedPowerIteration:
         self.row_lo, self.row_hi = lo, hi
         Cm = op.B
         p0, p1 = int(Cm.d_row_ptr[lo]), int(Cm.d_row_ptr[hi])
-        local = CsrMatrix._from_device(hi - lo, self.n, (Cm.d_row_ptr[lo : hi + 1] - p0).contiguous(),
+        local = CsrMatrix._from_device(hi - lo, self.n,
+                                       (Cm.d_row_ptr[lo : hi + 1] - p0).to(_cuda.row_ptr_dtype(p1 - p0)).contiguous(),
                                        Cm.d_col_idx[p0:p1].clone(), Cm.d_values[p0:p1].clone())
         self.local = local
         self.lay = seg_of(local, full_last=True, split_rows=False)  # its epilogue pass stores to peers

@@ -38,6 +38,8 @@ def auto_seg_panels(m: CsrMatrix, l2_fraction: float = 0.38) -> int:
 
     xb = m.n_cols * m.d_values.element_size()
     p = max(1, math.ceil(xb / (l2_bytes() * l2_fraction)))
+    # int32 slot positions per panel: keep every panel near 2^30 slots at most (nnz >= 2^31)
+    p = max(p, math.ceil((m.nnz + m.n_rows) / (1 << 30)))
     return max(p, math.ceil(m.n_cols / MAX_PANEL_COLS))
 
 
@@ -61,10 +63,11 @@ class SegLayout:
         ws = _cuda.workspace(_lib.query_size("sme_seg_workspace_size", n, P))
         pos = torch.empty(P * (n + 1), dtype=torch.int32, device=dev)
         self.full_last = bool(full_last)
-        _lib.call("sme_seg_positions", n, ptr(m.d_row_ptr), ptr(m.d_col_idx), P, ptr(self.bounds), int(full_last),
-                  ptr(pos), ptr(ws),
-                  ws.numel(), s)
+        _lib.call_rp("sme_seg_positions", m.d_row_ptr, n, ptr(m.d_row_ptr), ptr(m.d_col_idx), P, ptr(self.bounds),
+                     int(full_last), ptr(pos), ptr(ws), ws.numel(), s)
         ent = pos.view(P, n + 1)[:, -1].to(torch.int64).cpu().numpy()
+        if (ent < 0).any():  # int32 slot positions wrapped: a panel of >= 2^31 slots
+            raise ValueError(f"a column panel holds >= 2^31 entries; use more than {P} panels")
         offs = np.zeros(P + 1, dtype=np.int64)
         for p in range(P):
             offs[p + 1] = offs[p] + -(-int(ent[p]) // CHUNK) * CHUNK
@@ -87,9 +90,9 @@ class SegLayout:
             self.val[int(offs[-1]):] = 0
         h_offs = (ctypes.c_int64 * P)(*[int(o) for o in offs[:P]])
         d_offs = torch.from_numpy(offs[:P].copy()).to(dev)
-        _lib.call("sme_seg_fill", _cuda.sme_dtype(m.d_values), n, ptr(m.d_row_ptr), ptr(m.d_col_idx),
-                  ptr(m.d_values), P, ptr(self.bounds), ptr(pos), ptr(d_offs), ctypes.cast(h_offs, ctypes.c_void_p),
-                  ptr(self.pk), ptr(self.val), ptr(self.hdr), ptr(ws), s)
+        _lib.call_rp("sme_seg_fill", m.d_row_ptr, _cuda.sme_dtype(m.d_values), n, ptr(m.d_row_ptr),
+                     ptr(m.d_col_idx), ptr(m.d_values), P, ptr(self.bounds), ptr(pos), ptr(d_offs),
+                     ctypes.cast(h_offs, ctypes.c_void_p), ptr(self.pk), ptr(self.val), ptr(self.hdr), ptr(ws), s)
         self.n_warps = int(n_warps or seg_warps())
         self.plans = torch.empty(P * (self.n_warps + 1), dtype=torch.int32, device=dev)
         # split-row plans when one row would dominate a warp's share (power-law rows): ranges

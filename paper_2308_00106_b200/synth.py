@@ -43,11 +43,16 @@ def random_rows(n_rows: int, n_cols: int, k: int, seed: int = C4_SEED, dtype=np.
     dev = _cuda.require_cuda()
     vdt = _vdt(dtype)
     nnz = n_rows * k
-    row_ptr = torch.empty(n_rows + 1, dtype=torch.int32, device=dev)
     col = torch.empty(nnz, dtype=torch.int32, device=dev)
     val = torch.empty(nnz, dtype=vdt, device=dev)
-    _lib.call("sme_synth_random_rows", _cuda.sme_dtype(val), n_rows, n_cols, k, seed, ptr(row_ptr), ptr(col),
-              ptr(val), stream())
+    if _cuda.wide_row_ptr(nnz):  # int64 row_ptr (nnz >= 2^31 - 1): row r starts at r * k
+        row_ptr = torch.arange(n_rows + 1, dtype=torch.int64, device=dev) * k
+        _lib.call("sme_synth_random_rows", _cuda.sme_dtype(val), n_rows, n_cols, k, seed, None, ptr(col),
+                  ptr(val), stream())
+    else:
+        row_ptr = torch.empty(n_rows + 1, dtype=torch.int32, device=dev)
+        _lib.call("sme_synth_random_rows", _cuda.sme_dtype(val), n_rows, n_cols, k, seed, ptr(row_ptr), ptr(col),
+                  ptr(val), stream())
     return CsrMatrix._from_device(n_rows, n_cols, row_ptr, col, val)
 
 
