@@ -225,9 +225,7 @@ def spmv_into(m: CsrMatrix, xd: torch.Tensor, y: torch.Tensor, kernel: str = "ve
         kernel = auto_kernel(m)
         if kernel in ("panel", "seg") and accumulate:
             kernel = "vector" if m.wide else "stream"
-    if m.wide and kernel not in WIDE_KERNELS:
-        raise ValueError(f"kernel {kernel!r} uses int32 row offsets; a CSR with int64 row_ptr "
-                         f"(nnz >= 2^31 - 1) runs one of {WIDE_KERNELS}")
+    _check_wide(m, kernel)
     if kernel == "vector":
         _lib.call_rp("sme_spmv_vector", m.d_row_ptr, dt, lanes or default_lanes(m), m.n_rows, m.n_cols,
                      ptr(m.d_row_ptr), ptr(m.d_col_idx), ptr(m.d_values), ptr(xd), ptr(y), int(accumulate), stream())
@@ -260,6 +258,12 @@ def spmv_into(m: CsrMatrix, xd: torch.Tensor, y: torch.Tensor, kernel: str = "ve
                   ptr(xd), ptr(y), stream())
     else:
         raise ValueError(f"unknown kernel {kernel!r}; expected one of {KERNELS}")
+
+
+def _check_wide(m: CsrMatrix, kernel: str) -> None:
+    if m.wide and kernel not in WIDE_KERNELS:
+        raise ValueError(f"kernel {kernel!r} uses int32 row offsets; a CSR with int64 row_ptr "
+                         f"(nnz >= 2^31 - 1) runs one of {WIDE_KERNELS}")
 
 
 def _check_out(out, m: CsrMatrix, dev) -> None:
@@ -301,6 +305,7 @@ def spmv_csr(m: CsrMatrix, x, kernel: str = "auto", *, out: torch.Tensor | None 
     y = out if out is not None else torch.empty(m.n_rows, dtype=m.dtype, device=dev)
     main = torch.cuda.current_stream(dev)
     kern = auto_kernel(m) if kernel == "auto" else kernel
+    _check_wide(m, kern)
     if kern in ("seg", "panel"):
         from .panels import panels_of
         from .seg import seg_of
@@ -347,6 +352,7 @@ def spmv_csr_pipelined(m: CsrMatrix, xs, ys=None, kernel: str = "auto") -> list:
     if len(ys) != len(xs):
         raise ValueError("need one output per input vector")
     kern = auto_kernel(m) if kernel == "auto" else kernel
+    _check_wide(m, kern)
     lay = None
     if kern == "seg":
         from .seg import seg_of

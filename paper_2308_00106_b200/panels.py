@@ -158,6 +158,8 @@ class PanelCsr:
 
 def panels_of(m: CsrMatrix, n_panels: int | None = None) -> PanelCsr:
     """The cached panel layout of m (built on first use)."""
+    if m.wide:
+        raise ValueError("the CSR column panels use int32 row offsets; a CSR with int64 row_ptr runs 'seg'")
     P = n_panels or m._cache.get("n_panels") or auto_panels(m)
     key = ("panels", P)
     if key not in m._cache:
