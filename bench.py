@@ -40,6 +40,11 @@ CONFIGS = {
     # name: (kind, n, k_or_grid, dtype, description)
     "c4": dict(kind="random_rows", n=50_000_000, k=20, dtype="f64",
                workload="C4: random-structured 50M x 50M, 20 nnz/row (1.0e9 nnz), f64, row+col permuted"),
+    # C4's structure past 2^31 nonzeros: int64 row_ptr, the `_i64` entry points (not a
+    # BASELINE config: the capability check for CSRs larger than int32 offsets)
+    "c4w": dict(kind="random_rows", n=108_000_000, k=20, dtype="f64",
+                workload="C4-wide: random-structured 108M x 108M, 20 nnz/row (2.16e9 nnz > 2^31, int64 row_ptr), "
+                         "f64, row+col permuted"),
     "c2": dict(kind="laplacian", g=2000, dtype="f64",
                workload="C2: 5-point Laplacian 2000^2 (4M rows, 19,992,000 nnz), f64, row+col permuted"),
     "c5": dict(kind="laplacian", g=2828, dtype="f64",
@@ -691,8 +696,10 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
                  statistics.median(e1.elapsed_time(e2) for _, e1, e2 in ev))
         del yb_, ya_
         others = {}
+        from paper_2308_00106_b200.kernels import WIDE_KERNELS
+
         for other in ("panel", "stream", "vector", "merge"):
-            if other != resolved:
+            if other != resolved and (not B.wide or other in WIDE_KERNELS):
                 o_total, _ = timed(B, xp, other, max(3, args.steps // 4), 2)
                 others[other] = round(2 * nnz / (o_total / max(3, args.steps // 4) * 1e-3) / 1e9, 3)
         ot_total = None
