@@ -365,6 +365,9 @@ int sme_seg_set_scatter_groups(int on);
 /* Test hook: 1 (default) places the entries of groups without empty rows entry-parallel
  * (row from a mask of the row starts in each 32-entry window); 0 = the per-row walk. */
 int sme_seg_set_fill_ballot(int on);
+/* Test hook: 1 (default) the grouped fill stores every entry straight to its slot; 0 =
+ * through the shared-memory image of the group's panel ranges (same layout bits). */
+int sme_seg_set_fill_direct(int on);
 int sme_spmv_seg_warps(int32_t* n_warps);
 /* Kernel variant (process-wide): 0 = the SpMV (default; accumulating passes add
  * with RED.ADD at L2), 3 = bound probe (the chunk stream and gathers without the

@@ -55,6 +55,7 @@ namespace sme {
 constexpr int SEG_NT = 256;
 static bool s_seg_scatter_groups = true;  // sme_seg_set_scatter_groups
 static bool s_seg_fill_ballot = true;     // sme_seg_set_fill_ballot
+static int s_seg_fill_direct = 1;        // sme_seg_set_fill_direct
 constexpr int SEG_CH = 128;
 constexpr int SEG_DBITS = 8;
 constexpr uint32_t SEG_DMASK = (1u << SEG_DBITS) - 1;
@@ -219,18 +220,23 @@ constexpr int SG_WARPS = 4;
 
 constexpr int SG_HMAX = SG_CAP / SEG_CH + 2;  // chunks a group's range of one panel can touch
 
-// per warp: the output image, the (panel, row) table, row starts, per-panel ranges and
-// the chunk headers of those ranges
-inline size_t sg_warp_bytes(int n_panels, size_t val_bytes) {
-  return align_up((size_t)SG_CAP * (4 + val_bytes) + (size_t)n_panels * 32 * 16 + 40 * 4 + 4 * 32 * 4 + 32 * 4 +
-                      32 * 8 + 32 * 16 + (size_t)n_panels * SG_HMAX * 4,
+// per warp: the output image (not with DIRECT), the (panel, row) table, row starts,
+// per-panel ranges and the chunk headers of those ranges
+inline size_t sg_warp_bytes(int n_panels, size_t val_bytes, bool direct) {
+  return align_up((direct ? 0 : (size_t)SG_CAP * (4 + val_bytes)) + (size_t)n_panels * 32 * 16 + 40 * 4 +
+                      4 * 32 * 4 + 32 * 4 + 32 * 8 + 32 * 16 + (size_t)n_panels * SG_HMAX * 4,
                   16);
 }
 
 // Row starts of a group are kept relative to its first entry (int32 even when row_ptr is
 // int64): the image paths address col / val through the group's base pointers.
-template <typename T, typename IP>
-__global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
+// DIRECT: no shared-memory image — every entry and explicit zero is stored straight to
+// its slot (consecutive slots of one (row, panel) piece are consecutive lanes' stores;
+// the partial sectors of a group's ranges merge in L2).  The image (18 KB per warp at
+// C4) held the kernel to 12 warps per SM and the col loads' latency dominated (ncu:
+// 18.75 % theoretical occupancy, 8.9 cycles per issued instruction).
+template <typename T, typename IP, bool DIRECT, int MINB = 1>
+__global__ void __launch_bounds__(SG_WARPS * 32, MINB) k_seg_scatter_groups(
     int64_t n_rows, const IP* __restrict__ row_ptr, const int32_t* __restrict__ col_all, const T* __restrict__ val_all,
     int32_t n_panels, const int32_t* __restrict__ bounds, const int32_t* __restrict__ counts,
     const int32_t* __restrict__ pos, const int64_t* __restrict__ offsets, uint32_t* __restrict__ out_pk,
@@ -241,9 +247,9 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
   const int P = n_panels;
   unsigned char* wb = sg_smem + (size_t)wib * warp_bytes;
   T* s_val = reinterpret_cast<T*>(wb);
-  uint32_t* s_pk = reinterpret_cast<uint32_t*>(wb + (size_t)SG_CAP * sizeof(T));
+  uint32_t* s_pk = reinterpret_cast<uint32_t*>(wb + (DIRECT ? 0 : (size_t)SG_CAP * sizeof(T)));
   // per (panel, row): {first entry, count, slot in the panel, slot - first}
-  int4* s_tab = reinterpret_cast<int4*>(s_pk + SG_CAP);          // [P][32]
+  int4* s_tab = reinterpret_cast<int4*>(DIRECT ? wb : reinterpret_cast<unsigned char*>(s_pk + SG_CAP));  // [P][32]
   int32_t* s_rp = reinterpret_cast<int32_t*>(s_tab + P * 32);    // [33] row starts
   int32_t* s_gs = s_rp + 40;                                     // [32] group range start per panel
   int32_t* s_sb = s_gs + 32;                                     // [32] staging base per panel
@@ -373,9 +379,15 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
         if (pnext > ppos) {
           const int32_t sidx = s_sb[p] + (ppos - s_gs[p]);
           const int64_t dst = c_off[p] + ppos;
-          s_pk[sidx] = (SEG_MARK << SEG_CSHIFT) | SEG_END |
-                       (uint32_t)(r - s_hdr[p * SG_HMAX + (int)(dst / SEG_CH - s_cb[p])]);
-          s_val[sidx] = T(0);
+          const uint32_t w = (SEG_MARK << SEG_CSHIFT) | SEG_END |
+                             (uint32_t)(r - s_hdr[p * SG_HMAX + (int)(dst / SEG_CH - s_cb[p])]);
+          if (DIRECT) {
+            out_pk[dst] = w;
+            out_val[dst] = T(0);
+          } else {
+            s_pk[sidx] = w;
+            s_val[sidx] = T(0);
+          }
         }
       }
     }
@@ -430,10 +442,17 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
             const int4 tb = s_tab[p * 32 + rr];
             const int4 pp = s_pp[p];
             const int32_t dip = tb.w + k;  // slot within the panel
-            s_pk[pp.x + dip] = (((uint32_t)cc - (uint32_t)pp.z) << SEG_CSHIFT) |
+            const uint32_t w = (((uint32_t)cc - (uint32_t)pp.z) << SEG_CSHIFT) |
                                (k - tb.x == tb.y - 1 ? SEG_END : 0u) |
                                (uint32_t)((int32_t)(r0 + rr) - s_hdr[p * SG_HMAX + ((pp.y + dip) >> 7)]);
-            s_val[pp.x + dip] = v[u];
+            if (DIRECT) {
+              const int64_t dst = c_off[p] + dip;
+              out_pk[dst] = w;
+              out_val[dst] = v[u];
+            } else {
+              s_pk[pp.x + dip] = w;
+              s_val[pp.x + dip] = v[u];
+            }
           }
         }
       }
@@ -459,10 +478,15 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
             clo = (uint32_t)c_lo[p];
           }
           const int32_t dip = pq + (k - f);  // slot within the panel
-          const int32_t sidx = sb + dip;
-          s_pk[sidx] = (((uint32_t)c - clo) << SEG_CSHIFT) | (k - f == pc - 1 ? SEG_END : 0u) |
-                       (uint32_t)(r_rel - hdr[(po + dip) / SEG_CH]);
-          s_val[sidx] = v;
+          const uint32_t w = (((uint32_t)c - clo) << SEG_CSHIFT) | (k - f == pc - 1 ? SEG_END : 0u) |
+                             (uint32_t)(r_rel - hdr[(po + dip) / SEG_CH]);
+          if (DIRECT) {
+            out_pk[po + dip] = w;
+            out_val[po + dip] = v;
+          } else {
+            s_pk[sb + dip] = w;
+            s_val[sb + dip] = v;
+          }
         }
       }
     } else {
@@ -481,13 +505,20 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
         const int t = p * 32 + lo;
         const int32_t f = s_tab[t].x, pc = s_tab[t].y;
         const int32_t dip = s_tab[t].z + (k - f);  // slot within the panel
-        const int32_t sidx = s_sb[p] - s_gs[p] + dip;
-        s_pk[sidx] = (((uint32_t)c - (uint32_t)c_lo[p]) << SEG_CSHIFT) | (k - f == pc - 1 ? SEG_END : 0u) |
-                     (uint32_t)((int32_t)(r0 + lo) - hdr[(c_off[p] + dip) / SEG_CH]);
-        s_val[sidx] = v;
+        const uint32_t w = (((uint32_t)c - (uint32_t)c_lo[p]) << SEG_CSHIFT) | (k - f == pc - 1 ? SEG_END : 0u) |
+                           (uint32_t)((int32_t)(r0 + lo) - hdr[(c_off[p] + dip) / SEG_CH]);
+        if (DIRECT) {
+          out_pk[c_off[p] + dip] = w;
+          out_val[c_off[p] + dip] = v;
+        } else {
+          const int32_t sidx = s_sb[p] - s_gs[p] + dip;
+          s_pk[sidx] = w;
+          s_val[sidx] = v;
+        }
       }
     }
     __syncwarp();
+    if (DIRECT) continue;
     // out, panel by panel, consecutive lanes on consecutive slots
     for (int p = 0; p < P; ++p) {
       const int32_t n_p = s_len[p], sb = s_sb[p];
@@ -1048,7 +1079,7 @@ static int seg_fill_impl(int dtype, int64_t n_rows, const IP* row_ptr, const int
   }
   if (n_panels <= 32 && s_seg_scatter_groups) {
     auto launch = [&](auto kern, size_t vb, auto* v, auto* ov) {
-      const size_t wbytes = sg_warp_bytes(n_panels, vb), smem = wbytes * SG_WARPS;
+      const size_t wbytes = sg_warp_bytes(n_panels, vb, s_seg_fill_direct), smem = wbytes * SG_WARPS;
       SME_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       const int64_t groups = (n_rows + 31) / 32;
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((groups + SG_WARPS - 1) / SG_WARPS,
@@ -1057,10 +1088,16 @@ static int seg_fill_impl(int dtype, int64_t n_rows, const IP* row_ptr, const int
                                              hdr, wbytes, (int)s_seg_fill_ballot);
       return SME_OK;
     };
-    if (dtype == SME_F64)
-      launch(k_seg_scatter_groups<double, IP>, 8, (const double*)val, (double*)out_val);
+    if (dtype == SME_F64 && s_seg_fill_direct == 2)  // experiment: register cap for 12 CTAs per SM
+      launch(k_seg_scatter_groups<double, IP, true, 12>, 8, (const double*)val, (double*)out_val);
+    else if (dtype == SME_F64 && s_seg_fill_direct == 3)
+      launch(k_seg_scatter_groups<double, IP, true, 9>, 8, (const double*)val, (double*)out_val);
+    else if (dtype == SME_F64)
+      s_seg_fill_direct ? launch(k_seg_scatter_groups<double, IP, true>, 8, (const double*)val, (double*)out_val)
+                        : launch(k_seg_scatter_groups<double, IP, false>, 8, (const double*)val, (double*)out_val);
     else
-      launch(k_seg_scatter_groups<float, IP>, 4, (const float*)val, (float*)out_val);
+      s_seg_fill_direct ? launch(k_seg_scatter_groups<float, IP, true>, 4, (const float*)val, (float*)out_val)
+                        : launch(k_seg_scatter_groups<float, IP, false>, 4, (const float*)val, (float*)out_val);
     SME_CHECK_LAUNCH("k_seg_scatter_groups");
     return SME_OK;
   }
@@ -1094,6 +1131,13 @@ SME_API int sme_seg_fill_i64(int dtype, int64_t n_rows, const int64_t* row_ptr, 
 
 // Groups of non-empty rows: entry-parallel placement (1, default) or the lane-per-row
 // walk / searched entry-parallel paths of earlier versions (0).  For A/B tests.
+// 1 (default): the fill stores entries straight to their slots; 0: through the
+// shared-memory image of each group's panel ranges (A/B and tests of that path)
+SME_API int sme_seg_set_fill_direct(int on) {
+  s_seg_fill_direct = on;
+  return SME_OK;
+}
+
 SME_API int sme_seg_set_fill_ballot(int on) {
   s_seg_fill_ballot = on != 0;
   return SME_OK;

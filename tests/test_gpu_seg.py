@@ -391,14 +391,17 @@ def test_ballot_fill_equals_per_row_fill(dev, rng, n_panels, shape):
     ptr, col, val = csr_from_lens(rng, lens, n)
     m = P.CsrMatrix(n, n, ptr, col, val)
     layouts = []
-    for groups, ballot in ((1, 1), (1, 0), (0, 1)):
+    # (grouped, entry-parallel, direct stores): the default, the image variants, the per-row fill
+    for groups, ballot, direct in ((1, 1, 1), (1, 0, 1), (1, 1, 0), (1, 0, 0), (0, 1, 1)):
         _lib.call("sme_seg_set_scatter_groups", groups)
         _lib.call("sme_seg_set_fill_ballot", ballot)
+        _lib.call("sme_seg_set_fill_direct", direct)
         try:
             layouts.append(SegLayout(m, n_panels))
         finally:
             _lib.call("sme_seg_set_scatter_groups", 1)
             _lib.call("sme_seg_set_fill_ballot", 1)
+            _lib.call("sme_seg_set_fill_direct", 1)
     a = layouts[0]
     for b in layouts[1:]:
         assert torch.equal(a.pk, b.pk) and torch.equal(a.val, b.val) and torch.equal(a.hdr, b.hdr)
