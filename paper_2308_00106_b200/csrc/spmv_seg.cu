@@ -55,7 +55,7 @@ namespace sme {
 constexpr int SEG_NT = 256;
 static bool s_seg_scatter_groups = true;  // sme_seg_set_scatter_groups
 static bool s_seg_fill_ballot = true;     // sme_seg_set_fill_ballot
-static int s_seg_fill_direct = 1;        // sme_seg_set_fill_direct
+static bool s_seg_fill_direct = true;    // sme_seg_set_fill_direct
 constexpr int SEG_CH = 128;
 constexpr int SEG_DBITS = 8;
 constexpr uint32_t SEG_DMASK = (1u << SEG_DBITS) - 1;
@@ -234,9 +234,11 @@ inline size_t sg_warp_bytes(int n_panels, size_t val_bytes, bool direct) {
 // its slot (consecutive slots of one (row, panel) piece are consecutive lanes' stores;
 // the partial sectors of a group's ranges merge in L2).  The image (18 KB per warp at
 // C4) held the kernel to 12 warps per SM and the col loads' latency dominated (ncu:
-// 18.75 % theoretical occupancy, 8.9 cycles per issued instruction).
-template <typename T, typename IP, bool DIRECT, int MINB = 1>
-__global__ void __launch_bounds__(SG_WARPS * 32, MINB) k_seg_scatter_groups(
+// 18.75 % theoretical occupancy, 8.9 cycles per issued instruction).  Direct: C4 fill
+// 14.5 -> 11.3 ms, whole layout build 19.8 -> 16.2 ms; C3 7.0 -> 5.0 ms; register caps for
+// 9 / 12 CTAs per SM measured slower (17.4 / 18.0 ms builds).
+template <typename T, typename IP, bool DIRECT>
+__global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
     int64_t n_rows, const IP* __restrict__ row_ptr, const int32_t* __restrict__ col_all, const T* __restrict__ val_all,
     int32_t n_panels, const int32_t* __restrict__ bounds, const int32_t* __restrict__ counts,
     const int32_t* __restrict__ pos, const int64_t* __restrict__ offsets, uint32_t* __restrict__ out_pk,
@@ -1088,11 +1090,7 @@ static int seg_fill_impl(int dtype, int64_t n_rows, const IP* row_ptr, const int
                                              hdr, wbytes, (int)s_seg_fill_ballot);
       return SME_OK;
     };
-    if (dtype == SME_F64 && s_seg_fill_direct == 2)  // experiment: register cap for 12 CTAs per SM
-      launch(k_seg_scatter_groups<double, IP, true, 12>, 8, (const double*)val, (double*)out_val);
-    else if (dtype == SME_F64 && s_seg_fill_direct == 3)
-      launch(k_seg_scatter_groups<double, IP, true, 9>, 8, (const double*)val, (double*)out_val);
-    else if (dtype == SME_F64)
+    if (dtype == SME_F64)
       s_seg_fill_direct ? launch(k_seg_scatter_groups<double, IP, true>, 8, (const double*)val, (double*)out_val)
                         : launch(k_seg_scatter_groups<double, IP, false>, 8, (const double*)val, (double*)out_val);
     else
@@ -1134,7 +1132,7 @@ SME_API int sme_seg_fill_i64(int dtype, int64_t n_rows, const int64_t* row_ptr, 
 // 1 (default): the fill stores entries straight to their slots; 0: through the
 // shared-memory image of each group's panel ranges (A/B and tests of that path)
 SME_API int sme_seg_set_fill_direct(int on) {
-  s_seg_fill_direct = on;
+  s_seg_fill_direct = on != 0;
   return SME_OK;
 }
 
