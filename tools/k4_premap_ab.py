@@ -16,8 +16,12 @@ n = A.n_rows
 p_r, p_c = P.random_permutation(n, 1), P.random_permutation(n, 2)
 p_r.d_inverse, p_c.d_inverse  # noqa: B018
 ref = None
-variants = [(False, 0, False, False)] + [(True, mb, pers, fuse) for mb in (40, 48, 64)
-                                          for pers in (False,) for fuse in (False, True)]
+VARIANTS = sys.argv[2] if len(sys.argv) > 2 else "slices"
+if VARIANTS == "persist":  # the persisting-L2 window over each slice, 3-5 slices
+    variants = [(True, mb, pers, False) for mb in (40, 48, 64) for pers in (False, True)]
+else:
+    variants = [(False, 0, False, False)] + [(True, mb, pers, fuse) for mb in (40, 48, 64)
+                                              for pers in (False,) for fuse in (False, True)]
 for rep in range(2):
     for on, mb, pers, fuse in variants:
         PM.PREMAP, PM.PREMAP_PERSIST, PM.PREMAP_FUSE_LAST = on, pers, fuse
