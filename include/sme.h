@@ -529,6 +529,11 @@ int sme_rowshard_remap_cols(int64_t nnz, int64_t n_cols, int32_t parts, int64_t 
  * for any launch shape.  n_bytes % 4 == 0, d_data 4-byte aligned. */
 int sme_hash64(const void* d_data, int64_t n_bytes, uint64_t seed, uint64_t* d_out, sme_stream_t stream);
 
+/* Load every kernel module of libsme.so now (CUDA lazy loading would load each on the
+ * first launch of one of its kernels, ~10-20 ms apiece, inside the first permuted-matrix
+ * setup of a process).  Call once after the context exists; idempotent. */
+int sme_preload(void);
+
 /* ------------------------------------------------------------------------ */
 /* int64 row_ptr ("wide" CSR): matrices with nnz >= 2^31 - 1                 */
 /* ------------------------------------------------------------------------ */

@@ -34,6 +34,9 @@ def nvtx(name: str):
     return wrap
 
 
+_PRELOADED: set[int] = set()
+
+
 def require_cuda() -> torch.device:
     if not torch.cuda.is_available():
         raise RuntimeError(
@@ -41,7 +44,12 @@ def require_cuda() -> torch.device:
             "(no CPU fallback)"
         )
     _lib.load()
-    return torch.device("cuda", torch.cuda.current_device())
+    dev = torch.cuda.current_device()
+    if dev not in _PRELOADED:  # once per device: load libsme's kernel modules up front
+        _PRELOADED.add(dev)
+        torch.zeros(1, device=f"cuda:{dev}")  # the context exists
+        _lib.call("sme_preload")
+    return torch.device("cuda", dev)
 
 
 def stream() -> int:

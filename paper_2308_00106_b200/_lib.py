@@ -32,6 +32,7 @@ SIGNATURES: dict[str, list] = {
     "sme_last_error": [],
     "sme_version": [],
     "sme_device_sm_count": [],
+    "sme_preload": [],
     "sme_device_info": [p],
     "sme_l2_set_persisting": [sz],
     "sme_l2_window": [p, sz, C.c_float, p],

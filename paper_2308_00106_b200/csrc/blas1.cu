@@ -161,3 +161,12 @@ SME_API int sme_axpby(int dtype, int64_t n, double a, const void* x, double b, v
   SME_CHECK_LAUNCH("k_axpby");
   return SME_OK;
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_blas1() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_dot_finish) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

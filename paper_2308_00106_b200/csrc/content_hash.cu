@@ -34,3 +34,12 @@ SME_API int sme_hash64(const void* d_data, int64_t n_bytes, uint64_t seed, uint6
   SME_CHECK_LAUNCH("k_hash_words");
   return SME_OK;
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_content_hash() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_hash_words) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

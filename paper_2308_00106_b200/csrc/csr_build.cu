@@ -1107,3 +1107,12 @@ SME_API int sme_sort_rows_set_key32(int enable) {
   g_sort_key32 = enable;
   return SME_OK;
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_csr_build() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_coo_count) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

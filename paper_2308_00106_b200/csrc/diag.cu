@@ -48,3 +48,12 @@ SME_API int sme_diag_gather(const double* x, int64_t n, int32_t blocks, int32_t 
   SME_CHECK_LAUNCH("k_diag_gather");
   return SME_OK;
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_diag() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_diag_gather<8>) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

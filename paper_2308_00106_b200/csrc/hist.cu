@@ -592,3 +592,12 @@ SME_API int sme_entropy(int64_t n_bins, const int64_t* counts, double base, doub
   SME_CHECK_LAUNCH("k_entropy");
   return SME_OK;
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_hist() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_hist2d_coo) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

@@ -110,3 +110,12 @@ SME_API int sme_panel_scatter(int dtype, int64_t n_rows, const int32_t* row_ptr,
   SME_CHECK_LAUNCH("k_panel_scatter");
   return SME_OK;
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_panel() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_panel_count) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

@@ -191,3 +191,12 @@ SME_API int sme_maxabs_diff(int dtype, int64_t n, const void* got, const void* e
   SME_CHECK_LAUNCH("k_maxabs_diff");
   return SME_OK;
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_perm() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_inverse_scatter) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

@@ -122,3 +122,12 @@ SME_API int sme_fy_apply(int64_t n, const uint32_t* d_j, int32_t* d_perm, void* 
   SME_CHECK_LAUNCH("k_fy_final");
   return SME_OK;
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_shuffle() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_fy_count) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

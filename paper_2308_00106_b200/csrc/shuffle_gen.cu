@@ -509,3 +509,12 @@ SME_API int sme_pcg64_swap_partners_gpu(uint64_t* st, int64_t n, int32_t* d_j, v
   }
   return SME_OK;
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_shuffle_gen() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_gg_draw_classify) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

@@ -102,3 +102,46 @@ SME_API int sme_l2_prefetch(const void* d_ptr, size_t bytes, sme_stream_t stream
   SME_CHECK_LAUNCH("k_l2_prefetch");
   return SME_OK;
 }
+
+namespace sme {
+int preload_blas1();
+int preload_content_hash();
+int preload_csr_build();
+int preload_diag();
+int preload_hist();
+int preload_panel();
+int preload_perm();
+int preload_shuffle();
+int preload_shuffle_gen();
+int preload_spmv();
+int preload_spmv_seg();
+int preload_spmv_stream();
+int preload_synth();
+int preload_synth_rmat();
+}  // namespace sme
+
+// Loads every kernel module of libsme.so now instead of on first launch (CUDA lazy
+// loading): the first permuted-matrix setup of a process otherwise pays ~100 ms of
+// module loading inside its K4, layout and permutation calls.  Idempotent.
+SME_API int sme_preload(void) {
+  int rc = 0;
+  rc |= sme::preload_blas1();
+  rc |= sme::preload_content_hash();
+  rc |= sme::preload_csr_build();
+  rc |= sme::preload_diag();
+  rc |= sme::preload_hist();
+  rc |= sme::preload_panel();
+  rc |= sme::preload_perm();
+  rc |= sme::preload_shuffle();
+  rc |= sme::preload_shuffle_gen();
+  rc |= sme::preload_spmv();
+  rc |= sme::preload_spmv_seg();
+  rc |= sme::preload_spmv_stream();
+  rc |= sme::preload_synth();
+  rc |= sme::preload_synth_rmat();
+  if (rc) {
+    sme::set_error("sme_preload: %s", cudaGetErrorString(cudaGetLastError()));
+    return SME_ECUDA;
+  }
+  return SME_OK;
+}

@@ -840,3 +840,12 @@ SME_API int sme_rows_epi(int64_t n_rows, const double* y, double* out, const int
   SME_CHECK_LAUNCH("k_rows_epi");
   return SME_OK;
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_spmv() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_spmv_plan) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

@@ -1301,3 +1301,12 @@ SME_API int sme_spmv_seg_split(int dtype, int32_t n_warps, const uint32_t* pk, c
   return launch_seg<float>(n_warps, pk, (const float*)val, hdr, plan, (const float*)xs, (float*)y, accumulate, s,
                            &e);
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_spmv_seg() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_seg_hdr) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

@@ -421,3 +421,12 @@ SME_API int sme_spmv_stream(int dtype, int64_t n_rows, int64_t n_cols, int64_t n
   return launch_stream<float>(n_rows, nnz, row_ptr, col, (const float*)val, (const float*)x, (float*)y, plan, n_warps,
                               accumulate, align_off, vec, s);
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_spmv_stream() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_stream_plan) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

@@ -147,3 +147,12 @@ SME_API int sme_synth_random_rows_sel(int dtype, int64_t n_sel, const int32_t* r
   SME_CHECK_LAUNCH("k_random_rows");
   return SME_OK;
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_synth() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_laplacian<double>) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme

@@ -73,3 +73,12 @@ SME_API int sme_synth_row_values(int dtype, int64_t n_rows, const int32_t* row_p
   SME_CHECK_LAUNCH("k_row_values");
   return SME_OK;
 }
+
+namespace sme {
+// Lazy module loading (CUDA 12 default) loads this file's module on the first launch of
+// any of its kernels, ~10-20 ms each; sme_preload() does it ahead of time.
+int preload_synth_rmat() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)k_rmat_edges) == cudaSuccess ? 0 : -1;
+}
+}  // namespace sme
