@@ -48,6 +48,20 @@ class SegLayout:
 
     def __init__(self, m: CsrMatrix, n_panels: int, n_warps: int | None = None, full_last: bool = False,
                  split_rows: bool | None = None):
+        P, n = self._geometry(m, n_panels, full_last)
+        s = stream()
+        ws = _cuda.workspace(_lib.query_size("sme_seg_workspace_size", n, P))
+        pos = torch.empty(P * (n + 1), dtype=torch.int32, device=self.bounds.device)
+        _lib.call_rp("sme_seg_positions", m.d_row_ptr, n, ptr(m.d_row_ptr), ptr(m.d_col_idx), P, ptr(self.bounds),
+                     int(full_last), ptr(pos), ptr(ws), ws.numel(), s)
+        h_offs, d_offs = self._allocate(pos)
+        _lib.call_rp("sme_seg_fill", m.d_row_ptr, _cuda.sme_dtype(m.d_values), n, ptr(m.d_row_ptr),
+                     ptr(m.d_col_idx), ptr(m.d_values), P, ptr(self.bounds), ptr(pos), ptr(d_offs),
+                     ctypes.cast(h_offs, ctypes.c_void_p), ptr(self.pk), ptr(self.val), ptr(self.hdr), ptr(ws), s)
+        self._finish(m, pos, n_warps, split_rows)
+
+    # -- construction pieces (shared with the K4-fused build, SegLayout.with_permute) ----
+    def _geometry(self, m: CsrMatrix, n_panels: int, full_last: bool) -> tuple[int, int]:
         P, n = int(n_panels), m.n_rows
         if P < 1 or P > max(1, m.n_cols):
             raise ValueError("panel count must lie in [1, n_cols]")
@@ -55,17 +69,16 @@ class SegLayout:
         if np.diff(bounds).max(initial=0) > MAX_PANEL_COLS:
             raise ValueError(f"panels of {int(np.diff(bounds).max())} columns exceed the 23-bit column field; "
                              f"use at least {math.ceil(m.n_cols / MAX_PANEL_COLS)} panels")
-        dev = m.d_row_ptr.device
-        s = stream()
         self.n_rows, self.n_cols, self.n_panels, self.dtype = n, m.n_cols, P, m.dtype
         self.bounds_host = bounds
-        self.bounds = torch.from_numpy(bounds).to(dev)
-        ws = _cuda.workspace(_lib.query_size("sme_seg_workspace_size", n, P))
-        pos = torch.empty(P * (n + 1), dtype=torch.int32, device=dev)
+        self.bounds = torch.from_numpy(bounds).to(m.d_col_idx.device)
         self.full_last = bool(full_last)
-        _lib.call_rp("sme_seg_positions", m.d_row_ptr, n, ptr(m.d_row_ptr), ptr(m.d_col_idx), P, ptr(self.bounds),
-                     int(full_last), ptr(pos), ptr(ws), ws.numel(), s)
-        ent = pos.view(P, n + 1)[:, -1].to(torch.int64).cpu().numpy()
+        return P, n
+
+    def _allocate(self, pos: torch.Tensor):
+        """Panel sizes from the positions (one host sync), pk / val / hdr, tail padding."""
+        P, n, dev = self.n_panels, self.n_rows, pos.device
+        ent = pos.view(P, n + 1)[:, -1].cpu().numpy().astype(np.int64)
         if (ent < 0).any():  # int32 slot positions wrapped: a panel of >= 2^31 slots
             raise ValueError(f"a column panel holds >= 2^31 entries; use more than {P} panels")
         offs = np.zeros(P + 1, dtype=np.int64)
@@ -77,7 +90,7 @@ class SegLayout:
         # the fill writes every entry slot and every chunk header; only each panel's tail
         # padding (< CHUNK slots) is set here, as explicit zeros
         self.pk = torch.empty(total, dtype=torch.int32, device=dev)
-        self.val = torch.empty(total, dtype=m.dtype, device=dev)
+        self.val = torch.empty(total, dtype=self.dtype, device=dev)
         self.hdr = torch.zeros(total // CHUNK, dtype=torch.int32, device=dev) if total == CHUNK else \
             torch.empty(total // CHUNK, dtype=torch.int32, device=dev)
         for p in range(P):
@@ -90,9 +103,11 @@ class SegLayout:
             self.val[int(offs[-1]):] = 0
         h_offs = (ctypes.c_int64 * P)(*[int(o) for o in offs[:P]])
         d_offs = torch.from_numpy(offs[:P].copy()).to(dev)
-        _lib.call_rp("sme_seg_fill", m.d_row_ptr, _cuda.sme_dtype(m.d_values), n, ptr(m.d_row_ptr),
-                     ptr(m.d_col_idx), ptr(m.d_values), P, ptr(self.bounds), ptr(pos), ptr(d_offs),
-                     ctypes.cast(h_offs, ctypes.c_void_p), ptr(self.pk), ptr(self.val), ptr(self.hdr), ptr(ws), s)
+        return h_offs, d_offs
+
+    def _finish(self, m: CsrMatrix, pos: torch.Tensor, n_warps: int | None, split_rows: bool | None) -> None:
+        P, n, dev, s = self.n_panels, self.n_rows, pos.device, stream()
+        ent = self.entries
         self.n_warps = int(n_warps or seg_warps())
         self.plans = torch.empty(P * (self.n_warps + 1), dtype=torch.int32, device=dev)
         # split-row plans when one row would dominate a warp's share (power-law rows): ranges
@@ -122,6 +137,42 @@ class SegLayout:
         self.persist = False
         self.hit_ratio = 1.0  # access-policy window hit ratio of the pinned x slice
         self.warm = False  # L2 prefetch sweep of each pass's x slice (experiment knob)
+
+    @classmethod
+    def with_permute(cls, src: CsrMatrix, n_panels: int, inv_r, fwd_r, src_col: torch.Tensor, cmap,
+                     row_ptr: torch.Tensor, col_out: torch.Tensor, val_out: torch.Tensor, lists_ws: torch.Tensor,
+                     flags) -> "SegLayout | None":
+        """K4 with this layout of its result built by the same row sort (sme_permute_csr_seg;
+        rows of <= 32 entries).  Writes the permuted CSR into col_out / val_out (row_ptr is
+        already computed) and returns the layout of that CSR — bit-identical to
+        SegLayout(permuted, n_panels) — or None when a row turned out longer than 32 (the
+        caller then runs the plain K4)."""
+        lay = cls.__new__(cls)
+        n = src.n_rows
+        shape = CsrMatrix._from_device(n, src.n_cols, row_ptr, col_out, val_out)  # geometry only
+        P, n = lay._geometry(shape, n_panels, False)
+        s = stream()
+        dev = row_ptr.device
+        counts = torch.empty(P * n, dtype=torch.int32, device=dev)
+        ws = _cuda.workspace(max(_lib.query_size("sme_seg_workspace_size", n, P),
+                                 _lib.query_size("sme_row_ptr_workspace_size", n)))
+        _lib.call_rp("sme_seg_count_src", src.d_row_ptr, n, ptr(src.d_row_ptr), ptr(src_col), ptr(cmap), ptr(fwd_r),
+                     P, ptr(lay.bounds), ptr(counts), ptr(ws), ws.numel(), flags.flag_ptr, s)
+        bits, _ = flags.read()
+        if bits & _lib.FLAG_RANGE:
+            return None
+        pos = torch.empty(P * (n + 1), dtype=torch.int32, device=dev)
+        _lib.call("sme_seg_positions_counts", n, P, 0, ptr(counts), ptr(pos), ptr(ws), ws.numel(), s)
+        h_offs, d_offs = lay._allocate(pos)
+        _lib.call("sme_seg_zeros_hdr", _cuda.sme_dtype(val_out), n, P, ptr(counts), ptr(pos),
+                  ctypes.cast(h_offs, ctypes.c_void_p), ptr(lay.pk), ptr(lay.val), ptr(lay.hdr), s)
+        del counts
+        _lib.call_rp("sme_permute_csr_seg", row_ptr, _cuda.sme_dtype(src.d_values), n, src.n_cols, src.nnz,
+                     ptr(src.d_row_ptr), ptr(src_col), ptr(src.d_values), ptr(inv_r), ptr(cmap), ptr(row_ptr),
+                     ptr(col_out), ptr(val_out), ptr(lists_ws), lists_ws.numel(), flags.flag_ptr, flags.dup_ptr, P,
+                     ptr(lay.bounds), ptr(pos), ptr(d_offs), ptr(lay.hdr), ptr(lay.pk), ptr(lay.val), s)
+        lay._finish(shape, pos, None, False)
+        return lay
 
     # -- passes --------------------------------------------------------------
     def _pass(self, p: int, xd: torch.Tensor, y: torch.Tensor) -> None:
@@ -262,11 +313,16 @@ def seg_of(m: CsrMatrix, n_panels: int | None = None, full_last: bool = False,
     P = n_panels or m._cache.get("seg_panels") or auto_seg_panels(m)
     key = ("seg", P, bool(full_last)) if split_rows is None else ("seg", P, bool(full_last), bool(split_rows))
     if key not in m._cache:
-        lay = SegLayout(m, P, full_last=full_last, split_rows=split_rows)
-        from .panels import device_info
-
-        slice_bytes = int(max(np.diff(lay.bounds_host))) * m.d_values.element_size()
-        if P > 1 and slice_bytes <= device_info()["max_persisting_l2"]:
-            lay.enable_persistence(True)
-        m._cache[key] = lay
+        install(m, key, SegLayout(m, P, full_last=full_last, split_rows=split_rows))
     return m._cache[key]
+
+
+def install(m: CsrMatrix, key, lay: SegLayout) -> None:
+    """Cache `lay` as m's layout `key` (pinning each pass's x slice in L2 when it fits
+    the persisting carve-out)."""
+    from .panels import device_info
+
+    slice_bytes = int(max(np.diff(lay.bounds_host))) * m.d_values.element_size()
+    if lay.n_panels > 1 and slice_bytes <= device_info()["max_persisting_l2"]:
+        lay.enable_persistence(True)
+    m._cache[key] = lay
