@@ -359,32 +359,6 @@ int sme_seg_fill(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const int3
                  const void* d_val, int32_t n_panels, const int32_t* d_bounds, const int32_t* d_pos,
                  const int64_t* d_offsets, const int64_t* h_offsets, uint32_t* d_pk, void* d_out_val,
                  int32_t* d_hdr, const void* d_ws, sme_stream_t stream);
-/* The seg layout of P_r A P_c built together with it (K4 fused, rows of <= 32 entries,
- * n_panels <= 32, n_cols <= 2^27), with no second pass over the permuted CSR:
- *  1. sme_seg_count_src: the per-panel row counts of the permuted matrix from the SOURCE
- *     rows (new column = col_map[col] or the pre-mapped col; new row = d_row_map[r], the
- *     forward p_r) -> d_counts[p * n_rows + r']; ws: sme_seg_workspace_size bytes; a row
- *     longer than 32 sets SME_FLAG_RANGE in *d_flag;
- *  2. sme_seg_positions_counts: the per-panel slot positions from those counts (the scans
- *     of sme_seg_positions; ws: sme_row_ptr_workspace_size);
- *  3. sme_seg_zeros_hdr: chunk headers and explicit zeros (the caller pre-fills each
- *     panel's tail padding with pk 0xFFFFFFFF, val 0, as for sme_seg_fill);
- *  4. sme_permute_csr_seg: sme_permute_csr (after sme_permute_csr_row_ptr) whose row sort
- *     also stores every entry in its panel slot.  ws: sme_permute_csr_workspace_size(n, nnz, 0).
- * The layout is bit-identical to sme_seg_positions + sme_seg_fill on the permuted CSR. */
-int sme_seg_count_src(int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_col, const int32_t* d_col_map,
-                      const int32_t* d_row_map, int32_t n_panels, const int32_t* d_bounds, int32_t* d_counts,
-                      void* d_ws, size_t ws_bytes, int32_t* d_flag, sme_stream_t stream);
-int sme_seg_positions_counts(int64_t n_rows, int32_t n_panels, int full_last, const int32_t* d_counts,
-                             int32_t* d_pos, void* d_ws, size_t ws_bytes, sme_stream_t stream);
-int sme_seg_zeros_hdr(int dtype, int64_t n_rows, int32_t n_panels, const int32_t* d_counts, const int32_t* d_pos,
-                      const int64_t* h_offsets, uint32_t* d_pk, void* d_val, int32_t* d_hdr, sme_stream_t stream);
-int sme_permute_csr_seg(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* d_row_ptr,
-                        const int32_t* d_col, const void* d_val, const int32_t* d_inv_row, const int32_t* d_col_map,
-                        const int32_t* d_row_ptr_out, int32_t* d_col_out, void* d_val_out, void* d_ws,
-                        size_t ws_bytes, int32_t* d_flag, uint64_t* d_dup_key, int32_t n_panels,
-                        const int32_t* d_bounds, const int32_t* d_pos, const int64_t* d_offsets,
-                        const int32_t* d_hdr, uint32_t* d_pk, void* d_seg_val, sme_stream_t stream);
 /* Test hook: 1 (default) fills the layout with a warp per 32-row group through a
  * shared-memory image of the group's panel ranges (coalesced writes); 0 = warp per row. */
 int sme_seg_set_scatter_groups(int on);
@@ -603,17 +577,6 @@ int sme_seg_fill_i64(int dtype, int64_t n_rows, const int64_t* d_row_ptr, const 
                      const void* d_val, int32_t n_panels, const int32_t* d_bounds, const int32_t* d_pos,
                      const int64_t* d_offsets, const int64_t* h_offsets, uint32_t* d_pk, void* d_out_val,
                      int32_t* d_hdr, const void* d_ws, sme_stream_t stream);
-int sme_seg_count_src_i64(int64_t n_rows, const int64_t* d_row_ptr, const int32_t* d_col,
-                          const int32_t* d_col_map, const int32_t* d_row_map, int32_t n_panels,
-                          const int32_t* d_bounds, int32_t* d_counts, void* d_ws, size_t ws_bytes, int32_t* d_flag,
-                          sme_stream_t stream);
-int sme_permute_csr_seg_i64(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* d_row_ptr,
-                            const int32_t* d_col, const void* d_val, const int32_t* d_inv_row,
-                            const int32_t* d_col_map, const int64_t* d_row_ptr_out, int32_t* d_col_out,
-                            void* d_val_out, void* d_ws, size_t ws_bytes, int32_t* d_flag, uint64_t* d_dup_key,
-                            int32_t n_panels, const int32_t* d_bounds, const int32_t* d_pos,
-                            const int64_t* d_offsets, const int32_t* d_hdr, uint32_t* d_pk, void* d_seg_val,
-                            sme_stream_t stream);
 int sme_spmv_vector_i64(int dtype, int lanes, int64_t n_rows, int64_t n_cols, const int64_t* d_row_ptr,
                         const int32_t* d_col, const void* d_val, const void* d_x, void* d_y, int accumulate,
                         sme_stream_t stream);

@@ -87,10 +87,6 @@ SIGNATURES: dict[str, list] = {
     "sme_seg_set_scatter_groups": [C.c_int],
     "sme_seg_set_fill_ballot": [C.c_int],
     "sme_seg_set_fill_direct": [C.c_int],
-    "sme_seg_count_src": [i64, p, p, p, p, i32, p, p, p, sz, p, p],
-    "sme_seg_positions_counts": [i64, i32, C.c_int, p, p, p, sz, p],
-    "sme_seg_zeros_hdr": [C.c_int, i64, i32, p, p, p, p, p, p, p],
-    "sme_permute_csr_seg": [C.c_int, i64, i64, i64, p, p, p, p, p, p, p, p, p, sz, p, p, i32, p, p, p, p, p, p, p],
     "sme_spmv_seg_set_mode": [C.c_int],
     "sme_seg_plan": [i64, p, i32, p, p],
     "sme_seg_plan_split": [i64, i32, p, p],
@@ -140,7 +136,7 @@ SIGNATURES: dict[str, list] = {
 WIDE_ENTRY_POINTS = (
     "sme_coo_row_ptr", "sme_coo_to_csr", "sme_permute_csr_row_ptr", "sme_permute_csr", "sme_long_row_nnz",
     "sme_row_stats", "sme_csr_validate", "sme_csr_expand_rows", "sme_hist2d_csr", "sme_row_hist_csr",
-    "sme_seg_positions", "sme_seg_fill", "sme_spmv_vector", "sme_seg_count_src", "sme_permute_csr_seg",
+    "sme_seg_positions", "sme_seg_fill", "sme_spmv_vector",
 )
 for _n in WIDE_ENTRY_POINTS:
     SIGNATURES[_n + "_i64"] = SIGNATURES[_n]

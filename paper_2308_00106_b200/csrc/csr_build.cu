@@ -139,30 +139,6 @@ __device__ __forceinline__ void bitonic_regs(K (&a)[N]) {
       }
 }
 
-// Seg layout outputs of the fused build (sme_permute_csr_seg): each sorted entry is also
-// placed in its column panel's slot of the segmented-chunk layout (spmv_seg.cu), so the
-// layout needs no second pass over the permuted CSR.
-template <typename T>
-struct SegSink {
-  uint32_t* pk;
-  T* val;
-  const int32_t* pos;      // [P][n_rows + 1] first slot of each row per panel (panel-relative)
-  const int32_t* hdr;      // chunk header rows, all panels (128-aligned panel offsets)
-  const int32_t* bounds;   // [P + 1] panel column bounds
-  const int64_t* offsets;  // [P] first slot of each panel
-  int32_t n_panels;
-};
-
-// per-CTA copies of the panel bounds / offsets and per-warp slot positions of the group's
-// rows (shared memory; only the fused build uses them)
-struct SegSmem {
-  const int32_t* hi;
-  const int32_t* lo;
-  const int64_t* off;
-  const int32_t* pos;  // [P][32] this warp's group
-  int ppow;
-};
-
 constexpr int SORT_STRIDE = 33;  // row pitch of the per-warp key tile (conflict-free rows and columns)
 constexpr int SORT_UNROLL = 8;   // rows per unrolled load / store step (loads in flight per lane)
 constexpr int TILE_NT = 128;     // k_sort_rows_warp block: 4 warps, 17 KB (32-bit keys) / 34 KB of tiles
@@ -179,14 +155,13 @@ constexpr int TILE_NT = 128;     // k_sort_rows_warp block: 4 warps, 17 KB (32-b
 //      flagging a key equal in column to its predecessor as a duplicate.
 // About 40 warp instructions per row of 20, against ~160 for a shuffle network with a
 // lane per entry, which left the kernel issue-bound (ncu, C4: 11 ms at 64 % issue).
-template <typename T, class Src, bool KEY32, int N, bool SEG = false>
+template <typename T, class Src, bool KEY32, int N>
 __device__ __forceinline__ void sort_group_tile(typename SortKey<KEY32>::K* tile, int lane, int64_t g,
                                                 int32_t len, int64_t dst, int64_t from,
                                                 const int32_t* __restrict__ src_col, const T* __restrict__ src_val,
                                                 const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
                                                 T* __restrict__ out_val, const SortLists& L, int32_t* flag,
-                                                unsigned long long* dup_key, uint64_t keep, uint64_t once,
-                                                const SegSink<T>& seg = SegSink<T>{}, const SegSmem& ss = SegSmem{}) {
+                                                unsigned long long* dup_key, uint64_t keep, uint64_t once) {
   using SK = SortKey<KEY32>;
   using K = typename SK::K;
   // A: keys into the tile, SORT_UNROLL rows per step (their loads in flight together)
@@ -246,70 +221,20 @@ __device__ __forceinline__ void sort_group_tile(typename SortKey<KEY32>::K* tile
         st_stream(out_val + md[u] + lane, w[u]);
       }
     }
-    if (SEG) {
-      // each entry's panel (branchless search of the bounds) and its rank among the row's
-      // entries of that panel (one panel's lanes are consecutive: the row is sorted) give
-      // its slot; the chunk-header loads of all SORT_UNROLL rows are issued together
-      int64_t slot[SORT_UNROLL];
-      uint32_t word[SORT_UNROLL];
-      int32_t h[SORT_UNROLL];
-#pragma unroll
-      for (int u = 0; u < SORT_UNROLL; ++u) {
-        const uint32_t col = SK::col(key[u]);
-        int p = 0;
-        if (in[u]) {
-#pragma unroll
-          for (int st = 16; st > 0; st >>= 1)
-            if (st < ss.ppow && (int32_t)col >= ss.hi[p + st - 1]) p += st;
-        }
-        const unsigned grp = __match_any_sync(0xffffffffu, in[u] ? p : 64 + lane);
-        const int first = __ffs(grp) - 1, last = 31 - __clz(grp);
-        slot[u] = in[u] ? ss.off[p] + ss.pos[p * 32 + r0 + u] + (lane - first) : 0;
-        word[u] = ((col - (uint32_t)ss.lo[p]) << 9) | (lane == last ? 256u : 0u);
-      }
-#pragma unroll
-      for (int u = 0; u < SORT_UNROLL; ++u) h[u] = in[u] ? __ldg(seg.hdr + (slot[u] >> 7)) : 0;
-#pragma unroll
-      for (int u = 0; u < SORT_UNROLL; ++u)
-        if (in[u]) {
-          seg.pk[slot[u]] = word[u] | (uint32_t)((int32_t)(g * 32 + r0 + u) - h[u]);
-          seg.val[slot[u]] = w[u];
-        }
-    }
   }
   __syncwarp();
 }
 
-template <typename T, class Src, bool KEY32, typename IP, bool SEG = false>
+template <typename T, class Src, bool KEY32, typename IP>
 __global__ void __launch_bounds__(TILE_NT) k_sort_rows_warp(
     int32_t n_rows, const IP* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
     const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
-    T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key,
-    SegSink<T> seg = SegSink<T>{}) {
+    T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key) {
   using SK = SortKey<KEY32>;
   using K = typename SK::K;
   __shared__ K s_tile[TILE_NT / 32][32 * SORT_STRIDE];
-  __shared__ int32_t c_hi[SEG ? 32 : 1], c_lo[SEG ? 32 : 1];
-  __shared__ int64_t c_off[SEG ? 32 : 1];
-  __shared__ int32_t s_pos[TILE_NT / 32][SEG ? 32 * 32 : 1];
   K* tile = s_tile[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
-  SegSmem ss{};
-  if (SEG) {
-    if (threadIdx.x < 32) {
-      const int t = threadIdx.x;
-      c_hi[t] = t < seg.n_panels ? seg.bounds[t + 1] : INT32_MAX;
-      c_lo[t] = t < seg.n_panels ? seg.bounds[t] : 0;
-      c_off[t] = t < seg.n_panels ? seg.offsets[t] : 0;
-    }
-    __syncthreads();
-    ss.hi = c_hi;
-    ss.lo = c_lo;
-    ss.off = c_off;
-    ss.pos = s_pos[threadIdx.x >> 5];
-    ss.ppow = 1;
-    while (ss.ppow < seg.n_panels) ss.ppow <<= 1;
-  }
   const int64_t n_groups = ((int64_t)n_rows + 31) / 32;
   const int64_t warp_global = ((int64_t)blockIdx.x * TILE_NT + threadIdx.x) >> 5;
   const int64_t warps_total = ((int64_t)gridDim.x * TILE_NT) >> 5;
@@ -335,15 +260,6 @@ __global__ void __launch_bounds__(TILE_NT) k_sort_rows_warp(
     const int64_t dst = n0;
     int32_t len = (int32_t)(n1 - n0);
     const int64_t my_from = from;
-    if (SEG) {  // this group's slot positions, one row per lane, every panel
-      __syncwarp();
-      for (int q = 0; q < seg.n_panels; ++q)
-        s_pos[threadIdx.x >> 5][q * 32 + lane] = r < n_rows ? seg.pos[(int64_t)q * (n_rows + 1) + r] : 0;
-      if (len > 32) {  // the fused build takes rows of <= 32 entries only
-        atomicOr(flag, SME_FLAG_RANGE);
-        len = 0;
-      }
-    }
     if (len > 32) {
       if (len <= SME_SORT_SMEM_MAX) {
         int slot = atomicAdd(&L.counters[0], 1);
@@ -362,14 +278,14 @@ __global__ void __launch_bounds__(TILE_NT) k_sort_rows_warp(
     from = n1 > n0 ? src.start_of(k, n0) : 0;  // next group's starts: in flight during this one
     if (maxlen == 0) continue;
     if (maxlen <= 8)
-      sort_group_tile<T, Src, KEY32, 8, SEG>(tile, lane, g, len, dst, my_from, src_col, src_val, cmap, out_col,
-                                             out_val, L, flag, dup_key, keep, once, seg, ss);
+      sort_group_tile<T, Src, KEY32, 8>(tile, lane, g, len, dst, my_from, src_col, src_val, cmap, out_col, out_val,
+                                        L, flag, dup_key, keep, once);
     else if (maxlen <= 16)
-      sort_group_tile<T, Src, KEY32, 16, SEG>(tile, lane, g, len, dst, my_from, src_col, src_val, cmap, out_col,
-                                              out_val, L, flag, dup_key, keep, once, seg, ss);
+      sort_group_tile<T, Src, KEY32, 16>(tile, lane, g, len, dst, my_from, src_col, src_val, cmap, out_col,
+                                         out_val, L, flag, dup_key, keep, once);
     else
-      sort_group_tile<T, Src, KEY32, 32, SEG>(tile, lane, g, len, dst, my_from, src_col, src_val, cmap, out_col,
-                                              out_val, L, flag, dup_key, keep, once, seg, ss);
+      sort_group_tile<T, Src, KEY32, 32>(tile, lane, g, len, dst, my_from, src_col, src_val, cmap, out_col,
+                                         out_val, L, flag, dup_key, keep, once);
   }
 }
 
@@ -961,76 +877,6 @@ SME_API int sme_permute_csr_i64(int dtype, int64_t n_rows, int64_t n_cols, int64
   CHECK_SIZES_WIDE(n_rows, n_cols, nnz);
   return permute_csr_impl(dtype, n_rows, n_cols, nnz, row_ptr, col, val, inv_row, col_map, row_ptr_out, col_out,
                           val_out, ws, ws_bytes, long_nnz, flag, dup_key, stream);
-}
-
-// K4 with the seg layout of the result placed by the same row sort (rows of <= 32
-// entries: the tile kernel only).  pos / hdr / explicit zeros / tail padding come first
-// (sme_seg_count_src -> sme_seg_positions_counts -> sme_seg_zeros_hdr); a longer row sets
-// SME_FLAG_RANGE in *d_flag and is left out (the caller then builds the layout itself).
-template <typename T, typename IP>
-static int permute_csr_seg_launch(int64_t n_rows, int64_t n_cols, const IP* row_ptr, const int32_t* col,
-                                  const T* val, const int32_t* inv_row, const int32_t* col_map,
-                                  const IP* row_ptr_out, int32_t* col_out, T* val_out, SortLists L,
-                                  int32_t* flag, uint64_t* dup_key, SegSink<T> seg, cudaStream_t s) {
-  const int64_t groups = (n_rows + 31) / 32;
-  const int blocks = grid_for(groups * 32, TILE_NT, 16);
-  SrcGather<IP> src{row_ptr, inv_row};
-  k_sort_rows_warp<T, SrcGather<IP>, true, IP, true><<<blocks, TILE_NT, 0, s>>>(
-      (int32_t)n_rows, row_ptr_out, src, col, val, col_map, col_out, val_out, L, flag, (unsigned long long*)dup_key,
-      seg);
-  SME_CHECK_LAUNCH("k_sort_rows_warp (seg)");
-  return SME_OK;
-}
-
-template <typename IP>
-static int permute_csr_seg_impl(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const IP* row_ptr,
-                                const int32_t* col, const void* val, const int32_t* inv_row, const int32_t* col_map,
-                                const IP* row_ptr_out, int32_t* col_out, void* val_out, void* ws, size_t ws_bytes,
-                                int32_t* flag, uint64_t* dup_key, int32_t n_panels, const int32_t* bounds,
-                                const int32_t* pos, const int64_t* offsets, const int32_t* hdr, uint32_t* pk,
-                                void* seg_val, sme_stream_t stream) {
-  SME_REQUIRE(dtype == SME_F64 || dtype == SME_F32, "unknown dtype %d", dtype);
-  SME_REQUIRE(n_panels >= 1 && n_panels <= 32, "the fused build takes 1..32 panels");
-  SME_REQUIRE(n_cols <= ((int64_t)1 << 27), "the fused build needs n_cols <= 2^27 (32-bit sort keys)");
-  const size_t need = lists_bytes(n_rows, 0);
-  SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
-  if (nnz == 0 || n_rows == 0) return SME_OK;
-  cudaStream_t s = as_stream(stream);
-  SortLists L = carve_lists((char*)ws, n_rows, 0);
-  SME_CUDA(cudaMemsetAsync(L.counters, 0, 64, s));
-  if (dtype == SME_F64)
-    return permute_csr_seg_launch<double>(n_rows, n_cols, row_ptr, col, (const double*)val, inv_row, col_map,
-                                          row_ptr_out, col_out, (double*)val_out, L, flag, dup_key,
-                                          SegSink<double>{pk, (double*)seg_val, pos, hdr, bounds, offsets, n_panels},
-                                          s);
-  return permute_csr_seg_launch<float>(n_rows, n_cols, row_ptr, col, (const float*)val, inv_row, col_map, row_ptr_out,
-                                       col_out, (float*)val_out, L, flag, dup_key,
-                                       SegSink<float>{pk, (float*)seg_val, pos, hdr, bounds, offsets, n_panels}, s);
-}
-
-SME_API int sme_permute_csr_seg(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* row_ptr,
-                                const int32_t* col, const void* val, const int32_t* inv_row, const int32_t* col_map,
-                                const int32_t* row_ptr_out, int32_t* col_out, void* val_out, void* ws,
-                                size_t ws_bytes, int32_t* flag, uint64_t* dup_key, int32_t n_panels,
-                                const int32_t* bounds, const int32_t* pos, const int64_t* offsets, const int32_t* hdr,
-                                uint32_t* pk, void* seg_val, sme_stream_t stream) {
-  CHECK_SIZES(n_rows, n_cols, nnz);
-  return permute_csr_seg_impl(dtype, n_rows, n_cols, nnz, row_ptr, col, val, inv_row, col_map, row_ptr_out, col_out,
-                              val_out, ws, ws_bytes, flag, dup_key, n_panels, bounds, pos, offsets, hdr, pk, seg_val,
-                              stream);
-}
-
-SME_API int sme_permute_csr_seg_i64(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
-                                    const int32_t* col, const void* val, const int32_t* inv_row,
-                                    const int32_t* col_map, const int64_t* row_ptr_out, int32_t* col_out,
-                                    void* val_out, void* ws, size_t ws_bytes, int32_t* flag, uint64_t* dup_key,
-                                    int32_t n_panels, const int32_t* bounds, const int32_t* pos,
-                                    const int64_t* offsets, const int32_t* hdr, uint32_t* pk, void* seg_val,
-                                    sme_stream_t stream) {
-  CHECK_SIZES_WIDE(n_rows, n_cols, nnz);
-  return permute_csr_seg_impl(dtype, n_rows, n_cols, nnz, row_ptr, col, val, inv_row, col_map, row_ptr_out, col_out,
-                              val_out, ws, ws_bytes, flag, dup_key, n_panels, bounds, pos, offsets, hdr, pk, seg_val,
-                              stream);
 }
 
 namespace sme {

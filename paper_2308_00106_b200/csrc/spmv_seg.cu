@@ -534,93 +534,6 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
   }
 }
 
-// ---------------------------------------------------------------------------
-// the seg layout of P_r A P_c built with K4 (sme_seg_count_src + sme_seg_positions_counts +
-// sme_seg_zeros, then sme_permute_csr_seg places the entries from the row sort)
-// ---------------------------------------------------------------------------
-// Panel counts of the permuted matrix straight from the source rows (rows of <= 32 entries):
-// warp per group of 32 consecutive source rows.  The group's entries are read coalesced
-// (lane = entry); each finds its new column (cmap[col], or col when the column pre-map
-// already ran), its panel (search of the bounds) and its row (search of the group's row
-// starts) and bumps a shared-memory counter [row][panel]; the group then writes each
-// row's P counts as one record at counts_rp[p_r[r] * P] (a single random sector per row).
-constexpr int CS_WARPS = 8;
-template <typename IP>
-__global__ void __launch_bounds__(CS_WARPS * 32) k_seg_count_src(
-    int64_t n_rows, const IP* __restrict__ row_ptr, const int32_t* __restrict__ col, const int32_t* __restrict__ cmap,
-    const int32_t* __restrict__ rmap, int32_t n_panels, const int32_t* __restrict__ bounds,
-    int32_t* __restrict__ counts_rp, int32_t* __restrict__ flag) {
-  __shared__ int32_t c_hi[32];
-  __shared__ int32_t s_cnt[CS_WARPS][32 * 32];
-  __shared__ int32_t s_rp[CS_WARPS][33];
-  if (threadIdx.x < 32) c_hi[threadIdx.x] = threadIdx.x < n_panels ? bounds[threadIdx.x + 1] : INT32_MAX;
-  __syncthreads();
-  const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int P = n_panels;
-  int ppow = 1;
-  while (ppow < P) ppow <<= 1;
-  int32_t* cnt = s_cnt[wib];
-  int32_t* rp = s_rp[wib];
-  const int64_t n_groups = (n_rows + 31) / 32;
-  for (int64_t g = (int64_t)blockIdx.x * CS_WARPS + wib; g < n_groups; g += (int64_t)gridDim.x * CS_WARPS) {
-    const int64_t r0 = g * 32;
-    const int nr = (int)min((int64_t)32, n_rows - r0);
-    const IP base = row_ptr[r0];
-    __syncwarp();
-    if (lane < nr) rp[lane] = (int32_t)min((int64_t)row_ptr[r0 + lane] - base, (int64_t)INT32_MAX);
-    if (lane == 0) rp[nr] = (int32_t)min((int64_t)row_ptr[r0 + nr] - base, (int64_t)INT32_MAX);
-    for (int i = lane; i < 32 * P; i += 32) cnt[i] = 0;
-    __syncwarp();
-    const bool longrow = lane < nr && rp[lane + 1] - rp[lane] > 32;
-    if (__any_sync(FULL, longrow)) {  // the fused build handles rows of <= 32 entries only
-      if (lane == 0) atomicOr(flag, SME_FLAG_RANGE);
-      continue;
-    }
-    const int32_t total = rp[nr];
-    for (int32_t k = lane; k < total; k += 32) {
-      const int32_t c0 = col[base + k];
-      const int32_t c = (int32_t)(cmap ? (c0 < 0 ? (c0 & 0x7fffffff) : __ldg(cmap + c0)) : (c0 & 0x7fffffff));
-      int p = 0;
-#pragma unroll
-      for (int st = 16; st > 0; st >>= 1)
-        if (st < ppow && c >= c_hi[p + st - 1]) p += st;
-      int lo = 0;  // the entry's row: largest i with rp[i] <= k
-#pragma unroll
-      for (int st = 16; st > 0; st >>= 1)
-        if (lo + st < nr && rp[lo + st] <= k) lo += st;
-      atomicAdd(&cnt[lo * P + p], 1);
-    }
-    __syncwarp();
-    for (int i = lane; i < nr * P; i += 32) {
-      const int row = i / P;
-      const int64_t nrow = rmap ? (int64_t)rmap[r0 + row] : r0 + row;
-      counts_rp[nrow * P + (i - row * P)] = cnt[i];
-    }
-  }
-}
-
-// counts[p * n + r] = counts_rp[r * P + p] (thread per row: one P-word record in, P
-// coalesced column writes out)
-__global__ void k_seg_counts_transpose(int64_t n_rows, int32_t n_panels, const int32_t* __restrict__ counts_rp,
-                                       int32_t* __restrict__ counts) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x)
-    for (int p = 0; p < n_panels; ++p) counts[(int64_t)p * n_rows + r] = counts_rp[r * n_panels + p];
-}
-
-// Explicit zeros of the layout (rows without entries in panel p that still own a slot:
-// panel 0, the full last panel, even rows elsewhere), from the counts and positions.
-__global__ void k_seg_zeros(int64_t n_rows, const int32_t* __restrict__ counts, const int32_t* __restrict__ pos,
-                            const int32_t* __restrict__ hdr, uint32_t* __restrict__ pk, double* __restrict__ v64,
-                            float* __restrict__ v32) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
-    if (counts[r] != 0 || pos[r + 1] == pos[r]) continue;
-    const int64_t dst = pos[r];
-    pk[dst] = (SEG_MARK << SEG_CSHIFT) | SEG_END | (uint32_t)(r - hdr[dst / SEG_CH]);
-    if (v64) v64[dst] = 0.0; else v32[dst] = 0.0f;
-  }
-}
-
 // plan[w] = pos[R_w], R_w = first row with pos[R_w] >= w * total / W (rows stay whole)
 __global__ void k_seg_plan(int64_t n_rows, const int32_t* __restrict__ pos, int32_t n_warps, int32_t* __restrict__ plan) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= n_warps; w += gridDim.x * blockDim.x) {
@@ -1398,78 +1311,3 @@ int preload_spmv_seg() {
   return cudaFuncGetAttributes(&a, (const void*)k_seg_hdr) == cudaSuccess ? 0 : -1;
 }
 }  // namespace sme
-
-// ---------------------------------------------------------------------------
-// seg layout of P_r A P_c from the source CSR (the K4-fused build, rows <= 32)
-// ---------------------------------------------------------------------------
-template <typename IP>
-static int seg_count_src_impl(int64_t n_rows, const IP* row_ptr, const int32_t* col, const int32_t* col_map,
-                              const int32_t* row_map, int32_t n_panels, const int32_t* bounds, int32_t* counts,
-                              void* ws, size_t ws_bytes, int32_t* flag, sme_stream_t stream) {
-  SME_REQUIRE(n_rows >= 0 && n_rows < INT32_MAX && n_panels >= 1 && n_panels <= 1024, "bad arguments");
-  const size_t need = align_up((size_t)n_panels * n_rows * 4);
-  SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
-  if (n_rows == 0) return SME_OK;
-  cudaStream_t s = as_stream(stream);
-  int32_t* counts_rp = (int32_t*)ws;
-  SME_REQUIRE(n_panels <= 32, "the fused build takes 1..32 panels");
-  const int64_t groups = (n_rows + 31) / 32;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((groups + CS_WARPS - 1) / CS_WARPS,
-                                                             (int64_t)sm_count() * 8));
-  k_seg_count_src<IP><<<grid, CS_WARPS * 32, 0, s>>>(n_rows, row_ptr, col, col_map, row_map, n_panels, bounds,
-                                                      counts_rp, flag);
-  SME_CHECK_LAUNCH("k_seg_count_src");
-  k_seg_counts_transpose<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, n_panels, counts_rp, counts);
-  SME_CHECK_LAUNCH("k_seg_counts_transpose");
-  return SME_OK;
-}
-
-SME_API int sme_seg_count_src(int64_t n_rows, const int32_t* row_ptr, const int32_t* col, const int32_t* col_map,
-                              const int32_t* row_map, int32_t n_panels, const int32_t* bounds, int32_t* counts,
-                              void* ws, size_t ws_bytes, int32_t* flag, sme_stream_t stream) {
-  return seg_count_src_impl(n_rows, row_ptr, col, col_map, row_map, n_panels, bounds, counts, ws, ws_bytes, flag,
-                            stream);
-}
-
-SME_API int sme_seg_count_src_i64(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, const int32_t* col_map,
-                                  const int32_t* row_map, int32_t n_panels, const int32_t* bounds, int32_t* counts,
-                                  void* ws, size_t ws_bytes, int32_t* flag, sme_stream_t stream) {
-  return seg_count_src_impl(n_rows, row_ptr, col, col_map, row_map, n_panels, bounds, counts, ws, ws_bytes, flag,
-                            stream);
-}
-
-SME_API int sme_seg_positions_counts(int64_t n_rows, int32_t n_panels, int full_last, const int32_t* counts,
-                                     int32_t* pos, void* ws, size_t ws_bytes, sme_stream_t stream) {
-  SME_REQUIRE(n_rows >= 0 && n_rows < INT32_MAX && n_panels >= 1 && n_panels <= 1024, "bad arguments");
-  const size_t need = scan_workspace_bytes(n_rows);
-  SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
-  cudaStream_t s = as_stream(stream);
-  for (int p = 0; p < n_panels; ++p) {
-    const bool full = full_last && p == n_panels - 1;
-    int rc = exclusive_scan_lengths(n_rows, SegLen{counts + (int64_t)p * n_rows, p, full},
-                                    pos + (int64_t)p * (n_rows + 1), ws, nullptr, s);
-    if (rc != SME_OK) return rc;
-  }
-  return SME_OK;
-}
-
-SME_API int sme_seg_zeros_hdr(int dtype, int64_t n_rows, int32_t n_panels, const int32_t* counts, const int32_t* pos,
-                              const int64_t* h_offsets, uint32_t* pk, void* val, int32_t* hdr, sme_stream_t stream) {
-  SME_REQUIRE(dtype == SME_F64 || dtype == SME_F32, "unknown dtype %d", dtype);
-  SME_REQUIRE(h_offsets, "host offsets required");
-  if (n_rows == 0) return SME_OK;
-  cudaStream_t s = as_stream(stream);
-  for (int p = 0; p < n_panels; ++p) {
-    SME_REQUIRE(h_offsets[p] % SEG_CH == 0, "panel offsets must be multiples of 128");
-    const int32_t* pp = pos + (int64_t)p * (n_rows + 1);
-    int32_t* hp = hdr + h_offsets[p] / SEG_CH;
-    k_seg_hdr<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, pp, hp);
-    SME_CHECK_LAUNCH("k_seg_hdr");
-    const int64_t o = h_offsets[p];
-    k_seg_zeros<<<grid_for(n_rows, 256), 256, 0, s>>>(
-        n_rows, counts + (int64_t)p * n_rows, pp, hp, pk + o, dtype == SME_F64 ? (double*)val + o : nullptr,
-        dtype == SME_F32 ? (float*)val + o : nullptr);
-    SME_CHECK_LAUNCH("k_seg_zeros");
-  }
-  return SME_OK;
-}

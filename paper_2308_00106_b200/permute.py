@@ -341,29 +341,6 @@ PREMAP_MIN_NNZ = 1 << 24
 PREMAP_PERSIST = False
 #: leave the last slice to the row sort (one pass over col fewer)
 PREMAP_FUSE_LAST = False
-#: build the seg layout of the result inside K4 (sme_permute_csr_seg) when the result will
-#: run 'seg' (x larger than 60 % of L2), rows have <= 32 entries and n_cols <= 2^27: the
-#: row sort places every entry in its panel slot too, so the layout needs no second pass
-#: over the permuted CSR.  Bit-identical to seg_of(result).  False: build it on first use.
-FUSE_SEG_LAYOUT = False
-
-
-def _fused_seg_panels(m: CsrMatrix) -> int:
-    """Panel count of the K4-fused seg layout for the permutation of m, or 0 (no fusion)."""
-    if not FUSE_SEG_LAYOUT or m.nnz == 0 or m.n_cols > (1 << 27):
-        return 0
-    from .kernels import row_stats
-    from .panels import l2_bytes
-    from .seg import auto_seg_panels
-
-    if m.n_cols * m.d_values.element_size() <= 0.6 * l2_bytes():  # auto_kernel's 'seg' rule for large x
-        return 0
-    if row_stats(m)[0] > 32:
-        return 0
-    P = auto_seg_panels(m)  # the result has m's shape, nnz and dtype: seg_of's choice
-    return P if P <= 32 else 0
-
-
 def _premap_slices(m: CsrMatrix) -> int:
     """Number of column slices for the pre-map (0: gather p_c inside the row sort)."""
     if PREMAP is False or m.d_col_idx.data_ptr() % 16:
@@ -418,23 +395,12 @@ def permute_csr(m: CsrMatrix, p_r: Permutation | None, p_c: Permutation | None) 
             _lib.call("sme_l2_reset_persisting")
         if n_passes == n_slices:
             cmap = None
-    lay, P = None, _fused_seg_panels(m)
-    if P:
-        from .seg import SegLayout
-
-        lay = SegLayout.with_permute(m, P, inv_r, p_r.d_forward if p_r is not None else None, src_col, cmap,
-                                     row_ptr, col, val, ws2, fl)
-    if lay is None:
-        _lib.call_rp("sme_permute_csr", row_ptr, _cuda.sme_dtype(m.d_values), m.n_rows, m.n_cols, m.nnz,
-                     ptr(m.d_row_ptr), ptr(src_col), ptr(m.d_values), ptr(inv_r), ptr(cmap), ptr(row_ptr), ptr(col),
-                     ptr(val), ptr(ws2), ws2.numel(), long_nnz, fl.flag_ptr, fl.dup_ptr, stream())
+    _lib.call_rp("sme_permute_csr", row_ptr, _cuda.sme_dtype(m.d_values), m.n_rows, m.n_cols, m.nnz,
+                 ptr(m.d_row_ptr), ptr(src_col), ptr(m.d_values), ptr(inv_r), ptr(cmap), ptr(row_ptr), ptr(col),
+                 ptr(val), ptr(ws2), ws2.numel(), long_nnz, fl.flag_ptr, fl.dup_ptr, stream())
     del src_col
     out = CsrMatrix._from_device(m.n_rows, m.n_cols, row_ptr, col, val)
     out._cache["long_nnz"] = long_nnz
-    if lay is not None:
-        from .seg import install
-
-        install(out, ("seg", P, False), lay)
     return out
 
 

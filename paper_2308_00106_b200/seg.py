@@ -60,7 +60,7 @@ class SegLayout:
                      ctypes.cast(h_offs, ctypes.c_void_p), ptr(self.pk), ptr(self.val), ptr(self.hdr), ptr(ws), s)
         self._finish(m, pos, n_warps, split_rows)
 
-    # -- construction pieces (shared with the K4-fused build, SegLayout.with_permute) ----
+    # -- construction pieces ------------------------------------------------------
     def _geometry(self, m: CsrMatrix, n_panels: int, full_last: bool) -> tuple[int, int]:
         P, n = int(n_panels), m.n_rows
         if P < 1 or P > max(1, m.n_cols):
@@ -137,42 +137,6 @@ class SegLayout:
         self.persist = False
         self.hit_ratio = 1.0  # access-policy window hit ratio of the pinned x slice
         self.warm = False  # L2 prefetch sweep of each pass's x slice (experiment knob)
-
-    @classmethod
-    def with_permute(cls, src: CsrMatrix, n_panels: int, inv_r, fwd_r, src_col: torch.Tensor, cmap,
-                     row_ptr: torch.Tensor, col_out: torch.Tensor, val_out: torch.Tensor, lists_ws: torch.Tensor,
-                     flags) -> "SegLayout | None":
-        """K4 with this layout of its result built by the same row sort (sme_permute_csr_seg;
-        rows of <= 32 entries).  Writes the permuted CSR into col_out / val_out (row_ptr is
-        already computed) and returns the layout of that CSR — bit-identical to
-        SegLayout(permuted, n_panels) — or None when a row turned out longer than 32 (the
-        caller then runs the plain K4)."""
-        lay = cls.__new__(cls)
-        n = src.n_rows
-        shape = CsrMatrix._from_device(n, src.n_cols, row_ptr, col_out, val_out)  # geometry only
-        P, n = lay._geometry(shape, n_panels, False)
-        s = stream()
-        dev = row_ptr.device
-        counts = torch.empty(P * n, dtype=torch.int32, device=dev)
-        ws = _cuda.workspace(max(_lib.query_size("sme_seg_workspace_size", n, P),
-                                 _lib.query_size("sme_row_ptr_workspace_size", n)))
-        _lib.call_rp("sme_seg_count_src", src.d_row_ptr, n, ptr(src.d_row_ptr), ptr(src_col), ptr(cmap), ptr(fwd_r),
-                     P, ptr(lay.bounds), ptr(counts), ptr(ws), ws.numel(), flags.flag_ptr, s)
-        bits, _ = flags.read()
-        if bits & _lib.FLAG_RANGE:
-            return None
-        pos = torch.empty(P * (n + 1), dtype=torch.int32, device=dev)
-        _lib.call("sme_seg_positions_counts", n, P, 0, ptr(counts), ptr(pos), ptr(ws), ws.numel(), s)
-        h_offs, d_offs = lay._allocate(pos)
-        _lib.call("sme_seg_zeros_hdr", _cuda.sme_dtype(val_out), n, P, ptr(counts), ptr(pos),
-                  ctypes.cast(h_offs, ctypes.c_void_p), ptr(lay.pk), ptr(lay.val), ptr(lay.hdr), s)
-        del counts
-        _lib.call_rp("sme_permute_csr_seg", row_ptr, _cuda.sme_dtype(src.d_values), n, src.n_cols, src.nnz,
-                     ptr(src.d_row_ptr), ptr(src_col), ptr(src.d_values), ptr(inv_r), ptr(cmap), ptr(row_ptr),
-                     ptr(col_out), ptr(val_out), ptr(lists_ws), lists_ws.numel(), flags.flag_ptr, flags.dup_ptr, P,
-                     ptr(lay.bounds), ptr(pos), ptr(d_offs), ptr(lay.hdr), ptr(lay.pk), ptr(lay.val), s)
-        lay._finish(shape, pos, None, False)
-        return lay
 
     # -- passes --------------------------------------------------------------
     def _pass(self, p: int, xd: torch.Tensor, y: torch.Tensor) -> None:
