@@ -193,6 +193,14 @@ int sme_coo_to_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz, const
 int sme_permute_csr_row_ptr(int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_inv_row,
                             int32_t* d_row_ptr_out, void* d_ws, size_t ws_bytes,
                             sme_stream_t stream); /* ws: sme_row_ptr_workspace_size */
+/* The same row_ptr plus d_starts_out[r] = d_row_ptr[d_inv_row[r]], the source start of
+ * every new row, with the old row_ptr gathered once (the scan's second pass reads the
+ * lengths back sequentially).  Passing d_starts_out as sme_permute_csr's d_row_ptr with
+ * d_inv_row = NULL then reads the sources in order (K4 without a second random gather).
+ * ws: sme_row_ptr_workspace_size. */
+int sme_permute_csr_row_ptr_starts(int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_inv_row,
+                                   int32_t* d_row_ptr_out, int32_t* d_starts_out, void* d_ws, size_t ws_bytes,
+                                   sme_stream_t stream);
 int sme_permute_csr_workspace_size(int64_t n_rows, int64_t nnz, int64_t long_nnz, size_t* bytes);
 int sme_permute_csr(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz,
                     const int32_t* d_row_ptr, const int32_t* d_col, const void* d_val,
@@ -559,6 +567,9 @@ int sme_permute_csr_i64(int dtype, int64_t n_rows, int64_t n_cols, int64_t nnz,
                         const int32_t* d_inv_row, const int32_t* d_col_map, const int64_t* d_row_ptr_out,
                         int32_t* d_col_out, void* d_val_out, void* d_ws, size_t ws_bytes,
                         int64_t long_nnz, int32_t* d_flag, uint64_t* d_dup_key, sme_stream_t stream);
+int sme_permute_csr_row_ptr_starts_i64(int64_t n_rows, const int64_t* d_row_ptr, const int32_t* d_inv_row,
+                                       int64_t* d_row_ptr_out, int64_t* d_starts_out, void* d_ws, size_t ws_bytes,
+                                       sme_stream_t stream);
 int sme_long_row_nnz_i64(int64_t n_rows, const int64_t* d_row_ptr, int64_t* d_out, sme_stream_t stream);
 int sme_row_stats_i64(int64_t n_rows, const int64_t* d_row_ptr, int64_t* d_out, sme_stream_t stream);
 int sme_csr_validate_i64(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* d_row_ptr,

@@ -56,6 +56,7 @@ SIGNATURES: dict[str, list] = {
     "sme_coo_to_csr_workspace_size": [i64, i64, i64, psz],
     "sme_coo_to_csr": [C.c_int, i64, i64, i64, p, p, p, p, p, p, p, p, p, sz, i64, p, p, p],
     "sme_permute_csr_row_ptr": [i64, p, p, p, p, sz, p],
+    "sme_permute_csr_row_ptr_starts": [i64, p, p, p, p, p, sz, p],
     "sme_permute_csr_workspace_size": [i64, i64, i64, psz],
     "sme_permute_csr": [C.c_int, i64, i64, i64, p, p, p, p, p, p, p, p, p, sz, i64, p, p, p],
     "sme_long_row_nnz": [i64, p, p, p],
@@ -134,7 +135,8 @@ SIGNATURES: dict[str, list] = {
 }
 # int64 row_ptr twins (nnz >= 2^31 - 1): same argument list as the int32 namesake
 WIDE_ENTRY_POINTS = (
-    "sme_coo_row_ptr", "sme_coo_to_csr", "sme_permute_csr_row_ptr", "sme_permute_csr", "sme_long_row_nnz",
+    "sme_coo_row_ptr", "sme_coo_to_csr", "sme_permute_csr_row_ptr", "sme_permute_csr_row_ptr_starts",
+    "sme_permute_csr", "sme_long_row_nnz",
     "sme_row_stats", "sme_csr_validate", "sme_csr_expand_rows", "sme_hist2d_csr", "sme_row_hist_csr",
     "sme_seg_positions", "sme_seg_fill", "sme_spmv_vector",
 )

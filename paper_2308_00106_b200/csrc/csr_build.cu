@@ -550,6 +550,24 @@ __global__ void k_coo_scatter(int64_t nnz, int64_t n_rows, int64_t n_cols, const
   }
 }
 
+// The permuted row lengths, gathered once: stores the length and the source start of new
+// row k (len_out[k], start_out[k]) while the scan's first pass sums them, so the second
+// pass and the row sort read them sequentially instead of gathering old row_ptr again.
+template <typename IP>
+struct LenGatherStore {
+  const IP* ptr;
+  const int32_t* inv;
+  int32_t* len_out;
+  IP* start_out;
+  __device__ __forceinline__ int64_t operator()(int64_t k) const {
+    const int32_t o = inv ? inv[k] : (int32_t)k;
+    const IP a = ptr[o], l = ptr[o + 1] - a;
+    len_out[k] = (int32_t)l;
+    start_out[k] = a;
+    return (int64_t)l;
+  }
+};
+
 struct LenFromCounts {
   const int32_t* counts;
   __device__ __forceinline__ int64_t operator()(int64_t k) const { return counts[k]; }
@@ -755,6 +773,45 @@ static int long_row_nnz_impl(int64_t n_rows, const IP* row_ptr, int64_t* out, sm
   k_long_row_nnz<IP><<<grid_for(n_rows, 256, 4), 256, 0, s>>>(n_rows, row_ptr, (unsigned long long*)out);
   SME_CHECK_LAUNCH("k_long_row_nnz");
   return SME_OK;
+}
+
+// sme_permute_csr_row_ptr plus the source start of every new row (starts_out[r] =
+// row_ptr[inv_row[r]]): the old row_ptr is gathered once, in the scan's first pass.  With
+// starts as its row_ptr and inv_row = NULL, sme_permute_csr then reads the sources in order.
+template <typename IP>
+static int permute_row_ptr_starts_impl(int64_t n_rows, const IP* row_ptr, const int32_t* inv_row, IP* row_ptr_out,
+                                       IP* starts_out, void* ws, size_t ws_bytes, sme_stream_t stream) {
+  SME_REQUIRE(n_rows >= 0 && n_rows < INT32_MAX, "bad n_rows");
+  const size_t need = align_up(n_rows * 4) + scan_workspace_bytes(n_rows);
+  SME_REQUIRE(ws_bytes >= need, "workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = as_stream(stream);
+  if (n_rows == 0) {
+    SME_CUDA(cudaMemsetAsync(row_ptr_out, 0, sizeof(IP), s));
+    return SME_OK;
+  }
+  int32_t* len = (int32_t*)ws;
+  int64_t* sums = reinterpret_cast<int64_t*>((char*)ws + align_up(n_rows * 4));
+  const int64_t tiles = scan_tiles(n_rows);
+  k_scan_tile_sums<<<(unsigned)tiles, SCAN_NT, 0, s>>>(n_rows, LenGatherStore<IP>{row_ptr, inv_row, len, starts_out},
+                                                      sums);
+  SME_CHECK_LAUNCH("k_scan_tile_sums");
+  k_scan_tile_offsets<<<1, 1024, 0, s>>>(tiles, sums);
+  SME_CHECK_LAUNCH("k_scan_tile_offsets");
+  k_scan_apply<<<(unsigned)tiles, SCAN_NT, 0, s>>>(n_rows, LenFromArray{len}, sums, row_ptr_out, (int32_t*)nullptr);
+  SME_CHECK_LAUNCH("k_scan_apply");
+  return SME_OK;
+}
+
+SME_API int sme_permute_csr_row_ptr_starts(int64_t n_rows, const int32_t* row_ptr, const int32_t* inv_row,
+                                           int32_t* row_ptr_out, int32_t* starts_out, void* ws, size_t ws_bytes,
+                                           sme_stream_t stream) {
+  return permute_row_ptr_starts_impl(n_rows, row_ptr, inv_row, row_ptr_out, starts_out, ws, ws_bytes, stream);
+}
+
+SME_API int sme_permute_csr_row_ptr_starts_i64(int64_t n_rows, const int64_t* row_ptr, const int32_t* inv_row,
+                                               int64_t* row_ptr_out, int64_t* starts_out, void* ws, size_t ws_bytes,
+                                               sme_stream_t stream) {
+  return permute_row_ptr_starts_impl(n_rows, row_ptr, inv_row, row_ptr_out, starts_out, ws, ws_bytes, stream);
 }
 
 SME_API int sme_long_row_nnz(int64_t n_rows, const int32_t* row_ptr, int64_t* out, sme_stream_t stream) {

@@ -341,6 +341,9 @@ PREMAP_MIN_NNZ = 1 << 24
 PREMAP_PERSIST = False
 #: leave the last slice to the row sort (one pass over col fewer)
 PREMAP_FUSE_LAST = False
+#: gather the source starts once with the permuted lengths (sme_permute_csr_row_ptr_starts)
+#: and let the row sort read them in order; False: the sort gathers row_ptr[inv_r[r]]
+K4_STARTS = True
 def _premap_slices(m: CsrMatrix) -> int:
     """Number of column slices for the pre-map (0: gather p_c inside the row sort)."""
     if PREMAP is False or m.d_col_idx.data_ptr() % 16:
@@ -373,9 +376,18 @@ def permute_csr(m: CsrMatrix, p_r: Permutation | None, p_c: Permutation | None) 
     dev = m.d_row_ptr.device
     inv_r = p_r.d_inverse if p_r is not None else None
     row_ptr = torch.empty(m.n_rows + 1, dtype=m.d_row_ptr.dtype, device=dev)  # int64 for nnz >= 2^31 - 1
+    # the source start of every new row, gathered once with the lengths: the row sort then
+    # reads its sources in order (starts as the source row_ptr, identity rows)
     ws1 = _cuda.workspace(_lib.query_size("sme_row_ptr_workspace_size", m.n_rows))
-    _lib.call_rp("sme_permute_csr_row_ptr", row_ptr, m.n_rows, ptr(m.d_row_ptr), ptr(inv_r), ptr(row_ptr),
-                 ptr(ws1), ws1.numel(), stream())
+    if K4_STARTS:
+        starts = torch.empty(max(1, m.n_rows), dtype=m.d_row_ptr.dtype, device=dev)
+        _lib.call_rp("sme_permute_csr_row_ptr_starts", row_ptr, m.n_rows, ptr(m.d_row_ptr), ptr(inv_r),
+                     ptr(row_ptr), ptr(starts), ptr(ws1), ws1.numel(), stream())
+        src_ptr, src_inv = starts, None
+    else:
+        _lib.call_rp("sme_permute_csr_row_ptr", row_ptr, m.n_rows, ptr(m.d_row_ptr), ptr(inv_r), ptr(row_ptr),
+                     ptr(ws1), ws1.numel(), stream())
+        src_ptr, src_inv = m.d_row_ptr, inv_r
     long_nnz = m.long_row_nnz()
     ws2 = _cuda.workspace(_lib.query_size("sme_permute_csr_workspace_size", m.n_rows, m.nnz, long_nnz))
     col = torch.empty_like(m.d_col_idx)
@@ -396,9 +408,9 @@ def permute_csr(m: CsrMatrix, p_r: Permutation | None, p_c: Permutation | None) 
         if n_passes == n_slices:
             cmap = None
     _lib.call_rp("sme_permute_csr", row_ptr, _cuda.sme_dtype(m.d_values), m.n_rows, m.n_cols, m.nnz,
-                 ptr(m.d_row_ptr), ptr(src_col), ptr(m.d_values), ptr(inv_r), ptr(cmap), ptr(row_ptr), ptr(col),
+                 ptr(src_ptr), ptr(src_col), ptr(m.d_values), ptr(src_inv), ptr(cmap), ptr(row_ptr), ptr(col),
                  ptr(val), ptr(ws2), ws2.numel(), long_nnz, fl.flag_ptr, fl.dup_ptr, stream())
-    del src_col
+    del src_col, src_ptr
     out = CsrMatrix._from_device(m.n_rows, m.n_cols, row_ptr, col, val)
     out._cache["long_nnz"] = long_nnz
     return out
