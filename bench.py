@@ -1145,18 +1145,29 @@ def run_iterative(args, cfg) -> dict:
     n, nnz = A.n_rows, A.nnz
     iters, graph_steps = 1000, 50
     x0 = P.input_vector(0, n)
+    torch.cuda.Stream()  # process init (torch's stream pool), not per-matrix setup
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    p_r, p_c = device_perms(n, n)
-    t1 = time.perf_counter()
-    op = PermutedOperator(A, p_r, p_c, kernel=args.kernel)
-    torch.cuda.synchronize()
-    build_s = time.perf_counter() - t1
-    t2 = time.perf_counter()
-    op.fused_layout()  # the seg layout (cached on the matrix, reused by the run): part of the setup
-    torch.cuda.synchronize()
-    layout_s = time.perf_counter() - t2
-    perm_s = time.perf_counter() - t0
+
+    def setup():
+        """One permuted operator from scratch: ROW_COLUMN permutations (seed 7), the folded
+        permuted CSR (K4), its seg layout with the fused epilogue.  Wall clock with device
+        syncs, ms per piece."""
+        t0 = time.perf_counter()
+        p_r, p_c = device_perms(n, n)
+        t1 = time.perf_counter()
+        o = PermutedOperator(A, p_r, p_c, kernel=args.kernel)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        o.fused_layout()  # the seg layout (cached on the matrix, reused by the run)
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
+        return o, p_r, p_c, {"total_ms": round((t3 - t0) * 1e3, 2), "generation_ms": round((t1 - t0) * 1e3, 2),
+                             "permuted_csr_build_ms": round((t2 - t1) * 1e3, 2),
+                             "seg_layout_build_ms": round((t3 - t2) * 1e3, 2)}
+
+    _, _, _, setup_first = setup()  # the first matrix of the process (allocator growth, first uses)
+    op, p_r, p_c, setup_warm = setup()  # the steady-state cost of one more permuted matrix
+    perm_s = setup_warm["total_ms"] * 1e-3
 
     def run(operator) -> tuple[float, float, PowerIteration]:
         pi = PowerIteration(operator, x0)
@@ -1246,11 +1257,14 @@ def run_iterative(args, cfg) -> dict:
                      "vs_unpermuted": round(unperm_ms / unf_ms, 4), "vs_folded": round(perm_ms / unf_ms, 4),
                      "permuted_csr_build_ms": round(unf_build_s * 1e3, 2), "step": unf_step},
         "amortisation": {"permutation_setup_ms": round(perm_s * 1e3, 2),
-                         "of_which_generation_ms": round(HOST_PERM_S.get("native", 0.0) * 1e3, 2),
-                         "of_which_permuted_csr_build_ms": round(build_s * 1e3, 2),
-                         "of_which_seg_layout_build_ms": round(layout_s * 1e3, 2),
+                         "setup": setup_warm, "setup_first_in_process": setup_first,
+                         "setup_note": "permutations + folded permuted CSR + seg layout, wall clock with syncs; "
+                                       "'setup' = one more matrix in a running process (the per-matrix cost), "
+                                       "'setup_first_in_process' = the first one (allocator growth, first uses "
+                                       "of torch kernels; libsme's modules are preloaded at import)",
                          "permuted_1000_iter_ms": round(perm_ms, 3), "unpermuted_1000_iter_ms": round(unperm_ms, 3),
                          "permuted_total_ms": round(total_perm, 3),
+                         "setup_share_of_1000_iter": round(perm_s * 1e3 / perm_ms, 4),
                          "break_even_note": "setup is paid once; per-iteration ratio permuted/unpermuted = "
                                             f"{perm_ms / unperm_ms:.3f}"},
         "x_norm_check": float(torch.linalg.vector_norm(x_p).item()),
