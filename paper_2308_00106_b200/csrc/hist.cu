@@ -550,7 +550,8 @@ SME_API int sme_hist2d_coo(int64_t n_rows, int64_t n_cols, int64_t nnz, const in
   int rc;
   if ((rc = check_bins(n_rows, bins_r, "row")) != SME_OK) return rc;
   if ((rc = check_bins(n_cols, bins_c, "column")) != SME_OK) return rc;
-  SME_REQUIRE(nnz >= 0 && nnz < INT32_MAX && n_rows < INT32_MAX && n_cols < INT32_MAX, "sizes exceed int32");
+  // entry positions are int64 (COO triplets of any count); row / column ids int32
+  SME_REQUIRE(nnz >= 0 && n_rows < INT32_MAX && n_cols < INT32_MAX, "sizes exceed int32");
   if (nnz == 0) return SME_OK;
   cudaStream_t s = as_stream(stream);
   Binner rb = make_binner(n_rows, bins_r), cb = make_binner(n_cols, bins_c);
