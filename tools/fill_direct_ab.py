@@ -25,7 +25,7 @@ torch.cuda.empty_cache()
 Pn = auto_seg_panels(B)
 ref = None
 for rep in range(3):
-    for direct in ((1, 2, 3, 0) if cfg == 'c4' else (1, 0)):
+    for direct in (1, 0):
         _lib.call("sme_seg_set_fill_direct", direct)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
