@@ -264,12 +264,6 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
   __shared__ int64_t c_off[32];
   int ppow = 1;  // smallest power of two >= P (steps of the panel search)
   while (ppow < P) ppow <<= 1;
-  // SegLayout's bounds are uniform (b_p = p * n_cols / P): an entry's panel is then
-  // floor(c * P / n_cols) up to one step of float rounding, fixed by one compare each way
-  // (C4: the 5-step bound search was a quarter of the fill's instructions)
-  const int32_t n_cols_all = bounds[P];
-  const bool uniform = __all_sync(FULL, lane > P || bounds[lane] == (int32_t)((int64_t)lane * n_cols_all / P));
-  const float pinv = (float)P / (float)max(1, n_cols_all);
   const int32_t my_hi = lane < P ? bounds[lane + 1] : INT32_MAX;
   const int32_t my_lo = lane < P ? bounds[lane] : 0;
   const int64_t my_off = lane < P ? offsets[lane] : 0;
@@ -442,16 +436,11 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
           row_at += __popc(m) + (__any_sync(FULL, my_start == base + 32) ? 1 : 0);
           if (k < k1) {
             const int32_t cc = c[u];
+            // panel: branchless search of the (INT32_MAX-padded) upper bounds
             int p = 0;
-            if (uniform) {
-              p = min(P - 1, __float2int_rz(__int2float_rn(cc) * pinv));
-              if (cc < c_lo[p]) --p;
-              else if (cc >= c_hi[p]) ++p;
-            } else {  // branchless search of the (INT32_MAX-padded) upper bounds
 #pragma unroll
-              for (int st = 16; st > 0; st >>= 1)
-                if (st < ppow && cc >= c_hi[p + st - 1]) p += st;
-            }
+            for (int st = 16; st > 0; st >>= 1)
+              if (st < ppow && cc >= c_hi[p + st - 1]) p += st;
             const int4 tb = s_tab[p * 32 + rr];
             const int4 pp = s_pp[p];
             const int32_t dip = tb.w + k;  // slot within the panel
