@@ -241,6 +241,10 @@ int sme_csr_compact(int dtype, int64_t n_rows, const int32_t* d_row_ptr, const i
                     int32_t cap, const int32_t* d_out_row_ptr, int32_t* d_out_col, void* d_out_val,
                     sme_stream_t stream);
 
+/* Column span col[last] - col[first] of n_samples evenly spaced rows (row i*(n_rows-1)/(n_samples-1)),
+ * -1 for rows with fewer than 2 entries: the banded-structure probe of the kernel policy. */
+int sme_row_spans(int64_t n_rows, const int32_t* d_row_ptr, const int32_t* d_col, int32_t n_samples,
+                  int32_t* d_out, sme_stream_t stream);
 /* Row-length statistics for kernel selection: out[0] = max row length, out[1] = empty rows. */
 int sme_row_stats(int64_t n_rows, const int32_t* d_row_ptr, int64_t* d_out, sme_stream_t stream);
 
@@ -572,6 +576,8 @@ int sme_permute_csr_row_ptr_starts_i64(int64_t n_rows, const int64_t* d_row_ptr,
                                        sme_stream_t stream);
 int sme_long_row_nnz_i64(int64_t n_rows, const int64_t* d_row_ptr, int64_t* d_out, sme_stream_t stream);
 int sme_row_stats_i64(int64_t n_rows, const int64_t* d_row_ptr, int64_t* d_out, sme_stream_t stream);
+int sme_row_spans_i64(int64_t n_rows, const int64_t* d_row_ptr, const int32_t* d_col, int32_t n_samples,
+                      int32_t* d_out, sme_stream_t stream);
 int sme_csr_validate_i64(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* d_row_ptr,
                          const int32_t* d_col, int32_t* d_flag, sme_stream_t stream);
 int sme_csr_expand_rows_i64(int64_t n_rows, const int64_t* d_row_ptr, int32_t* d_row_out,

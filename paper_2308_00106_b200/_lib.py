@@ -64,6 +64,7 @@ SIGNATURES: dict[str, list] = {
     "sme_map_cols_sliced_partial": [i64, i64, p, p, p, i32, i32, p],
     "sme_csr_validate": [i64, i64, i64, p, p, p, p],
     "sme_row_stats": [i64, p, p, p],
+    "sme_row_spans": [i64, p, p, i32, p, p],
     "sme_csr_expand_rows": [i64, p, p, p],
     "sme_hist2d_csr": [i64, i64, i64, p, p, i32, i32, p, p],
     "sme_hist2d_coo": [i64, i64, i64, p, p, i32, i32, p, p],
@@ -137,7 +138,7 @@ SIGNATURES: dict[str, list] = {
 WIDE_ENTRY_POINTS = (
     "sme_coo_row_ptr", "sme_coo_to_csr", "sme_permute_csr_row_ptr", "sme_permute_csr_row_ptr_starts",
     "sme_permute_csr", "sme_long_row_nnz",
-    "sme_row_stats", "sme_csr_validate", "sme_csr_expand_rows", "sme_hist2d_csr", "sme_row_hist_csr",
+    "sme_row_stats", "sme_row_spans", "sme_csr_validate", "sme_csr_expand_rows", "sme_hist2d_csr", "sme_row_hist_csr",
     "sme_seg_positions", "sme_seg_fill", "sme_spmv_vector",
 )
 for _n in WIDE_ENTRY_POINTS:

@@ -613,6 +613,18 @@ __global__ void k_row_stats(int64_t n_rows, const IP* __restrict__ ptr, unsigned
   }
 }
 
+// Column span (last - first column) of n_samples evenly spaced rows (-1 for rows with < 2
+// entries): the banded-structure probe of the kernel policy (kernels.banded).
+template <typename IP>
+__global__ void k_row_spans(int64_t n_rows, const IP* __restrict__ ptr, const int32_t* __restrict__ col,
+                            int32_t n_samples, int32_t* __restrict__ out) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_samples; i += gridDim.x * blockDim.x) {
+    const int64_t r = n_samples > 1 ? (int64_t)i * (n_rows - 1) / (n_samples - 1) : 0;
+    const IP a = ptr[r], b = ptr[r + 1];
+    out[i] = b - a >= 2 ? col[b - 1] - col[a] : -1;
+  }
+}
+
 template <typename IP>
 __global__ void k_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const IP* __restrict__ ptr,
                                const int32_t* __restrict__ col, int32_t* flag) {
@@ -1047,6 +1059,25 @@ static int row_stats_impl(int64_t n_rows, const IP* row_ptr, int64_t* out, sme_s
   k_row_stats<IP><<<grid_for(n_rows, 256, 4), 256, 0, s>>>(n_rows, row_ptr, (unsigned long long*)out);
   SME_CHECK_LAUNCH("k_row_stats");
   return SME_OK;
+}
+
+template <typename IP>
+static int row_spans_impl(int64_t n_rows, const IP* row_ptr, const int32_t* col, int32_t n_samples, int32_t* out,
+                          sme_stream_t stream) {
+  SME_REQUIRE(n_rows >= 1 && n_samples >= 1, "bad arguments");
+  k_row_spans<IP><<<(n_samples + 255) / 256, 256, 0, as_stream(stream)>>>(n_rows, row_ptr, col, n_samples, out);
+  SME_CHECK_LAUNCH("k_row_spans");
+  return SME_OK;
+}
+
+SME_API int sme_row_spans(int64_t n_rows, const int32_t* row_ptr, const int32_t* col, int32_t n_samples, int32_t* out,
+                          sme_stream_t stream) {
+  return row_spans_impl(n_rows, row_ptr, col, n_samples, out, stream);
+}
+
+SME_API int sme_row_spans_i64(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, int32_t n_samples,
+                              int32_t* out, sme_stream_t stream) {
+  return row_spans_impl(n_rows, row_ptr, col, n_samples, out, stream);
 }
 
 SME_API int sme_row_stats(int64_t n_rows, const int32_t* row_ptr, int64_t* out, sme_stream_t stream) {

@@ -109,18 +109,19 @@ def banded(m: CsrMatrix, samples: int = 4096) -> bool:
     """True when sampled rows span a small column window (median last-first column
     <= n_cols / 256): x gathers then coalesce and the CSR-vector kernel wins
     (C5 unpermuted: 'vector' 610 GFLOP/s vs 'seg' 497).  Rows are column-sorted,
-    so each sampled row costs two index loads; cached."""
+    so each sampled row costs two index loads (sme_row_spans); cached."""
     if "banded" not in m._cache:
-        dev = m.d_row_ptr.device
-        r = torch.linspace(0, max(0, m.n_rows - 1), min(samples, max(1, m.n_rows)), device=dev).long()
-        a, b = m.d_row_ptr[r].long(), m.d_row_ptr[r + 1].long()
-        ok = b - a >= 2
-        if m.nnz == 0 or not bool(ok.any()):
-            m._cache["banded"] = True
-        else:
-            lo = m.d_col_idx[a[ok]].long()
-            hi = m.d_col_idx[b[ok] - 1].long()
-            m._cache["banded"] = bool((hi - lo).float().median() <= m.n_cols / 256)
+        spans = np.zeros(0, dtype=np.int32)
+        if m.nnz and m.n_rows:
+            s = min(samples, m.n_rows)
+            out = torch.empty(s, dtype=torch.int32, device=m.d_row_ptr.device)
+            _lib.call_rp("sme_row_spans", m.d_row_ptr, m.n_rows, ptr(m.d_row_ptr), ptr(m.d_col_idx), s, ptr(out),
+                         stream())
+            spans = out.cpu().numpy()
+            spans = spans[spans >= 0]
+        # torch's median of an even count is the lower middle value
+        m._cache["banded"] = (True if spans.size == 0
+                              else bool(np.sort(spans)[(spans.size - 1) // 2] <= m.n_cols / 256))
     return m._cache["banded"]
 
 
