@@ -275,6 +275,9 @@ int sme_hist2d_set_mode(int mode);
 /* Row-sort keys of the CSR builds (process-wide; tests): 1 = 32-bit (mapped col << 5 |
  * slot) whenever n_cols <= 2^27 (default), 0 = always 64-bit (col << 32 | slot). */
 int sme_sort_rows_set_key32(int enable);
+/* Test hook: 1 (default) sorts rows of 257..SME_SORT_SMEM_MAX entries with the CTA-wide
+ * register / shuffle / shared-memory bitonic network; 0 = all in shared memory. */
+int sme_sort_rows_set_cta(int enable);
 /* Rows with 32 < len <= 512 of the CSR builds (process-wide; tests): 1 = one warp per
  * row, keys in registers (default), 0 = one CTA per row, bitonic in shared memory. */
 int sme_sort_rows_set_wmed(int enable);

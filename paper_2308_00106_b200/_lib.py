@@ -71,6 +71,7 @@ SIGNATURES: dict[str, list] = {
     "sme_hist2d_set_mode": [C.c_int],
     "sme_sort_rows_set_wmed": [C.c_int],
     "sme_sort_rows_set_key32": [C.c_int],
+    "sme_sort_rows_set_cta": [C.c_int],
     "sme_hist2d_set_variant": [C.c_int],
     "sme_row_hist_csr": [i64, p, i32, p, p],
     "sme_entropy": [i64, p, f64, p, p, p],

@@ -28,10 +28,12 @@ constexpr int SORT_NT = 256;
 constexpr int LONG_NT = 512;
 
 struct SortLists {
-  int32_t* med;       // [n_rows] row ids with 32 < len <= SMEM_MAX
+  int32_t* med;       // [n_rows] row ids with 32 < len <= big_min (warp-wide register sort)
+  int32_t* big;       // [n_rows] row ids with big_min < len <= SMEM_MAX (one CTA per row)
   int32_t* lng;       // [n_rows] row ids with len > SMEM_MAX
   int64_t* lng_off;   // [n_rows] offset of each long row in the long scratch
-  int32_t* counters;  // [0] = #med, [1] = #long
+  int32_t* counters;  // [0] = #med, [1] = #long, [2] = #big
+  int big_min;        // the warp sort's largest row (rows above go to `big`)
   unsigned long long* lng_cursor;  // running long scratch offset
   uint64_t* scratch_a;             // long_nnz keys
   uint64_t* scratch_b;             // long_nnz keys
@@ -39,12 +41,13 @@ struct SortLists {
 };
 
 inline size_t lists_bytes(int64_t n_rows, int64_t long_nnz) {
-  return align_up(n_rows * 4) * 2 + align_up(n_rows * 8) + align_up(64) + align_up(long_nnz * 8) * 2;
+  return align_up(n_rows * 4) * 3 + align_up(n_rows * 8) + align_up(64) + align_up(long_nnz * 8) * 2;
 }
 
 inline SortLists carve_lists(char* p, int64_t n_rows, int64_t long_nnz) {
   SortLists L;
   L.med = (int32_t*)p;           p += align_up(n_rows * 4);
+  L.big = (int32_t*)p;           p += align_up(n_rows * 4);
   L.lng = (int32_t*)p;           p += align_up(n_rows * 4);
   L.lng_off = (int64_t*)p;       p += align_up(n_rows * 8);
   L.counters = (int32_t*)p;
@@ -53,6 +56,7 @@ inline SortLists carve_lists(char* p, int64_t n_rows, int64_t long_nnz) {
   L.scratch_a = (uint64_t*)p;    p += align_up(long_nnz * 8);
   L.scratch_b = (uint64_t*)p;
   L.mark_dups = 0;
+  L.big_min = 32;
   return L;
 }
 
@@ -95,6 +99,9 @@ static int g_sort_key32 = 1;
 // 1: rows with 32 < len <= WMED_MAX are sorted warp-wide in registers (default); 0: by the
 // CTA-wide shared-memory kernel (A/B and tests of that path)
 static int g_sort_wmed = 3;  // rows 33..256 (C3 K4: 26.2 -> 20.0 ms; 512 spills: 27.8)
+// 1: rows of 257..SME_SORT_SMEM_MAX entries sorted by the register/shuffle/smem hybrid
+// network (default); 0: the all-shared-memory bitonic (A/B and tests of that path)
+static int g_sort_cta = 1;
 
 // Keys: 64-bit (mapped col << 32 | slot) in general; 32-bit (mapped col << 5 |
 // slot) when every mapped column is < 2^27 (KEY32: one shuffle per exchange
@@ -261,9 +268,12 @@ __global__ void __launch_bounds__(TILE_NT) k_sort_rows_warp(
     int32_t len = (int32_t)(n1 - n0);
     const int64_t my_from = from;
     if (len > 32) {
-      if (len <= SME_SORT_SMEM_MAX) {
+      if (len <= L.big_min) {
         int slot = atomicAdd(&L.counters[0], 1);
         L.med[slot] = r;
+      } else if (len <= SME_SORT_SMEM_MAX) {
+        int slot = atomicAdd(&L.counters[2], 1);
+        L.big[slot] = r;
       } else {
         int slot = atomicAdd(&L.counters[1], 1);
         L.lng[slot] = r;
@@ -409,26 +419,108 @@ __device__ void smem_bitonic(uint64_t* s, int P) {
   }
 }
 
-// rows with 32 < len <= SME_SORT_SMEM_MAX: one CTA per row
+// CTA-wide bitonic sort of N = SORT_NT * E keys held E per thread in registers (blocked:
+// thread t holds elements t*E .. t*E+E-1).  Steps with j < E are compare-exchanges inside a
+// thread, j < 32*E one shuffle per key inside a warp, and only the j >= 32*E steps (6 of
+// the 55 at N = 1024) go through shared memory with barriers — instead of a barrier after
+// every one of the N log^2 N / 2 steps (smem_bitonic).
+template <int E, int J>
+__device__ __forceinline__ void cta_bitonic_local(uint64_t (&v)[E], int base, int k) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if ((e & J) == 0) {
+      const bool asc = ((base + e) & k) == 0;
+      const uint64_t a = v[e], b = v[e | J];
+      if ((a > b) == asc) {
+        v[e] = b;
+        v[e | J] = a;
+      }
+    }
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void cta_bitonic(uint64_t (&v)[E], uint64_t* s) {
+  constexpr int N = SORT_NT * E;
+  const int tid = threadIdx.x, base = tid * E;
+  for (int k = 2; k <= N; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32 * E) {  // partner in another warp
+#pragma unroll
+        for (int e = 0; e < E; ++e) s[base + e] = v[e];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = base + e;
+          const uint64_t o = s[i ^ j];
+          const bool asc = (i & k) == 0, lower = (i & j) == 0;
+          v[e] = (lower == asc) ? (v[e] < o ? v[e] : o) : (v[e] < o ? o : v[e]);
+        }
+        __syncthreads();
+      } else if (j >= E) {  // partner in another lane of this warp
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = base + e;
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, v[e], j / E);
+          const bool asc = (i & k) == 0, lower = (i & j) == 0;
+          v[e] = (lower == asc) ? (v[e] < o ? v[e] : o) : (v[e] < o ? o : v[e]);
+        }
+      } else if (j == 1) {
+        cta_bitonic_local<E, 1>(v, base, k);
+      } else if (j == 2) {
+        if constexpr (E > 2) cta_bitonic_local<E, 2>(v, base, k);
+      } else if (j == 4) {
+        if constexpr (E > 4) cta_bitonic_local<E, 4>(v, base, k);
+      } else if (j == 8) {
+        if constexpr (E > 8) cta_bitonic_local<E, 8>(v, base, k);
+      }
+    }
+  }
+}
+
+template <int E, typename T>
+__device__ __forceinline__ void sort_row_cta(int32_t len, int64_t from, const int32_t* __restrict__ src_col,
+                                             const int32_t* __restrict__ cmap, uint64_t* s) {
+  uint64_t v[E];
+  const int base = threadIdx.x * E;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = base + e;
+    v[e] = i < len ? (((uint64_t)map_col(cmap, src_col[from + i]) << 32) | (uint32_t)i) : ~0ull;
+  }
+  cta_bitonic<E>(v, s);
+#pragma unroll
+  for (int e = 0; e < E; ++e) s[base + e] = v[e];
+  __syncthreads();
+}
+
+// rows with 32 < len <= SME_SORT_SMEM_MAX: one CTA per row (rows of > 256 entries: the
+// register / shuffle / shared-memory hybrid network; C3 R-MAT rows 257..1024)
 template <typename T, class Src, typename IP>
 __global__ void __launch_bounds__(SORT_NT) k_sort_rows_block(
     const IP* __restrict__ new_ptr, Src src, const int32_t* __restrict__ src_col,
     const T* __restrict__ src_val, const int32_t* __restrict__ cmap, int32_t* __restrict__ out_col,
-    T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key, int wmed_max) {
+    T* __restrict__ out_val, SortLists L, int32_t* flag, unsigned long long* dup_key, int wmed_max, int use_cta) {
   __shared__ uint64_t s[SME_SORT_SMEM_MAX];
-  const int count = L.counters[0];
+  const int count = L.counters[2];
   for (int it = blockIdx.x; it < count; it += gridDim.x) {
-    const int32_t r = L.med[it];
+    const int32_t r = L.big[it];
     const int64_t dst = new_ptr[r];
     const int32_t len = (int32_t)(new_ptr[r + 1] - dst);
-    if (len <= wmed_max) continue;  // k_sort_rows_wmed
     const int64_t from = src.start(r, dst);
     int P = 64;
     while (P < len) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += SORT_NT)
-      s[i] = i < len ? (((uint64_t)map_col(cmap, src_col[from + i]) << 32) | (uint32_t)i) : ~0ull;
-    __syncthreads();
-    smem_bitonic<SORT_NT>(s, P);
+    if (P >= 2 * SORT_NT && use_cta) {
+      if (P == 2 * SORT_NT) sort_row_cta<2, T>(len, from, src_col, cmap, s);
+      else if (P == 4 * SORT_NT) sort_row_cta<4, T>(len, from, src_col, cmap, s);
+      else if (P == 8 * SORT_NT) sort_row_cta<8, T>(len, from, src_col, cmap, s);
+      else sort_row_cta<16, T>(len, from, src_col, cmap, s);
+    } else {
+      for (int i = threadIdx.x; i < P; i += SORT_NT)
+        s[i] = i < len ? (((uint64_t)map_col(cmap, src_col[from + i]) << 32) | (uint32_t)i) : ~0ull;
+      __syncthreads();
+      smem_bitonic<SORT_NT>(s, P);
+    }
     for (int i = threadIdx.x; i < len; i += SORT_NT) {
       uint64_t v = s[i];
       uint32_t key = (uint32_t)(v >> 32);
@@ -673,6 +765,9 @@ int launch_sorts(int64_t n_rows, const IP* new_ptr, Src src, const int32_t* src_
                  uint64_t* dup_key, cudaStream_t s, int64_t n_cols = INT32_MAX) {
   int64_t groups = (n_rows + 31) / 32;
   int blocks = grid_for(groups * 32, TILE_NT, 16);
+  // rows up to the warp sort's limit go to its list, longer ones (<= SMEM_MAX) to the CTA
+  // sort's: each kernel walks only its own rows
+  L.big_min = g_sort_wmed > 0 ? 32 << g_sort_wmed : 32;
   if (n_cols <= ((int64_t)1 << 27) && g_sort_key32)  // mapped columns < 2^27: 32-bit keys (col << 5 | slot)
     k_sort_rows_warp<T, Src, true, IP><<<blocks, TILE_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
                                                                cmap, out_col, out_val, L, flag,
@@ -691,7 +786,7 @@ int launch_sorts(int64_t n_rows, const IP* new_ptr, Src src, const int32_t* src_
   }
   k_sort_rows_block<T, Src, IP><<<sm_count() * 4, SORT_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
                                                                 out_val, L, flag, (unsigned long long*)dup_key,
-                                                                wmed_max);
+                                                                wmed_max, g_sort_cta);
   SME_CHECK_LAUNCH("k_sort_rows_block");
   k_sort_rows_long<T, Src, IP><<<sm_count(), LONG_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
                                                            out_val, L, flag, (unsigned long long*)dup_key);
@@ -1187,6 +1282,11 @@ SME_API int sme_csr_compact(int dtype, int64_t n_rows, const int32_t* row_ptr, c
 SME_API int sme_sort_rows_set_wmed(int level) {
   SME_REQUIRE(level >= 0 && level <= 4, "level must lie in [0, 4]");
   g_sort_wmed = level;
+  return SME_OK;
+}
+
+SME_API int sme_sort_rows_set_cta(int enable) {
+  g_sort_cta = enable != 0;
   return SME_OK;
 }
 

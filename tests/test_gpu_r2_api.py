@@ -184,3 +184,48 @@ def test_warp_medium_row_sort_equals_block_sort_and_oracle(dtype):
     c = P.coo_to_csr(coo)
     assert torch.equal(c.d_col_idx, a.d_col_idx) and torch.equal(c.d_values.view(torch.uint8),
                                                                   a.d_values.view(torch.uint8))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_cta_hybrid_row_sort_equals_smem_sort_and_oracle(dtype):
+    """K4 rows of 257..4096 entries take the CTA-wide register / shuffle / shared-memory
+    bitonic network (E = 2..16 keys per thread); it must equal the all-shared-memory sort
+    bit for bit and the oracle, on the CSR (gathered source) and the COO (staged) paths,
+    including a duplicate reported like the reference's lexsort would."""
+    from paper_2308_00106_b200 import _lib
+
+    rng = np.random.default_rng(4)
+    n = 6000
+    lens = np.concatenate([[257, 300, 511, 512, 513, 1000, 1023, 1024, 1025, 2047, 2048, 2049, 3000, 4095, 4096],
+                           rng.integers(257, 4097, 60), rng.integers(0, 40, 2000)])
+    lens = np.concatenate([lens, np.zeros(n - lens.size, dtype=lens.dtype)])
+    rng.shuffle(lens)
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    col = np.concatenate([np.sort(rng.choice(n, size=int(l), replace=False)) for l in lens])
+    val = rng.standard_normal(col.size).astype(dtype)
+    A = P.CsrMatrix(n, n, ptr, col, val)
+    fr, fc = rng.permutation(n), rng.permutation(n)
+    outs = []
+    for cta in (1, 0):
+        _lib.call("sme_sort_rows_set_cta", cta)
+        try:
+            outs.append(P.permute_csr(A, P.Permutation(fr), P.Permutation(fc)))
+        finally:
+            _lib.call("sme_sort_rows_set_cta", 1)
+    a, b = outs
+    assert torch.equal(a.d_row_ptr, b.d_row_ptr) and torch.equal(a.d_col_idx, b.d_col_idx)
+    assert torch.equal(a.d_values.view(torch.uint8), b.d_values.view(torch.uint8))
+    pr, pc = O.permute_coo(O.csr_to_coo_rows(ptr), col, fr, fc)
+    ptr_o, col_o, val_o = O.coo_to_csr(n, pr, pc, val.astype(np.float64))
+    assert np.array_equal(a.row_ptr, ptr_o) and np.array_equal(a.col_idx, col_o)
+    assert np.array_equal(a.values, val_o)
+    c = P.coo_to_csr(P.CooMatrix(n, n, pr, pc, val))
+    assert torch.equal(c.d_col_idx, a.d_col_idx)
+    # a duplicate inside a long row: the reference's first duplicate in lexsort order
+    r_long = int(np.argmax(lens))
+    rows_d = np.append(pr, pr[ptr[r_long]])
+    cols_d = np.append(pc, pc[ptr[r_long]])
+    vals_d = np.append(val, val[0])
+    with pytest.raises(ValueError, match="duplicate"):
+        P.CooMatrix(n, n, rows_d, cols_d, vals_d)
