@@ -86,32 +86,57 @@ static __global__ void __launch_bounds__(1024) k_scan_tile_offsets(int64_t n_til
   if (threadIdx.x == 0) tile_sums[n_tiles] = carry;
 }
 
-// out[k] = exclusive prefix (k < n); out[n] = total.  Items are thread-strided
-// (coalesced) inside a tile: item i of thread t is k = base + i*NT + t, so the
-// scan order within the tile is item-major — handled by scanning each item
-// column across the block in turn.
+// out[k] = exclusive prefix (k < n); out[n] = total.  The tile's items are loaded coalesced
+// (item i of thread t is k = base + i*NT + t) into shared memory, each thread then scans its
+// SCAN_IPT consecutive items in registers, one block-wide scan adds the thread offsets, and
+// the positions leave through shared memory with coalesced stores.  (The previous version
+// ran SCAN_IPT block-wide scans per tile, each with its barriers: 219 us per 50M-row scan at
+// 1.6 TB/s, latency-bound.)
+__device__ __forceinline__ int scan_pad(int i) { return i + (i >> 5); }  // bank-conflict padding
+
 template <class LenFn, typename OutT>
 __global__ void __launch_bounds__(SCAN_NT) k_scan_apply(int64_t n, LenFn len, const int64_t* tile_offsets,
                                                         OutT* out, int32_t* flag) {
   constexpr bool NARROW = sizeof(OutT) == 4;
+  constexpr int SLOTS = SCAN_TILE + SCAN_TILE / 32;
+  __shared__ __align__(16) unsigned char s_buf[SLOTS * sizeof(OutT) > SLOTS * 4 ? SLOTS * sizeof(OutT) : SLOTS * 4];
   __shared__ int64_t s_total;
-  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
-  int64_t run = tile_offsets[blockIdx.x];
-#pragma unroll 1
+  int32_t* s_len = reinterpret_cast<int32_t*>(s_buf);
+  OutT* s_out = reinterpret_cast<OutT*>(s_buf);
+  const int t = threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+#pragma unroll
   for (int i = 0; i < SCAN_IPT; ++i) {
-    int64_t k = base + (int64_t)i * SCAN_NT + threadIdx.x;
-    int64_t v = k < n ? len(k) : 0;
-    int64_t ex = block_exclusive_scan<SCAN_NT>(v, &s_total);
-    __syncthreads();
-    int64_t pos = run + ex;
-    if (k < n) {
-      if (NARROW && pos > INT32_MAX && flag) atomicOr(flag, SME_FLAG_RANGE);
-      out[k] = (OutT)pos;
-    }
-    run += s_total;
-    __syncthreads();
+    const int64_t k = base + (int64_t)i * SCAN_NT + t;
+    s_len[scan_pad(i * SCAN_NT + t)] = k < n ? (int32_t)len(k) : 0;
   }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+  __syncthreads();
+  int32_t v[SCAN_IPT];
+  int64_t tot = 0;
+#pragma unroll
+  for (int j = 0; j < SCAN_IPT; ++j) {
+    v[j] = s_len[scan_pad(t * SCAN_IPT + j)];
+    tot += v[j];
+  }
+  const int64_t off = tile_offsets[blockIdx.x] + block_exclusive_scan<SCAN_NT>(tot, &s_total);
+  __syncthreads();  // every s_len read is done before s_out overwrites the buffer
+  int64_t run = off;
+  bool over = false;
+#pragma unroll
+  for (int j = 0; j < SCAN_IPT; ++j) {
+    over |= NARROW && run > INT32_MAX;
+    s_out[scan_pad(t * SCAN_IPT + j)] = (OutT)run;
+    run += v[j];
+  }
+  if (over && flag) atomicOr(flag, SME_FLAG_RANGE);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < SCAN_IPT; ++i) {
+    const int64_t k = base + (int64_t)i * SCAN_NT + t;
+    if (k < n) out[k] = s_out[scan_pad(i * SCAN_NT + t)];
+  }
+  if (blockIdx.x == gridDim.x - 1 && t == SCAN_NT - 1) {
+    // the last thread's run is the grand total (items past n contribute 0)
     if (NARROW && run > INT32_MAX && flag) atomicOr(flag, SME_FLAG_RANGE);
     out[n] = (OutT)run;
   }
