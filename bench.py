@@ -680,7 +680,9 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
                                        y_cpu=None if cpu is None else cpu.pop("_y"), R=R)
             log(f"[bench] parity: {parity}")
             del par_in, sample
-        un_total, un_per = timed(A, x, args.kernel, args.steps, args.warmup)
+        # the same untimed preload as the permuted loop: both loops start from the power-capped
+        # steady state (after the parity leg's CPU work the GPU has cooled and clocks up)
+        un_total, un_per = timed(A, x, args.kernel, args.steps, args.warmup, preload_s=1.0)
         # the same comparison with the two matrices alternating step by step (no clock/thermal drift
         # between two separate loops): medians of per-step events
         yb_, ya_ = torch.empty(n, dtype=B.dtype, device=dev), torch.empty(n, dtype=A.dtype, device=dev)
