@@ -48,7 +48,8 @@ def require_cuda() -> torch.device:
     if dev not in _PRELOADED:  # once per device: load libsme's kernel modules up front
         _PRELOADED.add(dev)
         torch.zeros(1, device=f"cuda:{dev}")  # the context exists
-        _lib.call("sme_preload")
+        # an optimisation only: a module that fails here fails loudly at its first launch
+        _lib.load().sme_preload()
     return torch.device("cuda", dev)
 
 
