@@ -81,7 +81,24 @@ class Permutation:
     def __eq__(self, other) -> bool:
         if not isinstance(other, Permutation):
             return NotImplemented
-        return self.n == other.n and torch.equal(self.d_forward, other.d_forward)
+        if self is other:
+            return True
+        if self.n != other.n:
+            return False
+        if self.n == 0:
+            return True
+        # different content hashes (one libsme pass each) settle the common case; equal
+        # hashes are confirmed element by element
+        if self._content_hash() != other._content_hash():
+            return False
+        return torch.equal(self.d_forward, other.d_forward)
+
+    def _content_hash(self) -> int:
+        if getattr(self, "_hash", None) is None:
+            out = torch.empty(1, dtype=torch.int64, device=self.d_forward.device)
+            _lib.call("sme_hash64", ptr(self.d_forward), self.d_forward.numel() * 4, 0x5EED, ptr(out), stream())
+            self._hash = int(out.item())
+        return self._hash
 
     __hash__ = object.__hash__
 
