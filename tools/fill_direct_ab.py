@@ -12,8 +12,8 @@ from paper_2308_00106_b200 import _lib, synth
 from paper_2308_00106_b200.seg import SegLayout, auto_seg_panels
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
-if cfg == "c4":
-    n = 50_000_000
+if cfg in ("c4", "c4w"):
+    n = 50_000_000 if cfg == "c4" else 108_000_000
     A = synth.random_rows(n, n, 20)
     B = P.permute_csr(A, P.random_permutation(n, 1), P.random_permutation(n, 2))
 else:
@@ -24,7 +24,7 @@ del A
 torch.cuda.empty_cache()
 Pn = auto_seg_panels(B)
 ref = None
-for rep in range(3):
+for rep in range(3 if cfg != 'c4w' else 2):
     for direct in (1, 0):
         _lib.call("sme_seg_set_fill_direct", direct)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
