@@ -12,6 +12,7 @@ is an sm_100a kernel (perm.cu, csr_build.cu).
 
 from __future__ import annotations
 
+import threading
 from enum import Enum
 
 import numpy as np
@@ -189,8 +190,26 @@ def pcg64_swap_partners(bitgen: np.random.PCG64, n: int, out: np.ndarray | None 
 GPU_PARTNERS_MIN = 1 << 20
 
 
+_SIDE_STREAMS: dict = {}
+_SIDE_LOCK = threading.Lock()
+
+
+def _side_stream(dev: torch.device, slot) -> torch.cuda.Stream:
+    """A long-lived side stream per (device, slot).  Work is stream-ordered, so sharing one
+    between callers only serialises them; reusing it lets torch's caching allocator, whose
+    blocks belong to the stream that allocated them, hand back the same scratch every call
+    (a fresh stream per call meant fresh cudaMallocs: C4 permutation pairs 22-134 ms)."""
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), slot)
+    with _SIDE_LOCK:
+        st = _SIDE_STREAMS.get(key)
+        if st is None:
+            st = _SIDE_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return st
+
+
 def pcg64_swap_partners_device(bitgen: np.random.PCG64, n: int, threads: int = 0,
-                               out: torch.Tensor | None = None, gpu_min: int | None = None) -> torch.Tensor:
+                               out: torch.Tensor | None = None, gpu_min: int | None = None,
+                               slot: int = 0) -> torch.Tensor:
     """pcg64_swap_partners straight into a CUDA int32 tensor.  From GPU_PARTNERS_MIN on
     they are drawn on the GPU (sme_pcg64_swap_partners_gpu: parallel PCG64 stream, draws
     decided in parallel inside statistical step windows, the few ambiguous ones in order
@@ -201,7 +220,7 @@ def pcg64_swap_partners_device(bitgen: np.random.PCG64, n: int, threads: int = 0
         raise ValueError("permutation size must be in [1, 2^31)")
     dev = _cuda.require_cuda()
     d_j = torch.empty(n, dtype=torch.int32, device=dev) if out is None else out
-    cs = torch.cuda.Stream(device=dev)
+    cs = _side_stream(dev, ("partners", slot))
     cs.wait_stream(torch.cuda.current_stream(dev))  # d_j's allocation is ordered before the copies
     words = _pcg64_words(bitgen)
     if n >= (GPU_PARTNERS_MIN if gpu_min is None else gpu_min) and n >= 2:
@@ -281,10 +300,10 @@ def random_permutations(specs) -> list[Permutation]:
 
     def one(k):
         (n, seed), (d_j, perm, ws) = specs[k], bufs[k]
-        s = torch.cuda.Stream(device=dev)
+        s = _side_stream(dev, ("axis", k))
         s.wait_stream(main)
         with torch.cuda.stream(s):
-            pcg64_swap_partners_device(np.random.PCG64(seed), n, threads=threads, out=d_j)
+            pcg64_swap_partners_device(np.random.PCG64(seed), n, threads=threads, out=d_j, slot=k)
             _lib.call("sme_fy_apply", n, ptr(d_j), ptr(perm), ptr(ws), ws.numel(), stream())
         s.synchronize()
 
