@@ -726,12 +726,15 @@ def run_ours(args, cfg, rank: int, world: int) -> dict | None:
         for _ in range(2):
             _lib.call("sme_diag_gather", _ptr(gx), gx.numel(), gblocks, gper, 1, _ptr(gout), _stream())
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record()
-        for _ in range(5):
-            _lib.call("sme_diag_gather", _ptr(gx), gx.numel(), gblocks, gper, 1, _ptr(gout), _stream())
-        g1.record()
-        torch.cuda.synchronize()
-        ceil_gps = gblocks * 256 * gper / (g0.elapsed_time(g1) / 5 * 1e-3)
+        g_ms = []
+        for _ in range(3):  # best of three: one C5 run's single sample read 187 G/s against 287 elsewhere
+            g0.record()
+            for _ in range(5):
+                _lib.call("sme_diag_gather", _ptr(gx), gx.numel(), gblocks, gper, 1, _ptr(gout), _stream())
+            g1.record()
+            torch.cuda.synchronize()
+            g_ms.append(g0.elapsed_time(g1) / 5)
+        ceil_gps = gblocks * 256 * gper / (min(g_ms) * 1e-3)
         ach_gps = nnz / (kern_ms * 1e-3)
         gather_roof = {"gathers_per_step": nnz, "achieved_gps": round(ach_gps / 1e9, 2),
                        "ceiling_gps": round(ceil_gps / 1e9, 2), "unit": "G gathers/s",

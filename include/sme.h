@@ -53,6 +53,9 @@ const char* sme_last_error(void);
 int sme_version(void);
 /* Number of SMs of the current device (grid sizing is done inside; exported for the host). */
 int sme_device_sm_count(void);
+/* Test hook (A/B timing only): -1 (default) the row sorts of the CSR builds run their
+ * tuned number of occupancy-sized waves; 0 = fixed per-SM caps; k > 0 = k waves. */
+int sme_set_resident_grids(int mode);
 /* out[6]: L2 bytes, max persisting L2 bytes, max access-policy window bytes, SMs,
  * shared memory per SM, max opt-in shared memory per block. */
 int sme_device_info(int64_t* out);

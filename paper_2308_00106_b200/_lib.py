@@ -90,6 +90,7 @@ SIGNATURES: dict[str, list] = {
     "sme_seg_set_scatter_groups": [C.c_int],
     "sme_seg_set_fill_ballot": [C.c_int],
     "sme_seg_set_fill_direct": [C.c_int],
+    "sme_set_resident_grids": [C.c_int],
     "sme_spmv_seg_set_mode": [C.c_int],
     "sme_seg_plan": [i64, p, i32, p, p],
     "sme_seg_plan_split": [i64, i32, p, p],

@@ -26,6 +26,29 @@ inline int grid_for(int64_t work_items, int threads, int per_sm = 8) {
   return (int)(need < cap ? need : cap);
 }
 
+// sme_set_resident_grids: -1 (default) each site's tuned wave count, 0 = the fixed per-SM
+// caps, k > 0 = k resident waves everywhere (sweeps)
+extern int g_resident_grids;
+
+// Grid for a grid-stride loop with equal static shares, in waves of the kernel's
+// occupancy at this block size and dynamic shared memory (the CTAs one pass of the
+// device holds), never more than the work needs.  A fixed per-SM cap ignores the
+// occupancy: the C4 tile sort ran 2.29 waves of 7 CTAs per SM and its last, partial
+// wave a full share at a third of the occupancy; several whole waves also let the SMs
+// that run ahead take more shares (C4 K4 16.6 -> 15.5 ms, C3 14.9 -> 13.8 ms at 16 waves,
+// profiles/round2/resident_grids.txt).  `legacy_per_sm`: the fixed cap (A/B only).
+template <typename K>
+inline int grid_waves(K kernel, int64_t work_items, int threads, size_t smem, int waves, int legacy_per_sm) {
+  if (g_resident_grids == 0) return grid_for(work_items, threads, legacy_per_sm);
+  if (g_resident_grids > 0) waves = g_resident_grids;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess || occ < 1) {
+    (void)cudaGetLastError();
+    occ = 1;
+  }
+  return grid_for(work_items, threads, occ * waves);
+}
+
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 }  // namespace sme

@@ -759,37 +759,44 @@ __global__ void k_csr_expand_rows(int64_t n_rows, const IP* __restrict__ ptr, in
   }
 }
 
+constexpr int SORT_WAVES = 16;
+
 template <typename T, class Src, typename IP>
 int launch_sorts(int64_t n_rows, const IP* new_ptr, Src src, const int32_t* src_col, const T* src_val,
                  const int32_t* cmap, int32_t* out_col, T* out_val, SortLists L, int32_t* flag,
                  uint64_t* dup_key, cudaStream_t s, int64_t n_cols = INT32_MAX) {
   int64_t groups = (n_rows + 31) / 32;
-  int blocks = grid_for(groups * 32, TILE_NT, 16);
   // rows up to the warp sort's limit go to its list, longer ones (<= SMEM_MAX) to the CTA
-  // sort's: each kernel walks only its own rows
+  // sort's: each kernel walks only its own rows, in equal static shares over SORT_WAVES
+  // occupancy-sized waves (grid_waves).
   L.big_min = g_sort_wmed > 0 ? 32 << g_sort_wmed : 32;
-  if (n_cols <= ((int64_t)1 << 27) && g_sort_key32)  // mapped columns < 2^27: 32-bit keys (col << 5 | slot)
-    k_sort_rows_warp<T, Src, true, IP><<<blocks, TILE_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
-                                                               cmap, out_col, out_val, L, flag,
-                                                               (unsigned long long*)dup_key);
-  else
-    k_sort_rows_warp<T, Src, false, IP><<<blocks, TILE_NT, 0, s>>>((int32_t)n_rows, new_ptr, src, src_col, src_val,
-                                                                cmap, out_col, out_val, L, flag,
-                                                                (unsigned long long*)dup_key);
+  if (n_cols <= ((int64_t)1 << 27) && g_sort_key32) {  // mapped columns < 2^27: 32-bit keys (col << 5 | slot)
+    auto kern = k_sort_rows_warp<T, Src, true, IP>;
+    kern<<<grid_waves(kern, groups * 32, TILE_NT, 0, SORT_WAVES, 16), TILE_NT, 0, s>>>(
+        (int32_t)n_rows, new_ptr, src, src_col, src_val, cmap, out_col, out_val, L, flag, (unsigned long long*)dup_key);
+  } else {
+    auto kern = k_sort_rows_warp<T, Src, false, IP>;
+    kern<<<grid_waves(kern, groups * 32, TILE_NT, 0, SORT_WAVES, 16), TILE_NT, 0, s>>>(
+        (int32_t)n_rows, new_ptr, src, src_col, src_val, cmap, out_col, out_val, L, flag, (unsigned long long*)dup_key);
+  }
   SME_CHECK_LAUNCH("k_sort_rows_warp");
+  const int64_t any_work = (int64_t)1 << 40;  // the list lengths are on the device: grid = the resident cap
   const int wmed_max = g_sort_wmed > 0 ? 32 << g_sort_wmed : 0;  // 1: <= 64, 2: <= 128, 3: <= 256, 4: <= 512
   if (wmed_max) {
-    k_sort_rows_wmed<T, Src, IP><<<sm_count() * 8, SORT_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
-                                                                 out_val, L, flag, (unsigned long long*)dup_key,
-                                                                 wmed_max);
+    auto kern = k_sort_rows_wmed<T, Src, IP>;
+    kern<<<grid_waves(kern, any_work, SORT_NT, 0, SORT_WAVES, 8), SORT_NT, 0, s>>>(
+        new_ptr, src, src_col, src_val, cmap, out_col, out_val, L, flag, (unsigned long long*)dup_key, wmed_max);
     SME_CHECK_LAUNCH("k_sort_rows_wmed");
   }
-  k_sort_rows_block<T, Src, IP><<<sm_count() * 4, SORT_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
-                                                                out_val, L, flag, (unsigned long long*)dup_key,
-                                                                wmed_max, g_sort_cta);
+  {
+    auto kern = k_sort_rows_block<T, Src, IP>;
+    kern<<<grid_waves(kern, any_work, SORT_NT, 0, SORT_WAVES, 4), SORT_NT, 0, s>>>(
+        new_ptr, src, src_col, src_val, cmap, out_col, out_val, L, flag, (unsigned long long*)dup_key, wmed_max,
+        g_sort_cta);
+  }
   SME_CHECK_LAUNCH("k_sort_rows_block");
-  k_sort_rows_long<T, Src, IP><<<sm_count(), LONG_NT, 0, s>>>(new_ptr, src, src_col, src_val, cmap, out_col,
-                                                           out_val, L, flag, (unsigned long long*)dup_key);
+  k_sort_rows_long<T, Src, IP><<<grid_waves(k_sort_rows_long<T, Src, IP>, any_work, LONG_NT, 0, SORT_WAVES, 1), LONG_NT, 0, s>>>(
+      new_ptr, src, src_col, src_val, cmap, out_col, out_val, L, flag, (unsigned long long*)dup_key);
   SME_CHECK_LAUNCH("k_sort_rows_long");
   return SME_OK;
 }

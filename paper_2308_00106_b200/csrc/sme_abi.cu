@@ -15,6 +15,8 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+int g_resident_grids = -1;
+
 int sm_count() {
   // cached per device (at most 64 devices per process)
   static int cache[64] = {0};
@@ -36,6 +38,11 @@ SME_API const char* sme_last_error(void) { return sme::g_err; }
 SME_API int sme_version(void) { return 1; }
 
 SME_API int sme_device_sm_count(void) { return sme::sm_count(); }
+
+SME_API int sme_set_resident_grids(int on) {
+  sme::g_resident_grids = on < -1 ? -1 : on;
+  return SME_OK;
+}
 
 // out[0] = L2 bytes, out[1] = max persisting L2 bytes, out[2] = max access-policy window bytes,
 // out[3] = SM count, out[4] = shared memory per SM, out[5] = max shared memory per block (opt-in)

@@ -1110,8 +1110,9 @@ static int seg_fill_impl(int dtype, int64_t n_rows, const IP* row_ptr, const int
       const size_t wbytes = sg_warp_bytes(n_panels, vb, s_seg_fill_direct), smem = wbytes * SG_WARPS;
       SME_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       const int64_t groups = (n_rows + 31) / 32;
-      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((groups + SG_WARPS - 1) / SG_WARPS,
-                                                                 (int64_t)sm_count() * 16));
+      // a fixed 16 CTAs per SM (2-3 waves): one to six occupancy-sized waves measured 2-10 %
+      // slower on C4 (profiles/round2/resident_grids.txt)
+      const int grid = grid_for(groups * 32, SG_WARPS * 32, 16);
       kern<<<grid, SG_WARPS * 32, smem, s>>>(n_rows, row_ptr, col, v, n_panels, bounds, counts, pos, offsets, pk, ov,
                                              hdr, wbytes, (int)s_seg_fill_ballot);
       return SME_OK;
