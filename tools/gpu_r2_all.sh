@@ -14,3 +14,6 @@ d=json.loads(open('gpurun_out/bench_$c.json').read().strip().splitlines()[-1])
 print('$c', {k:d.get(k) for k in ['value','ms_per_step','permute_warm_ms','layout_build_ms','layout_build_warm_ms','setup_warm_ms']}, d.get('roofline',{}).get('frac'), d.get('e2e',{}).get('value'), d.get('permuted_vs_unpermuted',{}).get('ratio'), d.get('clocks'))
 PY
 done
+# launch list of the default bench command (kernel shares; cold-cache, serialised: not bench values)
+timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  --log-file gpurun_out/launches_bench_c4.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-parity > gpurun_out/launches_bench_c4.log 2>&1; echo "ncu list rc=$?"
