@@ -1,7 +1,8 @@
 """Resident-wave grids (sme_set_resident_grids) vs the fixed per-SM caps for the
 grid-stride setup kernels: K4 (permute_csr) and the seg layout build, alternated in
 one process, CUDA events around each, outputs compared bit for bit.
-Usage: resident_ab.py [c4|c3|c4w] [modes, e.g. 1,0: 0 = fixed caps, k = k resident waves]"""
+Usage: resident_ab.py [c4|c3|c4w] [modes, e.g. 1,0: 0 = fixed caps, k = k resident waves] [hook]
+(hook sme_sort_rows_set_dynamic: modes 1,0 = row lists by ticket / static shares)"""
 import sys
 from pathlib import Path
 
@@ -35,9 +36,10 @@ def timed(fn):
 
 
 modes = [int(m) for m in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1, 0]
+hook = sys.argv[3] if len(sys.argv) > 3 else "sme_set_resident_grids"  # or sme_sort_rows_set_dynamic
 for rep in range(3 if cfg != "c4w" else 2):
     for on in modes:
-        _lib.call("sme_set_resident_grids", on)
+        _lib.call(hook, on)
         B, t_k4 = timed(lambda: P.permute_csr(A, p_r, p_c))
         Pn = auto_seg_panels(B)
         lay, t_lay = timed(lambda: SegLayout(B, Pn))
@@ -47,8 +49,9 @@ for rep in range(3 if cfg != "c4w" else 2):
             same = ""
         else:
             same = f" identical={all(torch.equal(a, b) for a, b in zip(ref, sig))}"
-        print(f"{cfg} rep={rep} resident={on}: K4 {t_k4:.2f} ms, layout ({Pn} panels) {t_lay:.2f} ms{same}", flush=True)
+        print(f"{cfg} rep={rep} {hook}={on}: K4 {t_k4:.2f} ms, layout ({Pn} panels) {t_lay:.2f} ms{same}", flush=True)
         del B, lay, sig
         if cfg == "c4w":
             torch.cuda.empty_cache()
-_lib.call("sme_set_resident_grids", 1)
+_lib.call("sme_set_resident_grids", -1)
+_lib.call("sme_sort_rows_set_dynamic", 1)
