@@ -1,8 +1,7 @@
 """Resident-wave grids (sme_set_resident_grids) vs the fixed per-SM caps for the
 grid-stride setup kernels: K4 (permute_csr) and the seg layout build, alternated in
 one process, CUDA events around each, outputs compared bit for bit.
-Usage: resident_ab.py [c4|c3|c4w] [modes, e.g. 1,0: 0 = fixed caps, k = k resident waves] [hook]
-(hook sme_sort_rows_set_dynamic: modes 1,0 = row lists by ticket / static shares)"""
+Usage: resident_ab.py [c4|c3|c4w] [modes, e.g. 1,0: 0 = fixed caps, k = k resident waves] [hook]"""
 import sys
 from pathlib import Path
 
@@ -36,7 +35,7 @@ def timed(fn):
 
 
 modes = [int(m) for m in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1, 0]
-hook = sys.argv[3] if len(sys.argv) > 3 else "sme_set_resident_grids"  # or sme_sort_rows_set_dynamic
+hook = sys.argv[3] if len(sys.argv) > 3 else "sme_set_resident_grids"
 for rep in range(3 if cfg != "c4w" else 2):
     for on in modes:
         _lib.call(hook, on)
@@ -54,4 +53,3 @@ for rep in range(3 if cfg != "c4w" else 2):
         if cfg == "c4w":
             torch.cuda.empty_cache()
 _lib.call("sme_set_resident_grids", -1)
-_lib.call("sme_sort_rows_set_dynamic", 1)
