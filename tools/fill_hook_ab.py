@@ -1,7 +1,6 @@
-"""Seg layout fill: entry-parallel windows with the next window's loads issued one
-iteration ahead (sme_seg_set_fill_ballot(2)) vs loaded at use (1), alternated in one
-process, CUDA events around the SegLayout build, layouts compared bit for bit.
-Usage: fill_pf_ab.py [c4|c4w|c3]"""
+"""Seg layout fill variants behind a test hook (e.g. sme_seg_set_fill_lut), alternated in
+one process, CUDA events around the SegLayout build, layouts compared bit for bit.
+Usage: fill_hook_ab.py [c4|c4w|c3] [hook] [modes, e.g. 1,0]"""
 import sys
 from pathlib import Path
 
@@ -24,9 +23,11 @@ del A
 torch.cuda.empty_cache()
 Pn = auto_seg_panels(B)
 ref = None
+hook = sys.argv[2] if len(sys.argv) > 2 else "sme_seg_set_fill_lut"
+modes = [int(m) for m in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 0]
 for rep in range(4 if cfg != "c4w" else 2):
-    for mode in (1, 2):
-        _lib.call("sme_seg_set_fill_ballot", mode)
+    for mode in modes:
+        _lib.call(hook, mode)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record()
@@ -38,6 +39,6 @@ for rep in range(4 if cfg != "c4w" else 2):
             ref = (lay.pk.clone(), lay.val.clone(), lay.hdr.clone())
         else:
             same = f" identical={bool(torch.equal(ref[0], lay.pk) and torch.equal(ref[1], lay.val) and torch.equal(ref[2], lay.hdr))}"
-        print(f"{cfg} panels={Pn} rep={rep} fill_ballot={mode}: layout build {e0.elapsed_time(e1):.2f} ms{same}", flush=True)
+        print(f"{cfg} panels={Pn} rep={rep} {hook}={mode}: layout build {e0.elapsed_time(e1):.2f} ms{same}", flush=True)
         del lay
-_lib.call("sme_seg_set_fill_ballot", 1)
+_lib.call(hook, 1)
