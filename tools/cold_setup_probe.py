@@ -37,11 +37,12 @@ def step(name, fn):
 
 
 for rep in range(3):
-    A = synth.laplacian5(2828) if cfg == "c5" else synth.random_rows(50_000_000, 50_000_000, 20)
+    A = (synth.laplacian5(2828) if cfg == "c5" else synth.rmat(24, 22, cap=1024) if cfg == "c3"
+         else synth.random_rows(50_000_000, 50_000_000, 20))
     n = A.n_rows
     (p_r, p_c), t_gen = step("gen", lambda: P.random_permutations([(n, axis_seed(7, 0)), (n, axis_seed(7, 1))]))
     _, t_inv = step("inv", lambda: (p_r.d_inverse, p_c.d_inverse))
     B, t_k4 = step("k4", lambda: P.permute_csr(A, p_r, p_c))
-    lay, t_seg = step("seg", lambda: seg_of(B, full_last=True))
+    lay, t_seg = step("seg", lambda: seg_of(B, full_last=(cfg == "c5")))
     print(f"rep {rep}: generation {t_gen:.1f} ms, inverse {t_inv:.1f} ms, K4 {t_k4:.1f} ms, seg layout {t_seg:.1f} ms", flush=True)
     del A, B, lay, p_r, p_c
