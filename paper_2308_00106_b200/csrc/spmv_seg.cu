@@ -767,9 +767,13 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
     const bool pass = endm == 0;  // the whole lane is the middle of one row
     T out = (endm & 8u) ? T(0) : run[3];
     T in_v;
+    // `carry` lives in lane 31 (its previous lane_out); lane 0 takes it through the same
+    // rotated shuffle that hands every other lane its left neighbour's tail, so the chunk's
+    // outgoing chain value needs no broadcast of its own (C4 a further -0.6 %)
     if (__ballot_sync(FULL, pass) == 0u) {
-      in_v = __shfl_up_sync(FULL, out, 1);
+      in_v = __shfl_sync(FULL, lane == 31 ? carry : out, (lane + 31) & 31);
     } else {
+      carry = __shfl_sync(FULL, carry, 31);  // (rare) every lane sees lane 31's carry
       // chains of whole-lane rows: inclusive scan of `out` continuing through pass lanes
       bool head = !pass;
       T sv = out;
@@ -785,11 +789,11 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
       }
       in_v = __shfl_up_sync(FULL, sv, 1);
       out = sv;
+      if (lane == 0) in_v = carry;
     }
-    if (lane == 0) in_v = carry;
     // the chain value leaving lane 31 (its tail plus everything flowing through it)
     const T lane_out = pass ? in_v + run[3] : out;
-    carry = __shfl_sync(FULL, lane_out, 31);
+    if (lane == 31) carry = lane_out;
     // row totals: entries up to the lane's first end get the incoming chain
     bool first = true;
     int slot = 0, n_ends = 0;
@@ -800,15 +804,16 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
         for (int k = 0; k < 4; ++k)
           if ((cur.w[k] >> SEG_CSHIFT) == SEG_MARK) emitm &= ~(1u << k);
       }
+      // exclusive prefix of the lanes' row-end counts (0..4) from three bit ballots instead
+      // of a five-step shuffle scan: the pass's warps wait on the MIO pipe (shuffles, shared
+      // memory) about as long as on memory (ncu short/long scoreboard 6.0 / 6.2 cycles per
+      // issue); C4 -2.1 %, C5 -1.5 %, same bits (profiles/round2/seg_mio.txt)
       const int cnt = __popc(emitm);
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += t;
-      }
-      slot = incl - cnt;
-      n_ends = __shfl_sync(FULL, incl, 31);
+      const unsigned lt = (1u << lane) - 1u;
+      const unsigned b0 = __ballot_sync(FULL, cnt & 1), b1 = __ballot_sync(FULL, cnt & 2),
+                     b2 = __ballot_sync(FULL, cnt & 4);
+      slot = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+      n_ends = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
       __syncwarp();  // the previous chunk's staged rows have been written out
     }
 #pragma unroll
@@ -869,7 +874,7 @@ __device__ __forceinline__ double seg_warp_body(const uint32_t* __restrict__ pk,
         const int last = P1 - 1 - c, kk = last & 3;
         const uint32_t wsel = kk == 0 ? cur.w[0] : kk == 1 ? cur.w[1] : kk == 2 ? cur.w[2] : cur.w[3];
         const uint32_t wl = __shfl_sync(FULL, wsel, last >> 2);
-        if (lane == 0) {
+        if (lane == 31) {  // the lane that holds `carry`
           const bool open = !(wl & SEG_END);
           epi.carry_row[warp] = open ? cur.h + (int)(wl & SEG_DMASK) : -1;
           epi.carry_val[warp] = open ? carry : T(0);
@@ -1015,6 +1020,7 @@ int launch_seg(int32_t n_warps, const uint32_t* pk, const T* val, const int32_t*
       k_spmv_seg<T, false, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
   } else if (s_seg_mode == 3)
     k_seg_probe<T><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y);
+
   else if (s_seg_mode == 7 && accumulate)
     k_spmv_seg<T, true, false, true, kStageRows<T>, true><<<grid, SEG_NT, 0, s>>>(pk, val, hdr, plan, n_warps, xs, y, e);
   else if (s_seg_mode == 7)
