@@ -45,8 +45,9 @@ for rep in range(4):
         if ref is None:
             ref = y.clone()
         same = bool(torch.equal(ref, y))
+        rel_vs0 = float((y - ref).abs().max() / ref.abs().max()) if not same else 0.0
         print(f"{cfg} panels={lay.n_panels} rep={rep} mode={m}: {ms:.4f} ms/SpMV  {2 * B.nnz / ms / 1e6:.1f} GFLOP/s"
-              f"  bitwise={same}", flush=True)
+              f"  bitwise={same} rel_vs0={rel_vs0:.2e}", flush=True)
 _lib.call("sme_spmv_seg_set_mode", 0)
 for m in modes:
     print(f"mode {m}: median {sorted(res[m])[len(res[m]) // 2]:.4f} ms")
