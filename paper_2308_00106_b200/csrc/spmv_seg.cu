@@ -576,15 +576,19 @@ __global__ void k_seg_plan(int64_t n_rows, const int32_t* __restrict__ pos, int3
 // ---------------------------------------------------------------------------
 // SpMV
 // ---------------------------------------------------------------------------
+// The chunk stream.  f64: L1-allocating loads (the L1::no_allocate ones measured C4 +1.0 %,
+// C5 +5.3 %, same bits; profiles/round2/seg_mio.txt); f32: no_allocate (equal on C3).
 template <typename T> struct SegVal;
 template <> struct SegVal<double> {
+  static constexpr bool kAlloc = true;
   static __device__ __forceinline__ void load(const double* p, double v[4]) {
-    const double2 a = ld_nc_na_d2(reinterpret_cast<const double2*>(p));
-    const double2 b = ld_nc_na_d2(reinterpret_cast<const double2*>(p) + 1);
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
   }
 };
 template <> struct SegVal<float> {
+  static constexpr bool kAlloc = false;
   static __device__ __forceinline__ void load(const float* p, float v[4]) {
     const float4 a = ld_nc_na_f4(reinterpret_cast<const float4*>(p));
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
@@ -598,10 +602,11 @@ struct SegChunk {
   int h;
   __device__ __forceinline__ void load(const uint32_t* __restrict__ pk, const T* __restrict__ val,
                                        const int32_t* __restrict__ hdr, int c, int lane) {
-    const int4 q = ld_nc_na_i4(reinterpret_cast<const int4*>(pk + c + 4 * lane));
+    const int4* qp = reinterpret_cast<const int4*>(pk + c + 4 * lane);
+    const int4 q = SegVal<T>::kAlloc ? __ldg(qp) : ld_nc_na_i4(qp);
     w[0] = (uint32_t)q.x; w[1] = (uint32_t)q.y; w[2] = (uint32_t)q.z; w[3] = (uint32_t)q.w;
     SegVal<T>::load(val + c + 4 * lane, v);
-    h = ld_nc_na_i1(hdr + c / SEG_CH);
+    h = SegVal<T>::kAlloc ? __ldg(hdr + c / SEG_CH) : ld_nc_na_i1(hdr + c / SEG_CH);
   }
 };
 
