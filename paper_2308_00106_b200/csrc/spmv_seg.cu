@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int32_t k = 32 * u + lane;
-        pre_c[u] = k < left ? ld_nc_na_i1(col + k) : 0;
+        pre_c[u] = k < left ? __ldg(col + k) : 0;
         pre_v[u] = k < left ? val[k] : T(0);
       }
     }
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_seg_scatter_groups(
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int32_t k = w0 + 32 * u + lane;
-            c[u] = k < k1 ? ld_nc_na_i1(col + k) : 0;
+            c[u] = k < k1 ? __ldg(col + k) : 0;
             v[u] = k < k1 ? val[k] : T(0);
           }
         }
