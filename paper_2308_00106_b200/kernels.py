@@ -64,9 +64,11 @@ def make_row_partition(n_rows: int, workers: int) -> RowPartition:
 
 
 def default_lanes(m: CsrMatrix) -> int:
-    """Threads per row of the CSR-vector kernel: the power of two nearest below
-    mean_row_length / 2.5 (each lane handles >= ~2.5 elements), in [1, 32].
-    Measured on B200: C2 (5 nnz/row) is fastest at 2 lanes, 0.103 ms vs 0.149 ms at 8."""
+    """Threads per row of the CSR-vector kernel: the largest power of two with
+    lanes * 5 <= mean_row_length (each lane handles >= ~2.5 elements), in [1, 32].
+    Measured on B200 (tools/vector_lanes_ab.py): C2 (4.998 nnz/row -> 1 lane) permuted
+    0.1017 ms at 1 lane, 0.1004 at 2, 0.110 at 4, 0.151 at 8; unpermuted 0.0592 at 1,
+    0.0615 at 2 (C5 unpermuted: 0.123 / 0.125) — 1 and 2 lanes are within 1-4 %."""
     if "lanes" not in m._cache:
         mean = m.nnz / max(1, m.n_rows)
         lanes = 1
