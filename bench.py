@@ -80,7 +80,7 @@ def measured_peaks() -> tuple[float, str]:
 class Clocks:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.limit")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
@@ -113,8 +113,20 @@ class Clocks:
             for name, v in zip(names, r[5:9]):
                 if v.strip().lower() == "active":
                     reasons.add(name)
+        def num(i):
+            out = []
+            for r in rows:
+                try:
+                    out.append(float(r[i]))
+                except (IndexError, ValueError):
+                    pass
+            return out
+
+        pw, pl = num(3), num(9)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(rows)}
+                "reasons": sorted(reasons), "samples": len(rows),
+                "power_w": round(statistics.median(pw), 1) if pw else None,
+                "power_limit_w": max(pl) if pl else None}
 
 
 # ---------------------------------------------------------------------------
