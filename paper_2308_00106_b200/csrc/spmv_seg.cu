@@ -582,9 +582,8 @@ template <typename T> struct SegVal;
 template <> struct SegVal<double> {
   static constexpr bool kAlloc = true;
   static __device__ __forceinline__ void load(const double* p, double v[4]) {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    // one 256-bit load per lane (LDG.E.ENL2.256): the lane's 4 values are one 32-byte sector
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
   }
 };
 template <> struct SegVal<float> {
